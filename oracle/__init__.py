@@ -1,0 +1,271 @@
+"""CPU ORACLE for the cascaded FP64x2 GEMM (arXiv 2303.04353).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_2303_04353_b200``) never imports it, and the two share
+no code: this wraps ``oracle/casc_oracle.c`` (plain C, binary64 RNE,
+-ffp-contract=off) through ctypes.
+
+Functions cite the PAPER.md passage they follow; see casc_oracle.c for the
+step-by-step arithmetic and DESIGN.md §3/§4 for the readings and pins.
+Parity unpinned: none.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "casc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+KC = 256
+
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+          "-fopenmp", "-Wall"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _setup(_lib)
+    return _lib
+
+
+_d = ctypes.c_double
+_i64 = ctypes.c_int64
+_pd = ctypes.POINTER(ctypes.c_double)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+_pu8 = ctypes.POINTER(ctypes.c_uint8)
+_pint = ctypes.POINTER(ctypes.c_int)
+
+
+def _setup(L):
+    L.orc_two_sum.argtypes = [_d, _d, _pd, _pd]
+    L.orc_fast_two_sum.argtypes = [_d, _d, _pd, _pd]
+    L.orc_two_prod.argtypes = [_d, _d, _pd, _pd]
+    L.orc_dd_add_d.argtypes = [_d, _d, _d, _pd, _pd]
+    L.orc_dd_add.argtypes = [_d, _d, _d, _d, _pd, _pd]
+    L.orc_dd_mul.argtypes = [_d, _d, _d, _d, _pd, _pd]
+    L.orc_select_widths.argtypes = [_i64, _pint]
+    L.orc_scale_exponent.argtypes = [_pd, _i64, _i64]
+    L.orc_scale_exponent.restype = ctypes.c_int
+    L.orc_split_scalar.argtypes = [_d, _d, ctypes.c_int, _pint, _pd]
+    L.orc_split_a_panel.argtypes = [_i64, _i64, _pd, _pd, _i64, _pint, _pd, _pi32]
+    L.orc_split_b_panel.argtypes = [_i64, _i64, _pd, _pd, _i64, _pint, _pd, _pi32]
+    L.orc_panel_bins.argtypes = [_i64, _i64, _i64, _pd, _pd, _pint, _pd]
+    L.orc_combine.argtypes = [_d, _d, _d, _d, ctypes.c_int, _pint, _pd, _pd]
+    L.orc_casc_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
+                                _i64, _pu8, ctypes.c_int]
+    L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
+                              _i64, ctypes.c_int]
+    L.orc_exact_entries.argtypes = [_i64, _pd, _pd, _i64, _pd, _pd, _i64, _i64, _pi64, _pi64,
+                                    _pd, _pd, _i64, _pd, _pd, _pd, _pd, ctypes.c_int]
+    L.orc_exact_sum.argtypes = [_i64, _pd, _pd, _pd]
+    L.orc_exact_dot.argtypes = [_i64, _pd, _pd, _pd, _pd]
+    L.orc_num_threads.restype = ctypes.c_int
+
+
+def _p(a, ptr=_pd):
+    return a.ctypes.data_as(ptr) if a is not None else None
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def num_threads() -> int:
+    return lib().orc_num_threads()
+
+
+# ---------------------------------------------------------------- DD primitives
+def _pair(fn, *args):
+    r1, r2 = _d(), _d()
+    fn(*args, ctypes.byref(r1), ctypes.byref(r2))
+    return r1.value, r2.value
+
+
+def two_sum(a, b):
+    """Knuth TwoSum (P:L756, P:L947 cite Dekker1971)."""
+    return _pair(lib().orc_two_sum, a, b)
+
+
+def fast_two_sum(a, b):
+    return _pair(lib().orc_fast_two_sum, a, b)
+
+
+def two_prod(a, b):
+    """FMA TwoProd."""
+    return _pair(lib().orc_two_prod, a, b)
+
+
+def dd_add_d(th, tl, x):
+    return _pair(lib().orc_dd_add_d, th, tl, x)
+
+
+def dd_add(xh, xl, yh, yl):
+    return _pair(lib().orc_dd_add, xh, xl, yh, yl)
+
+
+def dd_mul(xh, xl, yh, yl):
+    return _pair(lib().orc_dd_mul, xh, xl, yh, yl)
+
+
+# ---------------------------------------------------------------- cascade steps
+def select_widths(k: int):
+    """(c0, c1, c2) from the §3.3 bit budgets with k_eff = min(k, 256)."""
+    c = (ctypes.c_int * 3)()
+    lib().orc_select_widths(k, c)
+    return tuple(c)
+
+
+def _cw(k):
+    c = (ctypes.c_int * 3)(*select_widths(k))
+    return c
+
+
+def scale_exponent(hi: np.ndarray) -> int:
+    """e with max|hi| in [2^(e-1), 2^e); 0 for all zeros."""
+    hi = _c64(hi).ravel()
+    return lib().orc_scale_exponent(_p(hi), hi.size, 1)
+
+
+def split_scalar(hi: float, lo: float, e: int, widths):
+    """Appendix A split of one FP64x2 value -> (chi0..chi3)."""
+    c = (ctypes.c_int * 3)(*widths)
+    out = (ctypes.c_double * 4)()
+    lib().orc_split_scalar(hi, lo, e, c, out)
+    return tuple(out)
+
+
+def split_a_panel(A_hi, A_lo, widths=None):
+    """Split an m x kp panel of A conformally per row (§3.4, App. A).
+    Returns slices (4, m, kp) in the paper's normalisation and e (m,)."""
+    A_hi, A_lo = _c64(A_hi), _c64(A_lo)
+    m, kp = A_hi.shape
+    c = (ctypes.c_int * 3)(*(widths or select_widths(kp)))
+    S = np.empty((4, m, kp))
+    e = np.empty(m, dtype=np.int32)
+    lib().orc_split_a_panel(m, kp, _p(A_hi), _p(A_lo), kp, c, _p(S), _p(e, _pi32))
+    return S, e
+
+
+def split_b_panel(B_hi, B_lo, widths=None):
+    """Split a kp x n panel of B conformally per column, plus B4, B5, B6
+    (P:L1403-1404).  Returns slices (7, kp, n) and f (n,)."""
+    B_hi, B_lo = _c64(B_hi), _c64(B_lo)
+    kp, n = B_hi.shape
+    c = (ctypes.c_int * 3)(*(widths or select_widths(kp)))
+    S = np.empty((7, kp, n))
+    f = np.empty(n, dtype=np.int32)
+    lib().orc_split_b_panel(kp, n, _p(B_hi), _p(B_lo), n, c, _p(S), _p(f, _pi32))
+    return S, f
+
+
+def panel_bins(SA, SB, widths):
+    """Bins 0, 1, 2, 3-6 of one panel (eqn:Gemm10)."""
+    SA, SB = _c64(SA), _c64(SB)
+    _, m, kp = SA.shape
+    n = SB.shape[2]
+    c = (ctypes.c_int * 3)(*widths)
+    bins = np.empty((4, m, n))
+    lib().orc_panel_bins(m, n, kp, _p(SA), _p(SB), c, _p(bins))
+    return bins
+
+
+def combine(bin0, bin1, bin2, bin36, escale, widths):
+    """fl_casc of one element -> (t_hi, t_lo)."""
+    c = (ctypes.c_int * 3)(*widths)
+    r1, r2 = _d(), _d()
+    lib().orc_combine(bin0, bin1, bin2, bin36, int(escale), c, ctypes.byref(r1),
+                      ctypes.byref(r2))
+    return r1.value, r2.value
+
+
+def casc_gemm(A_hi, A_lo, B_hi, B_lo, nthreads: int = 0):
+    """ORACLE-CASCADE: C := A B through ten cascading FP64 GEMMs per k_C panel.
+    Returns (C_hi, C_lo, flags)."""
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    C_hi = np.empty((m, n))
+    C_lo = np.empty((m, n))
+    flags = np.empty((m, n), dtype=np.uint8)
+    lib().orc_casc_gemm(m, n, k, _p(A_hi), _p(A_lo), k, _p(B_hi), _p(B_lo), n, _p(C_hi),
+                        _p(C_lo), n, _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags
+
+
+def dd_gemm(A_hi, A_lo, B_hi, B_lo, nthreads: int = 0):
+    """ORACLE-DD: triple-loop FP64x2 GEMM."""
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    C_hi = np.empty((m, n))
+    C_lo = np.empty((m, n))
+    lib().orc_dd_gemm(m, n, k, _p(A_hi), _p(A_lo), k, _p(B_hi), _p(B_lo), n, _p(C_hi),
+                      _p(C_lo), n, nthreads)
+    return C_hi, C_lo
+
+
+def exact_entries(A_hi, A_lo, B_hi, B_lo, ii, jj, C_hi=None, C_lo=None, nthreads: int = 0):
+    """ORACLE-EXACT for entries (ii[t], jj[t]): exact C* as RN double-double,
+    err = RN((C_hi + C_lo) - C*) if C given, and |A||B| rounded.
+    Returns dict(ex_hi, ex_lo, err, absab)."""
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    ii = np.ascontiguousarray(ii, dtype=np.int64)
+    jj = np.ascontiguousarray(jj, dtype=np.int64)
+    T = ii.size
+    ex_hi, ex_lo, absab = np.empty(T), np.empty(T), np.empty(T)
+    err = np.empty(T) if C_hi is not None else None
+    if C_hi is not None:
+        C_hi, C_lo = _c64(C_hi), _c64(C_lo)
+        ldc = C_hi.shape[1]
+    else:
+        ldc = 0
+    lib().orc_exact_entries(k, _p(A_hi), _p(A_lo), k, _p(B_hi), _p(B_lo), n, T,
+                            _p(ii, _pi64), _p(jj, _pi64), _p(C_hi), _p(C_lo), ldc, _p(ex_hi),
+                            _p(ex_lo), _p(err), _p(absab), nthreads)
+    return dict(ex_hi=ex_hi, ex_lo=ex_lo, err=err, absab=absab)
+
+
+def exact_sum(x):
+    x = _c64(x).ravel()
+    return _pair(lib().orc_exact_sum, x.size, _p(x))
+
+
+def exact_dot(x, y):
+    x, y = _c64(x).ravel(), _c64(y).ravel()
+    return _pair(lib().orc_exact_dot, x.size, _p(x), _p(y))
+
+
+def north_star_bound(k: int, absab):
+    """|C_gpu - C*| <= 4 k 2^-104 (|A||B|)_ij (BASELINE.json north_star)."""
+    return 4.0 * k * 2.0 ** -104 * np.asarray(absab)
+
+
+def cascerr_bound(k: int, absab, normx, normy, widths):
+    """eq:cascerr: |x|^T|y| eps_hat + 40 k^2 eps_tilde ||x|| ||y||,
+    eps_hat = 2^-106, eps_tilde = 2^-(D2 + 53)."""
+    D2 = sum(widths)
+    return (np.asarray(absab) * 2.0 ** -106
+            + 40.0 * k * k * 2.0 ** -(D2 + 53) * np.asarray(normx) * np.asarray(normy))

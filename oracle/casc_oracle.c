@@ -1,0 +1,550 @@
+/*
+ * casc_oracle.c — CPU ORACLE for the cascaded FP64x2 GEMM (arXiv 2303.04353).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this library. The
+ * product path (paper_2303_04353_b200/) never imports, links or executes it and
+ * shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, obviously-correct C (binary64, round-to-nearest-even, compiled
+ * with -ffp-contract=off and no fast-math so every +, -, * is one IEEE op).
+ * Loops are parallelised over output rows with OpenMP only; nothing is blocked,
+ * fused or reordered beyond what the cited passage states.
+ *
+ * Citations: P:Lnnn = PAPER.md line, S:Lnnn = SPEC.md line, "reading Rn" =
+ * the numbered reading in DESIGN.md §3 (SURVEY.md §8(c) ambiguity table).
+ *
+ * Three parts:
+ *   ORACLE-CASCADE  orc_select_widths, orc_scale_exponent, orc_split_scalar,
+ *                   orc_split_a_panel, orc_split_b_panel, orc_panel_bins,
+ *                   orc_combine, orc_casc_gemm   — the paper's method, step by step.
+ *   ORACLE-DD       orc_dd_gemm                  — triple-loop FP64x2 GEMM.
+ *   ORACLE-EXACT    orc_exact_entries            — exact products via a fixed-point
+ *                   superaccumulator (stands in for the paper's FP128x2 reference,
+ *                   P:L3474).
+ *
+ * Pins: tests/test_oracle_*.py check every function here against Python
+ * Fraction brute force, paper-printed values and closed-form bounds.
+ * Parity unpinned: none (see DESIGN.md §4 for the pin of each function).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define KC 256 /* k_C, the rank-k update depth: P:L3131, reading R3 */
+
+/* ------------------------------------------------------------------------- */
+/* DD primitives. Textbook error-free transformations; the paper only says    */
+/* "FP64x2 addition or quick two-sum arithmetic [Dekker1971]" */
+/* ------------------------------------------------------------------------- */
+
+/* Knuth TwoSum: s = fl(a+b), s + e = a + b exactly (6 adds, branch-free). */
+void orc_two_sum(double a, double b, double* s, double* e) {
+  double ss = a + b;
+  double bb = ss - a;
+  double err = (a - (ss - bb)) + (b - bb);
+  *s = ss;
+  *e = err;
+}
+
+/* Dekker Fast2Sum: valid when |a| >= |b| (or a == 0). */
+void orc_fast_two_sum(double a, double b, double* s, double* e) {
+  double ss = a + b;
+  *e = b - (ss - a);
+  *s = ss;
+}
+
+/* TwoProd with a correctly rounded FMA: p = fl(a*b), p + e = a*b exactly
+ * ("emulating FP64x2 multiplication only requires 1 FMA and 1 multiply"). */
+void orc_two_prod(double a, double b, double* p, double* e) {
+  double pp = a * b;
+  *e = fma(a, b, -pp);
+  *p = pp;
+}
+
+/* DD + double: (s,e) = TwoSum(T.hi, x); e += T.lo; Fast2Sum(s, e). */
+void orc_dd_add_d(double th, double tl, double x, double* rh, double* rl) {
+  double s, e;
+  orc_two_sum(th, x, &s, &e);
+  e = e + tl;
+  orc_fast_two_sum(s, e, rh, rl);
+}
+
+/* DD + DD (the "accurate" variant, two TwoSums). */
+void orc_dd_add(double xh, double xl, double yh, double yl, double* rh, double* rl) {
+  double s1, s2, t1, t2;
+  orc_two_sum(xh, yh, &s1, &s2);
+  orc_two_sum(xl, yl, &t1, &t2);
+  s2 = s2 + t1;
+  orc_fast_two_sum(s1, s2, &s1, &s2);
+  s2 = s2 + t2;
+  orc_fast_two_sum(s1, s2, rh, rl);
+}
+
+/* DD * DD: p = TwoProd(xh, yh); p.lo += xh*yl + xl*yh; renormalise. */
+void orc_dd_mul(double xh, double xl, double yh, double yl, double* rh, double* rl) {
+  double p, e;
+  orc_two_prod(xh, yh, &p, &e);
+  e = e + (xh * yl + xl * yh);
+  orc_fast_two_sum(p, e, rh, rl);
+}
+
+/* ------------------------------------------------------------------------- */
+/* a1. Split widths (§3.3; reading R3: widths from min(k, k_C)).  */
+/*   2c0 + L <= 53;  c0 + c1 + L + 1 <= 53 and 2c1 + L + 2 <= 53;            */
+/*   c0 + c2 + L + 2 <= 53;  L = ceil(log2 k_eff); greedy c0, then c1, c2.    */
+/* ------------------------------------------------------------------------- */
+static int ceil_log2(int64_t k) {
+  int L = 0;
+  while (((int64_t)1 << L) < k) L++;
+  return L;
+}
+
+void orc_select_widths(int64_t k, int* c) {
+  int64_t keff = k < KC ? k : KC;
+  if (keff < 1) keff = 1;
+  int L = ceil_log2(keff);
+  int c0 = 0, c1 = 0, c2 = 0;
+  while (2 * (c0 + 1) + L <= 53) c0++;
+  while (c0 + (c1 + 1) + L + 1 <= 53 && 2 * (c1 + 1) + L + 2 <= 53) c1++;
+  while (c0 + (c2 + 1) + L + 2 <= 53) c2++;
+  c[0] = c0;
+  c[1] = c1;
+  c[2] = c2;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a2. Scale exponent of a vector ("smallest power of two greater      */
+/* than" the max magnitude; P:L1139 ||x|| <= sigma <= 2||x||;   */
+/* reading R1): e = frexp exponent of max |hi|, so max|hi| in [2^(e-1), 2^e). */
+/* All-zero vector: e = 0.                                                    */
+/* ------------------------------------------------------------------------- */
+int orc_scale_exponent(const double* hi, int64_t n, int64_t stride) {
+  double mx = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double a = fabs(hi[i * stride]);
+    if (a > mx) mx = a;
+  }
+  if (mx == 0.0) return 0;
+  int e;
+  frexp(mx, &e);
+  return e;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a3. Appendix A conditional-free split of one FP64x2 value. */
+/* Each limb separately: v = limb * 2^-e; for t = 0,1,2:                      */
+/*   s_t = (v + M_t) - M_t with M_t = 2^(53-c_t) + 2^(52-c_t) (readings R4,   */
+/*   R5: one precomputed constant, "powers of two can be precomputed")*/
+/*   v = (v - s_t) * 2^(c_t);  s_3 = v.   Then chi_t = s_t(hi) + s_t(lo).     */
+/* Output chi[0..3] in the paper's normalisation: value ~ 2^e * (chi0 +       */
+/* sigma1 chi1 + sigma2 chi2 + sigma3 chi3), sigma_t = 2^-D_(t-1)*/
+/* ------------------------------------------------------------------------- */
+static void split_limb(double x, int e, const int* c, double* s) {
+  double v = ldexp(x, -e);
+  for (int t = 0; t < 3; ++t) {
+    double M = ldexp(1.0, 53 - c[t]) + ldexp(1.0, 52 - c[t]);
+    double r = v + M;
+    r = r - M;
+    s[t] = r;
+    v = (v - r) * ldexp(1.0, c[t]);
+  }
+  s[3] = v;
+}
+
+void orc_split_scalar(double hi, double lo, int e, const int* c, double* chi) {
+  double sh[4], sl[4];
+  split_limb(hi, e, c, sh);
+  split_limb(lo, e, c, sl);
+  for (int t = 0; t < 4; ++t) chi[t] = sh[t] + sl[t];
+}
+
+/* ------------------------------------------------------------------------- */
+/* Panel splits (§3.4: rows of A and columns of B */
+/* split conformally; reading R2: one scale per (row, k_C panel) and per      */
+/* (column, k_C panel)).                                                      */
+/*   A panel: rows 0..m-1, columns p0..p0+kp-1 of A (row-major, lda).         */
+/*     out: S[t*m*kp + i*kp + p], t = 0..3 (canonical, unaligned); e[i].      */
+/*   B panel: rows p0..p0+kp-1, columns 0..n-1 of B (row-major, ldb).         */
+/*     out: S[t*kp*n + p*n + j], t = 0..6; f[j].                              */
+/*     B4 = B2 + 2^-c2 B3; B5 = B1 + 2^-c1 B4; B6 = B0 + 2^-c0 B5 (P:L1403-    */
+/*     1404; reading R7: nested, one RNE add each).                           */
+/* ------------------------------------------------------------------------- */
+void orc_split_a_panel(int64_t m, int64_t kp, const double* Ahi, const double* Alo,
+                       int64_t lda, const int* c, double* S, int32_t* e) {
+  for (int64_t i = 0; i < m; ++i) {
+    int ei = orc_scale_exponent(Ahi + i * lda, kp, 1);
+    e[i] = ei;
+    for (int64_t p = 0; p < kp; ++p) {
+      double chi[4];
+      orc_split_scalar(Ahi[i * lda + p], Alo[i * lda + p], ei, c, chi);
+      for (int t = 0; t < 4; ++t) S[(int64_t)t * m * kp + i * kp + p] = chi[t];
+    }
+  }
+}
+
+void orc_split_b_panel(int64_t kp, int64_t n, const double* Bhi, const double* Blo,
+                       int64_t ldb, const int* c, double* S, int32_t* f) {
+  const int64_t sz = kp * n;
+  for (int64_t j = 0; j < n; ++j) {
+    int fj = orc_scale_exponent(Bhi + j, kp, ldb);
+    f[j] = fj;
+    for (int64_t p = 0; p < kp; ++p) {
+      double psi[4];
+      orc_split_scalar(Bhi[p * ldb + j], Blo[p * ldb + j], fj, c, psi);
+      double b4 = psi[2] + ldexp(psi[3], -c[2]); /* sigma3/sigma2 = 2^-c2 */
+      double b5 = psi[1] + ldexp(b4, -c[1]);     /* sigma2/sigma1 = 2^-c1 */
+      double b6 = psi[0] + ldexp(b5, -c[0]);     /* sigma1 = 2^-c0        */
+      double out[7] = {psi[0], psi[1], psi[2], psi[3], b4, b5, b6};
+      for (int t = 0; t < 7; ++t) S[t * sz + p * n + j] = out[t];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
+/* a5. Bins of one k_C panel (eqn:Gemm10 P:L1407-1440; bins P:L633-745;      */
+/* reading R8: exact in-bin alignment factors).                               */
+/*   bin0  = sum_p A0 B0                                     (ref scale 1)    */
+/*   bin1  = sum_p (A0 B1 + A1 B0)                           (ref sigma1)     */
+/*   bin2  = sum_p (A0 B2 + 2^(c1-c0) A1 B1 + A2 B0)         (ref sigma2)     */
+/*   bin36 = sum_p (A0 B3 + 2^(c2-c0) A1 B4 + 2^(c2-c0) A2 B5 + A3 B6)        */
+/*                                                           (ref sigma3)     */
+/* Bins 0-2 are exact, so their order is irrelevant; bin36 is       */
+/* evaluated in FP64 with p ascending and terms in the order written.         */
+/* bins out: bins[b*m*n + i*n + j], b = 0..3.                                 */
+/* ------------------------------------------------------------------------- */
+void orc_panel_bins(int64_t m, int64_t n, int64_t kp, const double* SA, const double* SB,
+                    const int* c, double* bins) {
+  const int64_t sa = m * kp, sb = kp * n, sc = m * n;
+#ifdef ORC_MUTATE_ALIGN
+  /* Mutation canary: a deliberately wrong alignment factor. Only the
+   * test suite builds this variant, to prove the bin identity test catches it. */
+  const double f11 = ldexp(1.0, c[1] - c[0] + 1);
+#else
+  const double f11 = ldexp(1.0, c[1] - c[0]); /* sigma1^2/sigma2 */
+#endif
+  const double f36 = ldexp(1.0, c[2] - c[0]); /* sigma1 sigma2 / sigma3 */
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i) {
+    for (int64_t j = 0; j < n; ++j) {
+      double b0 = 0, b1 = 0, b2 = 0, b36 = 0;
+      for (int64_t p = 0; p < kp; ++p) {
+        const double a0 = SA[0 * sa + i * kp + p], a1 = SA[1 * sa + i * kp + p];
+        const double a2 = SA[2 * sa + i * kp + p], a3 = SA[3 * sa + i * kp + p];
+        const double y0 = SB[0 * sb + p * n + j], y1 = SB[1 * sb + p * n + j];
+        const double y2 = SB[2 * sb + p * n + j], y3 = SB[3 * sb + p * n + j];
+        const double y4 = SB[4 * sb + p * n + j], y5 = SB[5 * sb + p * n + j];
+        const double y6 = SB[6 * sb + p * n + j];
+        b0 = b0 + a0 * y0;
+        b1 = b1 + a0 * y1;
+        b1 = b1 + a1 * y0;
+        b2 = b2 + a0 * y2;
+        b2 = b2 + f11 * (a1 * y1);
+        b2 = b2 + a2 * y0;
+        b36 = b36 + a0 * y3;
+        b36 = b36 + f36 * (a1 * y4);
+        b36 = b36 + f36 * (a2 * y5);
+        b36 = b36 + a3 * y6;
+      }
+      bins[0 * sc + i * n + j] = b0;
+      bins[1 * sc + i * n + j] = b1;
+      bins[2 * sc + i * n + j] = b2;
+      bins[3 * sc + i * n + j] = b36;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
+/* a6. Combine one element's bins (fl_casc: bin0 (+) (bin1 (+)  */
+/* (bin2 (+) fl(bin3-6))) with (+) in FP64x2; order bin 6 -> bin 0, P:L948-   */
+/* 949; Sigma, T applied after; reading R9 for the DD ops). */
+/*   T = TwoSum(sigma2 bin2, sigma3 bin36); T = T (+) sigma1 bin1;            */
+/*   T = T (+) bin0; T *= 2^(e+f).                                            */
+/* ------------------------------------------------------------------------- */
+void orc_combine(double bin0, double bin1, double bin2, double bin36, int escale,
+                 const int* c, double* th, double* tl) {
+  const int D0 = c[0], D1 = c[0] + c[1], D2 = c[0] + c[1] + c[2];
+  double h, l;
+  orc_two_sum(ldexp(bin2, -D1), ldexp(bin36, -D2), &h, &l);
+  orc_dd_add_d(h, l, ldexp(bin1, -D0), &h, &l);
+  orc_dd_add_d(h, l, bin0, &h, &l);
+  *th = ldexp(h, escale);
+  *tl = ldexp(l, escale);
+}
+
+/* ------------------------------------------------------------------------- */
+/* ORACLE-CASCADE: C := A B staged as rank-k_C updates (§3.5 P:L1474- */
+/* 1484, §4.2): for each panel q ascending: split A and B        */
+/* panels, 10-product bins, combine, C (+)= T in FP64x2 (P:L2839;    */
+/* reading R10), flag |= (bin0 == 0) (§3.7, §4.4;        */
+/* reading R11). k == 0 gives C = 0, flags = 0 (reading R18).                 */
+/* flags may be NULL. C is m x n row-major with ldc.                          */
+/* ------------------------------------------------------------------------- */
+void orc_casc_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const double* Alo,
+                   int64_t lda, const double* Bhi, const double* Blo, int64_t ldb, double* Chi,
+                   double* Clo, int64_t ldc, uint8_t* flags, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  int c[3];
+  orc_select_widths(k, c);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Chi[i * ldc + j] = 0.0;
+      Clo[i * ldc + j] = 0.0;
+      if (flags) flags[i * n + j] = 0;
+    }
+  if (m == 0 || n == 0 || k == 0) return;
+  const int64_t kpmax = k < KC ? k : KC;
+  double* SA = (double*)malloc(sizeof(double) * 4 * m * kpmax);
+  double* SB = (double*)malloc(sizeof(double) * 7 * kpmax * n);
+  double* bins = (double*)malloc(sizeof(double) * 4 * m * n);
+  int32_t* e = (int32_t*)malloc(sizeof(int32_t) * m);
+  int32_t* f = (int32_t*)malloc(sizeof(int32_t) * n);
+  for (int64_t p0 = 0; p0 < k; p0 += KC) {
+    const int64_t kp = (k - p0) < KC ? (k - p0) : KC;
+    orc_split_a_panel(m, kp, Ahi + p0, Alo + p0, lda, c, SA, e);
+    orc_split_b_panel(kp, n, Bhi + p0 * ldb, Blo + p0 * ldb, ldb, c, SB, f);
+    orc_panel_bins(m, n, kp, SA, SB, c, bins);
+    const int64_t sc = m * n;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        const double b0 = bins[0 * sc + i * n + j];
+        double th, tl;
+        orc_combine(b0, bins[1 * sc + i * n + j], bins[2 * sc + i * n + j],
+                    bins[3 * sc + i * n + j], e[i] + f[j], c, &th, &tl);
+        orc_dd_add(Chi[i * ldc + j], Clo[i * ldc + j], th, tl, &Chi[i * ldc + j],
+                   &Clo[i * ldc + j]);
+        if (flags && b0 == 0.0) flags[i * n + j] = 1;
+      }
+  }
+  free(SA);
+  free(SB);
+  free(bins);
+  free(e);
+  free(f);
+}
+
+/* Rows [r0, r0+mr) of ORACLE-CASCADE, for bounded CPU-baseline samples and
+ * sampled parity at full size: identical arithmetic, C rows only. */
+void orc_casc_gemm_rows(int64_t r0, int64_t mr, int64_t n, int64_t k, const double* Ahi,
+                        const double* Alo, int64_t lda, const double* Bhi, const double* Blo,
+                        int64_t ldb, double* Chi, double* Clo, int64_t ldc, uint8_t* flags,
+                        int nthreads) {
+  orc_casc_gemm(mr, n, k, Ahi + r0 * lda, Alo + r0 * lda, lda, Bhi, Blo, ldb, Chi, Clo, ldc,
+                flags, nthreads);
+}
+
+/* ------------------------------------------------------------------------- */
+/* ORACLE-DD: plain triple-loop FP64x2 GEMM, the paper's accuracy comparator */
+/* (§5.2 P:L3549 "a simple triple-nested loop in FP64x2 arithmetic";          */
+/* S:L399-405). C := A B, loop order i, j, p; dd_mul then dd_add.             */
+/* ------------------------------------------------------------------------- */
+void orc_dd_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const double* Alo,
+                 int64_t lda, const double* Bhi, const double* Blo, int64_t ldb, double* Chi,
+                 double* Clo, int64_t ldc, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double ch = 0.0, cl = 0.0;
+      for (int64_t p = 0; p < k; ++p) {
+        double ph, pl;
+        orc_dd_mul(Ahi[i * lda + p], Alo[i * lda + p], Bhi[p * ldb + j], Blo[p * ldb + j], &ph,
+                   &pl);
+        orc_dd_add(ch, cl, ph, pl, &ch, &cl);
+      }
+      Chi[i * ldc + j] = ch;
+      Clo[i * ldc + j] = cl;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* ORACLE-EXACT: fixed-point superaccumulator (Kulisch style,     */
+/* S:L172-173). Value = sum_i dig[i] * 2^(32 i + SA_MINEXP); digits int64,    */
+/* base 2^32, so each digit absorbs >= 2^30 additions before normalisation.   */
+/* Covers every product of two finite doubles (exponents -2148 .. 2047).      */
+/* ------------------------------------------------------------------------- */
+#define SA_MINEXP (-2240)
+#define SA_NDIG 140 /* 140 * 32 = 4480 bits: 2^-2240 .. 2^2240 */
+
+typedef struct {
+  int64_t d[SA_NDIG];
+  int64_t nadd;
+} superacc;
+
+static void sa_clear(superacc* s) { memset(s, 0, sizeof(*s)); }
+
+static void sa_normalize(superacc* s) {
+  int64_t carry = 0;
+  for (int i = 0; i < SA_NDIG; ++i) {
+    int64_t v = s->d[i] + carry;
+    int64_t lo = v & 0xFFFFFFFFLL;     /* in [0, 2^32) */
+    carry = (v - lo) / 4294967296LL;   /* exact: v - lo is a multiple of 2^32 */
+    s->d[i] = lo;
+  }
+  s->d[SA_NDIG - 1] += carry * 4294967296LL; /* top digit keeps the sign */
+  s->nadd = 0;
+}
+
+static void sa_add_double(superacc* s, double x) {
+  if (x == 0.0) return;
+  int ex;
+  double fr = frexp(fabs(x), &ex);                   /* |x| = fr * 2^ex, fr in [0.5,1) */
+  uint64_t mant = (uint64_t)ldexp(fr, 53);            /* exact: 53-bit integer */
+  int q = ex - 53;                                    /* |x| = mant * 2^q */
+  if (q < -1074 - 53) {                               /* subnormal: mant has fewer bits */
+    /* ldexp(fr,53) is still exact; q as computed remains correct */
+  }
+  int pos = q - SA_MINEXP;
+  int di = pos / 32, sh = pos % 32;
+  unsigned __int128 v = (unsigned __int128)mant << sh;
+  int64_t p0 = (int64_t)(uint64_t)(v & 0xFFFFFFFFu);
+  int64_t p1 = (int64_t)(uint64_t)((v >> 32) & 0xFFFFFFFFu);
+  int64_t p2 = (int64_t)(uint64_t)((v >> 64) & 0xFFFFFFFFu);
+  if (x > 0) {
+    s->d[di] += p0; s->d[di + 1] += p1; s->d[di + 2] += p2;
+  } else {
+    s->d[di] -= p0; s->d[di + 1] -= p1; s->d[di + 2] -= p2;
+  }
+  if (++s->nadd >= (1LL << 29)) sa_normalize(s);
+}
+
+/* Add the exact product a*b (TwoProd: two doubles, exact). */
+static void sa_add_prod(superacc* s, double a, double b) {
+  double p, e;
+  orc_two_prod(a, b, &p, &e);
+  sa_add_double(s, p);
+  sa_add_double(s, e);
+}
+
+/* Correctly rounded (RNE) double nearest to the accumulator (no overflow). */
+static double sa_to_double(superacc* s) {
+  sa_normalize(s);
+  int neg = s->d[SA_NDIG - 1] < 0;
+  int64_t dig[SA_NDIG];
+  if (neg) {
+    /* two's complement negate in base 2^32: value -> -value */
+    int64_t carry = 1;
+    for (int i = 0; i < SA_NDIG; ++i) {
+      int64_t v = (~s->d[i] & 0xFFFFFFFFLL) + carry;
+      carry = v >> 32;
+      dig[i] = v & 0xFFFFFFFFLL;
+    }
+  } else {
+    memcpy(dig, s->d, sizeof(dig));
+  }
+  int h = SA_NDIG - 1;
+  while (h >= 0 && dig[h] == 0) --h;
+  if (h < 0) return 0.0;
+  int lo = h - 2 < 0 ? 0 : h - 2;
+  unsigned __int128 v = 0;
+  for (int i = h; i >= lo; --i) v = (v << 32) | (unsigned __int128)(uint64_t)dig[i];
+  int sticky = 0;
+  for (int i = lo - 1; i >= 0; --i)
+    if (dig[i]) { sticky = 1; break; }
+  /* v has >= 65 significant bits when h >= 2; setting bit 0 as a sticky bit is
+   * exact for round-to-nearest to 53 bits. (__int128 -> double rounds RNE.) */
+  v = (v << 1) | (unsigned __int128)sticky;
+  double r = ldexp((double)v, 32 * lo + SA_MINEXP - 1);
+  return neg ? -r : r;
+}
+
+/* For each requested entry (ii[t], jj[t]):
+ *   exact C*_{ij} = sum_p (Ahi+Alo)(Bhi+Blo)  -> (ex_hi, ex_lo) RN double-double
+ *   err  = RN( (Chi + Clo) - C*_{ij} )          (if Chi != NULL)
+ *   absab = RN( sum_p |A_ip| |B_pj| )            (|A| = |Ahi + Alo| exactly)
+ * Any output pointer may be NULL. */
+void orc_exact_entries(int64_t k, const double* Ahi, const double* Alo, int64_t lda,
+                       const double* Bhi, const double* Blo, int64_t ldb, int64_t nent,
+                       const int64_t* ii, const int64_t* jj, const double* Chi,
+                       const double* Clo, int64_t ldc, double* ex_hi, double* ex_lo,
+                       double* err, double* absab, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t t = 0; t < nent; ++t) {
+    const int64_t i = ii[t], j = jj[t];
+    superacc* s = (superacc*)malloc(sizeof(superacc));
+    superacc* sa = (superacc*)malloc(sizeof(superacc));
+    sa_clear(s);
+    sa_clear(sa);
+    for (int64_t p = 0; p < k; ++p) {
+      const double ah = Ahi[i * lda + p], al = Alo[i * lda + p];
+      const double bh = Bhi[p * ldb + j], bl = Blo[p * ldb + j];
+      sa_add_prod(s, ah, bh);
+      sa_add_prod(s, ah, bl);
+      sa_add_prod(s, al, bh);
+      sa_add_prod(s, al, bl);
+      /* |a| |b| with a = ah + al exactly: sign of a is sign of ah (non-overlap). */
+      const double sgna = (ah < 0) ? -1.0 : 1.0, sgnb = (bh < 0) ? -1.0 : 1.0;
+      sa_add_prod(sa, sgna * ah, sgnb * bh);
+      sa_add_prod(sa, sgna * ah, sgnb * bl);
+      sa_add_prod(sa, sgna * al, sgnb * bh);
+      sa_add_prod(sa, sgna * al, sgnb * bl);
+    }
+    if (absab) absab[t] = sa_to_double(sa);
+    if (ex_hi || ex_lo || err) {
+      superacc cp = *s;
+      double h = sa_to_double(&cp);
+      sa_add_double(&cp, -h);
+      double l = sa_to_double(&cp);
+      if (ex_hi) ex_hi[t] = h;
+      if (ex_lo) ex_lo[t] = l;
+    }
+    if (err && Chi) {
+      sa_add_double(s, -Chi[i * ldc + j]);
+      sa_add_double(s, -Clo[i * ldc + j]);
+      err[t] = -sa_to_double(s); /* (C_hi + C_lo) - exact */
+    }
+    free(s);
+    free(sa);
+  }
+}
+
+/* Exact sum of a list of doubles (RN double-double), for pins of the exact  */
+/* bins and the DD primitives.                                               */
+void orc_exact_sum(int64_t n, const double* x, double* rh, double* rl) {
+  superacc* s = (superacc*)malloc(sizeof(superacc));
+  sa_clear(s);
+  for (int64_t i = 0; i < n; ++i) sa_add_double(s, x[i]);
+  double h = sa_to_double(s);
+  sa_add_double(s, -h);
+  *rh = h;
+  *rl = sa_to_double(s);
+  free(s);
+}
+
+/* Exact dot product sum_p x_p y_p, RN double-double. */
+void orc_exact_dot(int64_t n, const double* x, const double* y, double* rh, double* rl) {
+  superacc* s = (superacc*)malloc(sizeof(superacc));
+  sa_clear(s);
+  for (int64_t i = 0; i < n; ++i) sa_add_prod(s, x[i], y[i]);
+  double h = sa_to_double(s);
+  sa_add_double(s, -h);
+  *rh = h;
+  *rl = sa_to_double(s);
+  free(s);
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
