@@ -1,0 +1,191 @@
+/*
+ * casc.h — C ABI of the B200-native cascaded FP64x2 GEMM (arXiv 2303.04353,
+ * "Cascading GEMM": FP64x2 GEMM as ten cascading FP64 GEMMs).
+ *
+ *   C := A B  for FP64x2 (double-double) A (m x k), B (k x n), C (m x n)
+ *   ("C := A B"; P:L228 fixed number of FP64 GEMMs, data-independent
+ *   time; P:L39-45 FP64 for all O(n^3) work, cheap cancellation detection).
+ *
+ * Method (all of it runs in this library's sm_100a kernels):
+ *   1. widths c0,c1,c2 from min(k, 256) (§3.3);
+ *   2. per (row of A, 256-wide k panel) and (column of B, panel) power-of-two
+ *      scales;
+ *   3. Appendix A conditional-free split of every FP64x2 element into four
+ *      FP64 slices A0..A3 / B0..B3, plus B4, B5, B6;
+ *   4. per panel, the ten FP64 products of eqn:Gemm10 on the FP64
+ *      tensor cores (DMMA) into four on-chip bins 0, 1, 2, 3-6;
+ *   5. per panel, the FP64x2 combine bin 3-6 -> 2 -> 1 -> 0 (P:L946-949,
+ *      P:L2506-2520), scaling by the row/column scales, and FP64x2 accumulation
+ *      into C across panels;
+ *   6. cancellation flag = OR over panels of (bin0 == 0) (§3.7, §4.4
+ *      P:L3380-3382).
+ *
+ * Conventions (all entry points):
+ *   - Matrices are row-major with a leading dimension (elements).  An FP64x2
+ *     value is the unevaluated sum hi + lo of two binary64 arrays (SoA).
+ *   - Unless stated otherwise, pointers are DEVICE pointers owned by the
+ *     caller; the library reads inputs and writes outputs only.
+ *   - Work is enqueued on `stream` (NULL = legacy default stream).  The library
+ *     never synchronises the host except where stated (allocation of its own
+ *     workspace); kernel faults surface at the caller's next synchronisation.
+ *   - Preconditions (not checked): inputs finite; pairs normalised
+ *     (|lo| <= ulp(hi)/2); every row-panel / column-panel max |hi| in
+ *     [2^-1000, 2^1000).  Outside them results are computed but the paper's
+ *     error bound is not guaranteed.
+ *   - Return value: a casc_status.  No exception crosses the ABI.
+ *   - Results are deterministic: the same inputs give the same bits on every
+ *     call, every grid size and every number of GPUs.
+ */
+#ifndef CASC_H_
+#define CASC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* An opaque CUDA stream handle (ABI-identical to cudaStream_t). */
+typedef struct CUstream_st* casc_stream_t;
+
+typedef enum {
+  CASC_OK = 0,
+  CASC_ERR_INVALID = 1,     /* negative size, ld too small, NULL with non-zero size, aliasing */
+  CASC_ERR_CUDA = 2,        /* CUDA launch / runtime / allocation failure */
+  CASC_ERR_UNSUPPORTED = 3  /* device is not sm_100 (B200) */
+} casc_status;
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* casc_status_string(int status);
+
+/* k_C, the rank-k update depth the digit budgets are tied to (§3.5 P:L1474-1484,
+ * §4.2): A and B are split and combined per 256-wide k panel. */
+#define CASC_KC 256
+
+/* Split widths c[0..2] = (c0, c1, c2) for inner dimension k (host function).
+ * §3.3 P:L916-945 with L = ceil(log2(min(k, 256))): greedy c0 (2c0 + L <= 53),
+ * then c1 (c0 + c1 + L + 1 <= 53, 2c1 + L + 2 <= 53), then c2
+ * (c0 + c2 + L + 2 <= 53).  k = 256 -> (22, 21, 21); k = 64 -> (23, 22, 22).
+ * Returns CASC_ERR_INVALID if c is NULL or k < 0. */
+int casc_select_widths(int64_t k, int* c);
+
+/* ------------------------------------------------------------------------ */
+/* The north-star entry point.                                               */
+/* ------------------------------------------------------------------------ */
+
+/* C := A B in cascaded FP64x2 (ten FP64 DMMA GEMMs per 256-wide k panel).
+ *   m, n, k   >= 0.  m == 0 or n == 0: no-op.  k == 0: C := 0, flags := 0.
+ *   A_hi, A_lo: m x k, leading dimension lda >= max(1, k).
+ *   B_hi, B_lo: k x n, leading dimension ldb >= max(1, n).
+ *   C_hi, C_lo: m x n outputs, leading dimension ldc >= max(1, n); must not
+ *               overlap A or B (CASC_ERR_INVALID).  C_hi + C_lo is the result.
+ *   flags:      m x n uint8 output (leading dimension n) or NULL.  flags[i*n+j]
+ *               = 1 iff bin 0 of entry (i, j) was exactly zero in some panel
+ *               (catastrophic cancellation suspected, §3.7); the library
+ *               performs no correction.
+ *   stream:     CUDA stream.
+ * Uses a library-owned device workspace of casc_workspace_bytes(m, n, k)
+ * bytes, allocated (host-synchronising cudaMalloc) on first use or growth
+ * and reused; release it with casc_finalize().  Not re-entrant across host
+ * threads on the same device. */
+int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
+                     const double* A_hi, const double* A_lo, int64_t lda,
+                     const double* B_hi, const double* B_lo, int64_t ldb,
+                     double* C_hi, double* C_lo, int64_t ldc,
+                     uint8_t* flags, casc_stream_t stream);
+
+/* Bytes of device workspace needed by casc_gemm_fp64x2 for (m, n, k):
+ * casc_packed_a_bytes(m, k) + casc_packed_b_bytes(k, n). */
+size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k);
+
+/* Same as casc_gemm_fp64x2 with a caller-owned device workspace of at least
+ * casc_workspace_bytes(m, n, k) bytes (256-byte aligned).  No allocation, no
+ * host synchronisation, re-entrant. */
+int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
+                        const double* A_hi, const double* A_lo, int64_t lda,
+                        const double* B_hi, const double* B_lo, int64_t ldb,
+                        double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* workspace, size_t workspace_bytes,
+                        casc_stream_t stream);
+
+/* Free the library-owned workspace of the current device (host-synchronising). */
+int casc_finalize(void);
+
+/* ------------------------------------------------------------------------ */
+/* Split ("packed") interface: phase 1 and phases 2-3 as separate calls, used */
+/* by the multi-GPU layer (each rank packs its rows of A and its column slab  */
+/* of B; B's packed slabs are all-gathered; each rank multiplies its rows).   */
+/* Packed buffers are opaque device byte arrays in the GEMM kernel's layout   */
+/* (DESIGN.md §6): 64-row (A) / 64-column (B) blocks, each block contiguous,  */
+/* so a contiguous range of blocks is a contiguous byte range.               */
+/* ------------------------------------------------------------------------ */
+
+/* Bytes of the packed A (m x k): 4 slices + per-(row, panel) exponents.
+ * Equals ceil(m/64) * casc_packed_a_block_bytes(k). */
+size_t casc_packed_a_bytes(int64_t m, int64_t k);
+size_t casc_packed_a_block_bytes(int64_t k);
+/* Bytes of the packed B (k x n): 7 slices + per-(column, panel) exponents.
+ * Equals ceil(n/64) * casc_packed_b_block_bytes(k); a column slab of B whose
+ * width is a multiple of 64 packs into exactly (width/64) blocks. */
+size_t casc_packed_b_bytes(int64_t k, int64_t n);
+size_t casc_packed_b_block_bytes(int64_t k);
+
+/* Phase 1 for A: per (row, panel) scale exponent and the Appendix A split
+ * into A0, A1, A2, A3 (A2 stored pre-multiplied by 2^(c0-c1), an exact
+ * power-of-two alignment).  Widths come from k (the FULL inner
+ * dimension).  packed_a: casc_packed_a_bytes(m, k) bytes, 16-byte aligned. */
+int casc_pack_a(int64_t m, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
+                void* packed_a, casc_stream_t stream);
+
+/* Phase 1 for B: per (column, panel) scale exponent, split into B0..B3 and
+ * the derived B4 = B2 + 2^-c2 B3, B5 = B1 + 2^-c1 B4, B6 = B0 + 2^-c0 B5
+ * (one RNE add each), stored pre-aligned (B2 x 2^(c0-c1),
+ * B4 x 2^(c2-c0), B5 x 2^(c1+c2-2c0)).  packed_b: casc_packed_b_bytes(k, n). */
+int casc_pack_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, int64_t ldb,
+                void* packed_b, casc_stream_t stream);
+
+/* Phases 2-3: C := A B from packed operands (same m, n, k as packed).
+ * Fused kernel: TMA bulk copies of the slice tiles into shared memory, the ten
+ * products on DMMA into four register bins, per-panel FP64x2 combine and
+ * detector.  flags as in casc_gemm_fp64x2 (leading dimension n). */
+int casc_gemm_packed(int64_t m, int64_t n, int64_t k, const void* packed_a,
+                     const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                     uint8_t* flags, casc_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Test / inspection entry points (same kernels as the product path).        */
+/* ------------------------------------------------------------------------ */
+
+/* Run casc_pack_a and export its result in the paper's normalisation:
+ *   slices: 4 x m x k doubles, slices[t*m*k + i*k + p] = chi_t of A(i, p)
+ *           (value ~ 2^e (chi0 + 2^-D0 chi1 + 2^-D1 chi2 + 2^-D2 chi3));
+ *   e:      P x m int32 (P = ceil(k/256)), e[q*m + i] = scale exponent of row i
+ *           in panel q (max |A_hi| over the panel in [2^(e-1), 2^e); 0 if zero).
+ * Uses a temporary device allocation (cudaMallocAsync on `stream`). */
+int casc_split_a(int64_t m, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
+                 double* slices, int32_t* e, casc_stream_t stream);
+
+/* As casc_split_a for B: slices 7 x k x n (B0..B6, paper normalisation, no
+ * pre-alignment), f: P x n int32. */
+int casc_split_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, int64_t ldb,
+                 double* slices, int32_t* f, casc_stream_t stream);
+
+/* Bins of one k panel `panel` (0 <= panel < ceil(k/256)) as computed by the
+ * fused kernel, in the paper's reference scales (bin0: 1, bin1: sigma1,
+ * bin2: sigma2, bin36: sigma3): bins[b*m*n + i*n + j], b = 0..3.  Bins 0-2 are
+ * exact and therefore bit-comparable with any exact evaluation. */
+int casc_debug_bins(int64_t m, int64_t n, int64_t k,
+                    const double* A_hi, const double* A_lo, int64_t lda,
+                    const double* B_hi, const double* B_lo, int64_t ldb,
+                    int64_t panel, double* bins, casc_stream_t stream);
+
+/* Number of kernel launches the last successful call of the given entry point
+ * family enqueued on this host thread (for launch accounting in bench.py). */
+int casc_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CASC_H_ */

@@ -1,0 +1,250 @@
+"""paper_2303_04353_b200 — B200-native cascaded FP64x2 GEMM (arXiv 2303.04353).
+
+Thin Python binding over the C ABI of ``libcasc.so`` (include/casc.h).  Every
+function here has the name of the C entry point it marshals to and does
+argument marshalling only (pointers, leading dimensions, the current CUDA
+stream); every step of the method runs in the library's sm_100a kernels.
+PyTorch is used for device memory and streams only.
+
+There is no CPU fallback: importing this package fails loudly if the CUDA
+library has not been built (``python -c "import __graft_entry__ as g; g.build()"``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcasc.so")
+KC = 256
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension first "
+                      "(__graft_entry__.build()); there is no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_sig("casc_status_string", [ctypes.c_int], ctypes.c_char_p)
+_sig("casc_select_widths", [_i64, ctypes.POINTER(ctypes.c_int)])
+_sig("casc_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp,
+                          _vp])
+_sig("casc_gemm_fp64x2_ws", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
+                             _vp, _vp, _sz, _vp])
+_sig("casc_workspace_bytes", [_i64, _i64, _i64], _sz)
+_sig("casc_finalize", [])
+_sig("casc_packed_a_bytes", [_i64, _i64], _sz)
+_sig("casc_packed_b_bytes", [_i64, _i64], _sz)
+_sig("casc_packed_a_block_bytes", [_i64], _sz)
+_sig("casc_packed_b_block_bytes", [_i64], _sz)
+_sig("casc_pack_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp])
+_sig("casc_pack_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp])
+_sig("casc_gemm_packed", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp])
+_sig("casc_split_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
+_sig("casc_split_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
+_sig("casc_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp])
+_sig("casc_last_launch_count", [])
+
+EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
+            "casc_gemm_fp64x2_ws", "casc_workspace_bytes", "casc_finalize",
+            "casc_packed_a_bytes", "casc_packed_b_bytes", "casc_packed_a_block_bytes",
+            "casc_packed_b_block_bytes", "casc_pack_a", "casc_pack_b", "casc_gemm_packed",
+            "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count"]
+
+
+class CascError(RuntimeError):
+    def __init__(self, status: int, fn: str):
+        super().__init__(f"{fn}: {_lib.casc_status_string(status).decode()}")
+        self.status = status
+
+
+def _check(status: int, fn: str):
+    if status != 0:
+        raise CascError(status, fn)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _mat(t, name):
+    if t.dtype != torch.float64 or not t.is_cuda or t.dim() != 2:
+        raise TypeError(f"{name} must be a 2-D float64 CUDA tensor")
+    if t.size(1) > 1 and t.stride(1) != 1:
+        raise TypeError(f"{name} must be row-major (unit column stride)")
+    return max(t.stride(0), 1) if t.size(0) > 1 else max(t.size(1), 1)
+
+
+def _ld_pair(hi, lo, name):
+    ldh, ldl = _mat(hi, name + "_hi"), _mat(lo, name + "_lo")
+    if hi.shape != lo.shape or ldh != ldl:
+        raise TypeError(f"{name}_hi and {name}_lo must have the same shape and layout")
+    return ldh
+
+
+def casc_status_string(status: int) -> str:
+    return _lib.casc_status_string(status).decode()
+
+
+def casc_select_widths(k: int):
+    c = (ctypes.c_int * 3)()
+    _check(_lib.casc_select_widths(k, c), "casc_select_widths")
+    return tuple(c)
+
+
+def casc_last_launch_count() -> int:
+    return _lib.casc_last_launch_count()
+
+
+def casc_workspace_bytes(m: int, n: int, k: int) -> int:
+    return _lib.casc_workspace_bytes(m, n, k)
+
+
+def casc_finalize():
+    _check(_lib.casc_finalize(), "casc_finalize")
+
+
+def _outputs(m, n, device, C_hi, C_lo, flags, want_flags):
+    if C_hi is None:
+        C_hi = torch.empty((m, n), dtype=torch.float64, device=device)
+    if C_lo is None:
+        C_lo = torch.empty((m, n), dtype=torch.float64, device=device)
+    if flags is None and want_flags:
+        flags = torch.empty((m, n), dtype=torch.uint8, device=device)
+    if flags is not None and (flags.dtype != torch.uint8 or not flags.is_contiguous()
+                              or tuple(flags.shape) != (m, n)):
+        raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
+    return C_hi, C_lo, flags
+
+
+def casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=None, C_lo=None, flags=None,
+                     want_flags=True, stream=None, workspace=None):
+    """C := A B (cascaded FP64x2).  Returns (C_hi, C_lo, flags).  With
+    `workspace` (uint8 CUDA tensor of casc_workspace_bytes(m, n, k)) this calls
+    casc_gemm_fp64x2_ws, otherwise the library-owned workspace is used."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    k2, n = B_hi.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    C_hi, C_lo, flags = _outputs(m, n, A_hi.device, C_hi, C_lo, flags, want_flags)
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    if workspace is None:
+        st = _lib.casc_gemm_fp64x2(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo),
+                                   ldb, _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags), _stream(stream))
+        _check(st, "casc_gemm_fp64x2")
+    else:
+        st = _lib.casc_gemm_fp64x2_ws(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                      _ptr(B_lo), ldb, _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
+                                      _ptr(workspace), workspace.numel(), _stream(stream))
+        _check(st, "casc_gemm_fp64x2_ws")
+    return C_hi, C_lo, flags
+
+
+def casc_gemm_fp64x2_ws(A_hi, A_lo, B_hi, B_lo, workspace, **kw):
+    return casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, workspace=workspace, **kw)
+
+
+def casc_packed_a_bytes(m: int, k: int) -> int:
+    return _lib.casc_packed_a_bytes(m, k)
+
+
+def casc_packed_b_bytes(k: int, n: int) -> int:
+    return _lib.casc_packed_b_bytes(k, n)
+
+
+def casc_packed_a_block_bytes(k: int) -> int:
+    return _lib.casc_packed_a_block_bytes(k)
+
+
+def casc_packed_b_block_bytes(k: int) -> int:
+    return _lib.casc_packed_b_block_bytes(k)
+
+
+def casc_pack_a(A_hi, A_lo, packed=None, stream=None):
+    """Phase 1 for A into the opaque packed layout (uint8 CUDA tensor)."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    m, k = A_hi.shape
+    if packed is None:
+        packed = torch.empty(casc_packed_a_bytes(m, k), dtype=torch.uint8, device=A_hi.device)
+    _check(_lib.casc_pack_a(m, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(packed), _stream(stream)),
+           "casc_pack_a")
+    return packed
+
+
+def casc_pack_b(B_hi, B_lo, packed=None, stream=None):
+    """Phase 1 for B (7 slices) into the opaque packed layout."""
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    k, n = B_hi.shape
+    if packed is None:
+        packed = torch.empty(casc_packed_b_bytes(k, n), dtype=torch.uint8, device=B_hi.device)
+    _check(_lib.casc_pack_b(k, n, _ptr(B_hi), _ptr(B_lo), ldb, _ptr(packed), _stream(stream)),
+           "casc_pack_b")
+    return packed
+
+
+def casc_gemm_packed(m, n, k, packed_a, packed_b, C_hi=None, C_lo=None, flags=None,
+                     want_flags=True, stream=None):
+    """Phases 2-3 from packed operands.  Returns (C_hi, C_lo, flags)."""
+    dev = packed_a.device if packed_a is not None else torch.device("cuda")
+    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags)
+    ldc = _ld_pair(C_hi, C_lo, "C") if m and n else max(n, 1)
+    _check(_lib.casc_gemm_packed(m, n, k, _ptr(packed_a), _ptr(packed_b), _ptr(C_hi),
+                                 _ptr(C_lo), ldc, _ptr(flags), _stream(stream)),
+           "casc_gemm_packed")
+    return C_hi, C_lo, flags
+
+
+def casc_split_a(A_hi, A_lo, stream=None):
+    """Slices (4, m, k) in the paper's normalisation and exponents (P, m)."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    m, k = A_hi.shape
+    P = (k + KC - 1) // KC
+    S = torch.empty((4, m, k), dtype=torch.float64, device=A_hi.device)
+    e = torch.empty((P, m), dtype=torch.int32, device=A_hi.device)
+    _check(_lib.casc_split_a(m, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(S), _ptr(e),
+                             _stream(stream)), "casc_split_a")
+    return S, e
+
+
+def casc_split_b(B_hi, B_lo, stream=None):
+    """Slices (7, k, n) = B0..B6 in the paper's normalisation and exponents (P, n)."""
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    k, n = B_hi.shape
+    P = (k + KC - 1) // KC
+    S = torch.empty((7, k, n), dtype=torch.float64, device=B_hi.device)
+    f = torch.empty((P, n), dtype=torch.int32, device=B_hi.device)
+    _check(_lib.casc_split_b(k, n, _ptr(B_hi), _ptr(B_lo), ldb, _ptr(S), _ptr(f),
+                             _stream(stream)), "casc_split_b")
+    return S, f
+
+
+def casc_debug_bins(A_hi, A_lo, B_hi, B_lo, panel: int, stream=None):
+    """Bins (4, m, n) of k panel `panel` as computed by the fused kernel."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    bins = torch.empty((4, m, n), dtype=torch.float64, device=A_hi.device)
+    _check(_lib.casc_debug_bins(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo),
+                                ldb, panel, _ptr(bins), _stream(stream)), "casc_debug_bins")
+    return bins

@@ -1,0 +1,388 @@
+// casc_api.cu — host side of the C ABI declared in include/casc.h:
+// argument validation, widths, workspace, kernel launches.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+
+#include "../../include/casc.h"
+#include "casc_layout.cuh"
+
+namespace casc {
+cudaError_t launch_split_a(const double*, const double*, int64_t, int64_t, int64_t, Widths, void*,
+                           cudaStream_t);
+cudaError_t launch_split_b(const double*, const double*, int64_t, int64_t, int64_t, Widths, void*,
+                           cudaStream_t);
+cudaError_t launch_unpack_a(const void*, int64_t, int64_t, Widths, double*, int32_t*,
+                            cudaStream_t);
+cudaError_t launch_unpack_b(const void*, int64_t, int64_t, Widths, double*, int32_t*,
+                            cudaStream_t);
+}  // namespace casc
+
+namespace {
+
+thread_local int g_launches = 0;
+
+inline cudaStream_t S(casc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// §3.3 P:L916-945 with L = ceil(log2 min(k, 256)) (reading R3).
+casc::Widths widths_for(int64_t k) {
+  int64_t keff = k < casc::KC ? k : casc::KC;
+  if (keff < 1) keff = 1;
+  int L = 0;
+  while ((int64_t(1) << L) < keff) ++L;
+  casc::Widths w{0, 0, 0};
+  while (2 * (w.c0 + 1) + L <= 53) ++w.c0;
+  while (w.c0 + (w.c1 + 1) + L + 1 <= 53 && 2 * (w.c1 + 1) + L + 2 <= 53) ++w.c1;
+  while (w.c0 + (w.c2 + 1) + L + 2 <= 53) ++w.c2;
+  return w;
+}
+
+struct DevInfo {
+  int checked = 0;
+  int ok = 0;
+  int sms = 0;
+};
+
+int device_check(int* sms) {
+  static DevInfo info[64];
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(mu);
+  DevInfo& d = info[dev];
+  if (!d.checked) {
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return CASC_ERR_CUDA;
+    d.ok = (major == 10 && minor == 0);
+    d.checked = 1;
+  }
+  if (sms) *sms = d.sms;
+  return d.ok ? CASC_OK : CASC_ERR_UNSUPPORTED;
+}
+
+inline bool ranges_overlap(const void* a, size_t an, const void* b, size_t bn) {
+  if (!a || !b || an == 0 || bn == 0) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+  return a0 < b0 + bn && b0 < a0 + an;
+}
+inline size_t extent(int64_t rows, int64_t cols, int64_t ld) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return size_t((rows - 1) * ld + cols) * sizeof(double);
+}
+
+int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
+  if (rows < 0 || cols < 0) return CASC_ERR_INVALID;
+  if (ld < (cols > 1 ? cols : 1)) return CASC_ERR_INVALID;
+  if (rows > 0 && cols > 0 && !p) return CASC_ERR_INVALID;
+  return CASC_OK;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
+
+int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb,
+                     double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
+                     cudaStream_t st, int st_begin, int st_end, double* dbg) {
+  const casc::Widths w = widths_for(k);
+  casc::GemmArgs a{};
+  a.pa = static_cast<const uint8_t*>(pa);
+  a.pb = static_cast<const uint8_t*>(pb);
+  a.a_blk = casc::a_block_bytes(k);
+  a.b_blk = casc::b_block_bytes(k);
+  a.a_exp = casc::a_exp_offset(k);
+  a.b_exp = casc::b_exp_offset(k);
+  a.m = m;
+  a.n = n;
+  a.mblocks = (int)((m + casc::TM - 1) / casc::TM);
+  a.nblocks = (int)((n + casc::TN - 1) / casc::TN);
+  a.st_begin = st_begin;
+  a.st_end = st_end;
+  a.c0 = w.c0;
+  a.D2 = w.c0 + w.c1 + w.c2;
+  a.C_hi = C_hi;
+  a.C_lo = C_lo;
+  a.ldc = ldc;
+  a.flags = flags;
+  a.dbg = dbg;
+  a.un_b2 = std::ldexp(1.0, w.c1 - w.c0);
+  cudaError_t e = casc::launch_gemm(a, sms, st);
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e);
+}
+
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+Workspace g_ws[64];
+std::mutex g_ws_mu;
+
+}  // namespace
+
+extern "C" {
+
+const char* casc_status_string(int status) {
+  switch (status) {
+    case CASC_OK: return "CASC_OK";
+    case CASC_ERR_INVALID: return "CASC_ERR_INVALID: invalid argument";
+    case CASC_ERR_CUDA: return "CASC_ERR_CUDA: CUDA runtime/launch/allocation error";
+    case CASC_ERR_UNSUPPORTED: return "CASC_ERR_UNSUPPORTED: device is not sm_100 (B200)";
+    default: return "CASC_ERR_UNKNOWN";
+  }
+}
+
+int casc_select_widths(int64_t k, int* c) {
+  if (!c || k < 0) return CASC_ERR_INVALID;
+  const casc::Widths w = widths_for(k);
+  c[0] = w.c0;
+  c[1] = w.c1;
+  c[2] = w.c2;
+  return CASC_OK;
+}
+
+size_t casc_packed_a_block_bytes(int64_t k) { return k > 0 ? (size_t)casc::a_block_bytes(k) : 0; }
+size_t casc_packed_b_block_bytes(int64_t k) { return k > 0 ? (size_t)casc::b_block_bytes(k) : 0; }
+size_t casc_packed_a_bytes(int64_t m, int64_t k) {
+  if (m <= 0 || k <= 0) return 0;
+  return (size_t)((m + casc::TM - 1) / casc::TM) * casc_packed_a_block_bytes(k);
+}
+size_t casc_packed_b_bytes(int64_t k, int64_t n) {
+  if (n <= 0 || k <= 0) return 0;
+  return (size_t)((n + casc::TN - 1) / casc::TN) * casc_packed_b_block_bytes(k);
+}
+size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k) {
+  const size_t a = (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
+  return a + casc_packed_b_bytes(k, n);
+}
+
+int casc_last_launch_count(void) { return g_launches; }
+
+int casc_pack_a(int64_t m, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
+                void* packed_a, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if ((r = check_mat(A_hi, m, k, lda)) || (r = check_mat(A_lo, m, k, lda))) return r;
+  if (m > 0 && k > 0 && !packed_a) return CASC_ERR_INVALID;
+  if ((r = device_check(nullptr))) return r;
+  if (m == 0 || k == 0) return CASC_OK;
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, widths_for(k), packed_a, S(stream));
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e);
+}
+
+int casc_pack_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, int64_t ldb,
+                void* packed_b, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if ((r = check_mat(B_hi, k, n, ldb)) || (r = check_mat(B_lo, k, n, ldb))) return r;
+  if (n > 0 && k > 0 && !packed_b) return CASC_ERR_INVALID;
+  if ((r = device_check(nullptr))) return r;
+  if (n == 0 || k == 0) return CASC_OK;
+  cudaError_t e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, widths_for(k), packed_b, S(stream));
+  if (e == cudaSuccess) ++g_launches;
+  return cuda_status(e);
+}
+
+static int zero_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                  cudaStream_t st) {
+  cudaError_t e = cudaMemset2DAsync(C_hi, ldc * sizeof(double), 0, n * sizeof(double), m, st);
+  if (e == cudaSuccess)
+    e = cudaMemset2DAsync(C_lo, ldc * sizeof(double), 0, n * sizeof(double), m, st);
+  if (e == cudaSuccess && flags) e = cudaMemsetAsync(flags, 0, (size_t)(m * n), st);
+  return cuda_status(e);
+}
+
+int casc_gemm_packed(int64_t m, int64_t n, int64_t k, const void* packed_a, const void* packed_b,
+                     double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                     casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  if ((r = check_mat(C_hi, m, n, ldc)) || (r = check_mat(C_lo, m, n, ldc))) return r;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  if (k == 0) return zero_c(m, n, C_hi, C_lo, ldc, flags, S(stream));
+  if (!packed_a || !packed_b) return CASC_ERR_INVALID;
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  return gemm_packed_impl(m, n, k, packed_a, packed_b, C_hi, C_lo, ldc, flags, sms, S(stream), 0,
+                          nst, nullptr);
+}
+
+static int validate_gemm(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                         int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                         double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags) {
+  int r;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  if ((r = check_mat(A_hi, m, k, lda)) || (r = check_mat(A_lo, m, k, lda))) return r;
+  if ((r = check_mat(B_hi, k, n, ldb)) || (r = check_mat(B_lo, k, n, ldb))) return r;
+  if ((r = check_mat(C_hi, m, n, ldc)) || (r = check_mat(C_lo, m, n, ldc))) return r;
+  const size_t ca = extent(m, k, lda), cb = extent(k, n, ldb), cc = extent(m, n, ldc);
+  const void* ins[4] = {A_hi, A_lo, B_hi, B_lo};
+  const size_t ine[4] = {ca, ca, cb, cb};
+  void* outs[3] = {C_hi, C_lo, flags};
+  const size_t oute[3] = {cc, cc, flags ? (size_t)(m * n) : 0};
+  for (int o = 0; o < 3; ++o) {
+    for (int i = 0; i < 4; ++i)
+      if (ranges_overlap(outs[o], oute[o], ins[i], ine[i])) return CASC_ERR_INVALID;
+    for (int o2 = o + 1; o2 < 3; ++o2)
+      if (ranges_overlap(outs[o], oute[o], outs[o2], oute[o2])) return CASC_ERR_INVALID;
+  }
+  return CASC_OK;
+}
+
+int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                        int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                        double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, void* workspace,
+                        size_t workspace_bytes, casc_stream_t stream) {
+  int r = validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  if (k == 0) return zero_c(m, n, C_hi, C_lo, ldc, flags, S(stream));
+  const size_t need = casc_workspace_bytes(m, n, k);
+  if (!workspace || workspace_bytes < need) return CASC_ERR_INVALID;
+  uint8_t* pa = static_cast<uint8_t*>(workspace);
+  uint8_t* pb = pa + (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
+  const casc::Widths w = widths_for(k);
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, S(stream));
+  if (e != cudaSuccess) return CASC_ERR_CUDA;
+  e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, S(stream));
+  if (e != cudaSuccess) return CASC_ERR_CUDA;
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr);
+  g_launches = (r == CASC_OK) ? 3 : 0;
+  return r;
+}
+
+int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                     int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                     double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                     casc_stream_t stream) {
+  int r = validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (m == 0 || n == 0 || k == 0)
+    return casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
+                               nullptr, 0, stream);
+  if ((r = device_check(nullptr))) return r;
+  const size_t need = casc_workspace_bytes(m, n, k);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  void* ws = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& W = g_ws[dev];
+    if (W.bytes < need) {
+      if (W.ptr) {
+        cudaDeviceSynchronize();
+        cudaFree(W.ptr);
+        W.ptr = nullptr;
+        W.bytes = 0;
+      }
+      if (cudaMalloc(&W.ptr, need) != cudaSuccess) {
+        W.ptr = nullptr;
+        return CASC_ERR_CUDA;
+      }
+      W.bytes = need;
+    }
+    ws = W.ptr;
+  }
+  return casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
+                             ws, need, stream);
+}
+
+int casc_finalize(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& W = g_ws[dev];
+  if (W.ptr) {
+    cudaDeviceSynchronize();
+    cudaFree(W.ptr);
+  }
+  W.ptr = nullptr;
+  W.bytes = 0;
+  return CASC_OK;
+}
+
+int casc_split_a(int64_t m, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
+                 double* slices, int32_t* e, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if ((r = check_mat(A_hi, m, k, lda)) || (r = check_mat(A_lo, m, k, lda))) return r;
+  if (m > 0 && k > 0 && (!slices || !e)) return CASC_ERR_INVALID;
+  if ((r = device_check(nullptr))) return r;
+  if (m == 0 || k == 0) return CASC_OK;
+  void* tmp = nullptr;
+  cudaStream_t st = S(stream);
+  if (cudaMallocAsync(&tmp, casc_packed_a_bytes(m, k), st) != cudaSuccess) return CASC_ERR_CUDA;
+  const casc::Widths w = widths_for(k);
+  cudaError_t err = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, tmp, st);
+  if (err == cudaSuccess) err = casc::launch_unpack_a(tmp, m, k, w, slices, e, st);
+  cudaFreeAsync(tmp, st);
+  if (err == cudaSuccess) g_launches = 2;
+  return cuda_status(err);
+}
+
+int casc_split_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, int64_t ldb,
+                 double* slices, int32_t* f, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if ((r = check_mat(B_hi, k, n, ldb)) || (r = check_mat(B_lo, k, n, ldb))) return r;
+  if (n > 0 && k > 0 && (!slices || !f)) return CASC_ERR_INVALID;
+  if ((r = device_check(nullptr))) return r;
+  if (n == 0 || k == 0) return CASC_OK;
+  void* tmp = nullptr;
+  cudaStream_t st = S(stream);
+  if (cudaMallocAsync(&tmp, casc_packed_b_bytes(k, n), st) != cudaSuccess) return CASC_ERR_CUDA;
+  const casc::Widths w = widths_for(k);
+  cudaError_t err = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, tmp, st);
+  if (err == cudaSuccess) err = casc::launch_unpack_b(tmp, k, n, w, slices, f, st);
+  cudaFreeAsync(tmp, st);
+  if (err == cudaSuccess) g_launches = 2;
+  return cuda_status(err);
+}
+
+int casc_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                    int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                    int64_t panel, double* bins, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  if ((r = check_mat(A_hi, m, k, lda)) || (r = check_mat(A_lo, m, k, lda))) return r;
+  if ((r = check_mat(B_hi, k, n, ldb)) || (r = check_mat(B_lo, k, n, ldb))) return r;
+  if (panel < 0 || panel >= casc::panels_of(k)) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  if (!bins) return CASC_ERR_INVALID;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  cudaStream_t st = S(stream);
+  void* pa = nullptr;
+  void* pb = nullptr;
+  if (cudaMallocAsync(&pa, casc_packed_a_bytes(m, k), st) != cudaSuccess) return CASC_ERR_CUDA;
+  if (cudaMallocAsync(&pb, casc_packed_b_bytes(k, n), st) != cudaSuccess) {
+    cudaFreeAsync(pa, st);
+    return CASC_ERR_CUDA;
+  }
+  const casc::Widths w = widths_for(k);
+  cudaError_t err = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, st);
+  if (err == cudaSuccess) err = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, st);
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  const int s0 = (int)panel * casc::STAGES_PER_PANEL;
+  const int s1 = s0 + casc::STAGES_PER_PANEL < nst ? s0 + casc::STAGES_PER_PANEL : nst;
+  if (err == cudaSuccess)
+    r = gemm_packed_impl(m, n, k, pa, pb, nullptr, nullptr, n, nullptr, sms, st, s0, s1, bins);
+  else
+    r = CASC_ERR_CUDA;
+  cudaFreeAsync(pa, st);
+  cudaFreeAsync(pb, st);
+  if (r == CASC_OK) g_launches = 3;
+  return r;
+}
+
+}  // extern "C"

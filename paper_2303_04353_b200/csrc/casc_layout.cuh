@@ -1,0 +1,85 @@
+// casc_layout.cuh — packed slice layout, tile shape and device helpers shared
+// by the split kernels and the fused cascaded-GEMM kernel (product path only;
+// nothing here is shared with oracle/).
+//
+// Packed layout.  The GEMM's CTA tile is 64 x 64 output elements
+// computed by 8 MMA warps arranged 2 (m) x 4 (n), each warp a 32 x 16 sub-tile
+// built from mma.sync.m8n8k4.f64 fragments (4 m-subtiles x 2 n-subtiles).
+// The split kernels write every slice directly in FRAGMENT ORDER, so that:
+//   * one pipeline stage (8 values of k) of a 64-row A block (4 slices) or a
+//     64-column B block (7 slices) is ONE contiguous chunk -> one TMA bulk copy;
+//   * inside shared memory each warp's fragment load for one (slice, subtile,
+//     k4-step) is 32 consecutive doubles -> conflict-free 256-byte loads.
+//
+// A block (64 rows), per k4-step (4 values of k), 1024 doubles:
+//   [slice s 0..3][mwarp 0..1][msub 0..3][lane 0..31]
+//   element (row r in block, k) with g = r%8, ms = (r%32)/8, mw = r/32,
+//   ks = k/4, c = k%4, lane = 4g + c (mma A fragment a0 = A[g][c]).
+// B block (64 columns), per k4-step, 1792 doubles:
+//   [slice s 0..6][nwarp 0..3][nsub 0..1][lane 0..31]
+//   element (k, col j in block) with g = j%8, ns = (j%16)/8, nw = j/16,
+//   lane = 4g + c (mma B fragment b0 = B[c][g]).
+// After the kpad/4 k4-steps of slices (kpad = k rounded up to 8), each block
+// holds its exponents: int32 [panel 0..P-1][64].
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace casc {
+
+constexpr int KC = 256;          // k_C panel depth
+constexpr int TM = 64;           // CTA tile rows
+constexpr int TN = 64;           // CTA tile cols
+constexpr int BK = 8;            // k per pipeline stage
+constexpr int STAGES_PER_PANEL = KC / BK;
+constexpr int A_SLICES = 4;
+constexpr int B_SLICES = 7;
+constexpr int A_KSTEP = A_SLICES * TM * 4;   // doubles per k4-step of an A block (1024)
+constexpr int B_KSTEP = B_SLICES * TN * 4;   // doubles per k4-step of a B block (1792)
+constexpr int A_STAGE = A_KSTEP * (BK / 4);  // doubles per stage (2048 = 16 KB)
+constexpr int B_STAGE = B_KSTEP * (BK / 4);  // doubles per stage (3584 = 28 KB)
+
+__host__ __device__ inline int64_t kpad_of(int64_t k) { return (k + BK - 1) / BK * BK; }
+__host__ __device__ inline int64_t panels_of(int64_t k) { return (k + KC - 1) / KC; }
+__host__ __device__ inline int64_t a_block_bytes(int64_t k) {
+  return kpad_of(k) / 4 * A_KSTEP * 8 + panels_of(k) * TM * 4;
+}
+__host__ __device__ inline int64_t b_block_bytes(int64_t k) {
+  return kpad_of(k) / 4 * B_KSTEP * 8 + panels_of(k) * TN * 4;
+}
+__host__ __device__ inline int64_t a_exp_offset(int64_t k) { return kpad_of(k) / 4 * A_KSTEP * 8; }
+__host__ __device__ inline int64_t b_exp_offset(int64_t k) { return kpad_of(k) / 4 * B_KSTEP * 8; }
+
+// Split widths and the derived constants used by the kernels.
+struct Widths {
+  int c0, c1, c2;
+};
+
+// ---------------------------------------------------------------- device math
+// Every rounding operation is an explicit _rn intrinsic (never contracted into
+// an FMA, never reassociated), so the split and combine are bit-reproducible.
+__device__ __forceinline__ double pow2i(int n) {  // 2^n for n in [-1022, 1023], exact
+  return __longlong_as_double((long long)(n + 1023) << 52);
+}
+
+// Arguments of the fused cascaded-GEMM kernel (casc_gemm.cu).
+struct GemmArgs {
+  const uint8_t* pa;
+  const uint8_t* pb;
+  int64_t a_blk, b_blk;  // bytes per packed block
+  int64_t a_exp, b_exp;  // byte offset of the exponents inside a block
+  int64_t m, n;
+  int mblocks, nblocks;
+  int st_begin, st_end;  // stage range [begin, end) (a single panel in debug mode)
+  int c0, D2;
+  double* C_hi;
+  double* C_lo;
+  int64_t ldc;
+  uint8_t* flags;  // m x n (ld n) or null
+  double* dbg;     // debug: bins of the single panel, 4 x m x n (canonical scales)
+  double un_b2;    // 2^(c1-c0): bin2' -> bin2 for the debug export
+};
+
+cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st);
+
+}  // namespace casc

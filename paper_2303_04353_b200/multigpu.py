@@ -1,0 +1,106 @@
+"""Multi-GPU layer: C row-block sharded over ranks, B's packed slices exchanged
+once over NVLink (BASELINE north star: "partitions C into row/column blocks
+across the 8xB200 box, with B (or A) slices broadcast over NVLink through
+NCCL").
+
+One process per GPU (torch.distributed, NCCL).  Rank r of W:
+  1. packs its rows [r0, r1) of A (casc_pack_a; per-row scales are row-local);
+  2. packs its column slab of B (casc_pack_b; per-column scales are
+     column-local, so the slab's packed bytes are bit-identical to the same
+     blocks of a single-GPU pack);
+  3. all-gathers the packed B slabs (one ncclAllGather of equal-size chunks;
+     the packed layout is 64-column-block major, so the gathered buffer IS
+     the packed B of the whole matrix);
+  4. runs the fused cascaded GEMM on its rows (casc_gemm_packed).
+k is never split, so there is no reduction and every element is computed by
+exactly the same arithmetic as on one GPU: C is bitwise independent of W
+(P-invariance).
+
+`ops` makes the kernels injectable so the host-side plumbing (sharding,
+padding, gather order) is testable on CPU with the gloo backend.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+BLOCK = 64  # packed column-block width (casc_layout.cuh TN)
+
+
+def row_shard(m: int, world: int, rank: int):
+    """Rows [r0, r1) of A and C owned by `rank` (balanced, contiguous)."""
+    return (rank * m) // world, ((rank + 1) * m) // world
+
+
+def col_slab(n: int, world: int, rank: int):
+    """Columns [c0, c1) of B packed by `rank`: equal 64-multiple slabs so every
+    rank contributes the same number of packed blocks to the all-gather."""
+    nb = -(-n // BLOCK)
+    per = -(-nb // world)
+    c0 = min(n, rank * per * BLOCK)
+    c1 = min(n, (rank + 1) * per * BLOCK)
+    return c0, c1, per
+
+
+@dataclass
+class Ops:
+    pack_a: object
+    pack_b: object
+    gemm_packed: object
+    packed_b_block_bytes: object
+
+
+def cuda_ops() -> Ops:
+    import paper_2303_04353_b200 as casc
+    return Ops(pack_a=casc.casc_pack_a, pack_b=casc.casc_pack_b,
+               gemm_packed=casc.casc_gemm_packed,
+               packed_b_block_bytes=casc.casc_packed_b_block_bytes)
+
+
+class ShardedCascGemm:
+    """Row-sharded cascaded FP64x2 GEMM for one (m, n, k) problem.  Buffers are
+    allocated once and reused across calls (bench steps)."""
+
+    def __init__(self, m: int, n: int, k: int, group=None, ops: Ops | None = None,
+                 device=None):
+        self.m, self.n, self.k = m, n, k
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.ops = ops or cuda_ops()
+        self.device = device if device is not None else torch.device("cuda")
+        self.r0, self.r1 = row_shard(m, self.world, self.rank)
+        self.c0, self.c1, self.blocks_per_rank = col_slab(n, self.world, self.rank)
+        blk = self.ops.packed_b_block_bytes(k)
+        self.chunk = self.blocks_per_rank * blk
+        self.packed_b_local = torch.zeros(self.chunk, dtype=torch.uint8, device=self.device)
+        self.packed_b_full = torch.empty(self.chunk * self.world, dtype=torch.uint8,
+                                         device=self.device)
+        self.packed_a = None
+
+    def __call__(self, A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi=None, C_lo=None,
+                 flags=None, events=None):
+        """A_*_rows: this rank's rows (r1-r0) x k.  B_*_slab: k x (c1-c0).
+        Returns this rank's (C_hi, C_lo, flags) rows.  `events`, if given, is a
+        list of 4 CUDA events recorded after pack_a, pack_b, all-gather, gemm."""
+        mloc = self.r1 - self.r0
+        self.packed_a = self.ops.pack_a(A_hi_rows, A_lo_rows, packed=self.packed_a)
+        rec = (lambda i: events[i].record()) if events else (lambda i: None)
+        rec(0)
+        if self.c1 > self.c0:
+            used = -(-(self.c1 - self.c0) // BLOCK) * self.ops.packed_b_block_bytes(self.k)
+            self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])
+        rec(1)
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.packed_b_full, self.packed_b_local, group=self.group)
+            pb = self.packed_b_full
+        else:
+            pb = self.packed_b_local
+        rec(2)
+        out = self.ops.gemm_packed(mloc, self.n, self.k, self.packed_a, pb, C_hi=C_hi,
+                                   C_lo=C_lo, flags=flags)
+        rec(3)
+        return out

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE north star):
+  * split slices and scale exponents: bit-exact (values, +-0 equal);
+  * bins 0-2 of every panel: bit-exact (they are exact);
+  * bin 3-6: within gamma_{4k+1} sum|terms| of its exact value (order differs,
+    DESIGN.md reading R17);
+  * epilogue: C equals the oracle's combine applied to the GPU's own bins,
+    bit for bit (same DD algorithm, reading R9);
+  * final C: |C_gpu - C*| <= 4 k 2^-104 (|A||B|)_ij for every checked entry;
+  * flags identical to the oracle's.
+"""
+
+import numpy as np
+import pytest
+
+import casc_inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def casc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2303_04353_b200 as casc
+    return casc
+
+
+def T(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+def run(casc, d, **kw):
+    return [N(x) if x is not None else None
+            for x in casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                           T(d["B_lo"]), **kw)]
+
+
+def same_values(x, y):
+    return bool(np.all((x == y) | (np.isnan(x) & np.isnan(y))))
+
+
+SHAPES = [(0, 64, 64, 64), (1, 77, 70, 600), (2, 96, 130, 513), (1, 1, 1, 1), (1, 3, 5, 9),
+          (1, 65, 129, 257), (1, 128, 64, 256)]
+
+
+# ------------------------------------------------------------------ split a2-a4
+@pytest.mark.parametrize("cfg,m,n,k", SHAPES)
+def test_split_bit_exact(casc, orc, cfg, m, n, k):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    SA, e = casc.casc_split_a(T(d["A_hi"]), T(d["A_lo"]))
+    SB, f = casc.casc_split_b(T(d["B_hi"]), T(d["B_lo"]))
+    SA, e, SB, f = N(SA), N(e), N(SB), N(f)
+    c = orc.select_widths(k)
+    assert casc.casc_select_widths(k) == c
+    for q, p0 in enumerate(range(0, k, 256)):
+        p1 = min(k, p0 + 256)
+        oa, oe = orc.split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], c)
+        ob, of = orc.split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], c)
+        assert np.array_equal(e[q], oe) and np.array_equal(f[q], of)
+        assert same_values(SA[:, :, p0:p1], oa)
+        assert same_values(SB[:, p0:p1, :], ob)
+
+
+def test_split_full_mantissa(casc, orc):
+    """Leading zeros / slice-3 rounding (full-mantissa set)."""
+    hi, lo = I.full_mantissa(3, 40, 520)
+    SA, e = casc.casc_split_a(T(hi), T(lo))
+    SB, f = casc.casc_split_b(T(hi.T.copy()), T(lo.T.copy()))
+    SA, e, SB, f = N(SA), N(e), N(SB), N(f)
+    c = orc.select_widths(520)
+    for q, p0 in enumerate(range(0, 520, 256)):
+        p1 = min(520, p0 + 256)
+        oa, oe = orc.split_a_panel(hi[:, p0:p1], lo[:, p0:p1], c)
+        assert np.array_equal(e[q], oe) and same_values(SA[:, :, p0:p1], oa)
+        ob, of = orc.split_b_panel(hi.T[p0:p1].copy(), lo.T[p0:p1].copy(), c)
+        assert np.array_equal(f[q], of) and same_values(SB[:, p0:p1, :], ob)
+
+
+# ------------------------------------------------------------------ bins a5
+@pytest.mark.parametrize("cfg,m,n,k", SHAPES[:6])
+def test_bins_bit_exact_and_bin36_bound(casc, orc, cfg, m, n, k):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    c = orc.select_widths(k)
+    f36 = 2.0 ** (c[2] - c[0])
+    u = 2.0**-53
+    for q, p0 in enumerate(range(0, k, 256)):
+        p1 = min(k, p0 + 256)
+        kp = p1 - p0
+        gb = N(casc.casc_debug_bins(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]), q))
+        oa, _ = orc.split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], c)
+        ob, _ = orc.split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], c)
+        obins = orc.panel_bins(oa, ob, c)
+        for b in range(3):
+            assert same_values(gb[b], obins[b]), f"bin {b} panel {q}"
+        # bin 3-6: gamma bound around the exact value of the same terms
+        x = np.concatenate([oa[0], f36 * oa[1], f36 * oa[2], oa[3]], axis=1)  # m x 4kp
+        y = np.concatenate([ob[3], ob[4], ob[5], ob[6]], axis=0)              # 4kp x n
+        absterms = np.abs(x) @ np.abs(y)
+        gamma = (4 * kp + 1) * u / (1 - (4 * kp + 1) * u)
+        for i in range(0, m, max(1, m // 9)):
+            for j in range(0, n, max(1, n // 7)):
+                eh, el = orc.exact_dot(x[i], y[:, j])
+                err = abs((gb[3, i, j] - eh) - el)
+                assert err <= gamma * absterms[i, j] * (1 + 1e-12) + 1e-300
+                assert abs(gb[3, i, j] - obins[3, i, j]) <= 2 * gamma * absterms[i, j] * (1 + 1e-12)
+
+
+# ------------------------------------------------------------------ combine a6
+@pytest.mark.parametrize("cfg,m,n,k", [(0, 64, 64, 64), (1, 33, 40, 700), (2, 70, 66, 300)])
+def test_epilogue_bitwise_on_gpu_bins(casc, orc, cfg, m, n, k):
+    """C_gpu == oracle combine + FP64x2 panel accumulation of the GPU's own bins."""
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    c = orc.select_widths(k)
+    C_hi, C_lo, flags = run(casc, d)
+    ref_hi = np.zeros((m, n))
+    ref_lo = np.zeros((m, n))
+    ref_fl = np.zeros((m, n), dtype=np.uint8)
+    for q, p0 in enumerate(range(0, k, 256)):
+        p1 = min(k, p0 + 256)
+        gb = N(casc.casc_debug_bins(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]), q))
+        _, e = orc.split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], c)
+        _, f = orc.split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], c)
+        for i in range(m):
+            for j in range(n):
+                th, tl = orc.combine(gb[0, i, j], gb[1, i, j], gb[2, i, j], gb[3, i, j],
+                                     int(e[i]) + int(f[j]), c)
+                ref_hi[i, j], ref_lo[i, j] = orc.dd_add(ref_hi[i, j], ref_lo[i, j], th, tl)
+                ref_fl[i, j] |= gb[0, i, j] == 0.0
+    assert same_values(C_hi, ref_hi) and same_values(C_lo, ref_lo)
+    assert np.array_equal(flags, ref_fl)
+
+
+# ------------------------------------------------------------------ final C
+def _exact_check(orc, d, C_hi, C_lo, ii, jj):
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii, jj, C_hi, C_lo)
+    bound = orc.north_star_bound(d["k"], r["absab"])
+    return np.max(np.abs(r["err"]) / np.maximum(bound, 1e-300))
+
+
+@pytest.mark.parametrize("cfg,m,n,k", SHAPES)
+def test_final_c_within_bound_and_flags(casc, orc, cfg, m, n, k):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    C_hi, C_lo, flags = run(casc, d)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    assert _exact_check(orc, d, C_hi, C_lo, ii.ravel(), jj.ravel()) <= 1.0
+    o_hi, o_lo, o_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    assert np.array_equal(flags, o_fl)
+    # both within the bound of C*, hence within twice the bound of each other
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel())
+    diff = np.abs((C_hi - o_hi) + (C_lo - o_lo)).ravel()
+    assert np.all(diff <= 2 * orc.north_star_bound(k, r["absab"]))
+
+
+def test_cfg1_full_size_sampled(casc, orc):
+    """cfg1 (1024^3) at full size: sampled exact entries, plus whole-row oracle
+    parity of flags and C for a few rows."""
+    d = I.make_config(1)
+    C_hi, C_lo, flags = run(casc, d)
+    rng = np.random.default_rng(0)
+    ii = rng.integers(0, 1024, 3000)
+    jj = rng.integers(0, 1024, 3000)
+    assert _exact_check(orc, d, C_hi, C_lo, ii, jj) <= 1.0
+    rows = [0, 511, 1023]
+    sub = dict(d, A_hi=d["A_hi"][rows], A_lo=d["A_lo"][rows], m=3)
+    o_hi, o_lo, o_fl = orc.casc_gemm(sub["A_hi"], sub["A_lo"], d["B_hi"], d["B_lo"])
+    assert np.array_equal(flags[rows], o_fl) and flags.sum() == 0
+
+
+def test_cancellation_configs(casc, orc):
+    """cfg3 structure (reading R13) at 256 x 256 x 4096: 3a and 3c raise no flags
+    and stay within the bound; 3b flags every entry; flags == oracle's."""
+    for variant in ("a", "b", "c"):
+        d = I.make_config(3, m=256, n=256, k=4096, variant=variant)
+        C_hi, C_lo, flags = run(casc, d)
+        rows = [0, 100, 255]
+        o_hi, o_lo, o_fl = orc.casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"], d["B_lo"])
+        assert np.array_equal(flags[rows], o_fl)
+        if variant == "b":
+            assert flags.all()
+        else:
+            assert flags.sum() == 0
+            rng = np.random.default_rng(1)
+            ii, jj = rng.integers(0, 256, 400), rng.integers(0, 256, 400)
+            assert _exact_check(orc, d, C_hi, C_lo, ii, jj) <= 1.0
+
+
+def test_worst_case_flagged(casc):
+    """§3.6 worst case through the GPU: bin 0 == 0 -> flagged."""
+    import torch
+    A_hi = torch.tensor([[1.0, 2.0**-100]], dtype=torch.float64).cuda()
+    A_lo = torch.zeros_like(A_hi)
+    B_hi = torch.tensor([[0.0], [1.0]], dtype=torch.float64).cuda()
+    B_lo = torch.zeros_like(B_hi)
+    C_hi, C_lo, fl = casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo)
+    assert fl.item() == 1 and C_hi.item() == 2.0**-100 and C_lo.item() == 0.0
+
+
+def test_edge_cases(casc):
+    import torch
+    z = lambda *s: torch.zeros(s, dtype=torch.float64, device="cuda")
+    # m == 0 / n == 0: no-op
+    C = casc.casc_gemm_fp64x2(z(0, 5), z(0, 5), z(5, 3), z(5, 3))
+    assert C[0].shape == (0, 3)
+    # k == 0: C := 0, flags := 0 (reading R18)
+    C_hi = torch.full((4, 3), 7.0, dtype=torch.float64, device="cuda")
+    C_lo = torch.full((4, 3), 7.0, dtype=torch.float64, device="cuda")
+    fl = torch.full((4, 3), 9, dtype=torch.uint8, device="cuda")
+    casc.casc_gemm_fp64x2(z(4, 0), z(4, 0), z(0, 3), z(0, 3), C_hi=C_hi, C_lo=C_lo, flags=fl)
+    assert C_hi.abs().sum().item() == 0 and C_lo.abs().sum().item() == 0 and fl.sum().item() == 0
+    # zero rows of A -> zero C rows, flagged
+    d = I.make_config(1, m=20, n=20, k=300, seed=4)
+    d["A_hi"][5] = 0.0
+    d["A_lo"][5] = 0.0
+    C_hi, C_lo, flags = run(casc, d)
+    assert np.all(C_hi[5] == 0) and np.all(C_lo[5] == 0) and np.all(flags[5] == 1)
+    assert flags.sum() == 20
+    # aliasing C with A is rejected
+    A = torch.rand(8, 8, dtype=torch.float64, device="cuda")
+    with pytest.raises(casc.CascError):
+        casc.casc_gemm_fp64x2(A, A, A, A, C_hi=A, C_lo=z(8, 8))
+
+
+def test_strided_inputs_and_outputs(casc, orc):
+    """Leading dimensions > width on A, B and C."""
+    import torch
+    d = I.make_config(1, m=40, n=36, k=300, seed=6)
+    big = lambda a, extra: torch.from_numpy(np.pad(a, ((0, 0), (0, extra)))).cuda()
+    A_hi, A_lo = big(d["A_hi"], 5)[:, :300], big(d["A_lo"], 5)[:, :300]
+    B_hi, B_lo = big(d["B_hi"], 3)[:, :36], big(d["B_lo"], 3)[:, :36]
+    Cb_hi = torch.zeros((40, 41), dtype=torch.float64, device="cuda")
+    Cb_lo = torch.zeros((40, 41), dtype=torch.float64, device="cuda")
+    casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=Cb_hi[:, :36], C_lo=Cb_lo[:, :36])
+    ref = run(casc, d)
+    assert same_values(N(Cb_hi)[:, :36], ref[0]) and same_values(N(Cb_lo)[:, :36], ref[1])
+    assert np.all(N(Cb_hi)[:, 36:] == 0)
+
+
+def test_determinism_and_scaling_neutrality(casc):
+    d = I.make_config(1, m=200, n=190, k=777, seed=3)
+    s = I.make_config(2, m=200, n=190, k=777, seed=3)
+    r1 = run(casc, d)
+    r2 = run(casc, d)
+    assert all(np.array_equal(a, b) for a, b in zip(r1, r2))
+    rs = run(casc, s)
+    u = I.int_uniform(3, I.STREAM_ROW_EXP, 200, -30, 30)
+    v = I.int_uniform(3, I.STREAM_COL_EXP, 190, -30, 30)
+    sc = np.ldexp(1.0, u[:, None] + v[None, :])
+    assert np.array_equal(r1[0] * sc, rs[0]) and np.array_equal(r1[1] * sc, rs[1])
+    assert np.array_equal(r1[2], rs[2])
+
+
+def test_workspace_and_packed_paths_agree(casc):
+    import torch
+    d = I.make_config(1, m=130, n=200, k=515, seed=8)
+    A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+    r0 = casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo)
+    ws = torch.empty(casc.casc_workspace_bytes(130, 200, 515), dtype=torch.uint8, device="cuda")
+    r1 = casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, workspace=ws)
+    pa = casc.casc_pack_a(A_hi, A_lo)
+    pb = casc.casc_pack_b(B_hi, B_lo)
+    r2 = casc.casc_gemm_packed(130, 200, 515, pa, pb)
+    for x, y in ((r0, r1), (r0, r2)):
+        assert all(torch.equal(a, b) for a, b in zip(x, y))
+
+
+def test_column_slab_packing_is_blockwise(casc):
+    """Packing a 64-multiple column slab of B gives exactly the corresponding
+    byte range of the full packed B (the multi-GPU all-gather premise)."""
+    import torch
+    d = I.make_config(4, m=64, n=256, k=300)
+    B_hi, B_lo = T(d["B_hi"]), T(d["B_lo"])
+    full = casc.casc_pack_b(B_hi, B_lo)
+    blk = casc.casc_packed_b_block_bytes(300)
+    for r in range(4):
+        part = casc.casc_pack_b(B_hi[:, 64 * r:64 * (r + 1)], B_lo[:, 64 * r:64 * (r + 1)])
+        assert torch.equal(part, full[r * blk:(r + 1) * blk])
