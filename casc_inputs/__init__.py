@@ -27,6 +27,9 @@ BASELINE.json configs 0-4):
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
@@ -88,12 +91,23 @@ def dd_uniform(seed: int, hi_stream: int, lo_stream: int, nrows: int, ncols: int
     n = cols.stop - cols.start
     hi = np.empty((m, n), dtype=np.float64)
     lo = np.empty((m, n), dtype=np.float64)
-    for r0 in range(0, m, chunk_rows):
+    chunk_rows = max(1, min(chunk_rows, (1 << 22) // max(n, 1)))
+
+    def fill(r0):
         r1 = min(m, r0 + chunk_rows)
         idx = _grid_index(slice(rows.start + r0, rows.start + r1), cols, ncols)
         h = uniform_pm1(seed, hi_stream, idx)
         l = (h * (2.0 ** -53)) * uniform_pm1(seed, lo_stream, idx)
         hi[r0:r1], lo[r0:r1] = _renormalise(h, l)
+
+    starts = list(range(0, m, chunk_rows))
+    if len(starts) > 1:
+        # numpy ufuncs release the GIL: chunks fill in parallel, output unchanged
+        with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for r0 in starts:
+            fill(r0)
     return hi, lo
 
 

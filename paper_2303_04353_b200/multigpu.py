@@ -77,8 +77,8 @@ class ShardedCascGemm:
         blk = self.ops.packed_b_block_bytes(k)
         self.chunk = self.blocks_per_rank * blk
         self.packed_b_local = torch.zeros(self.chunk, dtype=torch.uint8, device=self.device)
-        self.packed_b_full = torch.empty(self.chunk * self.world, dtype=torch.uint8,
-                                         device=self.device)
+        self.packed_b_full = (torch.empty(self.chunk * self.world, dtype=torch.uint8,
+                                          device=self.device) if self.world > 1 else None)
         self.packed_a = None
 
     def __call__(self, A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi=None, C_lo=None,
@@ -95,7 +95,12 @@ class ShardedCascGemm:
             self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])
         rec(1)
         if self.world > 1:
-            dist.all_gather_into_tensor(self.packed_b_full, self.packed_b_local, group=self.group)
+            if dist.get_backend(self.group) == "gloo":  # CPU plumbing tests
+                dist.all_gather(list(self.packed_b_full.chunk(self.world)), self.packed_b_local,
+                                group=self.group)
+            else:  # NCCL over NVLink / NVSwitch
+                dist.all_gather_into_tensor(self.packed_b_full, self.packed_b_local,
+                                            group=self.group)
             pb = self.packed_b_full
         else:
             pb = self.packed_b_local

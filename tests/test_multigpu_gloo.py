@@ -1,0 +1,109 @@
+"""Multi-GPU host logic on CPU (-m "not gpu"): world_size 2 with the gloo
+backend.  The CUDA kernels are replaced by CPU stand-ins built on the oracle
+(tests may call the oracle); what is under test is the product's plumbing in
+paper_2303_04353_b200/multigpu.py: row sharding, 64-column slab assignment
+with padding, the all-gather of packed slabs, and P-invariance of C."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import casc_inputs as I
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_arithmetic():
+    from paper_2303_04353_b200.multigpu import col_slab, row_shard
+    for m in (1, 7, 64, 1000, 16384):
+        for w in (1, 2, 3, 4, 8):
+            rows = [row_shard(m, w, r) for r in range(w)]
+            assert rows[0][0] == 0 and rows[-1][1] == m
+            assert all(rows[i][1] == rows[i + 1][0] for i in range(w - 1))
+    for n in (1, 63, 64, 150, 1000, 16384):
+        for w in (1, 2, 4, 8):
+            slabs = [col_slab(n, w, r) for r in range(w)]
+            assert slabs[0][0] == 0 and slabs[-1][1] == n
+            per = slabs[0][2]
+            assert all(s[2] == per for s in slabs) and per * w * 64 >= n
+            for c0, c1, _ in slabs:
+                assert c1 == c0 or (c0 % 64 == 0 and c1 - c0 <= per * 64)
+
+
+class _CpuOps:
+    """CPU stand-ins with the same contracts as the CUDA entry points: packed B
+    is 64-column-block major (each block = raw hi | lo of k x 64, zero-padded)."""
+
+    def __init__(self, k):
+        self.k = k
+
+    def packed_b_block_bytes(self, k):
+        return 2 * k * 64 * 8
+
+    def pack_a(self, A_hi, A_lo, packed=None):
+        return (A_hi.clone(), A_lo.clone())
+
+    def pack_b(self, B_hi, B_lo, packed):
+        k, w = B_hi.shape
+        nb = -(-w // 64)
+        buf = packed.view(torch.float64).view(nb, 2, k, 64)
+        buf.zero_()
+        for j in range(nb):
+            c = B_hi[:, 64 * j:64 * (j + 1)]
+            buf[j, 0, :, :c.shape[1]] = c
+            buf[j, 1, :, :c.shape[1]] = B_lo[:, 64 * j:64 * (j + 1)]
+        return packed
+
+    def gemm_packed(self, m, n, k, pa, pb, C_hi=None, C_lo=None, flags=None):
+        import oracle
+        nb = -(-n // 64)
+        blocks = pb.view(torch.float64)[:nb * 2 * k * 64].view(nb, 2, k, 64)
+        B_hi = torch.cat([blocks[j, 0] for j in range(nb)], dim=1)[:, :n].numpy()
+        B_lo = torch.cat([blocks[j, 1] for j in range(nb)], dim=1)[:, :n].numpy()
+        h, l, f = oracle.casc_gemm(pa[0].numpy(), pa[1].numpy(), B_hi, B_lo)
+        return torch.from_numpy(h), torch.from_numpy(l), torch.from_numpy(f)
+
+
+def _worker(rank, world, port, m, n, k, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2303_04353_b200.multigpu import ShardedCascGemm
+    op = ShardedCascGemm(m, n, k, ops=_CpuOps(k), device=torch.device("cpu"))
+    d = I.make_config(1, m=m, n=n, k=k, seed=21, rows=slice(op.r0, op.r1))
+    A_hi, A_lo = torch.from_numpy(d["A_hi"]), torch.from_numpy(d["A_lo"])
+    B_hi = torch.from_numpy(d["B_hi"][:, op.c0:op.c1].copy())
+    B_lo = torch.from_numpy(d["B_lo"][:, op.c0:op.c1].copy())
+    C_hi, C_lo, fl = op(A_hi, A_lo, B_hi, B_lo)
+    np.savez(os.path.join(out, f"r{rank}.npz"), C_hi=C_hi.numpy(), C_lo=C_lo.numpy(),
+             fl=fl.numpy(), r0=op.r0, r1=op.r1)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,k", [(10, 150, 300), (7, 64, 40)])
+def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path)), nprocs=world,
+             join=True)
+    d = I.make_config(1, m=m, n=n, k=k, seed=21)
+    ref_hi, ref_lo, ref_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    rows = 0
+    for r in range(world):
+        z = np.load(tmp_path / f"r{r}.npz")
+        r0, r1 = int(z["r0"]), int(z["r1"])
+        assert np.array_equal(z["C_hi"], ref_hi[r0:r1])
+        assert np.array_equal(z["C_lo"], ref_lo[r0:r1])
+        assert np.array_equal(z["fl"], ref_fl[r0:r1])
+        rows += r1 - r0
+    assert rows == m
