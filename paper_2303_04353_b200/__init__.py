@@ -18,7 +18,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcasc.so")
+LIB_PATH = os.environ.get("CASC_LIB_PATH") or os.path.join(_HERE, "libcasc.so")
 KC = 256
 
 if not os.path.exists(LIB_PATH):

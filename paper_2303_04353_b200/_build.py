@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcasc.so")
 SOURCES = ["casc_split.cu", "casc_gemm.cu", "casc_api.cu"]
-HEADERS = ["casc_layout.cuh", os.path.join("..", "..", "include", "casc.h")]
+HEADERS = ["casc_layout.cuh", "casc_ptx.cuh", os.path.join("..", "..", "include", "casc.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -62,6 +62,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print("\n".join(logs))
     return LIB
+
+
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment builds (timing studies only): libcasc_<name>.so with -D flags."""
+    out = os.path.join(HERE, f"libcasc_{name}.so")
+    objs = []
+    for s in SOURCES:
+        obj = os.path.join(CSRC, f"{name}_" + s.replace(".cu", ".o"))
+        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s),
+               "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {s} ({name})")
+        objs.append(obj)
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o",
+                           out, *objs, "-lcudart"])
+    for o in objs:
+        os.remove(o)
+    return out
 
 
 if __name__ == "__main__":

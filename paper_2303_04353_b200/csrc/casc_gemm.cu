@@ -14,24 +14,31 @@
 //       T = T (+) bin0; T *= 2^(e_i + f_j);  C (+)= T (FP64x2);
 //       flag |= (bin0 == 0)  (§3.7, §4.4).
 //
-// Structure (Blackwell): persistent CTAs (one per SM), warp-specialised.
-//   warp 8      producer: one elected lane issues TMA bulk copies
-//               (cp.async.bulk ... mbarrier::complete_tx) of each stage's
-//               A chunk (4 slices x 64 rows x 8 k = 16 KB) and B chunk
-//               (7 slices x 64 cols x 8 k = 28 KB) into a 4-deep smem ring;
-//   warps 0..7  MMA + epilogue: 2 (m) x 4 (n) warps, 32 x 16 outputs each,
-//               4 bins x 8 m8n8 sub-tiles in registers; fragments are read
-//               from smem as 32 consecutive doubles (fragment-ordered layout).
-// The combine runs on the MMA warps at each panel end while the producer
-// keeps prefetching; C is read-modified-written in global memory once per
-// panel per element (16 B r + 16 B w per 2560 FMAs: negligible).
+// Structure (Blackwell): persistent CTAs (one per SM), 384 threads,
+// warp-specialised with setmaxnreg (producer 40 / MMA 232 registers).
+//   warpgroup 0   producer: one elected lane issues TMA bulk copies
+//                 (cp.async.bulk ... mbarrier::complete_tx) of each stage's
+//                 A chunk (4 slices x 64 rows x 8 k = 16 KB) and B chunk
+//                 (7 slices x 64 cols x 8 k = 28 KB) into a 4-deep smem ring,
+//                 plus each panel's 64 + 64 scale exponents into an 8-deep ring;
+//   warpgroups 1-2  8 MMA + epilogue warps, 2 (m) x 4 (n), 32 x 16 outputs each,
+//                 4 bins x 8 m8n8 sub-tiles in registers; fragments are read
+//                 from smem as 32 consecutive doubles (fragment-ordered layout).
+// At each panel end the MMA warps combine their bins while the producer keeps
+// prefetching; the FP64x2 C accumulator of the tile lives in TENSOR MEMORY
+// (tcgen05.ld/st, 64 KB of the 256 KB) between panels and goes to global
+// memory once, after the tile's last panel.
 #include <cuda_runtime.h>
 
 #include "casc_layout.cuh"
+#include "casc_ptx.cuh"
 
 namespace casc {
 
-constexpr int NSTAGE = 4;
+#ifndef CASC_NSTAGE
+#define CASC_NSTAGE 4
+#endif
+constexpr int NSTAGE = CASC_NSTAGE;  // smem ring depth
 constexpr int NCW = 8;                        // MMA / epilogue warps (warpgroups 1, 2)
 constexpr int GEMM_THREADS = (NCW + 4) * 32;  // + producer warpgroup 0
 // Register budget per thread after setmaxnreg: producer warpgroup 40,
@@ -39,53 +46,12 @@ constexpr int GEMM_THREADS = (NCW + 4) * 32;  // + producer warpgroup 0
 constexpr int PRODUCER_REGS = 40;
 constexpr int MMA_REGS = 232;
 constexpr int GROUP_M = 16;                  // tile raster grouping (L2 reuse)
-constexpr size_t GEMM_SMEM =
-    (size_t)NSTAGE * (A_STAGE + B_STAGE) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t);
+constexpr int EXP_RING = 8;  // > NSTAGE: a panel's exponents outlive the stages that carried them
+constexpr size_t EXP_OFFSET =
+    (size_t)NSTAGE * (A_STAGE + B_STAGE) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t) + 16;
+constexpr size_t GEMM_SMEM = EXP_OFFSET + (size_t)EXP_RING * (TM + TN) * sizeof(int32_t);
 
 
-
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-// TMA engine 1-D bulk copy global -> shared, completion signalled on `bar`.
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
 
 // ------------------------------------------------------------ DD helpers
 // Textbook EFTs with explicit _rn intrinsics (bit-reproducible, no FMA).
@@ -132,6 +98,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   double* Bs = As + NSTAGE * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(Bs + NSTAGE * B_STAGE);
   uint64_t* empty = full + NSTAGE;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + NSTAGE);
+  // ring of per-panel scale exponents [EXP_RING][A 64 | B 64] int32, filled by TMA
+  int32_t* sexp = reinterpret_cast<int32_t*>(smem + EXP_OFFSET);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -149,7 +118,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     // ===================== TMA producer (warpgroup 0) =====================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PRODUCER_REGS));
     if (warp == 0 && lane == 0) {
-      uint32_t it = 0;
+      uint32_t it = 0, pc = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int mb, nb;
         tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
@@ -157,10 +126,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
         const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)p.st_begin * B_STAGE * 8;
         for (int st = p.st_begin; st < p.st_end; ++st, ++it) {
           const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1;
+          const bool pstart = (st == p.st_begin) || (st % STAGES_PER_PANEL) == 0;
           mbar_wait(&empty[slot], ph ^ 1);
-          mbar_arrive_expect_tx(&full[slot], (A_STAGE + B_STAGE) * 8);
+          mbar_arrive_expect_tx(&full[slot],
+                                (A_STAGE + B_STAGE) * 8 + (pstart ? (TM + TN) * 4 : 0));
           tma_bulk_g2s(As + slot * A_STAGE, srcA, A_STAGE * 8, &full[slot]);
           tma_bulk_g2s(Bs + slot * B_STAGE, srcB, B_STAGE * 8, &full[slot]);
+          if (pstart) {  // this panel's row / column exponents ride along with its first stage
+            const int q = st / STAGES_PER_PANEL;
+            int32_t* dst = sexp + (pc % EXP_RING) * (TM + TN);
+            tma_bulk_g2s(dst, p.pa + mb * p.a_blk + p.a_exp + q * TM * 4, TM * 4, &full[slot]);
+            tma_bulk_g2s(dst + TM, p.pb + nb * p.b_blk + p.b_exp + q * TN * 4, TN * 4, &full[slot]);
+            ++pc;
+          }
           srcA += A_STAGE * 8;
           srcB += B_STAGE * 8;
         }
@@ -174,10 +152,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   const int cw = warp - 4;
   const int wm = cw >> 2, wn = cw & 3;
   const int g = lane >> 2, c = lane & 3;
-  const double s_bin1 = pow2i(-p.c0), s_bin2 = pow2i(-2 * p.c0), s_bin36 = pow2i(-p.D2);
+
+  // The FP64x2 C accumulator of the current tile lives in TENSOR MEMORY between
+  // panels: warp (wm, wn) owns lane quarter wn (= warp % 4) and columns
+  // 64 wm .. 64 wm + 63, i.e. its 32 lanes x 16 elements x (hi, lo).  FP64 MMA
+  // has no tcgen05 kind, so TMEM is otherwise idle; keeping C there frees the
+  // registers and shared memory the DMMA pipeline needs.
+  if (cw == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  named_bar_sync<NCW * 32>();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot + ((uint32_t)(wn * 32) << 16) + (uint32_t)(wm * 64);
 
   double acc[4][4][2][2];  // [bin][msub][nsub][pair]
-  uint32_t it = 0;
+  uint32_t it = 0, pc = 0;  // stage counter (smem ring), panel counter (exponent ring)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int mb, nb;
     tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
@@ -197,15 +190,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       const double* b_s = Bs + slot * B_STAGE + wn * 64 + lane;
 #pragma unroll
       for (int kk = 0; kk < BK / 4; ++kk) {
+        const double* ak = a_s + kk * A_KSTEP;
+        const double* bk = b_s + kk * B_KSTEP;
         double a[4][4], b[7][2];
 #pragma unroll
         for (int s = 0; s < 4; ++s)
 #pragma unroll
-          for (int ms = 0; ms < 4; ++ms) a[s][ms] = a_s[kk * A_KSTEP + s * 256 + ms * 32];
+          for (int ms = 0; ms < 4; ++ms) a[s][ms] = ak[s * 256 + ms * 32];
 #pragma unroll
         for (int s = 0; s < 7; ++s)
 #pragma unroll
-          for (int ns = 0; ns < 2; ++ns) b[s][ns] = b_s[kk * B_KSTEP + s * 256 + ns * 32];
+          for (int ns = 0; ns < 2; ++ns) b[s][ns] = bk[s * 256 + ns * 32];
         // ten products, eqn:Gemm10, sub-tile loop innermost
 #define CASC_PROD(BIN, SA, SB)                      \
   _Pragma("unroll") for (int ms = 0; ms < 4; ++ms)  \
@@ -227,52 +222,89 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
 
       const bool panel_end = ((st + 1) % STAGES_PER_PANEL) == 0 || st + 1 == p.st_end;
       if (!panel_end) continue;
+      // this panel's scale exponents landed in smem with its first stage
+      const int32_t* pex = sexp + (pc % EXP_RING) * (TM + TN);
+      ++pc;
+#ifdef CASC_EXPERIMENT_NO_COMBINE  // timing experiment only: combine the last panel alone
+      if (st + 1 != p.st_end) continue;
+#endif
       // ------------------------------ phase 3: combine this panel
-      const int q = st / STAGES_PER_PANEL;
-      const int32_t* eA =
-          reinterpret_cast<const int32_t*>(p.pa + mb * p.a_blk + p.a_exp) + q * TM;
-      const int32_t* fB =
-          reinterpret_cast<const int32_t*>(p.pb + nb * p.b_blk + p.b_exp) + q * TN;
-      const bool first = (st + 1 - p.st_begin) <= STAGES_PER_PANEL;
+      const bool first = (st + 1 - p.st_begin) <= STAGES_PER_PANEL;  // first panel of the tile
+      const bool last = (st + 1 == p.st_end);
 #pragma unroll
-      for (int ms = 0; ms < 4; ++ms) {
-        const int rl = wm * 32 + ms * 8 + g;
-        const int64_t row = (int64_t)mb * TM + rl;
-        const int e = __ldg(eA + rl);
+      for (int ms = 0; ms < 4; ++ms)
 #pragma unroll
-        for (int ns = 0; ns < 2; ++ns) {
+        for (int ns = 0; ns < 2; ++ns)
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int cl = wn * 16 + ns * 8 + 2 * c + i;
-            const int64_t col = (int64_t)nb * TN + cl;
-            const double b0 = acc[0][ms][ns][i], b1 = acc[1][ms][ns][i];
-            const double b2 = acc[2][ms][ns][i], b36 = acc[3][ms][ns][i];
-            flagbits |= (b0 == 0.0 ? 1u : 0u) << (ms * 4 + ns * 2 + i);
-            if (row >= p.m || col >= p.n) continue;
-            if (p.dbg) {
+          for (int i = 0; i < 2; ++i)
+            flagbits |= (acc[0][ms][ns][i] == 0.0 ? 1u : 0u) << (ms * 4 + ns * 2 + i);
+      if (p.dbg) {  // debug export of the single panel's bins (canonical scales)
+#pragma unroll
+        for (int ms = 0; ms < 4; ++ms)
+#pragma unroll
+          for (int ns = 0; ns < 2; ++ns)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
+              const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
+              if (row >= p.m || col >= p.n) continue;
               const int64_t o = row * p.n + col, mn = p.m * p.n;
-              p.dbg[o] = b0;
-              p.dbg[mn + o] = b1;
-              p.dbg[2 * mn + o] = __dmul_rn(b2, p.un_b2);
-              p.dbg[3 * mn + o] = b36;
-              continue;
+              p.dbg[o] = acc[0][ms][ns][i];
+              p.dbg[mn + o] = acc[1][ms][ns][i];
+              p.dbg[2 * mn + o] = __dmul_rn(acc[2][ms][ns][i], p.un_b2);
+              p.dbg[3 * mn + o] = acc[3][ms][ns][i];
             }
-            const int f = __ldg(fB + cl);
-            double th, tl;
-            two_sum(__dmul_rn(b2, s_bin2), __dmul_rn(b36, s_bin36), th, tl);
-            dd_add_d(th, tl, __dmul_rn(b1, s_bin1));
-            dd_add_d(th, tl, b0);
-            const double sc = pow2i(e + f);
-            th = __dmul_rn(th, sc);
-            tl = __dmul_rn(tl, sc);
-            double* ch = p.C_hi + row * p.ldc + col;
-            double* cl_ = p.C_lo + row * p.ldc + col;
-            if (!first) dd_add(*ch, *cl_, th, tl, th, tl);
-            *ch = th;
-            *cl_ = tl;
-          }
-        }
+        continue;
       }
+      // bin reference scales: sigma1 = 2^-c0; bin2' carries 2^(c0-c1) so sigma2 bin2 =
+      // 2^-2c0 bin2'; sigma3 = 2^-D2
+      const double s_bin1 = pow2i(-p.c0), s_bin2 = pow2i(-2 * p.c0), s_bin36 = pow2i(-p.D2);
+      // two halves (m-subtiles 0-1, 2-3): 8 elements = 32 TMEM columns each
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t cv[32];
+        if (!first) {
+          tmem_ld32(tmem + h * 32, cv);
+          tmem_wait_ld();
+        }
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2) {
+          const int ms = 2 * h + m2;
+          const int e = pex[wm * 32 + ms * 8 + g];
+#pragma unroll
+          for (int ns = 0; ns < 2; ++ns)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int x = (m2 * 4 + ns * 2 + i) * 4;
+              double th, tl;
+              two_sum(__dmul_rn(acc[2][ms][ns][i], s_bin2), __dmul_rn(acc[3][ms][ns][i], s_bin36),
+                      th, tl);
+              dd_add_d(th, tl, __dmul_rn(acc[1][ms][ns][i], s_bin1));
+              dd_add_d(th, tl, acc[0][ms][ns][i]);
+              const double sc = pow2i(e + pex[TM + wn * 16 + ns * 8 + 2 * c + i]);
+              th = __dmul_rn(th, sc);
+              tl = __dmul_rn(tl, sc);
+              if (!first)
+                dd_add(__hiloint2double(cv[x + 1], cv[x]), __hiloint2double(cv[x + 3], cv[x + 2]),
+                       th, tl, th, tl);
+              if (last) {
+                const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
+                const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
+                if (row < p.m && col < p.n) {
+                  p.C_hi[row * p.ldc + col] = th;
+                  p.C_lo[row * p.ldc + col] = tl;
+                }
+              } else {
+                cv[x] = __double2loint(th);
+                cv[x + 1] = __double2hiint(th);
+                cv[x + 2] = __double2loint(tl);
+                cv[x + 3] = __double2hiint(tl);
+              }
+            }
+        }
+        if (!last) tmem_st32(tmem + h * 32, cv);
+      }
+      if (!last) tmem_wait_st();
     }
     // ------------------------------ cancellation flags of this tile
     if (p.flags && !p.dbg) {
@@ -289,6 +321,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           }
       }
     }
+  }
+  // ------------------------------ teardown: the allocating warp frees TMEM
+  tc_fence_before();
+  named_bar_sync<NCW * 32>();
+  if (cw == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tmem_slot)
+                 : "memory");
   }
 }
 

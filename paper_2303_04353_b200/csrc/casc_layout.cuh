@@ -30,7 +30,10 @@ namespace casc {
 constexpr int KC = 256;          // k_C panel depth
 constexpr int TM = 64;           // CTA tile rows
 constexpr int TN = 64;           // CTA tile cols
-constexpr int BK = 8;            // k per pipeline stage
+#ifndef CASC_BK
+#define CASC_BK 8
+#endif
+constexpr int BK = CASC_BK;      // k per pipeline stage (multiple of 4, divides 256)
 constexpr int STAGES_PER_PANEL = KC / BK;
 constexpr int A_SLICES = 4;
 constexpr int B_SLICES = 7;

@@ -51,6 +51,72 @@ __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters, double 
   if (s == 12345.678) out[blockIdx.x * blockDim.x + t] = s;
 }
 
+// Plain DADD / DMUL chains (8 independent per thread): are they full rate like DFMA?
+__global__ void __launch_bounds__(256) dadd_loop(double* out, int iters, double seed) {
+  int t = threadIdx.x;
+  double a = seed + t * 1e-9;
+  double c[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) c[j] = j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = __dadd_rn(c[j], a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += c[j];
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + t] = s;
+}
+__global__ void __launch_bounds__(256) dmul_loop(double* out, int iters, double seed) {
+  int t = threadIdx.x;
+  double a = 1.0 + t * 1e-15;
+  double c[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) c[j] = seed + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = __dmul_rn(c[j], a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += c[j];
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + t] = s;
+}
+
+// Mixed: even warps run the DMMA loop, odd warps the DFMA loop.  If DMMA and
+// DFMA use separate pipes, the time equals the slower half alone; if they share
+// the FP64 datapath, it is the sum.
+__global__ void __launch_bounds__(256) mixed_loop(double* out, int iters, double seed) {
+  const int t = threadIdx.x;
+  double s = 0;
+  if ((t >> 5) & 1) {
+    double a = seed + t * 1e-9, b = 1.0 - 1e-12;
+    double c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[j] = fma(c[j], b, a);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += c[j];
+  } else {
+    double a = seed + t * 1e-3, b = seed - t * 1e-3;
+    double c[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { c[j][0] = j; c[j][1] = -j; }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += c[j][0] + c[j][1];
+  }
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + t] = s;
+}
+
 struct Res { double burst, sustained; };
 
 template <typename F>
@@ -87,6 +153,23 @@ int main() {
   CK(cudaGetLastError());
   Res rf = run([&] { dfma_loop<<<grid, threads>>>(out, iters, 1.0); }, dfma_flops);
   CK(cudaGetLastError());
+  double dadd_ops = (double)grid * threads * iters * 8;
+  Res ra = run([&] { dadd_loop<<<grid, threads>>>(out, iters, 1.0); }, dadd_ops);
+  Res rmu = run([&] { dmul_loop<<<grid, threads>>>(out, iters, 1.0); }, dadd_ops);
+  printf("{\"dadd_gops\": %.1f, \"dmul_gops\": %.1f, \"dfma_gops\": %.1f}\n", ra.burst * 1e3,
+         rmu.burst * 1e3, rf.burst * 1e3 / 2);
+  // mixed: half the warps DMMA, half DFMA, each doing the same per-warp work as above
+  double mixed_flops = 0.5 * dmma_flops + 0.5 * dfma_flops;
+  Res rx = run([&] { mixed_loop<<<grid, threads>>>(out, iters, 1.0); }, mixed_flops);
+  CK(cudaGetLastError());
+  // time of each half alone at the rates measured above (ms per launch)
+  double t_dmma_half = 0.5 * dmma_flops / (rm.burst * 1e12) * 1e3;
+  double t_dfma_half = 0.5 * dfma_flops / (rf.burst * 1e12) * 1e3;
+  double t_mixed = mixed_flops / (rx.burst * 1e12) * 1e3;
+  printf("{\"mixed_ms\": %.3f, \"dmma_half_alone_ms\": %.3f, \"dfma_half_alone_ms\": %.3f, "
+         "\"verdict\": \"%s\"}\n", t_mixed, t_dmma_half, t_dfma_half,
+         t_mixed < 0.75 * (t_dmma_half + t_dfma_half) ? "DMMA and DFMA overlap (separate pipes)"
+                                                        : "DMMA and DFMA share the FP64 datapath");
   printf("{\"sms\": %d, \"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, "
          "\"dfma_tflops_burst\": %.3f, \"dfma_tflops_sustained\": %.3f, "
          "\"how\": \"register-only mma.sync m8n8k4 f64 (8 chains/warp) and fma.rn.f64 (8 chains/thread), "

@@ -281,3 +281,70 @@ def test_column_slab_packing_is_blockwise(casc):
     for r in range(4):
         part = casc.casc_pack_b(B_hi[:, 64 * r:64 * (r + 1)], B_lo[:, 64 * r:64 * (r + 1)])
         assert torch.equal(part, full[r * blk:(r + 1) * blk])
+
+
+# ------------------------------------------------------------------ full sizes
+def _sub_oracle(orc, d, rows, c0, c1):
+    """ORACLE-CASCADE on rows x [c0, c1): columns are independent (per-column
+    scales), so this equals the same block of the full oracle result."""
+    return orc.casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"][:, c0:c1].copy(),
+                         d["B_lo"][:, c0:c1].copy())
+
+
+@pytest.mark.parametrize("cfg,variant", [(2, "a"), (3, "a"), (4, "a")])
+def test_full_size_configs_sampled(casc, orc, cfg, variant):
+    """BASELINE configs 2, 3 and 4 at FULL size through casc_gemm_fp64x2 (the
+    kernels and launch configuration bench.py times): sampled entries vs the
+    exact product (north-star bound), and a row x column block vs ORACLE-CASCADE
+    (flags identical, C within twice the bound)."""
+    import torch
+    d = I.make_config(cfg, variant=variant)
+    m, n, k = d["m"], d["n"], d["k"]
+    C_hi, C_lo, flags = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                              T(d["B_lo"]))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(cfg)
+    ii = np.concatenate([rng.integers(0, m, 120), [0, m - 1]])
+    jj = np.concatenate([rng.integers(0, n, 120), [n - 1, 0]])
+    C_hi, C_lo, flags = N(C_hi), N(C_lo), N(flags)
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii, jj, C_hi, C_lo)
+    assert np.max(np.abs(r["err"]) / orc.north_star_bound(k, r["absab"])) <= 1.0
+    rows = [0, m // 2, m - 1]
+    c0, c1 = n - 96, n
+    o_hi, o_lo, o_fl = _sub_oracle(orc, d, rows, c0, c1)
+    assert np.array_equal(flags[rows, c0:c1], o_fl)
+    rr = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"],
+                           np.repeat(rows, c1 - c0), np.tile(np.arange(c0, c1), len(rows)))
+    diff = np.abs((C_hi[rows, c0:c1] - o_hi) + (C_lo[rows, c0:c1] - o_lo)).ravel()
+    assert np.all(diff <= 2 * orc.north_star_bound(k, rr["absab"]))
+    assert flags.sum() == 0
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_p_invariance_emulated_ranks(casc, world):
+    """The multi-GPU data path run rank by rank on one GPU (no collective is
+    needed to emulate it: rank r packs its rows of A and its column slab of B;
+    the packed slabs concatenated in rank order are the all-gathered buffer):
+    C is bitwise identical to the single-call result for any world size."""
+    import torch
+    from paper_2303_04353_b200.multigpu import col_slab, row_shard
+    m, n, k = 300, 700, 530
+    d = I.make_config(1, m=m, n=n, k=k, seed=13)
+    A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+    ref = casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo)
+    blk = casc.casc_packed_b_block_bytes(k)
+    chunks = []
+    for r in range(world):
+        c0, c1, per = col_slab(n, world, r)
+        buf = torch.zeros(per * blk, dtype=torch.uint8, device="cuda")
+        if c1 > c0:
+            used = -(-(c1 - c0) // 64) * blk
+            casc.casc_pack_b(B_hi[:, c0:c1], B_lo[:, c0:c1], packed=buf[:used])
+        chunks.append(buf)
+    pb = torch.cat(chunks)
+    for r in range(world):
+        r0, r1 = row_shard(m, world, r)
+        pa = casc.casc_pack_a(A_hi[r0:r1], A_lo[r0:r1])
+        out = casc.casc_gemm_packed(r1 - r0, n, k, pa, pb)
+        for x, y in zip(out, ref):
+            assert torch.equal(x, y[r0:r1])
