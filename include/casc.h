@@ -180,6 +180,36 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k,
                     const double* B_hi, const double* B_lo, int64_t ldb,
                     int64_t panel, double* bins, casc_stream_t stream);
 
+/* ------------------------------------------------------------------------ */
+/* The paper's simple path (§4.2): phases as separate kernels.  */
+/* ------------------------------------------------------------------------ */
+
+/* C := A B exactly as casc_gemm_fp64x2 (same widths, split, combine and flag
+ * semantics) but staged like §4.2: per 256-wide k panel, ten separate
+ * slice-GEMM launches (DMMA) accumulate the products of eqn:Gemm10 into four
+ * m x n bins in HBM, then a standalone HBM-bound epilogue kernel adds the bins
+ * into C in FP64x2 (bin 3-6, 2, 1, 0) and applies Sigma, T.  Bins 0-2 and the
+ * flags equal the fused path's bit for bit; C agrees within the error bound
+ * (bin 3-6 is summed in another order).  Uses temporary device memory
+ * (cudaMallocAsync on `stream`): packed slices + 32 m n bytes of bins.
+ * Arguments and errors as casc_gemm_fp64x2. */
+int casc_gemm_fp64x2_simple(int64_t m, int64_t n, int64_t k,
+                            const double* A_hi, const double* A_lo, int64_t lda,
+                            const double* B_hi, const double* B_lo, int64_t ldb,
+                            double* C_hi, double* C_lo, int64_t ldc,
+                            uint8_t* flags, casc_stream_t stream);
+
+/* One slice GEMM of one k panel: out (m x n, leading dimension n) :=
+ * sum_{p in panel} A_sa[i, p] B_sb[p, j] in the paper's normalisation
+ * (sa in 0..3 = A0..A3, sb in 0..6 = B0..B6), computed by the simple path's
+ * slice-GEMM kernel.  The six products A0B0, A0B1, A1B0, A0B2, A1B1, A2B0 are
+ * exact and therefore bit-comparable.  CASC_ERR_INVALID for slice or
+ * panel out of range. */
+int casc_slice_product(int64_t m, int64_t n, int64_t k,
+                       const double* A_hi, const double* A_lo, int64_t lda,
+                       const double* B_hi, const double* B_lo, int64_t ldb,
+                       int sa, int sb, int64_t panel, double* out, casc_stream_t stream);
+
 /* Number of kernel launches the last successful call of the given entry point
  * family enqueued on this host thread (for launch accounting in bench.py). */
 int casc_last_launch_count(void);

@@ -57,12 +57,17 @@ _sig("casc_split_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_split_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp])
 _sig("casc_last_launch_count", [])
+_sig("casc_gemm_fp64x2_simple", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                                 _i64, _vp, _vp])
+_sig("casc_slice_product", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_int,
+                            ctypes.c_int, _i64, _vp, _vp])
 
 EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_gemm_fp64x2_ws", "casc_workspace_bytes", "casc_finalize",
             "casc_packed_a_bytes", "casc_packed_b_bytes", "casc_packed_a_block_bytes",
             "casc_packed_b_block_bytes", "casc_pack_a", "casc_pack_b", "casc_gemm_packed",
-            "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count"]
+            "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count",
+            "casc_gemm_fp64x2_simple", "casc_slice_product"]
 
 
 class CascError(RuntimeError):
@@ -248,3 +253,35 @@ def casc_debug_bins(A_hi, A_lo, B_hi, B_lo, panel: int, stream=None):
     _check(_lib.casc_debug_bins(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo),
                                 ldb, panel, _ptr(bins), _stream(stream)), "casc_debug_bins")
     return bins
+
+
+def casc_gemm_fp64x2_simple(A_hi, A_lo, B_hi, B_lo, C_hi=None, C_lo=None, flags=None,
+                            want_flags=True, stream=None):
+    """The paper's simple path (§4.2): ten slice-GEMM launches into four HBM bins
+    per panel + standalone epilogue.  Returns (C_hi, C_lo, flags)."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    k2, n = B_hi.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    C_hi, C_lo, flags = _outputs(m, n, A_hi.device, C_hi, C_lo, flags, want_flags)
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    _check(_lib.casc_gemm_fp64x2_simple(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                        _ptr(B_lo), ldb, _ptr(C_hi), _ptr(C_lo), ldc,
+                                        _ptr(flags), _stream(stream)),
+           "casc_gemm_fp64x2_simple")
+    return C_hi, C_lo, flags
+
+
+def casc_slice_product(A_hi, A_lo, B_hi, B_lo, sa: int, sb: int, panel: int, stream=None):
+    """One slice GEMM A_sa . B_sb of k panel `panel` (paper normalisation), (m, n)."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    out = torch.empty((m, n), dtype=torch.float64, device=A_hi.device)
+    _check(_lib.casc_slice_product(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                   _ptr(B_lo), ldb, sa, sb, panel, _ptr(out), _stream(stream)),
+           "casc_slice_product")
+    return out

@@ -385,4 +385,124 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, const d
   return r;
 }
 
+// ---------------------------------------------------------------- simple path
+// Ten products of eqn:Gemm10 in the order of the fused kernel: {bin, A slice, B slice}.
+static const int kProducts[10][3] = {{0, 0, 0}, {1, 0, 1}, {1, 1, 0}, {2, 0, 2}, {2, 1, 1},
+                                     {2, 2, 0}, {3, 0, 3}, {3, 1, 4}, {3, 2, 5}, {3, 3, 6}};
+
+static int slice_args(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb, int sa,
+                      int sb, int64_t panel, double* out, int64_t ldo, int accumulate,
+                      double scale, casc::SliceArgs& a) {
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  a.pa = static_cast<const uint8_t*>(pa);
+  a.pb = static_cast<const uint8_t*>(pb);
+  a.a_blk = casc::a_block_bytes(k);
+  a.b_blk = casc::b_block_bytes(k);
+  a.m = m;
+  a.n = n;
+  a.mblocks = (int)((m + casc::TM - 1) / casc::TM);
+  a.nblocks = (int)((n + casc::TN - 1) / casc::TN);
+  a.st_begin = (int)panel * casc::STAGES_PER_PANEL;
+  a.st_end = a.st_begin + casc::STAGES_PER_PANEL < nst ? a.st_begin + casc::STAGES_PER_PANEL : nst;
+  a.sa = sa;
+  a.sb = sb;
+  a.out = out;
+  a.ldo = ldo;
+  a.accumulate = accumulate;
+  a.scale = scale;
+  return CASC_OK;
+}
+
+int casc_gemm_fp64x2_simple(int64_t m, int64_t n, int64_t k, const double* A_hi,
+                            const double* A_lo, int64_t lda, const double* B_hi,
+                            const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                            int64_t ldc, uint8_t* flags, casc_stream_t stream) {
+  g_launches = 0;
+  int r = validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  cudaStream_t st = S(stream);
+  if (k == 0) return zero_c(m, n, C_hi, C_lo, ldc, flags, st);
+  void *pa = nullptr, *pb = nullptr, *bins = nullptr;
+  const size_t bin_bytes = (size_t)4 * m * n * sizeof(double);
+  if (cudaMallocAsync(&pa, casc_packed_a_bytes(m, k), st) != cudaSuccess) return CASC_ERR_CUDA;
+  if (cudaMallocAsync(&pb, casc_packed_b_bytes(k, n), st) != cudaSuccess ||
+      cudaMallocAsync(&bins, bin_bytes, st) != cudaSuccess) {
+    cudaFreeAsync(pa, st);
+    if (pb) cudaFreeAsync(pb, st);
+    return CASC_ERR_CUDA;
+  }
+  const casc::Widths w = widths_for(k);
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, st);
+  if (e == cudaSuccess) e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, st);
+  int launches = 2;
+  const int64_t P = casc::panels_of(k);
+  double* B = static_cast<double*>(bins);
+  for (int64_t q = 0; q < P && e == cudaSuccess; ++q) {
+    for (int t = 0; t < 10 && e == cudaSuccess; ++t) {
+      const int bin = kProducts[t][0];
+      const bool first_of_bin = (t == 0 || kProducts[t - 1][0] != bin);
+      casc::SliceArgs a{};
+      slice_args(m, n, k, pa, pb, kProducts[t][1], kProducts[t][2], q, B + bin * m * n, n,
+                 first_of_bin ? 0 : 1, 1.0, a);
+      e = casc::launch_slice_gemm(a, sms, st);
+      ++launches;
+    }
+    if (e == cudaSuccess)
+      e = casc::launch_epilogue(B, pa, pb, k, (int)q, m, n, C_hi, C_lo, ldc, flags, q == 0, w,
+                                sms, st);
+    ++launches;
+  }
+  cudaFreeAsync(bins, st);
+  cudaFreeAsync(pa, st);
+  cudaFreeAsync(pb, st);
+  if (e != cudaSuccess) return CASC_ERR_CUDA;
+  g_launches = launches;
+  return CASC_OK;
+}
+
+int casc_slice_product(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                       int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb, int sa,
+                       int sb, int64_t panel, double* out, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  if ((r = check_mat(A_hi, m, k, lda)) || (r = check_mat(A_lo, m, k, lda))) return r;
+  if ((r = check_mat(B_hi, k, n, ldb)) || (r = check_mat(B_lo, k, n, ldb))) return r;
+  if (sa < 0 || sa > 3 || sb < 0 || sb > 6) return CASC_ERR_INVALID;
+  if (panel < 0 || panel >= casc::panels_of(k)) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  if (!out) return CASC_ERR_INVALID;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  cudaStream_t st = S(stream);
+  void *pa = nullptr, *pb = nullptr;
+  if (cudaMallocAsync(&pa, casc_packed_a_bytes(m, k), st) != cudaSuccess) return CASC_ERR_CUDA;
+  if (cudaMallocAsync(&pb, casc_packed_b_bytes(k, n), st) != cudaSuccess) {
+    cudaFreeAsync(pa, st);
+    return CASC_ERR_CUDA;
+  }
+  const casc::Widths w = widths_for(k);
+  // undo the exact pre-alignment: paper normalisation of A2, B2, B4, B5
+  int sh = 0;
+  if (sa == 2) sh += w.c1 - w.c0;
+  if (sb == 2) sh += w.c1 - w.c0;
+  if (sb == 4) sh += w.c0 - w.c2;
+  if (sb == 5) sh += 2 * w.c0 - w.c1 - w.c2;
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, st);
+  if (e == cudaSuccess) e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, st);
+  if (e == cudaSuccess) {
+    casc::SliceArgs a{};
+    slice_args(m, n, k, pa, pb, sa, sb, panel, out, n, 0, std::ldexp(1.0, sh), a);
+    e = casc::launch_slice_gemm(a, sms, st);
+  }
+  cudaFreeAsync(pa, st);
+  cudaFreeAsync(pb, st);
+  if (e != cudaSuccess) return CASC_ERR_CUDA;
+  g_launches = 3;
+  return CASC_OK;
+}
+
 }  // extern "C"

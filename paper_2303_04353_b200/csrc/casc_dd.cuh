@@ -1,0 +1,52 @@
+// casc_dd.cuh — double-double error-free transformations and the fl_casc bin
+// combine shared by the fused kernel and the simple-path
+// epilogue (product path only; the oracle has its own, independent code).
+#pragma once
+#include "casc_layout.cuh"
+
+namespace casc {
+
+// ------------------------------------------------------------ DD helpers
+// Textbook EFTs with explicit _rn intrinsics (bit-reproducible, no FMA).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  e = __dsub_rn(b, __dsub_rn(s, a));
+}
+__device__ __forceinline__ void dd_add_d(double& h, double& l, double x) {
+  double s, e;
+  two_sum(h, x, s, e);
+  e = __dadd_rn(e, l);
+  fast_two_sum(s, e, h, l);
+}
+__device__ __forceinline__ void dd_add(double xh, double xl, double yh, double yl, double& rh,
+                                       double& rl) {
+  double s1, s2, t1, t2;
+  two_sum(xh, yh, s1, s2);
+  two_sum(xl, yl, t1, t2);
+  s2 = __dadd_rn(s2, t1);
+  fast_two_sum(s1, s2, s1, s2);
+  s2 = __dadd_rn(s2, t2);
+  fast_two_sum(s1, s2, rh, rl);
+}
+
+
+// fl_casc of one element (reading R9), bins in the
+// kernel's pre-aligned scales: T = TwoSum(2^-2c0 bin2', 2^-D2 bin36);
+// T = T (+) 2^-c0 bin1; T = T (+) bin0; T *= 2^escale.
+__device__ __forceinline__ void combine_bins(double b0, double b1, double b2p, double b36,
+                                             int c0, int D2, int escale, double& th,
+                                             double& tl) {
+  two_sum(__dmul_rn(b2p, pow2i(-2 * c0)), __dmul_rn(b36, pow2i(-D2)), th, tl);
+  dd_add_d(th, tl, __dmul_rn(b1, pow2i(-c0)));
+  dd_add_d(th, tl, b0);
+  const double sc = pow2i(escale);
+  th = __dmul_rn(th, sc);
+  tl = __dmul_rn(tl, sc);
+}
+
+}  // namespace casc

@@ -30,8 +30,14 @@
 // memory once, after the tile's last panel.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
+#include "casc_dd.cuh"
 #include "casc_layout.cuh"
 #include "casc_ptx.cuh"
+
+// DBG instantiation: the combine below its early `continue` is unreachable by design
+#pragma nv_diag_suppress 128
 
 namespace casc {
 
@@ -53,34 +59,6 @@ constexpr size_t GEMM_SMEM = EXP_OFFSET + (size_t)EXP_RING * (TM + TN) * sizeof(
 
 
 
-// ------------------------------------------------------------ DD helpers
-// Textbook EFTs with explicit _rn intrinsics (bit-reproducible, no FMA).
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = __dadd_rn(a, b);
-  const double bb = __dsub_rn(s, a);
-  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-}
-__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e) {
-  s = __dadd_rn(a, b);
-  e = __dsub_rn(b, __dsub_rn(s, a));
-}
-__device__ __forceinline__ void dd_add_d(double& h, double& l, double x) {
-  double s, e;
-  two_sum(h, x, s, e);
-  e = __dadd_rn(e, l);
-  fast_two_sum(s, e, h, l);
-}
-__device__ __forceinline__ void dd_add(double xh, double xl, double yh, double yl, double& rh,
-                                       double& rl) {
-  double s1, s2, t1, t2;
-  two_sum(xh, yh, s1, s2);
-  two_sum(xl, yl, t1, t2);
-  s2 = __dadd_rn(s2, t1);
-  fast_two_sum(s1, s2, s1, s2);
-  s2 = __dadd_rn(s2, t2);
-  fast_two_sum(s1, s2, rh, rl);
-}
-
 __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, int& mb,
                                             int& nb) {
   const int per_group = GROUP_M * nblocks;
@@ -92,6 +70,8 @@ __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, 
   nb = r / gsize;
 }
 
+// DBG: debug export of one panel's bins instead of the combine (casc_debug_bins)
+template <bool DBG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -119,7 +99,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PRODUCER_REGS));
     if (warp == 0 && lane == 0) {
       uint32_t it = 0, pc = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int nwaves = (ntiles + gridDim.x - 1) / gridDim.x;
+      for (int wave = 0; wave < nwaves; ++wave) {
+        const int tile = blockIdx.x + wave * gridDim.x;
+        if (p.wave_counter && wave > 0) {
+          // Re-align all producers at every tile wave so that the tiles in flight
+          // (a GROUP_M x ~9 block of C sharing A and B blocks) sweep k in step and
+          // hit each other's slices in L2 instead of re-reading HBM.  A CTA without
+          // a tile in this wave still arrives, so the count always completes.
+          atomicAdd(p.wave_counter, 1u);
+          if (tile < ntiles) {
+            const unsigned int target = (unsigned int)wave * gridDim.x;
+            unsigned int v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
+                           : "=r"(v)
+                           : "l"(p.wave_counter)
+                           : "memory");
+            } while (v < target);
+          }
+        }
+        if (tile >= ntiles) continue;
         int mb, nb;
         tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
         const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)p.st_begin * A_STAGE * 8;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
 #pragma unroll
           for (int i = 0; i < 2; ++i)
             flagbits |= (acc[0][ms][ns][i] == 0.0 ? 1u : 0u) << (ms * 4 + ns * 2 + i);
-      if (p.dbg) {  // debug export of the single panel's bins (canonical scales)
+      if constexpr (DBG) {  // debug export of the single panel's bins (canonical scales)
 #pragma unroll
         for (int ms = 0; ms < 4; ++ms)
 #pragma unroll
@@ -256,9 +256,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
             }
         continue;
       }
-      // bin reference scales: sigma1 = 2^-c0; bin2' carries 2^(c0-c1) so sigma2 bin2 =
-      // 2^-2c0 bin2'; sigma3 = 2^-D2
-      const double s_bin1 = pow2i(-p.c0), s_bin2 = pow2i(-2 * p.c0), s_bin36 = pow2i(-p.D2);
       // two halves (m-subtiles 0-1, 2-3): 8 elements = 32 TMEM columns each
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -277,13 +274,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
             for (int i = 0; i < 2; ++i) {
               const int x = (m2 * 4 + ns * 2 + i) * 4;
               double th, tl;
-              two_sum(__dmul_rn(acc[2][ms][ns][i], s_bin2), __dmul_rn(acc[3][ms][ns][i], s_bin36),
-                      th, tl);
-              dd_add_d(th, tl, __dmul_rn(acc[1][ms][ns][i], s_bin1));
-              dd_add_d(th, tl, acc[0][ms][ns][i]);
-              const double sc = pow2i(e + pex[TM + wn * 16 + ns * 8 + 2 * c + i]);
-              th = __dmul_rn(th, sc);
-              tl = __dmul_rn(tl, sc);
+              combine_bins(acc[0][ms][ns][i], acc[1][ms][ns][i], acc[2][ms][ns][i],
+                           acc[3][ms][ns][i], p.c0, p.D2,
+                           e + pex[TM + wn * 16 + ns * 8 + 2 * c + i], th, tl);
               if (!first)
                 dd_add(__hiloint2double(cv[x + 1], cv[x]), __hiloint2double(cv[x + 3], cv[x + 2]),
                        th, tl, th, tl);
@@ -307,7 +300,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       if (!last) tmem_wait_st();
     }
     // ------------------------------ cancellation flags of this tile
-    if (p.flags && !p.dbg) {
+    if (!DBG && p.flags) {
 #pragma unroll
       for (int ms = 0; ms < 4; ++ms) {
         const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
@@ -332,19 +325,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   }
 }
 
-cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st) {
+cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel,
+    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)GEMM_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(casc_gemm_kernel<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  GemmArgs a = a_in;
   const int ntiles = a.mblocks * a.nblocks;
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
-  casc_gemm_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+  static int wave_sync = -1;
+  if (wave_sync < 0) {
+    // default on: 6x less HBM traffic for the fused kernel at ~0.2% time cost
+    // (profiles/r01c); CASC_WAVE_SYNC=0 turns it off
+    const char* s = getenv("CASC_WAVE_SYNC");
+    wave_sync = (s && s[0] == '0') ? 0 : 1;
+  }
+  a.wave_counter = nullptr;
+  if (a.dbg) {
+    casc_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+    return cudaGetLastError();
+  }
+  if (wave_sync && ntiles > grid) {
+    static unsigned int* counters[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!counters[dev] && cudaMalloc(&counters[dev], sizeof(unsigned int)) != cudaSuccess)
+      return cudaErrorMemoryAllocation;
+    a.wave_counter = counters[dev];
+    cudaError_t e = cudaMemsetAsync(a.wave_counter, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+    // co-residency of all CTAs is required by the wave barrier: cooperative launch
+    void* args[] = {&a};
+    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<false>, dim3(grid),
+                                       dim3(GEMM_THREADS), args, GEMM_SMEM, st);
+  }
+  casc_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
   return cudaGetLastError();
 }
 

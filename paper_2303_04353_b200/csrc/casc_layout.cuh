@@ -80,9 +80,30 @@ struct GemmArgs {
   int64_t ldc;
   uint8_t* flags;  // m x n (ld n) or null
   double* dbg;     // debug: bins of the single panel, 4 x m x n (canonical scales)
+  unsigned int* wave_counter;  // zeroed per launch; producers meet here at each tile wave
   double un_b2;    // 2^(c1-c0): bin2' -> bin2 for the debug export
 };
 
 cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st);
+
+// Arguments of the single slice-GEMM kernel of the simple path (casc_simple.cu).
+struct SliceArgs {
+  const uint8_t* pa;
+  const uint8_t* pb;
+  int64_t a_blk, b_blk;
+  int64_t m, n;
+  int mblocks, nblocks;
+  int st_begin, st_end;  // stages of one panel
+  int sa, sb;            // slice of A (0..3) and of B (0..6)
+  double* out;           // m x n, leading dimension ldo
+  int64_t ldo;
+  int accumulate;        // out = out + scale * P  (else out = scale * P)
+  double scale;          // exact power of two (un-alignment for the debug export)
+};
+
+cudaError_t launch_slice_gemm(const SliceArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_epilogue(const double* bins, const void* pa, const void* pb, int64_t k, int q,
+                            int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc,
+                            uint8_t* flags, int first, Widths w, int num_sms, cudaStream_t st);
 
 }  // namespace casc

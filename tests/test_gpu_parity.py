@@ -348,3 +348,62 @@ def test_p_invariance_emulated_ranks(casc, world):
         out = casc.casc_gemm_packed(r1 - r0, n, k, pa, pb)
         for x, y in zip(out, ref):
             assert torch.equal(x, y[r0:r1])
+
+
+# ------------------------------------------------------------------ simple path (NEXT-2)
+EXACT_PRODUCTS = [(0, 0), (0, 1), (1, 0), (0, 2), (1, 1), (2, 0)]
+ROUNDED_PRODUCTS = [(0, 3), (1, 4), (2, 5), (3, 6)]
+
+
+@pytest.mark.parametrize("cfg,m,n,k", [(0, 64, 64, 64), (1, 70, 90, 600), (2, 65, 33, 300)])
+def test_slice_products(casc, orc, cfg, m, n, k):
+    """Every slice GEMM of the simple path: the six exact products of
+    eqn:Gemm10 equal the exact sums bit for bit (BASELINE north star "match
+    bit-exactly on each slice-GEMM wherever the digit budgets make FP64
+    accumulation exact"); the four others are within gamma_{k+1} sum|terms|."""
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    c = orc.select_widths(k)
+    A = [T(d[x]) for x in ("A_hi", "A_lo")]
+    B = [T(d[x]) for x in ("B_hi", "B_lo")]
+    u = 2.0**-53
+    for q, p0 in enumerate(range(0, k, 256)):
+        p1 = min(k, p0 + 256)
+        oa, _ = orc.split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], c)
+        ob, _ = orc.split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], c)
+        for sa, sb in EXACT_PRODUCTS + ROUNDED_PRODUCTS:
+            P = N(casc.casc_slice_product(*A, *B, sa, sb, q))
+            rows = range(0, m, max(1, m // 6))
+            cols = range(0, n, max(1, n // 5))
+            for i in rows:
+                for j in cols:
+                    eh, el = orc.exact_dot(oa[sa][i], ob[sb][:, j])
+                    if (sa, sb) in EXACT_PRODUCTS:
+                        assert el == 0.0 and P[i, j] == eh, (sa, sb, i, j)
+                    else:
+                        bound = (p1 - p0 + 1) * u * float(np.abs(oa[sa][i]) @ np.abs(ob[sb][:, j]))
+                        assert abs((P[i, j] - eh) - el) <= bound * (1 + 1e-12)
+            if (sa, sb) in EXACT_PRODUCTS:  # all entries: any exact evaluation agrees
+                assert np.array_equal(P, oa[sa] @ ob[sb])
+
+
+@pytest.mark.parametrize("cfg,m,n,k", [(0, 64, 64, 64), (1, 77, 70, 600), (2, 96, 130, 513),
+                                       (3, 64, 64, 1024)])
+def test_simple_path_agrees_with_fused(casc, orc, cfg, m, n, k):
+    """§4.2 simple path vs the fused kernel: identical flags, C within twice the
+    north-star bound of each other (both within it of C*)."""
+    d = I.make_config(cfg, m=m, n=n, k=k, variant="b") if cfg == 3 else \
+        I.make_config(cfg, m=m, n=n, k=k)
+    args = [T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo")]
+    s_hi, s_lo, s_fl = (N(x) for x in casc.casc_gemm_fp64x2_simple(*args))
+    f_hi, f_lo, f_fl = (N(x) for x in casc.casc_gemm_fp64x2(*args))
+    assert np.array_equal(s_fl, f_fl)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel(),
+                          s_hi, s_lo)
+    bound = orc.north_star_bound(k, r["absab"])
+    if cfg != 3:
+        assert np.all(np.abs(r["err"]) <= bound)
+        diff = np.abs((s_hi - f_hi) + (s_lo - f_lo)).ravel()
+        assert np.all(diff <= 2 * bound)
+    else:
+        assert s_fl.all()
