@@ -244,10 +244,10 @@ def main():
     c0, c1, _ = col_slab(n, world, rank)
 
     # ---- inputs: this rank's rows of A and column slab of B (seeded, blockwise)
-    full = I.make_config(args.config, rows=slice(r0, r1))
+    full = I.make_config(args.config, rows=slice(r0, r1), cols=slice(c0, c1))
     A_hi_h, A_lo_h = full["A_hi"], full["A_lo"]
-    B_hi_h, B_lo_h = full["B_hi"][:, c0:c1].copy(), full["B_lo"][:, c0:c1].copy()
-    B_full_hi, B_full_lo = full["B_hi"], full["B_lo"]
+    B_hi_h, B_lo_h = full["B_hi"], full["B_lo"]
+    B_full_hi, B_full_lo = full["B_hi"], full["B_lo"]  # == B when world == 1 (cpu baseline)
     del full
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     hA_hi, hA_lo, hB_hi, hB_lo = pin(A_hi_h), pin(A_lo_h), pin(B_hi_h), pin(B_lo_h)

@@ -119,7 +119,7 @@ def int_uniform(seed: int, stream: int, count: int, lo: int, hi: int) -> np.ndar
 
 def make_config(cfg: int, seed: int | None = None, m: int | None = None,
                 n: int | None = None, k: int | None = None, variant: str = "a",
-                rows: slice | None = None):
+                rows: slice | None = None, cols: slice | None = None):
     """Inputs for BASELINE.json config `cfg` (optionally shrunk to m, n, k for
     parity tests that keep the structure but not the size).
 
@@ -136,7 +136,10 @@ def make_config(cfg: int, seed: int | None = None, m: int | None = None,
            variant "c": cross-panel pairing - A[:, p+256] = A[:, p],
                         B[p+256, :] = -B[p, :] + 2^-60 U for even panels.
     cfg 4: 16384^3 uniform (headline; C row-block sharded over GPUs).
-    `rows` restricts A (and the output) to a row block; B is always whole.
+    `rows` restricts A (and the output) to a row block, `cols` restricts B (and
+    the output) to a column slab; either block is bit-identical to the same
+    block of the full matrices (global-index RNG).  (cfg 3 builds the full B and
+    slices it: its column pairing crosses slabs.)
     """
     defaults = {0: (64, 64, 64), 1: (1024, 1024, 1024), 2: (4096, 4096, 4096),
                 3: (4096, 4096, 32768), 4: (16384, 16384, 16384)}
@@ -148,12 +151,14 @@ def make_config(cfg: int, seed: int | None = None, m: int | None = None,
     k = dk if k is None else k
     seed = cfg if seed is None else seed
     rows = rows or slice(0, m)
+    cols = cols or slice(0, n)
     A_hi, A_lo = dd_uniform(seed, STREAM_A_HI, STREAM_A_LO, m, k, rows=rows)
-    B_hi, B_lo = dd_uniform(seed, STREAM_B_HI, STREAM_B_LO, k, n)
+    B_hi, B_lo = dd_uniform(seed, STREAM_B_HI, STREAM_B_LO, k, n,
+                            cols=None if cfg == 3 else cols)
     name = f"cfg{cfg}_{m}x{n}x{k}"
     if cfg == 2:
         u = int_uniform(seed, STREAM_ROW_EXP, m, -30, 30)[rows]
-        v = int_uniform(seed, STREAM_COL_EXP, n, -30, 30)
+        v = int_uniform(seed, STREAM_COL_EXP, n, -30, 30)[cols]
         su = np.ldexp(1.0, u)[:, None]
         sv = np.ldexp(1.0, v)[None, :]
         A_hi *= su
@@ -181,6 +186,8 @@ def make_config(cfg: int, seed: int | None = None, m: int | None = None,
                 B_lo[p0 + span:p0 + span + w, :] = -B_lo[p0:p0 + w, :] + pert
         else:
             raise ValueError(f"unknown cfg3 variant {variant}")
+        B_hi = np.ascontiguousarray(B_hi[:, cols])
+        B_lo = np.ascontiguousarray(B_lo[:, cols])
     return dict(A_hi=A_hi, A_lo=A_lo, B_hi=B_hi, B_lo=B_lo, m=m, n=n, k=k, name=name)
 
 

@@ -181,6 +181,34 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k,
                     int64_t panel, double* bins, casc_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* BLAS-style generality ("other level-3 BLAS").  */
+/* ------------------------------------------------------------------------ */
+typedef enum { CASC_OP_N = 0, CASC_OP_T = 1 } casc_op;
+
+/* C := alpha (x) op(A) op(B) (+) beta (x) C, all FP64x2, op(X) = X or X^T.
+ *   op(A) is m x k: A stored m x k (transa = CASC_OP_N, lda >= max(1,k)) or
+ *     k x m (CASC_OP_T, lda >= max(1,m)); op(B) is k x n likewise.
+ *   alpha = alpha_hi + alpha_lo, beta = beta_hi + beta_lo (normalised pairs).
+ *   The product op(A) op(B) is the cascaded one of casc_gemm_fp64x2 (bitwise
+ *   identical for the same operands); the update uses FP64x2 multiplication
+ *   (TwoProd by FMA) and FP64x2 addition: C := (alpha (x) P) (+) (beta (x) C),
+ *   DESIGN.md reading R21.  beta == 0: C is not read (may hold NaN).
+ *   k == 0 or alpha == 0: A and B are not referenced, C := beta (x) C, flags := 0.
+ *   flags: as casc_gemm_fp64x2 (of the product), or NULL.
+ *   workspace: NULL (temporary stream-ordered allocation) or a caller buffer of
+ *   casc_workspace_bytes(m, n, k) bytes.
+ * Errors as casc_gemm_fp64x2; CASC_ERR_INVALID also for trans values other than
+ * CASC_OP_N / CASC_OP_T. */
+int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                        double alpha_hi, double alpha_lo,
+                        const double* A_hi, const double* A_lo, int64_t lda,
+                        const double* B_hi, const double* B_lo, int64_t ldb,
+                        double beta_hi, double beta_lo,
+                        double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* workspace, size_t workspace_bytes,
+                        casc_stream_t stream);
+
+/* ------------------------------------------------------------------------ */
 /* The paper's simple path (§4.2): phases as separate kernels.  */
 /* ------------------------------------------------------------------------ */
 

@@ -343,6 +343,71 @@ void orc_casc_gemm_rows(int64_t r0, int64_t mr, int64_t n, int64_t k, const doub
 }
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-4 (BLAS generality): C := alpha (x) op(A) op(B) (+)     */
+/* beta (x) C (reading R21).  op() is a plain copy into row-major arrays; the */
+/* product is ORACLE-CASCADE; the update is FP64x2 mul then FP64x2 add.       */
+/* k == 0 or alpha == 0: C := beta (x) C (0 if beta == 0), flags := 0.        */
+/* alpha == 1 and beta == 0: C := product (no update arithmetic).             */
+/* ------------------------------------------------------------------------- */
+void orc_casc_gemm_ex(int transa, int transb, int64_t m, int64_t n, int64_t k, double ah,
+                      double al, const double* Ahi, const double* Alo, int64_t lda,
+                      const double* Bhi, const double* Blo, int64_t ldb, double bh, double bl,
+                      double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int nthreads) {
+  const int use_beta = !(bh == 0.0 && bl == 0.0);
+  if (k == 0 || (ah == 0.0 && al == 0.0)) {
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double rh = 0.0, rl = 0.0;
+        if (use_beta) orc_dd_mul(bh, bl, Chi[i * ldc + j], Clo[i * ldc + j], &rh, &rl);
+        Chi[i * ldc + j] = rh;
+        Clo[i * ldc + j] = rl;
+        if (flags) flags[i * n + j] = 0;
+      }
+    return;
+  }
+  double* a_h = (double*)malloc(sizeof(double) * m * k);
+  double* a_l = (double*)malloc(sizeof(double) * m * k);
+  double* b_h = (double*)malloc(sizeof(double) * k * n);
+  double* b_l = (double*)malloc(sizeof(double) * k * n);
+  double* p_h = (double*)malloc(sizeof(double) * m * n);
+  double* p_l = (double*)malloc(sizeof(double) * m * n);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t p = 0; p < k; ++p) {
+      const int64_t s = transa ? p * lda + i : i * lda + p;
+      a_h[i * k + p] = Ahi[s];
+      a_l[i * k + p] = Alo[s];
+    }
+  for (int64_t p = 0; p < k; ++p)
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t s = transb ? j * ldb + p : p * ldb + j;
+      b_h[p * n + j] = Bhi[s];
+      b_l[p * n + j] = Blo[s];
+    }
+  orc_casc_gemm(m, n, k, a_h, a_l, k, b_h, b_l, n, p_h, p_l, n, flags, nthreads);
+  const int unit_alpha = (ah == 1.0 && al == 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double th = p_h[i * n + j], tl = p_l[i * n + j];
+      if (!unit_alpha || use_beta) {
+        orc_dd_mul(ah, al, th, tl, &th, &tl);
+        if (use_beta) {
+          double uh, ul;
+          orc_dd_mul(bh, bl, Chi[i * ldc + j], Clo[i * ldc + j], &uh, &ul);
+          orc_dd_add(th, tl, uh, ul, &th, &tl);
+        }
+      }
+      Chi[i * ldc + j] = th;
+      Clo[i * ldc + j] = tl;
+    }
+  free(a_h);
+  free(a_l);
+  free(b_h);
+  free(b_l);
+  free(p_h);
+  free(p_l);
+}
+
+/* ------------------------------------------------------------------------- */
 /* ORACLE-DD: plain triple-loop FP64x2 GEMM, the paper's accuracy comparator */
 /* (§5.2 P:L3549 "a simple triple-nested loop in FP64x2 arithmetic";          */
 /* S:L399-405). C := A B, loop order i, j, p; dd_mul then dd_add.             */

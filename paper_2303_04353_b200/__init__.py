@@ -67,7 +67,42 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_packed_a_bytes", "casc_packed_b_bytes", "casc_packed_a_block_bytes",
             "casc_packed_b_block_bytes", "casc_pack_a", "casc_pack_b", "casc_gemm_packed",
             "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count",
-            "casc_gemm_fp64x2_simple", "casc_slice_product"]
+            "casc_gemm_fp64x2_simple", "casc_slice_product", "casc_gemm_fp64x2_ex"]
+
+_sig("casc_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
+                             ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
+                             ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _sz, _vp])
+CASC_OP_N, CASC_OP_T = 0, 1
+
+
+def casc_gemm_fp64x2_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo,
+                        flags=None, workspace=None, stream=None):
+    """C := alpha op(A) op(B) + beta C (FP64x2; NEXT-4).  transa/transb in
+    {'N', 'T', 0, 1}; alpha, beta are (hi, lo) pairs or floats.  C_hi / C_lo
+    (m x n) are updated in place; returns (C_hi, C_lo, flags)."""
+    ta = 1 if transa in ("T", "t", 1, True) else 0
+    tb = 1 if transb in ("T", "t", 1, True) else 0
+    ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
+    bh, bl = (beta, 0.0) if isinstance(beta, (int, float)) else beta
+    m, n = C_hi.shape
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    no_product = A_hi is None
+    if not no_product:
+        lda = _ld_pair(A_hi, A_lo, "A")
+        ldb = _ld_pair(B_hi, B_lo, "B")
+        k = A_hi.shape[0] if ta else A_hi.shape[1]
+    else:
+        lda = ldb = 1
+        k = 0
+    if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (m, n)):
+        raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
+    _check(_lib.casc_gemm_fp64x2_ex(ta, tb, m, n, k, float(ah), float(al), _ptr(A_hi),
+                                    _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo), ldb, float(bh),
+                                    float(bl), _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
+                                    _ptr(workspace), 0 if workspace is None else workspace.numel(),
+                                    _stream(stream)),
+           "casc_gemm_fp64x2_ex")
+    return C_hi, C_lo, flags
 
 
 class CascError(RuntimeError):

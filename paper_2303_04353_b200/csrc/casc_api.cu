@@ -10,10 +10,13 @@
 #include "casc_layout.cuh"
 
 namespace casc {
+cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
+                           double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
+                           cudaStream_t st);
 cudaError_t launch_split_a(const double*, const double*, int64_t, int64_t, int64_t, Widths, void*,
-                           cudaStream_t);
+                           cudaStream_t, bool trans = false);
 cudaError_t launch_split_b(const double*, const double*, int64_t, int64_t, int64_t, Widths, void*,
-                           cudaStream_t);
+                           cudaStream_t, bool trans = false);
 cudaError_t launch_unpack_a(const void*, int64_t, int64_t, Widths, double*, int32_t*,
                             cudaStream_t);
 cudaError_t launch_unpack_b(const void*, int64_t, int64_t, Widths, double*, int32_t*,
@@ -84,11 +87,22 @@ int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
 
+struct AlphaBeta {
+  int ab = 0;  // 0 none, 1 alpha, 2 alpha and beta
+  double ah = 1.0, al = 0.0, bh = 0.0, bl = 0.0;
+};
+
 int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb,
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
-                     cudaStream_t st, int st_begin, int st_end, double* dbg) {
+                     cudaStream_t st, int st_begin, int st_end, double* dbg,
+                     const AlphaBeta& abv = AlphaBeta()) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
+  a.ab = abv.ab;
+  a.alpha_hi = abv.ah;
+  a.alpha_lo = abv.al;
+  a.beta_hi = abv.bh;
+  a.beta_lo = abv.bl;
   a.pa = static_cast<const uint8_t*>(pa);
   a.pb = static_cast<const uint8_t*>(pb);
   a.a_blk = casc::a_block_bytes(k);
@@ -381,6 +395,79 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, const d
     r = CASC_ERR_CUDA;
   cudaFreeAsync(pa, st);
   cudaFreeAsync(pb, st);
+  if (r == CASC_OK) g_launches = 3;
+  return r;
+}
+
+// ---------------------------------------------------------------- BLAS-style (NEXT-4)
+int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                        double alpha_hi, double alpha_lo, const double* A_hi, const double* A_lo,
+                        int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                        double beta_hi, double beta_lo, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* workspace, size_t workspace_bytes,
+                        casc_stream_t stream) {
+  g_launches = 0;
+  if ((transa != CASC_OP_N && transa != CASC_OP_T) || (transb != CASC_OP_N && transb != CASC_OP_T))
+    return CASC_ERR_INVALID;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  // stored shapes: op(A) is m x k (A stored k x m if transposed), op(B) is k x n
+  const int64_t ar = transa ? k : m, ac = transa ? m : k;
+  const int64_t br = transb ? n : k, bc = transb ? k : n;
+  const bool no_product = (k == 0) || (alpha_hi == 0.0 && alpha_lo == 0.0);
+  int r;
+  if (!no_product) {
+    if ((r = check_mat(A_hi, ar, ac, lda)) || (r = check_mat(A_lo, ar, ac, lda))) return r;
+    if ((r = check_mat(B_hi, br, bc, ldb)) || (r = check_mat(B_lo, br, bc, ldb))) return r;
+  }
+  if ((r = check_mat(C_hi, m, n, ldc)) || (r = check_mat(C_lo, m, n, ldc))) return r;
+  if (!no_product) {
+    const size_t ea = extent(ar, ac, lda), eb = extent(br, bc, ldb), ec = extent(m, n, ldc);
+    const void* ins[4] = {A_hi, A_lo, B_hi, B_lo};
+    const size_t ine[4] = {ea, ea, eb, eb};
+    void* outs[3] = {C_hi, C_lo, flags};
+    const size_t oute[3] = {ec, ec, flags ? (size_t)(m * n) : 0};
+    for (int o = 0; o < 3; ++o)
+      for (int i = 0; i < 4; ++i)
+        if (ranges_overlap(outs[o], oute[o], ins[i], ine[i])) return CASC_ERR_INVALID;
+  }
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  cudaStream_t st = S(stream);
+  const bool use_beta = !(beta_hi == 0.0 && beta_lo == 0.0);
+  if (no_product) {  // C := beta C (BLAS: A and B are not referenced)
+    cudaError_t e = casc::launch_scale_c(m, n, beta_hi, beta_lo, use_beta, C_hi, C_lo, ldc, flags,
+                                         sms, st);
+    if (e == cudaSuccess) g_launches = 1;
+    return cuda_status(e);
+  }
+  const size_t need = casc_workspace_bytes(m, n, k);
+  void* ws = workspace;
+  bool owned = false;
+  if (!ws) {
+    if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+    owned = true;
+  } else if (workspace_bytes < need) {
+    return CASC_ERR_INVALID;
+  }
+  uint8_t* pa = static_cast<uint8_t*>(ws);
+  uint8_t* pb = pa + (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
+  const casc::Widths w = widths_for(k);
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, st, transa == CASC_OP_T);
+  if (e == cudaSuccess)
+    e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, st, transb == CASC_OP_T);
+  AlphaBeta abv;
+  const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
+  abv.ab = use_beta ? 2 : (unit_alpha ? 0 : 1);
+  abv.ah = alpha_hi;
+  abv.al = alpha_lo;
+  abv.bh = beta_hi;
+  abv.bl = beta_lo;
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  r = (e == cudaSuccess) ? gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
+                                            nst, nullptr, abv)
+                         : CASC_ERR_CUDA;
+  if (owned) cudaFreeAsync(ws, st);
   if (r == CASC_OK) g_launches = 3;
   return r;
 }

@@ -1,0 +1,47 @@
+// casc_blas.cu — BLAS-style generality around the cascaded GEMM:
+// the degenerate updates of C := alpha op(A) op(B) + beta C that need no
+// product (k == 0 or alpha == 0): C := beta (x) C in FP64x2, flags := 0.
+// The general case runs in the fused kernel (alpha/beta applied at each tile's
+// last panel, casc_gemm.cu) after transposed splits (casc_split.cu).
+#include <cuda_runtime.h>
+
+#include "casc_dd.cuh"
+#include "casc_layout.cuh"
+
+namespace casc {
+
+__global__ void __launch_bounds__(256) scale_c_kernel(int64_t m, int64_t n, double bh, double bl,
+                                                      int use_beta, double* __restrict__ C_hi,
+                                                      double* __restrict__ C_lo, int64_t ldc,
+                                                      uint8_t* __restrict__ flags) {
+  const int64_t mn = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n, j = idx - (idx / n) * n;
+    double* ch = C_hi + i * ldc + j;
+    double* cl = C_lo + i * ldc + j;
+    if (use_beta) {
+      double rh, rl;
+      dd_mul(bh, bl, *ch, *cl, rh, rl);
+      *ch = rh;
+      *cl = rl;
+    } else {
+      *ch = 0.0;
+      *cl = 0.0;
+    }
+    if (flags) flags[idx] = 0;
+  }
+}
+
+cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
+                           double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
+                           cudaStream_t st) {
+  const int64_t mn = m * n;
+  if (mn == 0) return cudaSuccess;
+  int64_t blocks = (mn + 255) / 256;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  scale_c_kernel<<<(unsigned)blocks, 256, 0, st>>>(m, n, bh, bl, use_beta, C_hi, C_lo, ldc, flags);
+  return cudaGetLastError();
+}
+
+}  // namespace casc

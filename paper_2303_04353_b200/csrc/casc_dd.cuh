@@ -35,6 +35,27 @@ __device__ __forceinline__ void dd_add(double xh, double xl, double yh, double y
 }
 
 
+// FP64x2 product (TwoProd by FMA; same sequence as the oracle's orc_dd_mul).
+__device__ __forceinline__ void dd_mul(double xh, double xl, double yh, double yl, double& rh,
+                                       double& rl) {
+  const double p = __dmul_rn(xh, yh);
+  double e = __fma_rn(xh, yh, -p);
+  e = __dadd_rn(e, __dadd_rn(__dmul_rn(xh, yl), __dmul_rn(xl, yh)));
+  fast_two_sum(p, e, rh, rl);
+}
+
+// BLAS-style update C := alpha (x) T (+) beta (x) C_old (NEXT-4, reading R21).
+__device__ __forceinline__ void apply_alpha_beta(double& th, double& tl, double ah, double al,
+                                                 double bh, double bl, double ch, double cl,
+                                                 bool use_beta) {
+  dd_mul(ah, al, th, tl, th, tl);
+  if (use_beta) {
+    double uh, ul;
+    dd_mul(bh, bl, ch, cl, uh, ul);
+    dd_add(th, tl, uh, ul, th, tl);
+  }
+}
+
 // fl_casc of one element (reading R9), bins in the
 // kernel's pre-aligned scales: T = TwoSum(2^-2c0 bin2', 2^-D2 bin36);
 // T = T (+) 2^-c0 bin1; T = T (+) bin0; T *= 2^escale.

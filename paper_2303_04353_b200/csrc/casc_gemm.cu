@@ -71,7 +71,8 @@ __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, 
 }
 
 // DBG: debug export of one panel's bins instead of the combine (casc_debug_bins)
-template <bool DBG>
+// AB:  BLAS update C := alpha AB + beta C at each tile's last panel (NEXT-4)
+template <bool DBG, bool AB>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -284,6 +285,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
                 const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
                 const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
                 if (row < p.m && col < p.n) {
+                  if (AB && p.ab)
+                    apply_alpha_beta(th, tl, p.alpha_hi, p.alpha_lo, p.beta_hi, p.beta_lo,
+                                     p.ab == 2 ? p.C_hi[row * p.ldc + col] : 0.0,
+                                     p.ab == 2 ? p.C_lo[row * p.ldc + col] : 0.0, p.ab == 2);
                   p.C_hi[row * p.ldc + col] = th;
                   p.C_lo[row * p.ldc + col] = tl;
                 }
@@ -325,35 +330,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   }
 }
 
-cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
+template <bool DBG, bool AB>
+static cudaError_t launch_variant(GemmArgs& a, int grid, bool coop, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<false>,
+    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)GEMM_SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(casc_gemm_kernel<true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  if (coop) {  // co-residency of all CTAs is required by the wave barrier
+    void* args[] = {&a};
+    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<DBG, AB>, dim3(grid),
+                                       dim3(GEMM_THREADS), args, GEMM_SMEM, st);
+  }
+  casc_gemm_kernel<DBG, AB><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   GemmArgs a = a_in;
   const int ntiles = a.mblocks * a.nblocks;
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
   static int wave_sync = -1;
   if (wave_sync < 0) {
-    // default on: 6x less HBM traffic for the fused kernel at ~0.2% time cost
+    // default on: 10x less HBM traffic for the fused kernel at ~0.2% time cost
     // (profiles/r01c); CASC_WAVE_SYNC=0 turns it off
     const char* s = getenv("CASC_WAVE_SYNC");
     wave_sync = (s && s[0] == '0') ? 0 : 1;
   }
   a.wave_counter = nullptr;
-  if (a.dbg) {
-    casc_gemm_kernel<true><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
-    return cudaGetLastError();
-  }
-  if (wave_sync && ntiles > grid) {
+  if (a.dbg) return launch_variant<true, false>(a, grid, false, st);
+  const bool coop = wave_sync && ntiles > grid;
+  if (coop) {
     static unsigned int* counters[64] = {nullptr};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -362,13 +373,9 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
     a.wave_counter = counters[dev];
     cudaError_t e = cudaMemsetAsync(a.wave_counter, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
-    // co-residency of all CTAs is required by the wave barrier: cooperative launch
-    void* args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<false>, dim3(grid),
-                                       dim3(GEMM_THREADS), args, GEMM_SMEM, st);
   }
-  casc_gemm_kernel<false><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
-  return cudaGetLastError();
+  return a.ab ? launch_variant<false, true>(a, grid, coop, st)
+              : launch_variant<false, false>(a, grid, coop, st);
 }
 
 }  // namespace casc

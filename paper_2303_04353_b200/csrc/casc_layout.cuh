@@ -81,6 +81,9 @@ struct GemmArgs {
   uint8_t* flags;  // m x n (ld n) or null
   double* dbg;     // debug: bins of the single panel, 4 x m x n (canonical scales)
   unsigned int* wave_counter;  // zeroed per launch; producers meet here at each tile wave
+  // NEXT-4 BLAS update at the tile's last panel: C := alpha (x) AB (+) beta (x) C
+  int ab;        // 0: plain C := AB; 1: apply alpha; 2: apply alpha and beta (reads C)
+  double alpha_hi, alpha_lo, beta_hi, beta_lo;
   double un_b2;    // 2^(c1-c0): bin2' -> bin2 for the debug export
 };
 

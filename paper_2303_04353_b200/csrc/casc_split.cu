@@ -82,6 +82,8 @@ __device__ __forceinline__ int group_exponent(double mx, int g, int c, int kq) {
   return sexp[g];
 }
 
+// TRANS: A is given transposed (stored k x m, element (i, p) at A[p * lda + i]; BLAS op 'T')
+template <bool TRANS>
 __global__ void __launch_bounds__(256) split_a_kernel(
     const double* __restrict__ Ahi, const double* __restrict__ Alo, int64_t lda, int64_t m,
     int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
@@ -100,8 +102,9 @@ __global__ void __launch_bounds__(256) split_a_kernel(
   for (int it = 0; it < 8; ++it) {
     const int64_t kk = k0 + 4 * (kq + 8 * it) + c;
     const bool ok = (row < m) && (kk < k);
-    h[it] = ok ? __ldg(Ahi + row * lda + kk) : 0.0;
-    l[it] = ok ? __ldg(Alo + row * lda + kk) : 0.0;
+    const int64_t off = TRANS ? kk * lda + row : row * lda + kk;
+    h[it] = ok ? __ldg(Ahi + off) : 0.0;
+    l[it] = ok ? __ldg(Alo + off) : 0.0;
     mx = fmax(mx, fabs(h[it]));
   }
   const int e = group_exponent(mx, g, c, kq);
@@ -130,6 +133,8 @@ __global__ void __launch_bounds__(256) split_a_kernel(
   }
 }
 
+// TRANS: B is given transposed (stored n x k, element (p, j) at B[j * ldb + p])
+template <bool TRANS>
 __global__ void __launch_bounds__(256) split_b_kernel(
     const double* __restrict__ Bhi, const double* __restrict__ Blo, int64_t ldb, int64_t n,
     int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
@@ -148,8 +153,9 @@ __global__ void __launch_bounds__(256) split_b_kernel(
   for (int it = 0; it < 8; ++it) {
     const int64_t kk = k0 + 4 * (kq + 8 * it) + c;
     const bool ok = (col < n) && (kk < k);
-    h[it] = ok ? __ldg(Bhi + kk * ldb + col) : 0.0;
-    l[it] = ok ? __ldg(Blo + kk * ldb + col) : 0.0;
+    const int64_t off = TRANS ? col * ldb + kk : kk * ldb + col;
+    h[it] = ok ? __ldg(Bhi + off) : 0.0;
+    l[it] = ok ? __ldg(Blo + off) : 0.0;
     mx = fmax(mx, fabs(h[it]));
   }
   const int f = group_exponent(mx, g, c, kq);
@@ -241,24 +247,26 @@ __global__ void unpack_b_kernel(const uint8_t* __restrict__ packed, int64_t k, i
 
 // ------------------------------------------------------------ launchers
 cudaError_t launch_split_a(const double* Ahi, const double* Alo, int64_t lda, int64_t m,
-                           int64_t k, Widths w, void* packed, cudaStream_t st) {
+                           int64_t k, Widths w, void* packed, cudaStream_t st, bool trans) {
   const int64_t mpad = (m + TM - 1) / TM * TM;
   const int64_t P = panels_of(k);
   if (mpad == 0 || P == 0) return cudaSuccess;
   dim3 grid((unsigned)(mpad / 8), (unsigned)P);
-  split_a_kernel<<<grid, 256, 0, st>>>(Ahi, Alo, lda, m, k, make_consts(w),
+  auto kern = trans ? split_a_kernel<true> : split_a_kernel<false>;
+  kern<<<grid, 256, 0, st>>>(Ahi, Alo, lda, m, k, make_consts(w),
                                        static_cast<uint8_t*>(packed), a_block_bytes(k),
                                        a_exp_offset(k), kpad_of(k) / 4);
   return cudaGetLastError();
 }
 
 cudaError_t launch_split_b(const double* Bhi, const double* Blo, int64_t ldb, int64_t k,
-                           int64_t n, Widths w, void* packed, cudaStream_t st) {
+                           int64_t n, Widths w, void* packed, cudaStream_t st, bool trans) {
   const int64_t npad = (n + TN - 1) / TN * TN;
   const int64_t P = panels_of(k);
   if (npad == 0 || P == 0) return cudaSuccess;
   dim3 grid((unsigned)(npad / 8), (unsigned)P);
-  split_b_kernel<<<grid, 256, 0, st>>>(Bhi, Blo, ldb, n, k, make_consts(w),
+  auto kern = trans ? split_b_kernel<true> : split_b_kernel<false>;
+  kern<<<grid, 256, 0, st>>>(Bhi, Blo, ldb, n, k, make_consts(w),
                                        static_cast<uint8_t*>(packed), b_block_bytes(k),
                                        b_exp_offset(k), kpad_of(k) / 4);
   return cudaGetLastError();

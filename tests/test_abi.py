@@ -55,7 +55,15 @@ def test_library_is_sm100a_only(lib):
                           text=True).stdout
     assert "DMMA.8x8x4" in sass      # FP64 tensor-core MMA in the fused kernel
     assert "UBLKCP" in sass          # TMA bulk copies
-    assert "LDL" not in sass and "STL" not in sass  # no register spills
+    assert "LDTM" in sass and "STTM" in sass  # tensor-memory C accumulator
+    # the product kernel (no debug export, no alpha/beta) and the split kernels
+    # are spill-free
+    funcs = re.split(r"\n\s*Function : ", sass)
+    main = [f for f in funcs if f.startswith("_ZN4casc16casc_gemm_kernelILb0ELb0E")]
+    splits = [f for f in funcs if "split_a_kernel" in f[:60] or "split_b_kernel" in f[:60]]
+    assert len(main) == 1 and len(splits) == 4
+    for f in main + splits:
+        assert "LDL" not in f and "STL" not in f
 
 
 def test_widths_and_sizes(lib):

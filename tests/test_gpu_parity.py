@@ -407,3 +407,62 @@ def test_simple_path_agrees_with_fused(casc, orc, cfg, m, n, k):
         assert np.all(diff <= 2 * bound)
     else:
         assert s_fl.all()
+
+
+# ------------------------------------------------------------------ BLAS-style (NEXT-4)
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_blas_ex_transposes_bitwise(casc, ta, tb):
+    """op(X) = X^T changes only how the split kernels read: the result is bitwise
+    the non-transposed product (alpha = 1, beta = 0)."""
+    import torch
+    m, n, k = 70, 90, 300
+    d = I.make_config(1, m=m, n=n, k=k, seed=23)
+    ref = run(casc, d)
+    A = (d["A_hi"].T.copy(), d["A_lo"].T.copy()) if ta == "T" else (d["A_hi"], d["A_lo"])
+    B = (d["B_hi"].T.copy(), d["B_lo"].T.copy()) if tb == "T" else (d["B_hi"], d["B_lo"])
+    C_hi = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")  # beta=0: unread
+    C_lo = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    fl = torch.empty((m, n), dtype=torch.uint8, device="cuda")
+    casc.casc_gemm_fp64x2_ex(ta, tb, 1.0, T(A[0]), T(A[1]), T(B[0]), T(B[1]), 0.0, C_hi, C_lo,
+                             flags=fl)
+    assert same_values(N(C_hi), ref[0]) and same_values(N(C_lo), ref[1])
+    assert np.array_equal(N(fl), ref[2])
+
+
+def test_blas_ex_alpha_beta(casc, orc):
+    """C := alpha P + beta C: bitwise equal to the oracle's FP64x2 update applied
+    to the GPU's own product P (reading R21), and within the bound of the exact
+    alpha A B + beta C; alpha = 0 / k = 0 give beta C without touching A, B."""
+    import torch
+    m, n, k = 65, 129, 513
+    d = I.make_config(2, m=m, n=n, k=k, seed=29)
+    P_hi, P_lo, P_fl = run(casc, d)
+    rng = np.random.default_rng(7)
+    C0 = rng.uniform(-1, 1, (m, n))
+    al, be = (1.0 / 3.0, 2.0 ** -56), (-0.7, 2.0 ** -60)
+    C_hi, C_lo = T(C0), T(np.zeros((m, n)))
+    casc.casc_gemm_fp64x2_ex("N", "N", al, T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                             T(d["B_lo"]), be, C_hi, C_lo)
+    g_hi, g_lo = N(C_hi), N(C_lo)
+    for i in range(0, m, 7):
+        for j in range(0, n, 11):
+            th, tl = orc.dd_mul(al[0], al[1], P_hi[i, j], P_lo[i, j])
+            uh, ul = orc.dd_mul(be[0], be[1], C0[i, j], 0.0)
+            th, tl = orc.dd_add(th, tl, uh, ul)
+            assert (g_hi[i, j], g_lo[i, j]) == (th, tl)
+    # vs the oracle's full BLAS update (bin 3-6 order differs: bound, not bits)
+    o_hi, o_lo, o_fl = orc.casc_gemm_ex("N", "N", al, d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"],
+                                        be, C0, np.zeros((m, n)))
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel())
+    bound = (abs(al[0]) * 2 * orc.north_star_bound(k, r["absab"])).reshape(m, n) \
+        + 2.0 ** -100 * (np.abs(g_hi))
+    assert np.all(np.abs((g_hi - o_hi) + (g_lo - o_lo)) <= bound)
+    # alpha == 0 and k == 0: C := beta C, flags := 0
+    C_hi, C_lo = T(C0), T(np.zeros((m, n)))
+    fl = torch.full((m, n), 5, dtype=torch.uint8, device="cuda")
+    casc.casc_gemm_fp64x2_ex("N", "N", 0.0, None, None, None, None, be, C_hi, C_lo, flags=fl)
+    for i in range(0, m, 9):
+        for j in range(0, n, 13):
+            assert (N(C_hi)[i, j], N(C_lo)[i, j]) == orc.dd_mul(be[0], be[1], C0[i, j], 0.0)
+    assert N(fl).sum() == 0

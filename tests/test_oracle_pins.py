@@ -398,6 +398,47 @@ def test_cancellation_variants(orc):
             assert flags.all()
 
 
+def test_blas_ex_oracle(orc):
+    """NEXT-4 oracle: alpha = 1, beta = 0 is the plain product (bitwise); op(X)
+    = X^T is pure data movement (bitwise); alpha = 2^p scales exactly; general
+    alpha, beta within the FP64x2 update bound of the exact alpha AB + beta C."""
+    d = I.make_config(1, m=9, n=7, k=300, seed=17)
+    P = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    C0 = (np.zeros((9, 7)), np.zeros((9, 7)))
+    E = orc.casc_gemm_ex("N", "N", (1.0, 0.0), d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"],
+                         (0.0, 0.0), *C0)
+    assert np.array_equal(E[0], P[0]) and np.array_equal(E[1], P[1]) and np.array_equal(E[2], P[2])
+    T = orc.casc_gemm_ex("T", "T", (1.0, 0.0), d["A_hi"].T.copy(), d["A_lo"].T.copy(),
+                         d["B_hi"].T.copy(), d["B_lo"].T.copy(), (0.0, 0.0), *C0)
+    assert np.array_equal(T[0], P[0]) and np.array_equal(T[1], P[1])
+    S = orc.casc_gemm_ex("N", "N", (0.25, 0.0), d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"],
+                         (0.0, 0.0), *C0)
+    assert np.array_equal(S[0], P[0] * 0.25) and np.array_equal(S[1], P[1] * 0.25)
+    rng = np.random.default_rng(4)
+    Ch, Cl = rng.uniform(-1, 1, (9, 7)), np.zeros((9, 7))
+    al, be = (1.0 / 3.0, 1.0 / 3.0 * 2.0 ** -54), (-0.7, 2.0 ** -60)
+    G = orc.casc_gemm_ex("N", "N", al, d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], be, Ch, Cl)
+    for i in range(9):
+        for j in range(7):
+            ab = sum((fr(d["A_hi"][i, p]) + fr(d["A_lo"][i, p]))
+                     * (fr(d["B_hi"][p, j]) + fr(d["B_lo"][p, j])) for p in range(300))
+            absab = sum(abs(fr(d["A_hi"][i, p]) + fr(d["A_lo"][i, p]))
+                        * abs(fr(d["B_hi"][p, j]) + fr(d["B_lo"][p, j])) for p in range(300))
+            A_ = fr(al[0]) + fr(al[1])
+            B_ = fr(be[0]) + fr(be[1])
+            ex = A_ * ab + B_ * fr(Ch[i, j])
+            bound = abs(A_) * 4 * 300 * F(2) ** -104 * absab + F(2) ** -102 * (
+                abs(A_ * ab) + abs(B_ * fr(Ch[i, j])))
+            assert abs(fr(G[0][i, j]) + fr(G[1][i, j]) - ex) <= bound
+    Z = orc.casc_gemm_ex("N", "N", (0.0, 0.0), d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], be,
+                         Ch, Cl)  # alpha = 0: C := beta C
+    for i in range(9):
+        for j in range(7):
+            assert abs(fr(Z[0][i, j]) + fr(Z[1][i, j]) - (fr(be[0]) + fr(be[1])) * fr(Ch[i, j])) \
+                <= F(2) ** -104 * abs(fr(Ch[i, j]))
+    assert Z[2].sum() == 0
+
+
 def test_exact_accumulator_vs_fractions(orc):
     """ORACLE-EXACT superaccumulator equals Fraction sums, over
     wide exponent ranges and with exact cancellation."""
@@ -441,3 +482,9 @@ def test_inputs_normalised_and_blockwise():
     assert np.array_equal(blk["A_hi"], d["A_hi"][16:40])
     assert np.array_equal(blk["A_lo"], d["A_lo"][16:40])
     assert np.abs(d["A_hi"]).max() <= 1.0
+    for cfg in (1, 2, 3, 4):  # column slabs of B (the multi-GPU slab generation)
+        kw = dict(m=12, n=200, k=300)
+        f = I.make_config(cfg, **kw)
+        s = I.make_config(cfg, cols=slice(64, 150), **kw)
+        assert np.array_equal(f["B_hi"][:, 64:150], s["B_hi"])
+        assert np.array_equal(f["B_lo"][:, 64:150], s["B_lo"])
