@@ -289,7 +289,7 @@ def main():
             for s in range(args.steps):
                 ev[s][0].record(stream)
                 step(ev[s][1:])
-                launches += 3  # split_a, split_b, casc_gemm (our kernels; NCCL not counted)
+                launches += op.launches  # split_a, split_b, casc_gemm (+ reduce in split mode)
             t_end.record(stream)
             barrier()
         total_ms = t_start.elapsed_time(t_end)

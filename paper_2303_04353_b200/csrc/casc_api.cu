@@ -4,12 +4,17 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/casc.h"
 #include "casc_layout.cuh"
 
 namespace casc {
+cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
+                                const double* t_lo, const uint8_t* fbuf, double* C_hi,
+                                double* C_lo, int64_t ldc, uint8_t* flags, int ab, double ah,
+                                double al, double bh, double bl, int num_sms, cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -63,6 +68,14 @@ int device_check(int* sms) {
       return CASC_ERR_CUDA;
     d.ok = (major == 10 && minor == 0);
     d.checked = 1;
+    // Stream-ordered temporaries (split-mode sums, debug exports) come from the
+    // default pool: keep freed blocks cached instead of unmapping them at every
+    // synchronisation (measured 0.5 ms per call otherwise).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
   }
   if (sms) *sms = d.sms;
   return d.ok ? CASC_OK : CASC_ERR_UNSUPPORTED;
@@ -92,10 +105,40 @@ struct AlphaBeta {
   double ah = 1.0, al = 0.0, bh = 0.0, bl = 0.0;
 };
 
+// Split mode for small problems: when one work item per 64x64 tile leaves the
+// last wave of the 148 SMs badly filled, use one item per (tile, k panel) and
+// reduce the FP64x2 panel sums in panel order afterwards (bitwise the same
+// result).  Returns P (> 1) or 0.
+int split_plan(int64_t m, int64_t n, int64_t k, int sms) {
+  const int64_t P = casc::panels_of(k);
+  if (P < 2 || sms <= 0) return 0;
+  const char* env = getenv("CASC_SPLIT_MODE");  // "0": never (tests compare both modes)
+  if (env && env[0] == '0') return 0;
+  const int64_t tiles = ((m + casc::TM - 1) / casc::TM) * ((n + casc::TN - 1) / casc::TN);
+  if (tiles >= 2 * (int64_t)sms) return 0;  // enough waves already
+  const int64_t units = tiles * P;
+  const double eff_t = (double)tiles / (double)(((tiles + sms - 1) / sms) * sms);
+  const double eff_s = (double)units / (double)(((units + sms - 1) / sms) * sms);
+  if (eff_s < eff_t + 0.04) return 0;
+  if ((double)P * m * n * 17.0 > (double)(1ull << 31)) return 0;
+  return (int)P;
+}
+size_t split_bytes(int64_t m, int64_t n, int P) { return P ? (size_t)P * m * n * 17 : 0; }
+
+int current_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;  // B200
+  }
+  return sms;
+}
+
 int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb,
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
-                     const AlphaBeta& abv = AlphaBeta()) {
+                     const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -123,8 +166,28 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.flags = flags;
   a.dbg = dbg;
   a.un_b2 = std::ldexp(1.0, w.c1 - w.c0);
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  const int P = (!dbg && st_begin == 0 && st_end == nst) ? split_plan(m, n, k, sms) : 0;
+  if (!P) {
+    cudaError_t e = casc::launch_gemm(a, sms, st);
+    if (e == cudaSuccess) ++g_launches;
+    return cuda_status(e);
+  }
+  void* buf = split_ws;
+  if (!buf && cudaMallocAsync(&buf, split_bytes(m, n, P), st) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  const int64_t mn = m * n;
+  a.split_p = P;
+  a.t_hi = static_cast<double*>(buf);
+  a.t_lo = a.t_hi + (int64_t)P * mn;
+  a.fbuf = reinterpret_cast<uint8_t*>(a.t_lo + (int64_t)P * mn);
+  a.ab = 0;  // alpha / beta go to the reduction
   cudaError_t e = casc::launch_gemm(a, sms, st);
-  if (e == cudaSuccess) ++g_launches;
+  if (e == cudaSuccess)
+    e = casc::launch_split_reduce(P, m, n, a.t_hi, a.t_lo, a.fbuf, C_hi, C_lo, ldc, flags, abv.ab,
+                                  abv.ah, abv.al, abv.bh, abv.bl, sms, st);
+  if (!split_ws) cudaFreeAsync(buf, st);
+  if (e == cudaSuccess) g_launches += 2;
   return cuda_status(e);
 }
 
@@ -170,7 +233,9 @@ size_t casc_packed_b_bytes(int64_t k, int64_t n) {
 }
 size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   const size_t a = (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
-  return a + casc_packed_b_bytes(k, n);
+  const size_t b = (casc_packed_b_bytes(k, n) + 255) / 256 * 256;
+  const int P = (m > 0 && n > 0 && k > 0) ? split_plan(m, n, k, current_sms()) : 0;
+  return a + b + split_bytes(m, n, P);
 }
 
 int casc_last_launch_count(void) { return g_launches; }
@@ -269,8 +334,11 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, S(stream));
   if (e != cudaSuccess) return CASC_ERR_CUDA;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
-  r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr);
-  g_launches = (r == CASC_OK) ? 3 : 0;
+  uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
+  g_launches = 0;
+  r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr,
+                       AlphaBeta(), ps);
+  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;  // + the two split kernels
   return r;
 }
 
@@ -464,11 +532,13 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
   abv.bh = beta_hi;
   abv.bl = beta_lo;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
+  g_launches = 0;
   r = (e == cudaSuccess) ? gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
-                                            nst, nullptr, abv)
+                                            nst, nullptr, abv, ps)
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
-  if (r == CASC_OK) g_launches = 3;
+  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
   return r;
 }
 

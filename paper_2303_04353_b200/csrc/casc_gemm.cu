@@ -70,6 +70,27 @@ __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, 
   nb = r / gsize;
 }
 
+// Work item -> tile and stage range.  Normal mode: one item per 64x64 tile over
+// all of its panels.  Split mode (small problems, p.split_p = P panels): one
+// item per (tile, panel); its FP64x2 panel sum T_q goes to t_hi/t_lo[q] and a
+// reduce kernel adds T_0 (+) T_1 (+) ... in panel order (bitwise the same
+// sequence as the normal mode's C accumulation).
+__device__ __forceinline__ void item_coords(const GemmArgs& p, int item, int& mb, int& nb,
+                                            int& s0, int& s1, int& q0) {
+  if (p.split_p) {
+    const int tile = item / p.split_p;
+    q0 = item - tile * p.split_p;
+    tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
+    s0 = q0 * STAGES_PER_PANEL;
+    s1 = min(s0 + STAGES_PER_PANEL, p.st_end);
+  } else {
+    tile_coords(item, p.mblocks, p.nblocks, mb, nb);
+    s0 = p.st_begin;
+    s1 = p.st_end;
+    q0 = 0;
+  }
+}
+
 // DBG: debug export of one panel's bins instead of the combine (casc_debug_bins)
 // AB:  BLAS update C := alpha AB + beta C at each tile's last panel (NEXT-4)
 template <bool DBG, bool AB>
@@ -93,7 +114,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   }
   __syncthreads();
 
-  const int ntiles = p.mblocks * p.nblocks;
+  const int ntiles = p.mblocks * p.nblocks * (p.split_p ? p.split_p : 1);  // work items
 
   if (warp < 4) {
     // ===================== TMA producer (warpgroup 0) =====================
@@ -121,13 +142,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           }
         }
         if (tile >= ntiles) continue;
-        int mb, nb;
-        tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
-        const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)p.st_begin * A_STAGE * 8;
-        const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)p.st_begin * B_STAGE * 8;
-        for (int st = p.st_begin; st < p.st_end; ++st, ++it) {
+        int mb, nb, s0, s1, q0;
+        item_coords(p, tile, mb, nb, s0, s1, q0);
+        const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)s0 * A_STAGE * 8;
+        const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)s0 * B_STAGE * 8;
+        for (int st = s0; st < s1; ++st, ++it) {
           const uint32_t slot = it % NSTAGE, ph = (it / NSTAGE) & 1;
-          const bool pstart = (st == p.st_begin) || (st % STAGES_PER_PANEL) == 0;
+          const bool pstart = (st == s0) || (st % STAGES_PER_PANEL) == 0;
           mbar_wait(&empty[slot], ph ^ 1);
           mbar_arrive_expect_tx(&full[slot],
                                 (A_STAGE + B_STAGE) * 8 + (pstart ? (TM + TN) * 4 : 0));
@@ -173,11 +194,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   double acc[4][4][2][2];  // [bin][msub][nsub][pair]
   uint32_t it = 0, pc = 0;  // stage counter (smem ring), panel counter (exponent ring)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int mb, nb;
-    tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
+    int mb, nb, s0, s1, q0;
+    item_coords(p, tile, mb, nb, s0, s1, q0);
+    // destination: C, or the panel-sum buffer T_q in split mode
+    double* dst_hi = p.split_p ? p.t_hi + (int64_t)q0 * p.m * p.n : p.C_hi;
+    double* dst_lo = p.split_p ? p.t_lo + (int64_t)q0 * p.m * p.n : p.C_lo;
+    const int64_t ldd = p.split_p ? p.n : p.ldc;
+    uint8_t* dst_fl = p.split_p ? p.fbuf + (int64_t)q0 * p.m * p.n : p.flags;
     uint32_t flagbits = 0;
-    for (int st = p.st_begin; st < p.st_end; ++st, ++it) {
-      if (st == p.st_begin || (st % STAGES_PER_PANEL) == 0) {
+    for (int st = s0; st < s1; ++st, ++it) {
+      if (st == s0 || (st % STAGES_PER_PANEL) == 0) {
 #pragma unroll
         for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -221,17 +247,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
 
-      const bool panel_end = ((st + 1) % STAGES_PER_PANEL) == 0 || st + 1 == p.st_end;
+      const bool panel_end = ((st + 1) % STAGES_PER_PANEL) == 0 || st + 1 == s1;
       if (!panel_end) continue;
       // this panel's scale exponents landed in smem with its first stage
       const int32_t* pex = sexp + (pc % EXP_RING) * (TM + TN);
       ++pc;
 #ifdef CASC_EXPERIMENT_NO_COMBINE  // timing experiment only: combine the last panel alone
-      if (st + 1 != p.st_end) continue;
+      if (st + 1 != s1) continue;
 #endif
       // ------------------------------ phase 3: combine this panel
-      const bool first = (st + 1 - p.st_begin) <= STAGES_PER_PANEL;  // first panel of the tile
-      const bool last = (st + 1 == p.st_end);
+      const bool first = (st + 1 - s0) <= STAGES_PER_PANEL;  // first panel of the item
+      const bool last = (st + 1 == s1);
 #pragma unroll
       for (int ms = 0; ms < 4; ++ms)
 #pragma unroll
@@ -289,8 +315,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
                     apply_alpha_beta(th, tl, p.alpha_hi, p.alpha_lo, p.beta_hi, p.beta_lo,
                                      p.ab == 2 ? p.C_hi[row * p.ldc + col] : 0.0,
                                      p.ab == 2 ? p.C_lo[row * p.ldc + col] : 0.0, p.ab == 2);
-                  p.C_hi[row * p.ldc + col] = th;
-                  p.C_lo[row * p.ldc + col] = tl;
+                  dst_hi[row * ldd + col] = th;
+                  dst_lo[row * ldd + col] = tl;
                 }
               } else {
                 cv[x] = __double2loint(th);
@@ -305,7 +331,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       if (!last) tmem_wait_st();
     }
     // ------------------------------ cancellation flags of this tile
-    if (!DBG && p.flags) {
+    if (!DBG && dst_fl) {
 #pragma unroll
       for (int ms = 0; ms < 4; ++ms) {
         const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
@@ -315,7 +341,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           for (int i = 0; i < 2; ++i) {
             const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
             if (row < p.m && col < p.n)
-              p.flags[row * p.n + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
+              dst_fl[row * p.n + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
           }
       }
     }
@@ -351,7 +377,7 @@ static cudaError_t launch_variant(GemmArgs& a, int grid, bool coop, cudaStream_t
 
 cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   GemmArgs a = a_in;
-  const int ntiles = a.mblocks * a.nblocks;
+  const int ntiles = a.mblocks * a.nblocks * (a.split_p ? a.split_p : 1);  // work items
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
   static int wave_sync = -1;
@@ -363,7 +389,7 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   }
   a.wave_counter = nullptr;
   if (a.dbg) return launch_variant<true, false>(a, grid, false, st);
-  const bool coop = wave_sync && ntiles > grid;
+  const bool coop = wave_sync && ntiles > grid && !a.split_p;  // small problems: no barrier
   if (coop) {
     static unsigned int* counters[64] = {nullptr};
     int dev = 0;

@@ -84,6 +84,12 @@ struct GemmArgs {
   // NEXT-4 BLAS update at the tile's last panel: C := alpha (x) AB (+) beta (x) C
   int ab;        // 0: plain C := AB; 1: apply alpha; 2: apply alpha and beta (reads C)
   double alpha_hi, alpha_lo, beta_hi, beta_lo;
+  // split mode (small problems): P > 0 -> one work item per (tile, panel), panel
+  // sums to t_hi/t_lo [P][m][n] and flags to fbuf [P][m][n]; 0 -> off
+  int split_p;
+  double* t_hi;
+  double* t_lo;
+  uint8_t* fbuf;
   double un_b2;    // 2^(c1-c0): bin2' -> bin2 for the debug export
 };
 

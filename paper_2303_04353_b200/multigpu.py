@@ -51,13 +51,15 @@ class Ops:
     pack_b: object
     gemm_packed: object
     packed_b_block_bytes: object
+    launch_count: object = None  # launches of the last call (our kernels)
 
 
 def cuda_ops() -> Ops:
     import paper_2303_04353_b200 as casc
     return Ops(pack_a=casc.casc_pack_a, pack_b=casc.casc_pack_b,
                gemm_packed=casc.casc_gemm_packed,
-               packed_b_block_bytes=casc.casc_packed_b_block_bytes)
+               packed_b_block_bytes=casc.casc_packed_b_block_bytes,
+               launch_count=casc.casc_last_launch_count)
 
 
 class ShardedCascGemm:
@@ -87,12 +89,16 @@ class ShardedCascGemm:
         Returns this rank's (C_hi, C_lo, flags) rows.  `events`, if given, is a
         list of 4 CUDA events recorded after pack_a, pack_b, all-gather, gemm."""
         mloc = self.r1 - self.r0
+        count = getattr(self.ops, "launch_count", None) or (lambda: 0)
+        self.launches = 0
         self.packed_a = self.ops.pack_a(A_hi_rows, A_lo_rows, packed=self.packed_a)
+        self.launches += count()
         rec = (lambda i: events[i].record()) if events else (lambda i: None)
         rec(0)
         if self.c1 > self.c0:
             used = -(-(self.c1 - self.c0) // BLOCK) * self.ops.packed_b_block_bytes(self.k)
             self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])
+            self.launches += count()
         rec(1)
         if self.world > 1:
             if dist.get_backend(self.group) == "gloo":  # CPU plumbing tests
@@ -107,5 +113,6 @@ class ShardedCascGemm:
         rec(2)
         out = self.ops.gemm_packed(mloc, self.n, self.k, self.packed_a, pb, C_hi=C_hi,
                                    C_lo=C_lo, flags=flags)
+        self.launches += count()
         rec(3)
         return out

@@ -466,3 +466,34 @@ def test_blas_ex_alpha_beta(casc, orc):
         for j in range(0, n, 13):
             assert (N(C_hi)[i, j], N(C_lo)[i, j]) == orc.dd_mul(be[0], be[1], C0[i, j], 0.0)
     assert N(fl).sum() == 0
+
+
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (200, 300, 700), (64, 64, 600)])
+def test_split_mode_bitwise(casc, m, n, k):
+    """Small problems run one work item per (tile, panel) plus an ordered FP64x2
+    reduction (casc_api.cu split_plan); the result must be bitwise the
+    one-item-per-tile result (same additions in the same order)."""
+    import os
+    d = I.make_config(1, m=m, n=n, k=k, seed=31)
+    args = [T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo")]
+    split = [N(x) for x in casc.casc_gemm_fp64x2(*args)]
+    os.environ["CASC_SPLIT_MODE"] = "0"
+    try:
+        whole = [N(x) for x in casc.casc_gemm_fp64x2(*args)]
+    finally:
+        del os.environ["CASC_SPLIT_MODE"]
+    for a, b in zip(split, whole):
+        assert np.array_equal(a, b)
+    # with alpha / beta through the reduction kernel as well
+    al, be = (0.75, 2.0**-60), (1.5, 0.0)
+    C0 = np.random.default_rng(3).uniform(-1, 1, (m, n))
+    outs = []
+    for mode in ("1", "0"):
+        os.environ["CASC_SPLIT_MODE"] = mode
+        try:
+            C_hi, C_lo = T(C0), T(np.zeros((m, n)))
+            casc.casc_gemm_fp64x2_ex("N", "N", al, *args, be, C_hi, C_lo)
+            outs.append((N(C_hi), N(C_lo)))
+        finally:
+            del os.environ["CASC_SPLIT_MODE"]
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
