@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "casc_oracle.c")
+_SRC_I8 = os.path.join(_HERE, "casc_i8_oracle.c")  # NEXT-3: the INT8 cascade
 _LIB = os.path.join(_HERE, "liboracle.so")
 KC = 256
 
@@ -30,9 +31,11 @@ CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-s
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (building the checker is not using it)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    stale = not os.path.exists(_LIB) or any(
+        os.path.getmtime(_LIB) < os.path.getmtime(s) for s in (_SRC, _SRC_I8))
+    if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC_I8, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -84,6 +87,15 @@ def _setup(L):
     L.orc_exact_sum.argtypes = [_i64, _pd, _pd, _pd]
     L.orc_exact_dot.argtypes = [_i64, _pd, _pd, _pd, _pd]
     L.orc_num_threads.restype = ctypes.c_int
+    _pi8 = ctypes.POINTER(ctypes.c_int8)
+    L.orc_i8_panel.restype = ctypes.c_int
+    L.orc_i8_split_scalar.argtypes = [_d, _d, ctypes.c_int, ctypes.c_int, _pi8]
+    L.orc_i8_split_rows.argtypes = [_i64, _i64, _pd, _pd, _i64, _i64, ctypes.c_int, _pi8, _pi32]
+    L.orc_i8_panel_bins.argtypes = [_i64, _i64, _i64, ctypes.c_int, _pi8, _pi8, ctypes.c_int,
+                                    _pi64]
+    L.orc_i8_group_value.argtypes = [_pi64, ctypes.c_int, _pd, _pd]
+    L.orc_i8_casc_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64,
+                                   ctypes.c_int, _pd, _pd, _i64, _pu8, ctypes.c_int]
 
 
 def _p(a, ptr=_pd):
@@ -290,3 +302,73 @@ def cascerr_bound(k: int, absab, normx, normy, widths):
     D2 = sum(widths)
     return (np.asarray(absab) * 2.0 ** -106
             + 40.0 * k * k * 2.0 ** -(D2 + 53) * np.asarray(normx) * np.asarray(normy))
+
+
+# ---------------------------------------------------------------- NEXT-3: INT8 cascade
+# (casc_i8_oracle.c; readings R22-R26 in DESIGN.md §3)
+_pi8 = ctypes.POINTER(ctypes.c_int8)
+
+
+def i8_panel() -> int:
+    """k_C8, the INT8 cascade's panel depth (reading R22)."""
+    return lib().orc_i8_panel()
+
+
+def i8_split_scalar(hi: float, lo: float, e: int, y: int):
+    """The y balanced base-256 int8 slices of one FP64x2 value (reading R23)."""
+    d = (ctypes.c_int8 * y)()
+    lib().orc_i8_split_scalar(hi, lo, int(e), int(y), d)
+    return tuple(d)
+
+
+def i8_split_a_panel(A_hi, A_lo, y: int):
+    """Slices of an m x kp panel of A per row -> (D (y, m, kp) int8, e (m,))."""
+    A_hi, A_lo = _c64(A_hi), _c64(A_lo)
+    m, kp = A_hi.shape
+    D = np.empty((y, m, kp), dtype=np.int8)
+    e = np.empty(m, dtype=np.int32)
+    lib().orc_i8_split_rows(m, kp, _p(A_hi), _p(A_lo), kp, 1, y, _p(D, _pi8), _p(e, _pi32))
+    return D, e
+
+
+def i8_split_b_panel(B_hi, B_lo, y: int):
+    """Slices of a kp x n panel of B per column -> (D (y, n, kp) int8, f (n,))."""
+    B_hi, B_lo = _c64(B_hi), _c64(B_lo)
+    kp, n = B_hi.shape
+    D = np.empty((y, n, kp), dtype=np.int8)
+    f = np.empty(n, dtype=np.int32)
+    lib().orc_i8_split_rows(n, kp, _p(B_hi), _p(B_lo), 1, n, y, _p(D, _pi8), _p(f, _pi32))
+    return D, f
+
+
+def i8_panel_bins(DA, DB, nbins: int | None = None):
+    """Exact bins of one panel (reading R24): bin_s = sum over i + j = s of
+    DA_i DB_j^T, s < nbins (default y: the paper's triangle)."""
+    DA = np.ascontiguousarray(DA, dtype=np.int8)
+    DB = np.ascontiguousarray(DB, dtype=np.int8)
+    y, m, kp = DA.shape
+    n = DB.shape[1]
+    nb = y if nbins is None else nbins
+    bins = np.empty((nb, m, n), dtype=np.int64)
+    lib().orc_i8_panel_bins(m, n, kp, y, _p(DA, _pi8), _p(DB, _pi8), nb, _p(bins, _pi64))
+    return bins
+
+
+def i8_group_value(b):
+    """Exact FP64x2 value of up to four consecutive bins (reading R25)."""
+    b = np.ascontiguousarray(b, dtype=np.int64)
+    return _pair(lib().orc_i8_group_value, _p(b, _pi64), b.size)
+
+
+def i8_casc_gemm(A_hi, A_lo, B_hi, B_lo, y: int = 14, nthreads: int = 0):
+    """ORACLE-I8CASCADE: C := A B through y int8 slices (NEXT-3).
+    Returns (C_hi, C_lo, flags)."""
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    C_hi = np.empty((m, n))
+    C_lo = np.empty((m, n))
+    flags = np.empty((m, n), dtype=np.uint8)
+    lib().orc_i8_casc_gemm(m, n, k, _p(A_hi), _p(A_lo), k, _p(B_hi), _p(B_lo), n, int(y),
+                           _p(C_hi), _p(C_lo), n, _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags

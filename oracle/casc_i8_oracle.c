@@ -1,0 +1,184 @@
+/*
+ * casc_i8_oracle.c — CPU ORACLE for the INT8 cascade of an FP64x2 GEMM
+ * (NEXT-3; arXiv 2303.04353 §6 "FP64x2 in terms of INT8",
+ * P:L3753-3756, and "FP64 in terms of INT8").
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this library. The
+ * product path (paper_2303_04353_b200/) never imports, links or executes it and
+ * shares no code, header, table or constant generator with it.
+ *
+ * The paper only sketches this variant: the FP64x2 matrix is "converted into
+ * fixed point numbers which can be stored in integers", cascaded into
+ * "approximately 14 to 15 INT8 splits" with "about 105 to 120 INT8 multiplies"
+ * (P:L3754), i.e. the y(y+1)/2 products A_i B_j with i + j < y, and "32-bit
+ * accumulation" plays the role the 2^53 budget plays for the
+ * FP64 cascade.  Everything the paper leaves open is fixed by the readings
+ * R22-R26 in DESIGN.md §3; this file follows them step by step:
+ *
+ *   R22 panel      k_C8 = 8192: one scale exponent per (row, panel) of A and
+ *                  (column, panel) of B, e = frexp exponent of max|hi| (the
+ *                  FP64 cascade's R1), and every bin of a panel is an exact
+ *                  int32 sum (y * 8192 * 2^14 < 2^31 for y <= 15).
+ *   R23 slices     F = 6 + 8(y-1) fraction bits; X = rint(hi 2^(F-e)) +
+ *                  rint(lo 2^(F-e)) (an exact integer, each limb rounded to
+ *                  nearest-even); the slices are the balanced base-256 digits of
+ *                  X: d_(y-1) .. d_1 in [-128, 127], d_0 in [-64, 64]; value of
+ *                  slice t is d_t 2^(e - 6 - 8t).
+ *   R24 products   bin_s = sum_p sum_(i+j=s) dA_i dB_j for s = 0 .. y-1 (the
+ *                  paper's triangle of y(y+1)/2 products), exact.
+ *   R25 combine    bins four at a time, most significant group first: the
+ *                  group value V = sum_u bin_(s+u) 2^(8(nb-1-u)) is exact in
+ *                  int64; G = (RN(V), V - RN(V)) scaled by 2^(e+f-12-8(s+nb-1));
+ *                  the panel value T = DDadd over the groups, then C = DDadd(C, T)
+ *                  over panels in ascending order (FP64x2; the FP64
+ *                  cascade's per-panel T of P:L3295).
+ *   R26 detector   flag |= (|T.hi| <= kp 2^(e+f-50)): the panel's exact-integer
+ *                  product lost at least ~50 bits against its operand scale.
+ *                  The paper's test "bin 0 is zero" asks whether the
+ *                  exact leading 22 x 22-bit products cancel; balanced int8
+ *                  slices are not symmetric under negation (the digit -128 has
+ *                  no negative), so exact zeros of leading bins do not survive
+ *                  x, -x pairs and the test is taken on the panel value instead.
+ * Pins: tests/test_i8_oracle_pins.py (Fraction brute force; the all-diagonals
+ * product equals the exact product of the reconstructed slices; the north-star
+ * bound against ORACLE-EXACT; scaling neutrality; the detector cases).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define KC8 8192 /* reading R22 */
+
+/* From casc_oracle.c (same library, same translation rules). */
+void orc_two_sum(double a, double b, double* s, double* e);
+void orc_dd_add(double xh, double xl, double yh, double yl, double* rh, double* rl);
+int orc_scale_exponent(const double* hi, int64_t n, int64_t stride);
+
+int orc_i8_panel(void) { return KC8; }
+
+/* Reading R23: the y int8 slices of one FP64x2 value with scale exponent e. */
+void orc_i8_split_scalar(double hi, double lo, int e, int y, int8_t* d) {
+  const int F = 6 + 8 * (y - 1);
+  __int128 X = (__int128)rint(ldexp(hi, F - e)) + (__int128)rint(ldexp(lo, F - e));
+  for (int t = y - 1; t >= 1; --t) {
+    int8_t b = (int8_t)(uint8_t)(X & 0xff); /* low byte as a signed digit */
+    d[t] = b;
+    X = (X - b) / 256; /* exact */
+  }
+  d[0] = (int8_t)X;
+}
+
+/* Split `rows` vectors of length kp: element (r, p) at x[r*ld + p*sk].
+ * D is y x rows x kp (digit t of (r, p) at D[(t*rows + r)*kp + p]), ex[r] the
+ * scale exponent of vector r (reading R1). */
+void orc_i8_split_rows(int64_t rows, int64_t kp, const double* hi, const double* lo, int64_t ld,
+                       int64_t sk, int y, int8_t* D, int32_t* ex) {
+  int8_t d[16];
+  for (int64_t r = 0; r < rows; ++r) {
+    const int e = orc_scale_exponent(hi + r * ld, kp, sk);
+    ex[r] = e;
+    for (int64_t p = 0; p < kp; ++p) {
+      orc_i8_split_scalar(hi[r * ld + p * sk], lo[r * ld + p * sk], e, y, d);
+      for (int t = 0; t < y; ++t) D[((int64_t)t * rows + r) * kp + p] = d[t];
+    }
+  }
+}
+
+/* Reading R24: bins of one panel, exact (int64).  DA: y x m x kp, DB: y x n x kp.
+ * nbins = y (the paper's triangle) or 2y-1 (every product, for the pins). */
+void orc_i8_panel_bins(int64_t m, int64_t n, int64_t kp, int y, const int8_t* DA,
+                       const int8_t* DB, int nbins, int64_t* bins) {
+  for (int s = 0; s < nbins; ++s)
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        int64_t acc = 0;
+        for (int a = 0; a < y; ++a) {
+          const int b = s - a;
+          if (b < 0 || b >= y) continue;
+          const int8_t* x = DA + ((int64_t)a * m + i) * kp;
+          const int8_t* z = DB + ((int64_t)b * n + j) * kp;
+          for (int64_t p = 0; p < kp; ++p) acc += (int64_t)x[p] * (int64_t)z[p];
+        }
+        bins[((int64_t)s * m + i) * n + j] = acc;
+      }
+}
+
+/* Reading R25: exact FP64x2 value of a group of nb <= 4 consecutive bins. */
+void orc_i8_group_value(const int64_t* b, int nb, double* hi, double* lo) {
+  int64_t V = 0;
+  for (int u = 0; u < nb; ++u) V = V * 256 + b[u];
+  const double h = (double)V; /* round to nearest even */
+  *hi = h;
+  *lo = (double)(V - (int64_t)h);
+}
+
+/* ORACLE-I8CASCADE: C := A B (FP64x2) through y int8 slices per operand.
+ * Row-major A (m x k, lda), B (k x n, ldb), C (m x n, ldc); flags m x n
+ * (ld = n, nullable).  k == 0 gives C = 0, flags = 0. */
+void orc_i8_casc_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const double* Alo,
+                      int64_t lda, const double* Bhi, const double* Blo, int64_t ldb, int y,
+                      double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int nthreads) {
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#else
+  (void)nthreads;
+#endif
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Chi[i * ldc + j] = 0.0;
+      Clo[i * ldc + j] = 0.0;
+      if (flags) flags[i * n + j] = 0;
+    }
+  const int64_t P = (k + KC8 - 1) / KC8;
+  for (int64_t q = 0; q < P; ++q) {
+    const int64_t k0 = q * KC8;
+    const int64_t kp = (k - k0 < KC8) ? k - k0 : KC8;
+    int8_t* DA = (int8_t*)malloc((size_t)y * m * kp + 1);
+    int8_t* DB = (int8_t*)malloc((size_t)y * n * kp + 1);
+    int32_t* e = (int32_t*)malloc(sizeof(int32_t) * (m + 1));
+    int32_t* f = (int32_t*)malloc(sizeof(int32_t) * (n + 1));
+    /* rows of A: stride 1 along k; columns of B: stride ldb along k */
+    orc_i8_split_rows(m, kp, Ahi + k0, Alo + k0, lda, 1, y, DA, e);
+    orc_i8_split_rows(n, kp, Bhi + k0 * ldb, Blo + k0 * ldb, 1, ldb, y, DB, f);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int64_t i = 0; i < m; ++i) {
+      int64_t b[16];
+      for (int64_t j = 0; j < n; ++j) {
+        /* bins of element (i, j), exact (reading R24) */
+        for (int s = 0; s < y; ++s) {
+          int64_t acc = 0;
+          for (int a = 0; a <= s; ++a) {
+            const int8_t* x = DA + ((int64_t)a * m + i) * kp;
+            const int8_t* z = DB + ((int64_t)(s - a) * n + j) * kp;
+            for (int64_t p = 0; p < kp; ++p) acc += (int64_t)x[p] * (int64_t)z[p];
+          }
+          b[s] = acc;
+        }
+        /* reading R25: groups of four, most significant first -> panel value T */
+        double th = 0.0, tl = 0.0;
+        for (int s = 0; s < y; s += 4) {
+          const int nb = (y - s < 4) ? y - s : 4;
+          double gh, gl;
+          orc_i8_group_value(b + s, nb, &gh, &gl);
+          const int w = e[i] + f[j] - 12 - 8 * (s + nb - 1);
+          orc_dd_add(th, tl, ldexp(gh, w), ldexp(gl, w), &th, &tl);
+        }
+        /* reading R26 */
+        if (flags && fabs(th) <= ldexp((double)kp, e[i] + f[j] - 50)) flags[i * n + j] = 1;
+        double ch = Chi[i * ldc + j], cl = Clo[i * ldc + j];
+        orc_dd_add(ch, cl, th, tl, &ch, &cl);
+        Chi[i * ldc + j] = ch;
+        Clo[i * ldc + j] = cl;
+      }
+    }
+    free(DA);
+    free(DB);
+    free(e);
+    free(f);
+  }
+}

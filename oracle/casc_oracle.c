@@ -365,10 +365,10 @@ void orc_casc_gemm_ex(int transa, int transb, int64_t m, int64_t n, int64_t k, d
       }
     return;
   }
-  double* a_h = (double*)malloc(sizeof(double) * m * k);
-  double* a_l = (double*)malloc(sizeof(double) * m * k);
-  double* b_h = (double*)malloc(sizeof(double) * k * n);
-  double* b_l = (double*)malloc(sizeof(double) * k * n);
+  double* a_h = (double*)calloc((size_t)(m * k), sizeof(double));
+  double* a_l = (double*)calloc((size_t)(m * k), sizeof(double));
+  double* b_h = (double*)calloc((size_t)(k * n), sizeof(double));
+  double* b_l = (double*)calloc((size_t)(k * n), sizeof(double));
   double* p_h = (double*)malloc(sizeof(double) * m * n);
   double* p_l = (double*)malloc(sizeof(double) * m * n);
   for (int64_t i = 0; i < m; ++i)
