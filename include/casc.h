@@ -238,6 +238,79 @@ int casc_slice_product(int64_t m, int64_t n, int64_t k,
                        const double* B_hi, const double* B_lo, int64_t ldb,
                        int sa, int sb, int64_t panel, double* out, casc_stream_t stream);
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-3: the INT8 cascade (paper §6 "FP64x2 in terms of INT8") */
+/* ------------------------------------------------------------------------ */
+/* The same product C := A B (FP64x2) computed from y int8 slices per operand
+ * with the y(y+1)/2 products A_i B_j, i + j < y ("14 to 15 INT8 splits and
+ * about 105 to 120 INT8 multiplies") on the INT8 tensor cores
+ * (tcgen05.mma kind::i8, int32 accumulation in tensor memory).
+ * DESIGN.md readings R22-R26 fix what the paper leaves open:
+ *   R22 k panel 8192; scale exponent per (row, panel) / (column, panel);
+ *   R23 X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)), F = 6 + 8(y-1), slices = the
+ *       balanced base-256 digits of X (d_0 in [-64, 64], d_t in [-128, 127]);
+ *   R24 bin_s = sum_p sum_(i+j=s) dA_i dB_j (exact int32), s < y;
+ *   R25 four bins at a time -> exact FP64x2 group value, scaled by
+ *       2^(e+f-12-8(s+nb-1)); panel value T = FP64x2 sum of the groups, most
+ *       significant first; C := C (+) T over panels (ascending);
+ *   R26 flags[i*n+j] = 1 iff |T.hi| <= kp 2^(e+f-50) in some panel (the panel's
+ *       product cancelled by at least ~50 bits against its operand scale).
+ * The result is bitwise deterministic and bitwise equal to the CPU oracle of
+ * the same readings (every step is exact integer work or a fixed sequence of
+ * RNE FP64 operations). */
+#define CASC_I8_KC 8192
+#define CASC_I8_DEFAULT_SLICES 14
+
+/* C := A B through y int8 slices, 3 <= y <= 15 (CASC_ERR_INVALID otherwise).
+ * Arguments, aliasing rules, k == 0 / m == 0 / n == 0 behaviour and errors as
+ * casc_gemm_fp64x2 (flags semantics: R26 above).  Uses a library-owned device
+ * workspace of casc_i8_workspace_bytes(m, n, k, y) bytes (allocated with a
+ * host-synchronising cudaMalloc on first use or growth; casc_i8_finalize frees it). */
+int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
+                        const double* A_hi, const double* A_lo, int64_t lda,
+                        const double* B_hi, const double* B_lo, int64_t ldb,
+                        double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, int y, casc_stream_t stream);
+
+/* As casc_i8_gemm_fp64x2 with a caller-owned device workspace (256-byte
+ * aligned, >= casc_i8_workspace_bytes(m, n, k, y)); no allocation, no host
+ * synchronisation. */
+int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
+                           const double* A_hi, const double* A_lo, int64_t lda,
+                           const double* B_hi, const double* B_lo, int64_t ldb,
+                           double* C_hi, double* C_lo, int64_t ldc,
+                           uint8_t* flags, int y, void* workspace, size_t workspace_bytes,
+                           casc_stream_t stream);
+
+/* Workspace bytes: packed A + packed B (y slices as 16 KB tcgen05 chunks,
+ * exponents) + 4 x 128 x 128 doubles per CTA of the GEMM (FP64x2 panel sum
+ * and C accumulator).  0 for empty problems or y out of range. */
+size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y);
+/* Bytes of one packed operand (rows = m for A, n for B). */
+size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y);
+/* Free the library-owned INT8-cascade workspace of the current device. */
+int casc_i8_finalize(void);
+
+/* Test export of the split (R22, R23) as computed by the GEMM's split kernels:
+ *   is_b == 0: A (rows x k, leading dimension ld >= k); is_b != 0: B (k x rows,
+ *   ld >= rows; "rows" are the columns of B).
+ *   digits: y x rows x k int8, digits[(t*rows + r)*k + p] = slice t of element
+ *           (r, p) of A, or (p, r) of B;
+ *   e:      P x rows int32 (P = ceil(k/8192)), scale exponent of row/column r
+ *           in panel q.
+ * Uses a temporary device allocation (cudaMallocAsync on `stream`). */
+int casc_i8_split(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
+                  int is_b, int y, int8_t* digits, int32_t* e, casc_stream_t stream);
+
+/* Test export of the exact int32 bins (R24) of k panel `panel` as accumulated
+ * in tensor memory by the GEMM kernel: bins[(s*m + i)*n + j], s = 0 .. y-1.
+ * Bit-comparable with any exact evaluation.  CASC_ERR_INVALID for a panel out
+ * of range. */
+int casc_i8_debug_bins(int64_t m, int64_t n, int64_t k,
+                       const double* A_hi, const double* A_lo, int64_t lda,
+                       const double* B_hi, const double* B_lo, int64_t ldb,
+                       int y, int64_t panel, int32_t* bins, casc_stream_t stream);
+
 /* Number of kernel launches the last successful call of the given entry point
  * family enqueued on this host thread (for launch accounting in bench.py). */
 int casc_last_launch_count(void);

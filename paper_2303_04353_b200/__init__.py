@@ -67,7 +67,22 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_packed_a_bytes", "casc_packed_b_bytes", "casc_packed_a_block_bytes",
             "casc_packed_b_block_bytes", "casc_pack_a", "casc_pack_b", "casc_gemm_packed",
             "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count",
-            "casc_gemm_fp64x2_simple", "casc_slice_product", "casc_gemm_fp64x2_ex"]
+            "casc_gemm_fp64x2_simple", "casc_slice_product", "casc_gemm_fp64x2_ex",
+            "casc_i8_gemm_fp64x2", "casc_i8_gemm_fp64x2_ws", "casc_i8_workspace_bytes",
+            "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins"]
+
+_sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
+                             _vp, ctypes.c_int, _vp])
+_sig("casc_i8_gemm_fp64x2_ws", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                                _i64, _vp, ctypes.c_int, _vp, _sz, _vp])
+_sig("casc_i8_workspace_bytes", [_i64, _i64, _i64, ctypes.c_int], _sz)
+_sig("casc_i8_packed_bytes", [_i64, _i64, ctypes.c_int], _sz)
+_sig("casc_i8_finalize", [])
+_sig("casc_i8_split", [_i64, _i64, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp])
+_sig("casc_i8_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_int,
+                            _i64, _vp, _vp])
+I8_KC = 8192
+I8_DEFAULT_SLICES = 14
 
 _sig("casc_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
                              ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
@@ -320,3 +335,78 @@ def casc_slice_product(A_hi, A_lo, B_hi, B_lo, sa: int, sb: int, panel: int, str
                                    _ptr(B_lo), ldb, sa, sb, panel, _ptr(out), _stream(stream)),
            "casc_slice_product")
     return out
+
+
+# ---------------------------------------------------------------- NEXT-3: INT8 cascade
+def casc_i8_workspace_bytes(m: int, n: int, k: int, y: int = I8_DEFAULT_SLICES) -> int:
+    return _lib.casc_i8_workspace_bytes(m, n, k, y)
+
+
+def casc_i8_packed_bytes(rows: int, k: int, y: int = I8_DEFAULT_SLICES) -> int:
+    return _lib.casc_i8_packed_bytes(rows, k, y)
+
+
+def casc_i8_finalize():
+    _check(_lib.casc_i8_finalize(), "casc_i8_finalize")
+
+
+def casc_i8_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, y: int = I8_DEFAULT_SLICES, C_hi=None,
+                        C_lo=None, flags=None, want_flags=True, stream=None, workspace=None):
+    """C := A B through y int8 slices on the INT8 tensor cores (NEXT-3; readings
+    R22-R26).  Returns (C_hi, C_lo, flags).  With `workspace` (uint8 CUDA tensor
+    of casc_i8_workspace_bytes(m, n, k, y)) this calls casc_i8_gemm_fp64x2_ws."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    k2, n = B_hi.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    C_hi, C_lo, flags = _outputs(m, n, A_hi.device, C_hi, C_lo, flags, want_flags)
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    if workspace is None:
+        st = _lib.casc_i8_gemm_fp64x2(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                      _ptr(B_lo), ldb, _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
+                                      int(y), _stream(stream))
+        _check(st, "casc_i8_gemm_fp64x2")
+    else:
+        st = _lib.casc_i8_gemm_fp64x2_ws(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                         _ptr(B_lo), ldb, _ptr(C_hi), _ptr(C_lo), ldc,
+                                         _ptr(flags), int(y), _ptr(workspace), workspace.numel(),
+                                         _stream(stream))
+        _check(st, "casc_i8_gemm_fp64x2_ws")
+    return C_hi, C_lo, flags
+
+
+def casc_i8_gemm_fp64x2_ws(A_hi, A_lo, B_hi, B_lo, workspace, **kw):
+    return casc_i8_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, workspace=workspace, **kw)
+
+
+def casc_i8_split(hi, lo, is_b: bool, y: int = I8_DEFAULT_SLICES, stream=None):
+    """Digits (y, rows, k) int8 and exponents (P, rows) int32 of A (is_b False,
+    rows x k) or of B's columns (is_b True, B is k x rows), from the GEMM's own
+    split kernels (R22, R23)."""
+    ld = _ld_pair(hi, lo, "X")
+    if is_b:
+        k, rows = hi.shape
+    else:
+        rows, k = hi.shape
+    P = (k + I8_KC - 1) // I8_KC
+    D = torch.empty((y, rows, k), dtype=torch.int8, device=hi.device)
+    E = torch.empty((P, rows), dtype=torch.int32, device=hi.device)
+    _check(_lib.casc_i8_split(rows, k, _ptr(hi), _ptr(lo), ld, int(bool(is_b)), int(y), _ptr(D),
+                              _ptr(E), _stream(stream)), "casc_i8_split")
+    return D, E
+
+
+def casc_i8_debug_bins(A_hi, A_lo, B_hi, B_lo, panel: int = 0, y: int = I8_DEFAULT_SLICES,
+                       stream=None):
+    """Exact int32 bins (y, m, n) of k panel `panel` as accumulated in tensor memory (R24)."""
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, k = A_hi.shape
+    n = B_hi.shape[1]
+    bins = torch.empty((y, m, n), dtype=torch.int32, device=A_hi.device)
+    _check(_lib.casc_i8_debug_bins(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo),
+                                   ldb, int(y), panel, _ptr(bins), _stream(stream)),
+           "casc_i8_debug_bins")
+    return bins

@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcasc.so")
-SOURCES = ["casc_split.cu", "casc_gemm.cu", "casc_simple.cu", "casc_blas.cu", "casc_api.cu"]
+SOURCES = ["casc_split.cu", "casc_gemm.cu", "casc_simple.cu", "casc_blas.cu", "casc_api.cu",
+           "casc_i8.cu"]
 HEADERS = ["casc_layout.cuh", "casc_ptx.cuh", "casc_dd.cuh", os.path.join("..", "..", "include", "casc.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -663,3 +663,24 @@ int casc_slice_product(int64_t m, int64_t n, int64_t k, const double* A_hi, cons
 }
 
 }  // extern "C"
+
+// Host helpers shared with the other entry-point files (casc_i8.cu).
+namespace casc {
+namespace host {
+int device_check(int* sms) { return ::device_check(sms); }
+int validate_gemm(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                  int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi,
+                  double* C_lo, int64_t ldc, uint8_t* flags) {
+  return ::validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+}
+int zero_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+           cudaStream_t st) {
+  return ::zero_c(m, n, C_hi, C_lo, ldc, flags, st);
+}
+int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
+  return ::check_mat(p, rows, cols, ld);
+}
+int current_sms() { return ::current_sms(); }
+void set_launches(int n) { g_launches = n; }
+}  // namespace host
+}  // namespace casc

@@ -1,0 +1,776 @@
+// casc_i8.cu — NEXT-3: the FP64x2 GEMM C := A B as a cascade
+// of INT8 tensor-core GEMMs, the variant the paper proposes in §6 "FP64x2 in
+// terms of INT8": the matrices are "converted into fixed point
+// numbers which can be stored in integers", cascaded into ~14-15
+// int8 splits, multiplied with the y(y+1)/2 products of the triangle i + j < y
+// and accumulated in 32-bit integers.
+// readings R22-R26 fix what the paper leaves open (the CPU oracle
+// oracle/casc_i8_oracle.c follows the same readings with its own code):
+//   R22  k panel of 8192; per (row, panel) / (column, panel) scale exponent e
+//        (frexp exponent of max |hi|); every bin of a panel is an exact int32.
+//   R23  X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)), F = 6 + 8(y-1); slices = the
+//        balanced base-256 digits of X (d_0 in [-64, 64], others [-128, 127]).
+//   R24  bin_s = sum_p sum_(i+j=s) dA_i dB_j, s < y.
+//   R25  groups of four bins -> exact FP64x2 group value G, scaled by
+//        2^(e+f-12-8(s+nb-1)); panel value T = FP64x2 sum of the groups, most
+//        significant first; C = C (+) T over panels.
+//   R26  flag |= |T.hi| <= kp 2^(e+f-50).
+//
+// Phase 1 (HBM-bound):
+//   i8_rowmax_kernel / i8_colmax_kernel  max |hi| per (row | column, panel) as
+//                                        an atomicMax on the bit pattern;
+//   i8_digits_kernel<A|B>                digits, written straight into the
+//        tcgen05 shared-memory layout: per (slice, 128-row block, 128-byte k
+//        block) one contiguous 16 KB chunk, K-major, 128-byte swizzle (row r at
+//        (r/8)*1024 + (r%8)*128, 16-byte unit u at u ^ (r%8)), so the GEMM
+//        moves every operand tile with ONE cp.async.bulk and points the MMA
+//        descriptor at it.
+// Phase 2+3: i8_gemm_kernel, persistent (one CTA per SM), 384 threads:
+//   warp 0     TMA producer: 16 KB chunks into an A ring (6 slots) and a B ring
+//              (4 slots), mbarrier complete_tx;
+//   warp 1     MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::i8,
+//              M = N = 128, K = 32, s8 x s8 -> s32; the four bins of a group
+//              accumulate in tensor memory (4 x 128 of the 512 columns).  Per
+//              128-byte k block the operands of a group are streamed as a chain
+//              A_top .. A_s, B_0, A_(s-1), B_1, ... so each B_j meets its (up to)
+//              four A_i partners while they sit in smem: every chunk is loaded
+//              once per k block and feeds up to four MMAs;
+//   warp 2     TMEM allocator (512 columns);
+//   warps 4-11 epilogue: tcgen05.ld of the int32 bins (warp w reads TMEM lane
+//              quarter w%4, column half (w-4)/4), exact group value, FP64x2
+//              panel sum T and C in a per-CTA workspace (L2-resident), detector,
+//              final store of C and the flags.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "../../include/casc.h"
+#include "casc_dd.cuh"
+#include "casc_ptx.cuh"
+
+// DBG instantiation: the combine below its early `continue` is unreachable by design
+#pragma nv_diag_suppress 128
+
+namespace casc {
+namespace i8 {
+
+constexpr int KC8 = 8192;          // R22 panel depth
+constexpr int KB = 128;            // k bytes per chunk (one 128-byte swizzle row)
+constexpr int KBP = KC8 / KB;      // k blocks per panel (64)
+constexpr int TR = 128;            // rows (A) / columns (B) per chunk = tile edge
+constexpr int CHUNK = TR * KB;     // 16384 bytes
+constexpr int YMIN = 3, YMAX = 15;
+constexpr int NSA = 6, NSB = 4;    // smem ring slots (16 KB each)
+constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
+constexpr int THREADS = 384;
+constexpr int EPI_WARP0 = 4, EPI_THREADS = 256;
+constexpr int GROUP_M = 12;        // tile raster: 12 row blocks sweep the column blocks
+constexpr size_t SMEM = (size_t)(NSA + NSB) * CHUNK + 1024 + 256;
+
+struct Pack {
+  int64_t R;    // 128-row blocks
+  int64_t KBn;  // 128-byte k blocks
+  int64_t P;    // k panels
+  int y;
+};
+__host__ __device__ inline Pack pack_of(int64_t rows, int64_t k, int y) {
+  return Pack{(rows + TR - 1) / TR, (k + KB - 1) / KB, (k + KC8 - 1) / KC8, y};
+}
+__host__ __device__ inline int64_t slice_bytes(const Pack& g) {
+  return (int64_t)g.y * g.R * g.KBn * CHUNK;
+}
+// packed operand = [slices][int32 exponents P x R*128][u64 max bits P x R*128]
+__host__ __device__ inline int64_t exp_off(const Pack& g) { return slice_bytes(g); }
+__host__ __device__ inline int64_t max_off(const Pack& g) {
+  return slice_bytes(g) + ((g.P * g.R * TR * 4 + 255) / 256) * 256;
+}
+__host__ __device__ inline int64_t packed_bytes(const Pack& g) {
+  return max_off(g) + g.P * g.R * TR * 8;
+}
+__host__ __device__ inline int64_t chunk_off(const Pack& g, int t, int64_t rb, int64_t kb) {
+  return ((t * g.R + rb) * g.KBn + kb) * (int64_t)CHUNK;
+}
+// byte of (row r, k byte c) inside a chunk: K-major, 128-byte swizzle
+__host__ __device__ inline uint32_t sw128(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((((c >> 4) ^ (r & 7)) & 7) << 4) + (c & 15));
+}
+
+// ------------------------------------------------------------------ phase 1
+__device__ __forceinline__ unsigned long long absbits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
+// max |A_hi| per (row, panel): warp = one row x 1024 k, 8 rows per block.
+__global__ void __launch_bounds__(256) i8_rowmax_kernel(const double* __restrict__ hi, int64_t ld,
+                                                        int64_t rows, int64_t k, int64_t Rp,
+                                                        unsigned long long* __restrict__ mx) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t p0 = (int64_t)blockIdx.y * 1024;
+  if (r >= rows) return;
+  unsigned long long m = 0;
+  const double* row = hi + r * ld;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int64_t p = p0 + i * 32 + lane;
+    if (p < k) m = max(m, absbits(__ldg(row + p)));
+  }
+  for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(~0u, m, o));
+  if (lane == 0 && m) atomicMax(mx + (p0 / KC8) * Rp + r, m);
+}
+
+// max |B_hi| per (column, panel): thread = one column x 64 k.
+__global__ void __launch_bounds__(256) i8_colmax_kernel(const double* __restrict__ hi, int64_t ld,
+                                                        int64_t cols, int64_t k, int64_t Rp,
+                                                        unsigned long long* __restrict__ mx) {
+  const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t p0 = (int64_t)blockIdx.y * 64;
+  if (j >= cols) return;
+  unsigned long long m = 0;
+#pragma unroll 8
+  for (int i = 0; i < 64; ++i) {
+    const int64_t p = p0 + i;
+    if (p < k) m = max(m, absbits(__ldg(hi + p * ld + j)));
+  }
+  if (m) atomicMax(mx + (p0 / KC8) * Rp + j, m);
+}
+
+// 2^n as a double for n in [-1022, 1023] (exact).
+__device__ __forceinline__ double p2(int n) { return __longlong_as_double((long long)(n + 1023) << 52); }
+// x * 2^n, exact whenever the result is a normal double (like ldexp).
+__device__ __forceinline__ double mulp2(double x, int n) {
+  if (n >= -1022 && n <= 1023) return __dmul_rn(x, p2(n));
+  const int h = n / 2;
+  return __dmul_rn(__dmul_rn(x, p2(h)), p2(n - h));
+}
+// exact conversion of an integer-valued double (|w| < 2^126) to int128
+__device__ __forceinline__ __int128 to_i128(double w) {
+  if (fabs(w) < 9.0e18) return (__int128)__double2ll_rz(w);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+  const int ex = (int)((b >> 52) & 0x7ff) - 1075;
+  const __int128 mant = (__int128)((b & 0xfffffffffffffull) | 0x10000000000000ull);
+  const __int128 v = mant << ex;
+  return (b >> 63) ? -v : v;
+}
+__device__ __forceinline__ int scale_exp(unsigned long long bits) {
+  if (!bits) return 0;
+  int e;
+  frexp(__longlong_as_double((long long)bits), &e);
+  return e;
+}
+
+// Digits (R23) of 32 consecutive k of one vector, written as two 16-byte units
+// per slice.  COLS = false: A rows (element (r, p) at hi[r*ld + p]); block =
+// 64 rows x 128 k.  COLS = true: B columns (element (p, j) at hi[p*ld + j]);
+// block = 128 columns x 128 k.  Padding rows / k are written as zero digits,
+// so the packed operand is fully defined.
+template <bool COLS>
+__global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict__ hi,
+                                                        const double* __restrict__ lo, int64_t ld,
+                                                        int64_t rows, int64_t k, Pack g,
+                                                        uint8_t* __restrict__ packed) {
+  const int t = threadIdx.x;
+  const int64_t kb = blockIdx.y;
+  int64_t r;
+  int cs[2];
+  int ncs;
+  if (COLS) {
+    r = (int64_t)blockIdx.x * 128 + (t & 127);
+    cs[0] = t >> 7;
+    cs[1] = (t >> 7) + 2;
+    ncs = 2;
+  } else {
+    r = (int64_t)blockIdx.x * 64 + (t >> 2);
+    cs[0] = t & 3;
+    ncs = 1;
+  }
+  if (r >= g.R * TR) return;
+  const int64_t q = kb / KBP;
+  const int64_t Rp = g.R * TR;
+  const unsigned long long* mx =
+      reinterpret_cast<const unsigned long long*>(packed + max_off(g)) + q * Rp;
+  const int e = r < rows ? scale_exp(mx[r]) : 0;
+  if ((kb % KBP) == 0 && cs[0] == 0)
+    reinterpret_cast<int32_t*>(packed + exp_off(g))[q * Rp + r] = e;
+  const int F = 6 + 8 * (g.y - 1);
+  const int s1 = min(F - e, 1023), s2 = F - e - s1;
+  const double sc1 = p2(s1), sc2 = p2(s2);
+  const int rl = (int)(r % TR);
+  const int64_t rb = r / TR;
+  for (int u = 0; u < ncs; ++u) {
+    const int c = cs[u];
+    const int64_t p0 = kb * KB + c * 32;
+    __int128 X[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int64_t p = p0 + i;
+      double h = 0.0, l = 0.0;
+      if (r < rows && p < k) {
+        const int64_t idx = COLS ? p * ld + r : r * ld + p;
+        h = __ldg(hi + idx);
+        l = __ldg(lo + idx);
+      }
+      X[i] = to_i128(rint(__dmul_rn(__dmul_rn(h, sc1), sc2))) +
+             to_i128(rint(__dmul_rn(__dmul_rn(l, sc1), sc2)));
+    }
+    const uint32_t o0 = sw128(rl, c * 32), o1 = sw128(rl, c * 32 + 16);
+    for (int s = g.y - 1; s >= 0; --s) {
+      uint32_t w[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) w[v] = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        int d;
+        if (s > 0) {
+          d = (int)(int8_t)(uint8_t)((unsigned long long)X[i] & 0xffull);
+          X[i] = (X[i] - d) >> 8;
+        } else {
+          d = (int)(long long)X[i];
+        }
+        w[i >> 2] |= (uint32_t)(uint8_t)d << (8 * (i & 3));
+      }
+      uint8_t* base = packed + chunk_off(g, s, rb, kb);
+      *reinterpret_cast<uint4*>(base + o0) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(base + o1) = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+}
+
+// Debug export: packed chunks -> canonical digits D[t][r][p] (rows x k) and
+// exponents E[q][r].
+__global__ void i8_unpack_kernel(const uint8_t* __restrict__ packed, Pack g, int64_t rows,
+                                 int64_t k, int8_t* __restrict__ D, int32_t* __restrict__ E) {
+  const int64_t total = (int64_t)g.y * rows * k;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = x % k, r = (x / k) % rows;
+    const int t = (int)(x / (k * rows));
+    D[x] = (int8_t)packed[chunk_off(g, t, r / TR, p / KB) + sw128((int)(r % TR), (int)(p % KB))];
+  }
+  const int32_t* ex = reinterpret_cast<const int32_t*>(packed + exp_off(g));
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < g.P * rows;
+       x += (int64_t)gridDim.x * blockDim.x)
+    E[x] = ex[(x / rows) * g.R * TR + x % rows];
+}
+
+// ------------------------------------------------------------------ phase 2+3
+struct GemmArgs {
+  const uint8_t* pa;
+  const uint8_t* pb;
+  Pack ga, gb;
+  int64_t m, n, k;
+  double* C_hi;
+  double* C_lo;
+  int64_t ldc;
+  uint8_t* flags;
+  double* ws;           // per CTA: T hi, T lo, C hi, C lo (4 x 16384 doubles)
+  int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
+  int64_t dbg_panel;
+};
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = N = 128
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(acc), "n"(IDESC));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tile_of(int tile, int64_t RA, int64_t RB, int64_t& rb,
+                                        int64_t& cb) {
+  const int64_t per = (int64_t)GROUP_M * RB;
+  const int64_t grp = tile / per;
+  const int64_t first = grp * GROUP_M;
+  const int64_t gs = min((int64_t)GROUP_M, RA - first);
+  const int64_t rr = tile % per;
+  rb = first + rr % gs;
+  cb = rr / gs;
+}
+
+template <bool DBG>
+__global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + NSA * CHUNK;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSB * CHUNK);
+  uint64_t* fullA = bars;
+  uint64_t* emptyA = fullA + NSA;
+  uint64_t* fullB = emptyA + NSA;
+  uint64_t* emptyB = fullB + NSB;
+  uint64_t* tfull = emptyB + NSB;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(&fullA[i], 1);
+      mbar_init(&emptyA[i], 1);
+    }
+    for (int i = 0; i < NSB; ++i) {
+      mbar_init(&fullB[i], 1);
+      mbar_init(&emptyB[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, EPI_THREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  const int y = p.ga.y;
+  const int ngroups = (y + NBIN - 1) / NBIN;
+  const int64_t RA = p.ga.R, RB = p.gb.R, KBn = p.ga.KBn;
+  const int P = (int)p.ga.P;
+  const int tiles = (int)(RA * RB);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ============================ TMA producer ============================
+      uint32_t aseq = 0, bseq = 0;
+      auto loadA = [&](int i, int64_t rb, int64_t kb) {
+        const uint32_t s = aseq % NSA;
+        mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
+        mbar_arrive_expect_tx(&fullA[s], CHUNK);
+        tma_bulk_g2s(sA + s * CHUNK, p.pa + chunk_off(p.ga, i, rb, kb), CHUNK, &fullA[s]);
+        ++aseq;
+      };
+      auto loadB = [&](int j, int64_t cb, int64_t kb) {
+        const uint32_t s = bseq % NSB;
+        mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
+        mbar_arrive_expect_tx(&fullB[s], CHUNK);
+        tma_bulk_g2s(sB + s * CHUNK, p.pb + chunk_off(p.gb, j, cb, kb), CHUNK, &fullB[s]);
+        ++bseq;
+      };
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        int64_t rb, cb;
+        tile_of(tile, RA, RB, rb, cb);
+        for (int q = 0; q < P; ++q) {
+          const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
+          for (int grp = 0; grp < ngroups; ++grp) {
+            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+            for (int64_t kb = kb0; kb < kb1; ++kb) {
+              for (int i = top; i >= s; --i) loadA(i, rb, kb);
+              loadB(0, cb, kb);
+              for (int j = 1; j <= top; ++j) {
+                if (s - j >= 0) loadA(s - j, rb, kb);
+                loadB(j, cb, kb);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ============================ MMA issuer ============================
+      uint32_t aseq = 0, bseq = 0, gcount = 0;
+      const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int q = 0; q < P; ++q) {
+          const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
+          for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+            mbar_wait(tempty, (gcount & 1) ^ 1);
+            tc_fence_after();
+            uint32_t touched = 0;
+            for (int64_t kb = kb0; kb < kb1; ++kb) {
+              const uint32_t abase = aseq;
+              for (int j = 0; j <= top; ++j) {
+                const uint32_t bs = bseq % NSB;
+                mbar_wait(&fullB[bs], (bseq / NSB) & 1);
+                const int ilo = max(0, s - j), ihi = top - j;
+                for (int i = ihi; i >= ilo; --i) {
+                  const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
+                  const uint32_t as = aq % NSA;
+                  mbar_wait(&fullA[as], (aq / NSA) & 1);
+                  tc_fence_after();
+                  const int b = i + j - s;
+                  const uint64_t ad = sdesc(a_base_addr + as * CHUNK);
+                  const uint64_t bd = sdesc(b_base_addr + bs * CHUNK);
+                  const uint32_t first = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
+#pragma unroll
+                  for (int kk = 0; kk < 4; ++kk)
+                    mma_i8(tmem + b * 128, ad + 2 * kk, bd + 2 * kk, kk ? 1u : first);
+                  touched |= 1u << b;
+                }
+                mma_commit(&emptyB[bs]);
+                ++bseq;
+                // A_(top-j) has met its last partner
+                const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
+                mma_commit(&emptyA[rq % NSA]);
+              }
+              aseq = abase + (uint32_t)(s + nb);
+            }
+            mma_commit(tfull);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= EPI_WARP0) {
+    // ============================ epilogue ============================
+    const int ew = warp - EPI_WARP0;
+    const int quarter = warp & 3, half = ew >> 2;
+    const int lr = quarter * 32 + lane;       // tile row = TMEM lane
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    double* Th = p.ws + (int64_t)blockIdx.x * 4 * (TR * TR);
+    double* Tl = Th + TR * TR;
+    double* Ch = Tl + TR * TR;
+    double* Cl = Ch + TR * TR;
+    const int32_t* EA = reinterpret_cast<const int32_t*>(p.pa + exp_off(p.ga));
+    const int32_t* EB = reinterpret_cast<const int32_t*>(p.pb + exp_off(p.gb));
+    uint32_t gcount = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int64_t rb, cb;
+      tile_of(tile, RA, RB, rb, cb);
+      const int64_t gi = rb * TR + lr;
+      uint64_t fl = 0;  // detector bits of this thread's 64 columns
+      for (int q = 0; q < P; ++q) {
+        const int64_t kp = min((int64_t)KC8, p.k - (int64_t)q * KC8);
+        const int ei = EA[(int64_t)q * RA * TR + gi];
+        for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+          const int s = grp * NBIN, nb = min(NBIN, y - s);
+          mbar_wait(tfull, gcount & 1);
+          tc_fence_after();
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c0 = half * 64 + cc * 16;
+            uint32_t r0[16], r1[16], r2[16], r3[16];
+            tmem_ld16(trow + 0 * 128 + c0, r0);
+            if (nb > 1) tmem_ld16(trow + 1 * 128 + c0, r1);
+            if (nb > 2) tmem_ld16(trow + 2 * 128 + c0, r2);
+            if (nb > 3) tmem_ld16(trow + 3 * 128 + c0, r3);
+            tmem_wait_ld();
+            if (cc == 3) {  // this warp's part of TMEM is read: the next group may start
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(tempty);
+            }
+            if (DBG) {
+              if (q == p.dbg_panel) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int64_t gj = cb * TR + c0 + i;
+                  if (gi < p.m && gj < p.n) {
+                    const int64_t mn = p.m * p.n, o = gi * p.n + gj;
+                    p.dbg[(int64_t)(s + 0) * mn + o] = (int32_t)r0[i];
+                    if (nb > 1) p.dbg[(int64_t)(s + 1) * mn + o] = (int32_t)r1[i];
+                    if (nb > 2) p.dbg[(int64_t)(s + 2) * mn + o] = (int32_t)r2[i];
+                    if (nb > 3) p.dbg[(int64_t)(s + 3) * mn + o] = (int32_t)r3[i];
+                  }
+                }
+              }
+              continue;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int lc = c0 + i;
+              const int64_t gj = cb * TR + lc;
+              const int fj = __ldg(EB + (int64_t)q * RB * TR + gj);
+              // R25: exact group value (hi = RN(V), lo = V - hi)
+              double gh, gl;
+              const double b0 = (double)(int32_t)r0[i];
+              if (nb == 4) {
+                const double P1 = __dadd_rn(__dmul_rn(b0, 256.0), (double)(int32_t)r1[i]);
+                const double P2 =
+                    __dadd_rn(__dmul_rn((double)(int32_t)r2[i], 256.0), (double)(int32_t)r3[i]);
+                two_sum(__dmul_rn(P1, 65536.0), P2, gh, gl);
+              } else {
+                gh = b0;
+                if (nb > 1) gh = __dadd_rn(__dmul_rn(gh, 256.0), (double)(int32_t)r1[i]);
+                if (nb > 2) gh = __dadd_rn(__dmul_rn(gh, 256.0), (double)(int32_t)r2[i]);
+                gl = 0.0;
+              }
+              const int w = ei + fj - 12 - 8 * (s + nb - 1);
+              gh = mulp2(gh, w);
+              gl = mulp2(gl, w);
+              const int widx = lc * TR + lr;
+              double th, tl;
+              if (grp == 0) {
+                th = gh;
+                tl = gl;
+              } else {
+                dd_add(Th[widx], Tl[widx], gh, gl, th, tl);
+              }
+              if (grp + 1 < ngroups) {
+                Th[widx] = th;
+                Tl[widx] = tl;
+              } else {
+                // R26 detector, then C (+)= T
+                if (fabs(th) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * 64);
+                double ch = th, cl = tl;
+                if (q > 0) dd_add(Ch[widx], Cl[widx], th, tl, ch, cl);
+                if (q + 1 < P) {
+                  Ch[widx] = ch;
+                  Cl[widx] = cl;
+                } else if (gi < p.m && gj < p.n) {
+                  p.C_hi[gi * p.ldc + gj] = ch;
+                  p.C_lo[gi * p.ldc + gj] = cl;
+                  if (p.flags) p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t pack(const double* hi, const double* lo, int64_t ld, int64_t rows, int64_t k, int y,
+                 bool cols, void* packed, cudaStream_t st) {
+  const Pack g = pack_of(rows, k, y);
+  uint8_t* pk = static_cast<uint8_t*>(packed);
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(pk + max_off(g));
+  cudaError_t e = cudaMemsetAsync(mx, 0, (size_t)(g.P * g.R * TR * 8), st);
+  if (e != cudaSuccess) return e;
+  if (cols) {
+    i8_colmax_kernel<<<dim3((unsigned)((rows + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0,
+                       st>>>(hi, ld, rows, k, g.R * TR, mx);
+    i8_digits_kernel<true><<<dim3((unsigned)g.R, (unsigned)g.KBn), 256, 0, st>>>(hi, lo, ld, rows,
+                                                                                k, g, pk);
+  } else {
+    i8_rowmax_kernel<<<dim3((unsigned)((rows + 7) / 8), (unsigned)((k + 1023) / 1024)), 256, 0,
+                       st>>>(hi, ld, rows, k, g.R * TR, mx);
+    i8_digits_kernel<false><<<dim3((unsigned)(g.R * 2), (unsigned)g.KBn), 256, 0, st>>>(
+        hi, lo, ld, rows, k, g, pk);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t unpack(const void* packed, int64_t rows, int64_t k, int y, int8_t* D, int32_t* E,
+                   cudaStream_t st) {
+  const Pack g = pack_of(rows, k, y);
+  i8_unpack_kernel<<<1024, 256, 0, st>>>(static_cast<const uint8_t*>(packed), g, rows, k, D, E);
+  return cudaGetLastError();
+}
+
+int grid_for(int64_t m, int64_t n, int sms) {
+  const int64_t tiles = ((m + TR - 1) / TR) * ((n + TR - 1) / TR);
+  return (int)(tiles < sms ? tiles : sms);
+}
+size_t cta_ws_bytes(int grid) { return (size_t)grid * 4 * TR * TR * sizeof(double); }
+
+cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
+                 double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
+                 int32_t* dbg, int64_t dbg_panel, cudaStream_t st) {
+  GemmArgs a{};
+  a.pa = static_cast<const uint8_t*>(pa);
+  a.pb = static_cast<const uint8_t*>(pb);
+  a.ga = pack_of(m, k, y);
+  a.gb = pack_of(n, k, y);
+  a.m = m;
+  a.n = n;
+  a.k = k;
+  a.C_hi = C_hi;
+  a.C_lo = C_lo;
+  a.ldc = ldc;
+  a.flags = flags;
+  a.ws = ws;
+  a.dbg = dbg;
+  a.dbg_panel = dbg_panel;
+  if (dbg) {
+    cudaFuncSetAttribute(i8_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
+    i8_gemm_kernel<true><<<grid, THREADS, SMEM, st>>>(a);
+  } else {
+    cudaFuncSetAttribute(i8_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
+    i8_gemm_kernel<false><<<grid, THREADS, SMEM, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace i8
+}  // namespace casc
+
+// ====================================================================== C ABI
+namespace casc {
+namespace host {
+int device_check(int* sms);
+int validate_gemm(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                  int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi,
+                  double* C_lo, int64_t ldc, uint8_t* flags);
+int zero_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+           cudaStream_t st);
+int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld);
+int current_sms();
+void set_launches(int n);
+}  // namespace host
+}  // namespace casc
+
+namespace {
+using namespace casc;
+inline cudaStream_t S8(casc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int st8(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
+inline size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+struct I8Ws {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+I8Ws g_i8ws[64];
+}  // namespace
+
+extern "C" {
+
+size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y) {
+  if (rows <= 0 || k <= 0 || y < i8::YMIN || y > i8::YMAX) return 0;
+  return (size_t)i8::packed_bytes(i8::pack_of(rows, k, y));
+}
+
+size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y) {
+  if (m <= 0 || n <= 0 || k <= 0 || y < i8::YMIN || y > i8::YMAX) return 0;
+  return al256(casc_i8_packed_bytes(m, k, y)) + al256(casc_i8_packed_bytes(n, k, y)) +
+         i8::cta_ws_bytes(i8::grid_for(m, n, host::current_sms()));
+}
+
+int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
+                           const double* A_lo, int64_t lda, const double* B_hi,
+                           const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                           int64_t ldc, uint8_t* flags, int y, void* workspace,
+                           size_t workspace_bytes, casc_stream_t stream) {
+  host::set_launches(0);
+  int r = host::validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  if (k == 0) return host::zero_c(m, n, C_hi, C_lo, ldc, flags, st);
+  const size_t need = casc_i8_workspace_bytes(m, n, k, y);
+  if (!workspace || workspace_bytes < need) return CASC_ERR_INVALID;
+  uint8_t* pa = static_cast<uint8_t*>(workspace);
+  uint8_t* pb = pa + al256(casc_i8_packed_bytes(m, k, y));
+  double* ws = reinterpret_cast<double*>(pb + al256(casc_i8_packed_bytes(n, k, y)));
+  cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
+  if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
+  if (e == cudaSuccess)
+    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, ws, i8::grid_for(m, n, sms), nullptr,
+                 0, st);
+  if (e == cudaSuccess) host::set_launches(5);
+  return st8(e);
+}
+
+int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                        int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                        double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int y,
+                        casc_stream_t stream) {
+  int r = host::validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  if ((r = host::device_check(nullptr))) return r;
+  if (k == 0) return host::zero_c(m, n, C_hi, C_lo, ldc, flags, S8(stream));
+  const size_t need = casc_i8_workspace_bytes(m, n, k, y);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  I8Ws& w = g_i8ws[dev];
+  if (w.bytes < need) {
+    if (w.ptr) {
+      cudaDeviceSynchronize();
+      cudaFree(w.ptr);
+      w.ptr = nullptr;
+      w.bytes = 0;
+    }
+    if (cudaMalloc(&w.ptr, need) != cudaSuccess) return CASC_ERR_CUDA;
+    w.bytes = need;
+  }
+  return casc_i8_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
+                                y, w.ptr, w.bytes, stream);
+}
+
+int casc_i8_finalize(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  I8Ws& w = g_i8ws[dev];
+  if (w.ptr) {
+    cudaDeviceSynchronize();
+    if (cudaFree(w.ptr) != cudaSuccess) return CASC_ERR_CUDA;
+  }
+  w.ptr = nullptr;
+  w.bytes = 0;
+  return CASC_OK;
+}
+
+int casc_i8_split(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
+                  int is_b, int y, int8_t* digits, int32_t* e, casc_stream_t stream) {
+  host::set_launches(0);
+  int r;
+  if (rows < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if (is_b) {
+    if ((r = host::check_mat(hi, k, rows, ld)) || (r = host::check_mat(lo, k, rows, ld))) return r;
+  } else {
+    if ((r = host::check_mat(hi, rows, k, ld)) || (r = host::check_mat(lo, rows, k, ld))) return r;
+  }
+  if (rows == 0 || k == 0) return CASC_OK;
+  if (!digits || !e) return CASC_ERR_INVALID;
+  if ((r = host::device_check(nullptr))) return r;
+  const cudaStream_t st = S8(stream);
+  void* buf = nullptr;
+  if (cudaMallocAsync(&buf, casc_i8_packed_bytes(rows, k, y), st) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  cudaError_t er = i8::pack(hi, lo, ld, rows, k, y, is_b != 0, buf, st);
+  if (er == cudaSuccess) er = i8::unpack(buf, rows, k, y, digits, e, st);
+  cudaFreeAsync(buf, st);
+  return st8(er);
+}
+
+int casc_i8_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                       int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb, int y,
+                       int64_t panel, int32_t* bins, casc_stream_t stream) {
+  host::set_launches(0);
+  int r;
+  if (m < 0 || n < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if ((r = host::check_mat(A_hi, m, k, lda)) || (r = host::check_mat(A_lo, m, k, lda))) return r;
+  if ((r = host::check_mat(B_hi, k, n, ldb)) || (r = host::check_mat(B_lo, k, n, ldb))) return r;
+  if (m == 0 || n == 0 || k == 0) return CASC_OK;
+  if (panel < 0 || panel >= (k + i8::KC8 - 1) / i8::KC8 || !bins) return CASC_ERR_INVALID;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  const size_t need = casc_i8_workspace_bytes(m, n, k, y);
+  void* buf = nullptr;
+  if (cudaMallocAsync(&buf, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+  uint8_t* pa = static_cast<uint8_t*>(buf);
+  uint8_t* pb = pa + al256(casc_i8_packed_bytes(m, k, y));
+  double* ws = reinterpret_cast<double*>(pb + al256(casc_i8_packed_bytes(n, k, y)));
+  cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
+  if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
+  if (e == cudaSuccess)
+    e = i8::gemm(pa, pb, m, n, k, y, nullptr, nullptr, n, nullptr, ws, i8::grid_for(m, n, sms),
+                 bins, panel, st);
+  cudaFreeAsync(buf, st);
+  return st8(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+"""GPU parity of the INT8 cascade (NEXT-3, readings R22-R26) through the C ABI
+against the CPU oracle (oracle/casc_i8_oracle.c).
+
+Every step of this variant is exact integer work or a fixed sequence of RNE
+FP64 operations, so the bar is bit-exact everywhere:
+  * int8 slices and scale exponents (R22, R23): bit-exact;
+  * the int32 bins accumulated in tensor memory (R24): bit-exact;
+  * C_hi, C_lo and the flags (R25, R26): bit-exact;
+and, against ORACLE-EXACT, the north-star bound |C - C*| <= 4 k 2^-104 |A||B|.
+Sizes span several 128 x 128 tiles with ragged edges, two k panels (k > 8192)
+and the bench workload (sampled rows / columns: a row of C depends only on
+that row of A and on B; a column only on that column of B and on A).
+"""
+
+import numpy as np
+import pytest
+
+import casc_inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def casc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2303_04353_b200 as casc
+    return casc
+
+
+def T(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+def gpu_gemm(casc, d, y=14, **kw):
+    return [N(x) for x in casc.casc_i8_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                                   T(d["B_lo"]), y=y, **kw)]
+
+
+def bitwise(x, y):
+    return np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+SHAPES = [(0, 64, 64, 64), (1, 130, 257, 300), (2, 200, 129, 1000), (1, 1, 1, 1),
+          (1, 3, 5, 9), (1, 128, 128, 128), (1, 40, 33, 8192 + 257)]
+
+
+# ------------------------------------------------------------------ split (R22, R23)
+@pytest.mark.parametrize("cfg,m,n,k", SHAPES)
+def test_i8_split_bit_exact(casc, orc, cfg, m, n, k):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    DA, EA = (N(x) for x in casc.casc_i8_split(T(d["A_hi"]), T(d["A_lo"]), False))
+    DB, EB = (N(x) for x in casc.casc_i8_split(T(d["B_hi"]), T(d["B_lo"]), True))
+    for q, p0 in enumerate(range(0, k, 8192)):
+        p1 = min(k, p0 + 8192)
+        oa, oe = orc.i8_split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], 14)
+        ob, of = orc.i8_split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], 14)
+        assert np.array_equal(EA[q], oe) and np.array_equal(EB[q], of)
+        assert np.array_equal(DA[:, :, p0:p1], oa)
+        assert np.array_equal(DB[:, :, p0:p1], ob)
+
+
+def test_i8_split_full_mantissa_and_slices(casc, orc):
+    """Leading zeros, full mantissas and every slice count y = 3 .. 15."""
+    hi, lo = I.full_mantissa(21, 70, 300, max_shift=60)
+    for y in (3, 7, 14, 15):
+        D, E = (N(x) for x in casc.casc_i8_split(T(hi), T(lo), False, y=y))
+        od, oe = orc.i8_split_a_panel(hi, lo, y)
+        assert np.array_equal(D, od) and np.array_equal(E[0], oe)
+
+
+# ------------------------------------------------------------------ bins (R24)
+@pytest.mark.parametrize("cfg,m,n,k,panel", [(1, 130, 257, 300, 0), (2, 64, 200, 1000, 0),
+                                             (1, 40, 33, 8192 + 257, 1),
+                                             (1, 40, 33, 8192 + 257, 0)])
+def test_i8_bins_bit_exact(casc, orc, cfg, m, n, k, panel):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    bins = N(casc.casc_i8_debug_bins(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]),
+                                     panel=panel))
+    p0, p1 = panel * 8192, min(k, panel * 8192 + 8192)
+    oa, _ = orc.i8_split_a_panel(d["A_hi"][:, p0:p1], d["A_lo"][:, p0:p1], 14)
+    ob, _ = orc.i8_split_b_panel(d["B_hi"][p0:p1], d["B_lo"][p0:p1], 14)
+    ob_bins = orc.i8_panel_bins(oa, ob)
+    assert np.array_equal(bins.astype(np.int64), ob_bins)
+
+
+# ------------------------------------------------------------------ C and flags (R25, R26)
+@pytest.mark.parametrize("cfg,m,n,k", SHAPES)
+def test_i8_gemm_bit_exact(casc, orc, cfg, m, n, k):
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo)
+    assert np.array_equal(fl, ofl)
+
+
+@pytest.mark.parametrize("y", [3, 5, 8, 15])
+def test_i8_gemm_slice_counts(casc, orc, y):
+    d = I.make_config(1, m=150, n=140, k=700, seed=y)
+    C_hi, C_lo, fl = gpu_gemm(casc, d, y=y)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], y)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
+
+
+def test_i8_within_north_star_bound(casc, orc):
+    d = I.make_config(2, m=160, n=150, k=2000, seed=5)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    ii, jj = np.meshgrid(np.arange(0, 160, 3), np.arange(0, 150, 7), indexing="ij")
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel(),
+                          C_hi, C_lo)
+    assert np.max(np.abs(r["err"]) / orc.north_star_bound(2000, r["absab"])) <= 1.0
+    assert fl.sum() == 0
+
+
+@pytest.mark.parametrize("variant,expect", [("a", "none"), ("b", "all"), ("c", "all")])
+def test_i8_cancellation_flags(casc, orc, variant, expect):
+    """cfg3 structure (R13 with the 8192 panel of R22): flags identical to the
+    oracle's; 3b / 3c cancel inside one panel and are flagged everywhere."""
+    d = I.make_config(3, m=70, n=64, k=2048, variant=variant)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
+    assert (fl.sum() == 0) if expect == "none" else fl.all()
+
+
+def test_i8_strided_and_edge_cases(casc, orc):
+    import torch
+    d = I.make_config(1, m=50, n=60, k=70, seed=3)
+    # leading dimensions larger than the logical sizes (views into wider buffers)
+    Ah = torch.zeros((50, 90), dtype=torch.float64, device="cuda")
+    Al = torch.zeros_like(Ah)
+    Bh = torch.zeros((70, 75), dtype=torch.float64, device="cuda")
+    Bl = torch.zeros_like(Bh)
+    Ah[:, :70] = T(d["A_hi"]); Al[:, :70] = T(d["A_lo"])
+    Bh[:, :60] = T(d["B_hi"]); Bl[:, :60] = T(d["B_lo"])
+    Ch = torch.full((50, 64), 7.0, dtype=torch.float64, device="cuda")
+    Cl = torch.full((50, 64), 7.0, dtype=torch.float64, device="cuda")
+    c_hi, c_lo, fl = casc.casc_i8_gemm_fp64x2(Ah[:, :70], Al[:, :70], Bh[:, :60], Bl[:, :60],
+                                              C_hi=Ch[:, :60], C_lo=Cl[:, :60])
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
+    assert bitwise(N(c_hi), o_hi) and bitwise(N(c_lo), o_lo) and np.array_equal(N(fl), ofl)
+    assert bool((Ch[:, 60:] == 7.0).all()) and bool((Cl[:, 60:] == 7.0).all())
+    # k == 0: C := 0, flags := 0
+    z = torch.zeros((4, 0), dtype=torch.float64, device="cuda")
+    zb = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    c_hi, c_lo, fl = casc.casc_i8_gemm_fp64x2(z, z, zb, zb)
+    assert not c_hi.any() and not c_lo.any() and not fl.any()
+    # invalid slice counts
+    with pytest.raises(casc.CascError):
+        casc.casc_i8_gemm_fp64x2(Ah[:, :70], Al[:, :70], Bh[:, :60], Bl[:, :60], y=2)
+    with pytest.raises(casc.CascError):
+        casc.casc_i8_gemm_fp64x2(Ah[:, :70], Al[:, :70], Bh[:, :60], Bl[:, :60], y=16)
+
+
+def test_i8_deterministic_and_workspace(casc, orc):
+    import torch
+    d = I.make_config(1, m=300, n=260, k=900, seed=8)
+    a = gpu_gemm(casc, d)
+    ws = torch.empty(casc.casc_i8_workspace_bytes(300, 260, 900), dtype=torch.uint8,
+                     device="cuda")
+    b = gpu_gemm(casc, d, workspace=ws)
+    assert all(np.array_equal(x, z) for x, z in zip(a, b))
+
+
+def test_i8_sampled_full_size_cfg1(casc, orc):
+    """cfg1 (1024^3) in one launch, 24 sampled rows x all columns bit-exact."""
+    d = I.make_config(1)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    rows = np.arange(0, 1024, 43)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"], d["B_lo"])
+    assert bitwise(C_hi[rows], o_hi) and bitwise(C_lo[rows], o_lo)
+    assert np.array_equal(fl[rows], ofl)
