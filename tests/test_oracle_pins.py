@@ -265,7 +265,7 @@ def test_mutation_canary_alignment(orc, tmp_path):
     import oracle
     so = str(tmp_path / "liboracle_mut.so")
     subprocess.check_call(["gcc", *oracle.CFLAGS, "-DORC_MUTATE_ALIGN", "-o", so,
-                           oracle._SRC, "-lm"])
+                           oracle._SRC, oracle._SRC_I8, "-lm"])
     L = ctypes.CDLL(so)
     oracle._setup(L)
     d = I.make_config(1, m=3, n=3, k=64, seed=5)
