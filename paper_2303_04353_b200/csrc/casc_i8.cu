@@ -26,7 +26,7 @@
 //        moves every operand tile with ONE cp.async.bulk and points the MMA
 //        descriptor at it.
 // Phase 2+3: i8_gemm_kernel, persistent (one CTA per SM), 384 threads:
-//   warp 0     TMA producer: 16 KB chunks into an A ring (6 slots) and a B ring
+//   warp 0     TMA producer: 16 KB chunks into an A ring (8 slots) and a B ring
 //              (4 slots), mbarrier complete_tx;
 //   warp 1     MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::i8,
 //              M = N = 128, K = 32, s8 x s8 -> s32; the four bins of a group
@@ -61,7 +61,7 @@ constexpr int KBP = KC8 / KB;      // k blocks per panel (64)
 constexpr int TR = 128;            // rows (A) / columns (B) per chunk = tile edge
 constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
-constexpr int NSA = 6, NSB = 4;    // smem ring slots (16 KB each)
+constexpr int NSA = 8, NSB = 4;    // smem ring slots (16 KB each)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
 constexpr int THREADS = 384;
 constexpr int EPI_WARP0 = 4, EPI_THREADS = 256;
@@ -276,16 +276,49 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 // instruction descriptor: s8 x s8 -> s32, K-major A and B, M = N = 128
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
                            ((uint32_t)(128 >> 4) << 24);
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+// One elected lane arms `bar` for CHUNK bytes and issues the TMA bulk copy.
+__device__ __forceinline__ void tma_load_elect(void* dst, const void* src, uint64_t* bar) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(acc), "n"(IDESC));
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(smem_u32(bar)), "n"(CHUNK)
+      : "memory");
 }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+// Four MMAs (K = 4 x 32 bytes, one 128-byte chunk) into accumulator tmem_d,
+// issued by one elected lane of the (converged) calling warp.  acc == 0: the
+// first overwrites the accumulator.
+__device__ __forceinline__ void mma_i8_x4(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred e, p, t;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %3, 0;\n"
+      "setp.eq.b32 t, 0, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %5, %6, %4, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %7, %8, %4, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %9, %10, %4, t;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(acc), "n"(IDESC), "l"(a + 2), "l"(b + 2), "l"(a + 4), "l"(b + 4),
+      "l"(a + 6), "l"(b + 6));
+}
+// tcgen05.commit to one / two mbarriers from one elected lane
+__device__ __forceinline__ void mma_commit1(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n}\n" ::"r"(
+          smem_u32(bar0)),
+      "r"(smem_u32(bar1))
+      : "memory");
 }
 
 __device__ __forceinline__ void tile_of(int tile, int64_t RA, int64_t RB, int64_t& rb,
@@ -346,90 +379,91 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
   const int tiles = (int)(RA * RB);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ============================ TMA producer ============================
-      uint32_t aseq = 0, bseq = 0;
-      auto loadA = [&](int i, int64_t rb, int64_t kb) {
-        const uint32_t s = aseq % NSA;
-        mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
-        mbar_arrive_expect_tx(&fullA[s], CHUNK);
-        tma_bulk_g2s(sA + s * CHUNK, p.pa + chunk_off(p.ga, i, rb, kb), CHUNK, &fullA[s]);
-        ++aseq;
-      };
-      auto loadB = [&](int j, int64_t cb, int64_t kb) {
-        const uint32_t s = bseq % NSB;
-        mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
-        mbar_arrive_expect_tx(&fullB[s], CHUNK);
-        tma_bulk_g2s(sB + s * CHUNK, p.pb + chunk_off(p.gb, j, cb, kb), CHUNK, &fullB[s]);
-        ++bseq;
-      };
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        int64_t rb, cb;
-        tile_of(tile, RA, RB, rb, cb);
-        for (int q = 0; q < P; ++q) {
-          const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
-          for (int grp = 0; grp < ngroups; ++grp) {
-            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
-            for (int64_t kb = kb0; kb < kb1; ++kb) {
-              for (int i = top; i >= s; --i) loadA(i, rb, kb);
-              loadB(0, cb, kb);
-              for (int j = 1; j <= top; ++j) {
-                if (s - j >= 0) loadA(s - j, rb, kb);
-                loadB(j, cb, kb);
-              }
+    // ============================ TMA producer ============================
+    // all lanes run the loop; one elected lane arms the barrier and issues the copy
+    uint32_t aseq = 0, bseq = 0;
+    auto loadA = [&](int i, int64_t rb, int64_t kb) {
+      const uint32_t s = aseq % NSA;
+      mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
+      tma_load_elect(sA + s * CHUNK, p.pa + chunk_off(p.ga, i, rb, kb), &fullA[s]);
+      ++aseq;
+    };
+    auto loadB = [&](int j, int64_t cb, int64_t kb) {
+      const uint32_t s = bseq % NSB;
+      mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
+      tma_load_elect(sB + s * CHUNK, p.pb + chunk_off(p.gb, j, cb, kb), &fullB[s]);
+      ++bseq;
+    };
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int64_t rb, cb;
+      tile_of(tile, RA, RB, rb, cb);
+      for (int q = 0; q < P; ++q) {
+        const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
+        for (int grp = 0; grp < ngroups; ++grp) {
+          const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+          for (int64_t kb = kb0; kb < kb1; ++kb) {
+            for (int i = top; i >= s; --i) loadA(i, rb, kb);
+            loadB(0, cb, kb);
+            for (int j = 1; j <= top; ++j) {
+              if (s - j >= 0) loadA(s - j, rb, kb);
+              loadB(j, cb, kb);
             }
           }
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ============================ MMA issuer ============================
-      uint32_t aseq = 0, bseq = 0, gcount = 0;
-      const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        for (int q = 0; q < P; ++q) {
-          const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
-          for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
-            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
-            mbar_wait(tempty, (gcount & 1) ^ 1);
-            tc_fence_after();
-            uint32_t touched = 0;
-            for (int64_t kb = kb0; kb < kb1; ++kb) {
-              const uint32_t abase = aseq;
-              for (int j = 0; j <= top; ++j) {
-                const uint32_t bs = bseq % NSB;
-                mbar_wait(&fullB[bs], (bseq / NSB) & 1);
-                const int ilo = max(0, s - j), ihi = top - j;
-                for (int i = ihi; i >= ilo; --i) {
-                  const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
-                  const uint32_t as = aq % NSA;
-                  mbar_wait(&fullA[as], (aq / NSA) & 1);
-                  tc_fence_after();
-                  const int b = i + j - s;
-                  const uint64_t ad = sdesc(a_base_addr + as * CHUNK);
-                  const uint64_t bd = sdesc(b_base_addr + bs * CHUNK);
-                  const uint32_t first = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
-#pragma unroll
-                  for (int kk = 0; kk < 4; ++kk)
-                    mma_i8(tmem + b * 128, ad + 2 * kk, bd + 2 * kk, kk ? 1u : first);
-                  touched |= 1u << b;
+    // ============================ MMA issuer ============================
+    // All 32 lanes run the loop (warp-uniform control flow, so the scalar state
+    // and the descriptors live in the uniform datapath); elect.sync inside the
+    // issue blocks picks the one lane that issues each tcgen05 operation.
+    uint32_t aseq = 0, bseq = 0, gcount = 0;
+    const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int q = 0; q < P; ++q) {
+        const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
+        for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+          const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+          mbar_wait(tempty, (gcount & 1) ^ 1);
+          tc_fence_after();
+          uint32_t touched = 0;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            const uint32_t abase = aseq;
+            for (int j = 0; j <= top; ++j) {
+              const uint32_t bs = bseq % NSB;
+              mbar_wait(&fullB[bs], (bseq / NSB) & 1);
+              // A operands first used at this step: A_top..A_s at j = 0, A_(s-j) after
+              if (j == 0) {
+                for (int i = 0; i < nb; ++i) {
+                  const uint32_t aq = abase + i;
+                  mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
                 }
-                mma_commit(&emptyB[bs]);
-                ++bseq;
-                // A_(top-j) has met its last partner
-                const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
-                mma_commit(&emptyA[rq % NSA]);
+              } else if (s - j >= 0) {
+                const uint32_t aq = abase + nb + (j - 1);
+                mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
               }
-              aseq = abase + (uint32_t)(s + nb);
+              tc_fence_after();
+              const uint64_t bd = sdesc(b_base_addr + bs * CHUNK);
+              const int ilo = max(0, s - j), ihi = top - j;
+              for (int i = ihi; i >= ilo; --i) {
+                const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
+                const uint64_t ad = sdesc(a_base_addr + (aq % NSA) * CHUNK);
+                const int b = i + j - s;
+                const uint32_t acc = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
+                mma_i8_x4(tmem + b * 128, ad, bd, acc);
+                touched |= 1u << b;
+              }
+              // B_j is done; A_(top-j) has met its last partner
+              const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
+              mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
+              ++bseq;
             }
-            mma_commit(tfull);
+            aseq = abase + (uint32_t)(s + nb);
           }
+          mma_commit1(tfull);
         }
       }
     }
-    __syncwarp();
   } else if (warp >= EPI_WARP0) {
     // ============================ epilogue ============================
     const int ew = warp - EPI_WARP0;
