@@ -40,6 +40,7 @@
 //              quarter w%4, column half (w-4)/4), exact group value, FP64x2
 //              panel sum T and C in a per-CTA workspace (L2-resident), detector,
 //              final store of C and the flags.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -61,12 +62,12 @@ constexpr int KBP = KC8 / KB;      // k blocks per panel (64)
 constexpr int TR = 128;            // rows (A) / columns (B) per chunk = tile edge
 constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
-constexpr int NSA = 8, NSB = 4;    // smem ring slots (16 KB each)
+constexpr int NSA = 8, NSB = 8;    // smem ring slots (A: 16 KB, B: 8 KB half chunks)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
 constexpr int THREADS = 384;
 constexpr int EPI_WARP0 = 4, EPI_THREADS = 256;
 constexpr int GROUP_M = 12;        // tile raster: 12 row blocks sweep the column blocks
-constexpr size_t SMEM = (size_t)(NSA + NSB) * CHUNK + 1024 + 256;
+constexpr size_t SMEM = (size_t)NSA * CHUNK + (size_t)NSB * (CHUNK / 2) + 1024 + 1024;
 
 struct Pack {
   int64_t R;    // 128-row blocks
@@ -75,7 +76,8 @@ struct Pack {
   int y;
 };
 __host__ __device__ inline Pack pack_of(int64_t rows, int64_t k, int y) {
-  return Pack{(rows + TR - 1) / TR, (k + KB - 1) / KB, (k + KC8 - 1) / KC8, y};
+  // R is even: the GEMM's CTA pairs take 128-row blocks two at a time
+  return Pack{(rows + 2 * TR - 1) / (2 * TR) * 2, (k + KB - 1) / KB, (k + KC8 - 1) / KC8, y};
 }
 __host__ __device__ inline int64_t slice_bytes(const Pack& g) {
   return (int64_t)g.y * g.R * g.KBn * CHUNK;
@@ -273,73 +275,124 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = N = 128
+// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 256 (CTA pair), N = 128
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
-// One elected lane arms `bar` for CHUNK bytes and issues the TMA bulk copy.
-__device__ __forceinline__ void tma_load_elect(void* dst, const void* src, uint64_t* bar) {
+                           ((uint32_t)(256 >> 4) << 24);
+constexpr int BHALF = CHUNK / 2;   // each CTA of the pair holds 64 of the 128 B rows
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same offset in CTA rank 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, [%2];\n"
+      "{\n.reg .pred P1;\nWAIT_C:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_C;\nbra WAIT_C;\nDONE_C:\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
+}
+// One elected lane: (leader only) arm the leader's barrier for both CTAs' bytes,
+// then a 2-SM TMA of `rows` 128-byte rows at row coordinate y of `map` into this
+// CTA's smem, completing on the LEADER's barrier (bar_cluster).
+__device__ __forceinline__ void tma_pair_elect(void* dst, const CUtensorMap* map, int y,
+                                               uint64_t* bar_local, uint32_t bar_cluster,
+                                               uint32_t arm_bytes) {
+  asm volatile(
+      "{\n.reg .pred e, l;\nelect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 l, %4, 0;\n"
+      "and.pred l, l, e;\n"
+      "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %4;\n"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%5, %2}], [%6];\n"
       "}\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(smem_u32(bar)), "n"(CHUNK)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(y), "r"(smem_u32(bar_local)), "r"(arm_bytes),
+      "r"(0), "r"(bar_cluster)
       : "memory");
 }
 // Four MMAs (K = 4 x 32 bytes, one 128-byte chunk) into accumulator tmem_d,
-// issued by one elected lane of the (converged) calling warp.  acc == 0: the
-// first overwrites the accumulator.
+// issued by one elected lane of the (converged) leader MMA warp for the pair.
+// acc == 0: the first overwrites the accumulator.
 __device__ __forceinline__ void mma_i8_x4(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred e, p, t;\n"
       "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %3, 0;\n"
       "setp.eq.b32 t, 0, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %5, %6, %4, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %7, %8, %4, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %9, %10, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %4, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %5, %6, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %7, %8, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %9, %10, %4, t;\n"
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(acc), "n"(IDESC), "l"(a + 2), "l"(b + 2), "l"(a + 4), "l"(b + 4),
       "l"(a + 6), "l"(b + 6));
 }
-// tcgen05.commit to one / two mbarriers from one elected lane
+// tcgen05.commit (multicast to both CTAs of the pair) to one / two mbarriers
 __device__ __forceinline__ void mma_commit1(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-          smem_u32(bar))
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n}\n" ::"r"(
-          smem_u32(bar0)),
-      "r"(smem_u32(bar1))
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %2;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%1], %2;\n}\n" ::"r"(smem_u32(bar0)),
+      "r"(smem_u32(bar1)), "h"((uint16_t)3)
       : "memory");
 }
 
-__device__ __forceinline__ void tile_of(int tile, int64_t RA, int64_t RB, int64_t& rb,
+// named barrier 1 over the 256 epilogue threads
+__device__ __forceinline__ void epi_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+}
+
+// pair tile (256 rows x 128 columns) -> (row-pair block, column block), raster
+// of GROUP_M row-pair blocks sweeping the column blocks
+__device__ __forceinline__ void tile_of(int tile, int64_t RP, int64_t RB, int64_t& rp,
                                         int64_t& cb) {
   const int64_t per = (int64_t)GROUP_M * RB;
   const int64_t grp = tile / per;
   const int64_t first = grp * GROUP_M;
-  const int64_t gs = min((int64_t)GROUP_M, RA - first);
+  const int64_t gs = min((int64_t)GROUP_M, RP - first);
   const int64_t rr = tile % per;
-  rb = first + rr % gs;
+  rp = first + rr % gs;
   cb = rr / gs;
 }
 
+// The fused kernel on CTA pairs (cluster of 2, tcgen05 cta_group::2): the pair
+// computes a 256 x 128 C tile; CTA r holds A rows 128r..128r+127 of it and
+// rows 64r..64r+63 of every 128 x 128-byte B chunk; the leader (r = 0) issues
+// the M = 256 MMAs for both, each CTA's tensor memory holds its 128 rows.
 template <bool DBG>
-__global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    i8_gemm_kernel(const GemmArgs p, const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapB) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + NSA * CHUNK;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSB * CHUNK);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NSB * BHALF);
   uint64_t* fullA = bars;
   uint64_t* emptyA = fullA + NSA;
   uint64_t* fullB = emptyA + NSA;
@@ -347,8 +400,11 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
   uint64_t* tfull = emptyB + NSB;
   uint64_t* tempty = tfull + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int32_t* sF = reinterpret_cast<int32_t*>(tempty + 2);  // column exponents [128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSA; ++i) {
       mbar_init(&fullA[i], 1);
@@ -359,44 +415,52 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
       mbar_init(&emptyB[i], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, EPI_THREADS / 32);
+    mbar_init(tempty, 2 * EPI_THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
   const int y = p.ga.y;
   const int ngroups = (y + NBIN - 1) / NBIN;
   const int64_t RA = p.ga.R, RB = p.gb.R, KBn = p.ga.KBn;
+  const int64_t RP = RA / 2;
   const int P = (int)p.ga.P;
-  const int tiles = (int)(RA * RB);
+  const int tiles = (int)(RP * RB);
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (warp == 0) {
-    // ============================ TMA producer ============================
-    // all lanes run the loop; one elected lane arms the barrier and issues the copy
+    // ============================ TMA producer (both CTAs) ============================
+    // all lanes run the loop; one elected lane arms / issues; the data of both
+    // CTAs completes on the leader's full barriers
     uint32_t aseq = 0, bseq = 0;
     auto loadA = [&](int i, int64_t rb, int64_t kb) {
       const uint32_t s = aseq % NSA;
       mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
-      tma_load_elect(sA + s * CHUNK, p.pa + chunk_off(p.ga, i, rb, kb), &fullA[s]);
+      const int row = (int)(((i * p.ga.R + rb) * KBn + kb) * TR);
+      tma_pair_elect(sA + s * CHUNK, &mapA, row, &fullA[s], leader_addr(&fullA[s]),
+                     leader ? 2 * CHUNK : 0);
       ++aseq;
     };
     auto loadB = [&](int j, int64_t cb, int64_t kb) {
       const uint32_t s = bseq % NSB;
       mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
-      tma_load_elect(sB + s * CHUNK, p.pb + chunk_off(p.gb, j, cb, kb), &fullB[s]);
+      const int row = (int)(((j * p.gb.R + cb) * KBn + kb) * TR + rank * (TR / 2));
+      tma_pair_elect(sB + s * BHALF, &mapB, row, &fullB[s], leader_addr(&fullB[s]),
+                     leader ? 2 * BHALF : 0);
       ++bseq;
     };
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      int64_t rb, cb;
-      tile_of(tile, RA, RB, rb, cb);
+    for (int tile = pair; tile < tiles; tile += npairs) {
+      int64_t rp, cb;
+      tile_of(tile, RP, RB, rp, cb);
+      const int64_t rb = 2 * rp + rank;
       for (int q = 0; q < P; ++q) {
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
         for (int grp = 0; grp < ngroups; ++grp) {
@@ -413,63 +477,66 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
       }
     }
   } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    // All 32 lanes run the loop (warp-uniform control flow, so the scalar state
-    // and the descriptors live in the uniform datapath); elect.sync inside the
-    // issue blocks picks the one lane that issues each tcgen05 operation.
-    uint32_t aseq = 0, bseq = 0, gcount = 0;
-    const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      for (int q = 0; q < P; ++q) {
-        const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
-        for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
-          const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
-          mbar_wait(tempty, (gcount & 1) ^ 1);
-          tc_fence_after();
-          uint32_t touched = 0;
-          for (int kb = kb0; kb < kb1; ++kb) {
-            const uint32_t abase = aseq;
-            for (int j = 0; j <= top; ++j) {
-              const uint32_t bs = bseq % NSB;
-              mbar_wait(&fullB[bs], (bseq / NSB) & 1);
-              // A operands first used at this step: A_top..A_s at j = 0, A_(s-j) after
-              if (j == 0) {
-                for (int i = 0; i < nb; ++i) {
-                  const uint32_t aq = abase + i;
+    if (leader) {
+      // ============================ MMA issuer (leader CTA) ============================
+      // All 32 lanes run the loop (warp-uniform control flow, so the scalar state
+      // and the descriptors live in the uniform datapath); elect.sync inside the
+      // issue blocks picks the one lane that issues each tcgen05 operation.
+      uint32_t aseq = 0, bseq = 0, gcount = 0;
+      const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        for (int q = 0; q < P; ++q) {
+          const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
+          for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+            mbar_wait_cluster(tempty, (gcount & 1) ^ 1);
+            tc_fence_after();
+            uint32_t touched = 0;
+            for (int kb = kb0; kb < kb1; ++kb) {
+              const uint32_t abase = aseq;
+              for (int j = 0; j <= top; ++j) {
+                const uint32_t bs = bseq % NSB;
+                mbar_wait(&fullB[bs], (bseq / NSB) & 1);
+                // A operands first used at this step: A_top..A_s at j = 0, A_(s-j) after
+                if (j == 0) {
+                  for (int i = 0; i < nb; ++i) {
+                    const uint32_t aq = abase + i;
+                    mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
+                  }
+                } else if (s - j >= 0) {
+                  const uint32_t aq = abase + nb + (j - 1);
                   mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
                 }
-              } else if (s - j >= 0) {
-                const uint32_t aq = abase + nb + (j - 1);
-                mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
+                tc_fence_after();
+                const uint64_t bd = sdesc(b_base_addr + bs * BHALF);
+                const int ilo = max(0, s - j), ihi = top - j;
+                for (int i = ihi; i >= ilo; --i) {
+                  const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
+                  const uint64_t ad = sdesc(a_base_addr + (aq % NSA) * CHUNK);
+                  const int b = i + j - s;
+                  const uint32_t acc = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
+                  mma_i8_x4(tmem + b * 128, ad, bd, acc);
+                  touched |= 1u << b;
+                }
+                // B_j is done; A_(top-j) has met its last partner
+                const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
+                mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
+                ++bseq;
               }
-              tc_fence_after();
-              const uint64_t bd = sdesc(b_base_addr + bs * CHUNK);
-              const int ilo = max(0, s - j), ihi = top - j;
-              for (int i = ihi; i >= ilo; --i) {
-                const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
-                const uint64_t ad = sdesc(a_base_addr + (aq % NSA) * CHUNK);
-                const int b = i + j - s;
-                const uint32_t acc = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
-                mma_i8_x4(tmem + b * 128, ad, bd, acc);
-                touched |= 1u << b;
-              }
-              // B_j is done; A_(top-j) has met its last partner
-              const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
-              mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
-              ++bseq;
+              aseq = abase + (uint32_t)(s + nb);
             }
-            aseq = abase + (uint32_t)(s + nb);
+            mma_commit1(tfull);
           }
-          mma_commit1(tfull);
         }
       }
     }
   } else if (warp >= EPI_WARP0) {
-    // ============================ epilogue ============================
+    // ============================ epilogue (both CTAs) ============================
     const int ew = warp - EPI_WARP0;
     const int quarter = warp & 3, half = ew >> 2;
     const int lr = quarter * 32 + lane;       // tile row = TMEM lane
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t tempty_leader = leader_addr(tempty);
     double* Th = p.ws + (int64_t)blockIdx.x * 4 * (TR * TR);
     double* Tl = Th + TR * TR;
     double* Ch = Tl + TR * TR;
@@ -477,35 +544,57 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
     const int32_t* EA = reinterpret_cast<const int32_t*>(p.pa + exp_off(p.ga));
     const int32_t* EB = reinterpret_cast<const int32_t*>(p.pb + exp_off(p.gb));
     uint32_t gcount = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      int64_t rb, cb;
-      tile_of(tile, RA, RB, rb, cb);
-      const int64_t gi = rb * TR + lr;
+    for (int tile = pair; tile < tiles; tile += npairs) {
+      int64_t rp, cb;
+      tile_of(tile, RP, RB, rp, cb);
+      const int64_t gi = (2 * rp + rank) * TR + lr;
       uint64_t fl = 0;  // detector bits of this thread's 64 columns
       for (int q = 0; q < P; ++q) {
         const int64_t kp = min((int64_t)KC8, p.k - (int64_t)q * KC8);
         const int ei = EA[(int64_t)q * RA * TR + gi];
+        // column exponents of this (tile, panel) -> shared memory
+        epi_bar_sync();
+        if (ew < 4) sF[ew * 32 + lane] = EB[(int64_t)q * RB * TR + cb * TR + ew * 32 + lane];
+        epi_bar_sync();
         for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
           const int s = grp * NBIN, nb = min(NBIN, y - s);
+          const bool needT = grp > 0, lastg = grp + 1 == ngroups, needC = lastg && q > 0;
           mbar_wait(tfull, gcount & 1);
           tc_fence_after();
-          for (int cc = 0; cc < 4; ++cc) {
-            const int c0 = half * 64 + cc * 16;
-            uint32_t r0[16], r1[16], r2[16], r3[16];
-            tmem_ld16(trow + 0 * 128 + c0, r0);
-            if (nb > 1) tmem_ld16(trow + 1 * 128 + c0, r1);
-            if (nb > 2) tmem_ld16(trow + 2 * 128 + c0, r2);
-            if (nb > 3) tmem_ld16(trow + 3 * 128 + c0, r3);
+          for (int cc = 0; cc < 8; ++cc) {
+            const int c0 = half * 64 + cc * 8;
+            uint32_t r0[8], r1[8], r2[8], r3[8];
+            tmem_ld8(trow + 0 * 128 + c0, r0);
+            if (nb > 1) tmem_ld8(trow + 1 * 128 + c0, r1);
+            if (nb > 2) tmem_ld8(trow + 2 * 128 + c0, r2);
+            if (nb > 3) tmem_ld8(trow + 3 * 128 + c0, r3);
+            // the running panel sum T and C of these 8 elements (independent loads,
+            // issued together while the TMEM loads are in flight)
+            double xth[8], xtl[8], xch[8], xcl[8];
+            if (!DBG && needT) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                xth[i] = Th[(c0 + i) * TR + lr];
+                xtl[i] = Tl[(c0 + i) * TR + lr];
+              }
+            }
+            if (!DBG && needC) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                xch[i] = Ch[(c0 + i) * TR + lr];
+                xcl[i] = Cl[(c0 + i) * TR + lr];
+              }
+            }
             tmem_wait_ld();
-            if (cc == 3) {  // this warp's part of TMEM is read: the next group may start
+            if (cc == 7) {  // this warp's part of TMEM is read: the next group may start
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(tempty);
+              if (lane == 0) mbar_arrive_cluster(tempty_leader);
             }
             if (DBG) {
               if (q == p.dbg_panel) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < 8; ++i) {
                   const int64_t gj = cb * TR + c0 + i;
                   if (gi < p.m && gj < p.n) {
                     const int64_t mn = p.m * p.n, o = gi * p.n + gj;
@@ -519,10 +608,9 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
               continue;
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < 8; ++i) {
               const int lc = c0 + i;
-              const int64_t gj = cb * TR + lc;
-              const int fj = __ldg(EB + (int64_t)q * RB * TR + gj);
+              const int fj = sF[lc];
               // R25: exact group value (hi = RN(V), lo = V - hi)
               double gh, gl;
               const double b0 = (double)(int32_t)r0[i];
@@ -541,28 +629,27 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
               gh = mulp2(gh, w);
               gl = mulp2(gl, w);
               const int widx = lc * TR + lr;
-              double th, tl;
-              if (grp == 0) {
-                th = gh;
-                tl = gl;
-              } else {
-                dd_add(Th[widx], Tl[widx], gh, gl, th, tl);
-              }
-              if (grp + 1 < ngroups) {
+              double th = gh, tl = gl;
+              if (needT) dd_add(xth[i], xtl[i], gh, gl, th, tl);
+              if (!lastg) {
                 Th[widx] = th;
                 Tl[widx] = tl;
               } else {
                 // R26 detector, then C (+)= T
                 if (fabs(th) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * 64);
                 double ch = th, cl = tl;
-                if (q > 0) dd_add(Ch[widx], Cl[widx], th, tl, ch, cl);
+                if (needC) dd_add(xch[i], xcl[i], th, tl, ch, cl);
                 if (q + 1 < P) {
                   Ch[widx] = ch;
                   Cl[widx] = cl;
-                } else if (gi < p.m && gj < p.n) {
-                  p.C_hi[gi * p.ldc + gj] = ch;
-                  p.C_lo[gi * p.ldc + gj] = cl;
-                  if (p.flags) p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
+                } else {
+                  const int64_t gj = cb * TR + lc;
+                  if (gi < p.m && gj < p.n) {
+                    p.C_hi[gi * p.ldc + gj] = ch;
+                    p.C_lo[gi * p.ldc + gj] = cl;
+                    if (p.flags)
+                      p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
+                  }
                 }
               }
             }
@@ -572,10 +659,10 @@ __global__ void __launch_bounds__(THREADS, 1) i8_gemm_kernel(const GemmArgs p) {
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -608,11 +695,41 @@ cudaError_t unpack(const void* packed, int64_t rows, int64_t k, int y, int8_t* D
   return cudaGetLastError();
 }
 
-int grid_for(int64_t m, int64_t n, int sms) {
-  const int64_t tiles = ((m + TR - 1) / TR) * ((n + TR - 1) / TR);
-  return (int)(tiles < sms ? tiles : sms);
+int grid_for(int64_t m, int64_t n, int sms) {  // CTAs: 2 per pair, one pair per 2 SMs
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
+  return (int)(2 * pairs);
 }
 size_t cta_ws_bytes(int grid) { return (size_t)grid * 4 * TR * TR * sizeof(double); }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D view of a packed operand's slices as 128-byte rows; `box_rows` rows per copy.
+// The chunks are pre-swizzled, so the map copies bytes verbatim (SWIZZLE_NONE).
+cudaError_t slice_map(CUtensorMap* map, const void* packed, const Pack& g, uint32_t box_rows) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !enc)
+      return cudaErrorNotSupported;
+  }
+  const uint64_t rows = (uint64_t)g.y * g.R * g.KBn * TR;
+  if (rows >= (1ull << 31)) return cudaErrorInvalidValue;  // int32 TMA coordinates
+  cuuint64_t dims[2] = {(cuuint64_t)KB, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)KB};
+  cuuint32_t box[2] = {(cuuint32_t)KB, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(packed), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
                  double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
@@ -632,14 +749,18 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   a.ws = ws;
   a.dbg = dbg;
   a.dbg_panel = dbg_panel;
+  CUtensorMap mA, mB;
+  cudaError_t e = slice_map(&mA, pa, a.ga, TR);
+  if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TR / 2);
+  if (e != cudaSuccess) return e;
   if (dbg) {
     cudaFuncSetAttribute(i8_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SMEM);
-    i8_gemm_kernel<true><<<grid, THREADS, SMEM, st>>>(a);
+    i8_gemm_kernel<true><<<grid, THREADS, SMEM, st>>>(a, mA, mB);
   } else {
     cudaFuncSetAttribute(i8_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SMEM);
-    i8_gemm_kernel<false><<<grid, THREADS, SMEM, st>>>(a);
+    i8_gemm_kernel<false><<<grid, THREADS, SMEM, st>>>(a, mA, mB);
   }
   return cudaGetLastError();
 }
