@@ -135,7 +135,11 @@ __global__ void __launch_bounds__(128) probe_tput(int32_t* out, int iters) {
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int t = threadIdx.x, w = t >> 5;
-  for (int i = t; i < (M + N) * 128; i += 128) smem[i] = (uint8_t)(i * 7 + blockIdx.x);
+  for (int i = t; i < (M + N) * 128; i += 128) {  // random bytes (realistic bit activity)
+    uint32_t h = (uint32_t)i * 0x9E3779B1u + blockIdx.x * 0x85EBCA6Bu;
+    h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+    smem[i] = (uint8_t)h;
+  }
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tbase)),
@@ -231,7 +235,7 @@ static void run_tput(int blocks_per_sm) {
   }
   const double ops = 2.0 * M * N * 128.0 * iters * grid;  // 4 MMAs of K=32 per iter
   // sustained: back to back for ~3 s
-  int launches = (int)(3000.0 / best) + 1;
+  int launches = (int)(5000.0 / best) + 1;
   CK(cudaEventRecord(e0));
   for (int r = 0; r < launches; ++r) probe_tput<N><<<grid, 128, smem>>>(out, iters);
   CK(cudaEventRecord(e1));

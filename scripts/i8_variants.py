@@ -1,0 +1,29 @@
+"""Experiment builds of the INT8-cascade GEMM (timing studies only):
+python scripts/i8_variants.py build [names] | run N [names]"""
+import json, os, subprocess, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+VARIANTS = {
+    "base": [],
+    "noepi": ["CASC_I8_NO_EPI"],
+    "sleep": ["CASC_I8_EPI_SLEEP=200"],
+    "g4": ["CASC_I8_GROUP_M=4"],
+    "g32": ["CASC_I8_GROUP_M=32"],
+}
+if sys.argv[1] == "build":
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_b", os.path.join(os.path.dirname(__file__), "..", "paper_2303_04353_b200", "_build.py"))
+    b = importlib.util.module_from_spec(spec); spec.loader.exec_module(b)
+    for n in sys.argv[2:] or list(VARIANTS):
+        print(n, b.build_variant(n, VARIANTS[n]), flush=True)
+elif sys.argv[1] == "run":
+    n = int(sys.argv[2])
+    for v in sys.argv[3:] or list(VARIANTS):
+        env = dict(os.environ, CASC_LIB_PATH=os.path.abspath(f"paper_2303_04353_b200/libcasc_{v}.so"))
+        smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+        r = subprocess.run([sys.executable, "scripts/i8_perf.py", str(n), "--reps", "3"], env=env, capture_output=True, text=True)
+        smi.terminate(); out = smi.communicate()[0]
+        vals = [tuple(float(x) for x in l.split(",")) for l in out.strip().splitlines() if l.strip()]
+        busy = [v_ for v_ in vals if v_[1] > 400]
+        mhz = sorted(x[0] for x in busy)[len(busy) // 2] if busy else None
+        pw = sorted(x[1] for x in busy)[len(busy) // 2] if busy else None
+        print(v, r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:], {"sm_mhz_median": mhz, "power_median": pw}, flush=True)
