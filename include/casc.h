@@ -282,12 +282,37 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                            uint8_t* flags, int y, void* workspace, size_t workspace_bytes,
                            casc_stream_t stream);
 
-/* Workspace bytes: packed A + packed B (y slices as 16 KB tcgen05 chunks,
- * exponents) + 4 x 128 x 128 doubles per CTA of the GEMM (FP64x2 panel sum
- * and C accumulator).  0 for empty problems or y out of range. */
+/* Workspace bytes: packed A + packed B + casc_i8_gemm_ws_bytes(m, n) (each
+ * part 256-byte aligned).  0 for empty problems or y out of range. */
 size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y);
-/* Bytes of one packed operand (rows = m for A, n for B). */
+
+/* Split ("packed") interface of the INT8 cascade, phase 1 and phases 2-3 as
+ * separate calls (timing, and the multi-GPU layer: each rank packs its rows of
+ * A and its column slab of B; packed B slabs are all-gathered).
+ * A packed operand is an opaque device byte array of 128-row (A) / 128-column
+ * (B) blocks, each casc_i8_packed_block_bytes(k, y) bytes and contiguous: y
+ * slices x ceil(k/128) chunks of 128 x 128 int8 in the tcgen05 shared-memory
+ * layout (K-major, 128-byte swizzle), then the int32 scale exponents of the
+ * block's 128 vectors per panel.  The number of blocks is rounded up to an
+ * even count (the GEMM runs on CTA pairs); a column slab of B whose width is a
+ * multiple of 256 packs into exactly width/128 blocks. */
+size_t casc_i8_packed_block_bytes(int64_t k, int y);
+/* Bytes of one packed operand: 2 ceil(rows/256) blocks (rows = m for A, n for B). */
 size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y);
+/* Phase 1 (R22, R23): scale exponents and int8 slices of A (is_b == 0: rows x k,
+ * ld >= k) or of B's columns (is_b != 0: B is k x rows, ld >= rows) into
+ * `packed` (casc_i8_packed_bytes(rows, k, y) bytes, 256-byte aligned). */
+int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
+                 int is_b, int y, void* packed, casc_stream_t stream);
+/* Bytes of the GEMM's own scratch: 4 x 128 x 128 doubles per CTA (the FP64x2
+ * panel sum T and the C accumulator of the tile in flight). */
+size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
+/* Phases 2-3 (R24-R26) from packed operands of the same m, n, k, y: the fused
+ * tcgen05 kernel on CTA pairs.  ws: >= casc_i8_gemm_ws_bytes(m, n) bytes of
+ * device scratch.  C, flags and errors as casc_i8_gemm_fp64x2. */
+int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
+                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream);
 /* Free the library-owned INT8-cascade workspace of the current device. */
 int casc_i8_finalize(void);
 

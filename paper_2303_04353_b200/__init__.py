@@ -69,7 +69,9 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_split_a", "casc_split_b", "casc_debug_bins", "casc_last_launch_count",
             "casc_gemm_fp64x2_simple", "casc_slice_product", "casc_gemm_fp64x2_ex",
             "casc_i8_gemm_fp64x2", "casc_i8_gemm_fp64x2_ws", "casc_i8_workspace_bytes",
-            "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins"]
+            "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins",
+            "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
+            "casc_i8_gemm_packed"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -81,6 +83,11 @@ _sig("casc_i8_finalize", [])
 _sig("casc_i8_split", [_i64, _i64, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp])
 _sig("casc_i8_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_int,
                             _i64, _vp, _vp])
+_sig("casc_i8_packed_block_bytes", [_i64, ctypes.c_int], _sz)
+_sig("casc_i8_pack", [_i64, _i64, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp, _vp])
+_sig("casc_i8_gemm_ws_bytes", [_i64, _i64], _sz)
+_sig("casc_i8_gemm_packed", [_i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp,
+                             _sz, _vp])
 I8_KC = 8192
 I8_DEFAULT_SLICES = 14
 
@@ -410,3 +417,38 @@ def casc_i8_debug_bins(A_hi, A_lo, B_hi, B_lo, panel: int = 0, y: int = I8_DEFAU
                                    ldb, int(y), panel, _ptr(bins), _stream(stream)),
            "casc_i8_debug_bins")
     return bins
+
+
+def casc_i8_packed_block_bytes(k: int, y: int = I8_DEFAULT_SLICES) -> int:
+    return _lib.casc_i8_packed_block_bytes(k, y)
+
+
+def casc_i8_gemm_ws_bytes(m: int, n: int) -> int:
+    return _lib.casc_i8_gemm_ws_bytes(m, n)
+
+
+def casc_i8_pack(hi, lo, is_b: bool, y: int = I8_DEFAULT_SLICES, packed=None, stream=None):
+    """Phase 1 of the INT8 cascade into the opaque packed layout (uint8 CUDA tensor):
+    A (rows x k) or, with is_b, B (k x rows, packed per column)."""
+    ld = _ld_pair(hi, lo, "X")
+    k, rows = hi.shape if is_b else hi.shape[::-1]
+    if packed is None:
+        packed = torch.empty(casc_i8_packed_bytes(rows, k, y), dtype=torch.uint8,
+                             device=hi.device)
+    _check(_lib.casc_i8_pack(rows, k, _ptr(hi), _ptr(lo), ld, int(bool(is_b)), int(y),
+                             _ptr(packed), _stream(stream)), "casc_i8_pack")
+    return packed
+
+
+def casc_i8_gemm_packed(m, n, k, packed_a, packed_b, y: int = I8_DEFAULT_SLICES, C_hi=None,
+                        C_lo=None, flags=None, want_flags=True, ws=None, stream=None):
+    """Phases 2-3 of the INT8 cascade from packed operands.  Returns (C_hi, C_lo, flags)."""
+    dev = packed_a.device if packed_a is not None else torch.device("cuda")
+    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags)
+    ldc = _ld_pair(C_hi, C_lo, "C") if m and n else max(n, 1)
+    if ws is None:
+        ws = torch.empty(max(casc_i8_gemm_ws_bytes(m, n), 1), dtype=torch.uint8, device=dev)
+    _check(_lib.casc_i8_gemm_packed(m, n, k, int(y), _ptr(packed_a), _ptr(packed_b), _ptr(C_hi),
+                                    _ptr(C_lo), ldc, _ptr(flags), _ptr(ws), ws.numel(),
+                                    _stream(stream)), "casc_i8_gemm_packed")
+    return C_hi, C_lo, flags

@@ -73,28 +73,37 @@ constexpr int GROUP_M = CASC_I8_GROUP_M;  // tile raster: GROUP_M row-pair block
 constexpr size_t SMEM = (size_t)NSA * CHUNK + (size_t)NSB * (CHUNK / 2) + 1024 + 1024;
 
 struct Pack {
-  int64_t R;    // 128-row blocks
+  int64_t R;    // 128-row blocks (even: the GEMM's CTA pairs take them two at a time)
   int64_t KBn;  // 128-byte k blocks
   int64_t P;    // k panels
   int y;
 };
 __host__ __device__ inline Pack pack_of(int64_t rows, int64_t k, int y) {
-  // R is even: the GEMM's CTA pairs take 128-row blocks two at a time
   return Pack{(rows + 2 * TR - 1) / (2 * TR) * 2, (k + KB - 1) / KB, (k + KC8 - 1) / KC8, y};
 }
-__host__ __device__ inline int64_t slice_bytes(const Pack& g) {
-  return (int64_t)g.y * g.R * g.KBn * CHUNK;
+// A packed operand is R contiguous blocks of 128 rows (A) / columns (B), so a
+// range of blocks (a row block of A, a column slab of B) is a contiguous byte
+// range.  Block layout: [y slices][KBn k blocks] 16 KB chunks, then the int32
+// scale exponents [P][128], then scratch u64 max |hi| bits [P][128].
+__host__ __device__ inline int64_t al256(int64_t b) { return (b + 255) / 256 * 256; }
+__host__ __device__ inline int64_t blk_exp_off(const Pack& g) {
+  return (int64_t)g.y * g.KBn * CHUNK;
 }
-// packed operand = [slices][int32 exponents P x R*128][u64 max bits P x R*128]
-__host__ __device__ inline int64_t exp_off(const Pack& g) { return slice_bytes(g); }
-__host__ __device__ inline int64_t max_off(const Pack& g) {
-  return slice_bytes(g) + ((g.P * g.R * TR * 4 + 255) / 256) * 256;
+__host__ __device__ inline int64_t blk_max_off(const Pack& g) {
+  return blk_exp_off(g) + al256(g.P * TR * 4);
 }
-__host__ __device__ inline int64_t packed_bytes(const Pack& g) {
-  return max_off(g) + g.P * g.R * TR * 8;
+__host__ __device__ inline int64_t blk_bytes(const Pack& g) {
+  return al256(blk_max_off(g) + g.P * TR * 8);
 }
+__host__ __device__ inline int64_t packed_bytes(const Pack& g) { return g.R * blk_bytes(g); }
 __host__ __device__ inline int64_t chunk_off(const Pack& g, int t, int64_t rb, int64_t kb) {
-  return ((t * g.R + rb) * g.KBn + kb) * (int64_t)CHUNK;
+  return rb * blk_bytes(g) + ((int64_t)t * g.KBn + kb) * CHUNK;
+}
+__host__ __device__ inline int64_t exp_at(const Pack& g, int64_t r, int64_t q) {
+  return (r / TR) * blk_bytes(g) + blk_exp_off(g) + (q * TR + r % TR) * 4;
+}
+__host__ __device__ inline int64_t max_at(const Pack& g, int64_t r, int64_t q) {
+  return (r / TR) * blk_bytes(g) + blk_max_off(g) + (q * TR + r % TR) * 8;
 }
 // byte of (row r, k byte c) inside a chunk: K-major, 128-byte swizzle
 __host__ __device__ inline uint32_t sw128(int r, int c) {
@@ -108,8 +117,8 @@ __device__ __forceinline__ unsigned long long absbits(double x) {
 
 // max |A_hi| per (row, panel): warp = one row x 1024 k, 8 rows per block.
 __global__ void __launch_bounds__(256) i8_rowmax_kernel(const double* __restrict__ hi, int64_t ld,
-                                                        int64_t rows, int64_t k, int64_t Rp,
-                                                        unsigned long long* __restrict__ mx) {
+                                                        int64_t rows, int64_t k, Pack g,
+                                                        uint8_t* __restrict__ packed) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * 8 + warp;
   const int64_t p0 = (int64_t)blockIdx.y * 1024;
@@ -122,13 +131,14 @@ __global__ void __launch_bounds__(256) i8_rowmax_kernel(const double* __restrict
     if (p < k) m = max(m, absbits(__ldg(row + p)));
   }
   for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(~0u, m, o));
-  if (lane == 0 && m) atomicMax(mx + (p0 / KC8) * Rp + r, m);
+  if (lane == 0 && m)
+    atomicMax(reinterpret_cast<unsigned long long*>(packed + max_at(g, r, p0 / KC8)), m);
 }
 
 // max |B_hi| per (column, panel): thread = one column x 64 k.
 __global__ void __launch_bounds__(256) i8_colmax_kernel(const double* __restrict__ hi, int64_t ld,
-                                                        int64_t cols, int64_t k, int64_t Rp,
-                                                        unsigned long long* __restrict__ mx) {
+                                                        int64_t cols, int64_t k, Pack g,
+                                                        uint8_t* __restrict__ packed) {
   const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const int64_t p0 = (int64_t)blockIdx.y * 64;
   if (j >= cols) return;
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(256) i8_colmax_kernel(const double* __restrict
     const int64_t p = p0 + i;
     if (p < k) m = max(m, absbits(__ldg(hi + p * ld + j)));
   }
-  if (m) atomicMax(mx + (p0 / KC8) * Rp + j, m);
+  if (m) atomicMax(reinterpret_cast<unsigned long long*>(packed + max_at(g, j, p0 / KC8)), m);
 }
 
 // 2^n as a double for n in [-1022, 1023] (exact).
@@ -192,12 +202,10 @@ __global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict
   }
   if (r >= g.R * TR) return;
   const int64_t q = kb / KBP;
-  const int64_t Rp = g.R * TR;
-  const unsigned long long* mx =
-      reinterpret_cast<const unsigned long long*>(packed + max_off(g)) + q * Rp;
-  const int e = r < rows ? scale_exp(mx[r]) : 0;
-  if ((kb % KBP) == 0 && cs[0] == 0)
-    reinterpret_cast<int32_t*>(packed + exp_off(g))[q * Rp + r] = e;
+  const int e =
+      r < rows ? scale_exp(*reinterpret_cast<const unsigned long long*>(packed + max_at(g, r, q)))
+               : 0;
+  if ((kb % KBP) == 0 && cs[0] == 0) *reinterpret_cast<int32_t*>(packed + exp_at(g, r, q)) = e;
   const int F = 6 + 8 * (g.y - 1);
   const int s1 = min(F - e, 1023), s2 = F - e - s1;
   const double sc1 = p2(s1), sc2 = p2(s2);
@@ -242,6 +250,14 @@ __global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict
   }
 }
 
+// zero the max |hi| scratch of every (block, panel) before the atomicMax passes
+__global__ void i8_zero_max_kernel(Pack g, uint8_t* __restrict__ packed) {
+  const int64_t total = g.R * g.P * TR;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x)
+    *reinterpret_cast<unsigned long long*>(packed + max_at(g, x % (g.R * TR), x / (g.R * TR))) = 0;
+}
+
 // Debug export: packed chunks -> canonical digits D[t][r][p] (rows x k) and
 // exponents E[q][r].
 __global__ void i8_unpack_kernel(const uint8_t* __restrict__ packed, Pack g, int64_t rows,
@@ -253,10 +269,9 @@ __global__ void i8_unpack_kernel(const uint8_t* __restrict__ packed, Pack g, int
     const int t = (int)(x / (k * rows));
     D[x] = (int8_t)packed[chunk_off(g, t, r / TR, p / KB) + sw128((int)(r % TR), (int)(p % KB))];
   }
-  const int32_t* ex = reinterpret_cast<const int32_t*>(packed + exp_off(g));
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < g.P * rows;
        x += (int64_t)gridDim.x * blockDim.x)
-    E[x] = ex[(x / rows) * g.R * TR + x % rows];
+    E[x] = *reinterpret_cast<const int32_t*>(packed + exp_at(g, x % rows, x / rows));
 }
 
 // ------------------------------------------------------------------ phase 2+3
@@ -458,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto loadA = [&](int i, int64_t rb, int64_t kb) {
       const uint32_t s = aseq % NSA;
       mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
-      const int row = (int)(((i * p.ga.R + rb) * KBn + kb) * TR);
+      const int row = (int)(chunk_off(p.ga, i, rb, kb) / KB);
       tma_pair_elect(sA + s * CHUNK, &mapA, row, &fullA[s], leader_addr(&fullA[s]),
                      leader ? 2 * CHUNK : 0);
       ++aseq;
@@ -466,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto loadB = [&](int j, int64_t cb, int64_t kb) {
       const uint32_t s = bseq % NSB;
       mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
-      const int row = (int)(((j * p.gb.R + cb) * KBn + kb) * TR + rank * (TR / 2));
+      const int row = (int)(chunk_off(p.gb, j, cb, kb) / KB + rank * (TR / 2));
       tma_pair_elect(sB + s * BHALF, &mapB, row, &fullB[s], leader_addr(&fullB[s]),
                      leader ? 2 * BHALF : 0);
       ++bseq;
@@ -555,8 +570,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     double* Tl = Th + TR * TR;
     double* Ch = Tl + TR * TR;
     double* Cl = Ch + TR * TR;
-    const int32_t* EA = reinterpret_cast<const int32_t*>(p.pa + exp_off(p.ga));
-    const int32_t* EB = reinterpret_cast<const int32_t*>(p.pb + exp_off(p.gb));
     uint32_t gcount = 0;
     for (int tile = pair; tile < tiles; tile += npairs) {
       int64_t rp, cb;
@@ -565,10 +578,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint64_t fl = 0;  // detector bits of this thread's 64 columns
       for (int q = 0; q < P; ++q) {
         const int64_t kp = min((int64_t)KC8, p.k - (int64_t)q * KC8);
-        const int ei = EA[(int64_t)q * RA * TR + gi];
+        const int ei = *reinterpret_cast<const int32_t*>(p.pa + exp_at(p.ga, gi, q));
         // column exponents of this (tile, panel) -> shared memory
         epi_bar_sync();
-        if (ew < 4) sF[ew * 32 + lane] = EB[(int64_t)q * RB * TR + cb * TR + ew * 32 + lane];
+        if (ew < 4)
+          sF[ew * 32 + lane] =
+              *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, cb * TR + ew * 32 + lane, q));
         epi_bar_sync();
         for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
           const int s = grp * NBIN, nb = min(NBIN, y - s);
@@ -693,17 +708,15 @@ cudaError_t pack(const double* hi, const double* lo, int64_t ld, int64_t rows, i
                  bool cols, void* packed, cudaStream_t st) {
   const Pack g = pack_of(rows, k, y);
   uint8_t* pk = static_cast<uint8_t*>(packed);
-  unsigned long long* mx = reinterpret_cast<unsigned long long*>(pk + max_off(g));
-  cudaError_t e = cudaMemsetAsync(mx, 0, (size_t)(g.P * g.R * TR * 8), st);
-  if (e != cudaSuccess) return e;
+  i8_zero_max_kernel<<<256, 256, 0, st>>>(g, pk);
   if (cols) {
     i8_colmax_kernel<<<dim3((unsigned)((rows + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0,
-                       st>>>(hi, ld, rows, k, g.R * TR, mx);
+                       st>>>(hi, ld, rows, k, g, pk);
     i8_digits_kernel<true><<<dim3((unsigned)g.R, (unsigned)g.KBn), 256, 0, st>>>(hi, lo, ld, rows,
                                                                                 k, g, pk);
   } else {
     i8_rowmax_kernel<<<dim3((unsigned)((rows + 7) / 8), (unsigned)((k + 1023) / 1024)), 256, 0,
-                       st>>>(hi, ld, rows, k, g.R * TR, mx);
+                       st>>>(hi, ld, rows, k, g, pk);
     i8_digits_kernel<false><<<dim3((unsigned)(g.R * 2), (unsigned)g.KBn), 256, 0, st>>>(
         hi, lo, ld, rows, k, g, pk);
   }
@@ -740,7 +753,7 @@ cudaError_t slice_map(CUtensorMap* map, const void* packed, const Pack& g, uint3
         q != cudaDriverEntryPointSuccess || !enc)
       return cudaErrorNotSupported;
   }
-  const uint64_t rows = (uint64_t)g.y * g.R * g.KBn * TR;
+  const uint64_t rows = (uint64_t)(packed_bytes(g) / KB);
   if (rows >= (1ull << 31)) return cudaErrorInvalidValue;  // int32 TMA coordinates
   cuuint64_t dims[2] = {(cuuint64_t)KB, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)KB};
@@ -809,7 +822,7 @@ namespace {
 using namespace casc;
 inline cudaStream_t S8(casc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int st8(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
-inline size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+inline size_t al256h(size_t b) { return (b + 255) / 256 * 256; }
 struct I8Ws {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -824,10 +837,58 @@ size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y) {
   return (size_t)i8::packed_bytes(i8::pack_of(rows, k, y));
 }
 
+size_t casc_i8_packed_block_bytes(int64_t k, int y) {
+  if (k <= 0 || y < i8::YMIN || y > i8::YMAX) return 0;
+  return (size_t)i8::blk_bytes(i8::pack_of(1, k, y));
+}
+
+size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n) {
+  if (m <= 0 || n <= 0) return 0;
+  return i8::cta_ws_bytes(i8::grid_for(m, n, host::current_sms()));
+}
+
 size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y) {
   if (m <= 0 || n <= 0 || k <= 0 || y < i8::YMIN || y > i8::YMAX) return 0;
-  return al256(casc_i8_packed_bytes(m, k, y)) + al256(casc_i8_packed_bytes(n, k, y)) +
-         i8::cta_ws_bytes(i8::grid_for(m, n, host::current_sms()));
+  return al256h(casc_i8_packed_bytes(m, k, y)) + al256h(casc_i8_packed_bytes(n, k, y)) +
+         casc_i8_gemm_ws_bytes(m, n);
+}
+
+int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
+                 int is_b, int y, void* packed, casc_stream_t stream) {
+  host::set_launches(0);
+  int r;
+  if (rows < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if (is_b) {
+    if ((r = host::check_mat(hi, k, rows, ld)) || (r = host::check_mat(lo, k, rows, ld))) return r;
+  } else {
+    if ((r = host::check_mat(hi, rows, k, ld)) || (r = host::check_mat(lo, rows, k, ld))) return r;
+  }
+  if (rows == 0 || k == 0) return CASC_OK;
+  if (!packed) return CASC_ERR_INVALID;
+  if ((r = host::device_check(nullptr))) return r;
+  const cudaError_t e = i8::pack(hi, lo, ld, rows, k, y, is_b != 0, packed, S8(stream));
+  if (e == cudaSuccess) host::set_launches(3);
+  return st8(e);
+}
+
+int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
+                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream) {
+  host::set_launches(0);
+  int r;
+  if (m < 0 || n < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  if ((r = host::check_mat(C_hi, m, n, ldc)) || (r = host::check_mat(C_lo, m, n, ldc))) return r;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  if (k == 0) return host::zero_c(m, n, C_hi, C_lo, ldc, flags, S8(stream));
+  if (!packed_a || !packed_b || !ws || ws_bytes < casc_i8_gemm_ws_bytes(m, n))
+    return CASC_ERR_INVALID;
+  const cudaError_t e = i8::gemm(packed_a, packed_b, m, n, k, y, C_hi, C_lo, ldc, flags,
+                                 static_cast<double*>(ws), i8::grid_for(m, n, sms), nullptr, 0,
+                                 S8(stream));
+  if (e == cudaSuccess) host::set_launches(1);
+  return st8(e);
 }
 
 int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
@@ -847,14 +908,14 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
   const size_t need = casc_i8_workspace_bytes(m, n, k, y);
   if (!workspace || workspace_bytes < need) return CASC_ERR_INVALID;
   uint8_t* pa = static_cast<uint8_t*>(workspace);
-  uint8_t* pb = pa + al256(casc_i8_packed_bytes(m, k, y));
-  double* ws = reinterpret_cast<double*>(pb + al256(casc_i8_packed_bytes(n, k, y)));
+  uint8_t* pb = pa + al256h(casc_i8_packed_bytes(m, k, y));
+  double* ws = reinterpret_cast<double*>(pb + al256h(casc_i8_packed_bytes(n, k, y)));
   cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
   if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
   if (e == cudaSuccess)
     e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, ws, i8::grid_for(m, n, sms), nullptr,
                  0, st);
-  if (e == cudaSuccess) host::set_launches(5);
+  if (e == cudaSuccess) host::set_launches(7);
   return st8(e);
 }
 
@@ -939,8 +1000,8 @@ int casc_i8_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, cons
   void* buf = nullptr;
   if (cudaMallocAsync(&buf, need, st) != cudaSuccess) return CASC_ERR_CUDA;
   uint8_t* pa = static_cast<uint8_t*>(buf);
-  uint8_t* pb = pa + al256(casc_i8_packed_bytes(m, k, y));
-  double* ws = reinterpret_cast<double*>(pb + al256(casc_i8_packed_bytes(n, k, y)));
+  uint8_t* pb = pa + al256h(casc_i8_packed_bytes(m, k, y));
+  double* ws = reinterpret_cast<double*>(pb + al256h(casc_i8_packed_bytes(n, k, y)));
   cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
   if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
   if (e == cudaSuccess)

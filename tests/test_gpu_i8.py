@@ -175,3 +175,23 @@ def test_i8_sampled_full_size_cfg1(casc, orc):
     o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"], d["B_lo"])
     assert bitwise(C_hi[rows], o_hi) and bitwise(C_lo[rows], o_lo)
     assert np.array_equal(fl[rows], ofl)
+
+
+def test_i8_packed_interface_and_slab_contiguity(casc, orc):
+    """casc_i8_pack + casc_i8_gemm_packed give the one-call result bit for bit,
+    and a 256-column slab of B packs into exactly the matching byte range of the
+    packed full B (the multi-GPU all-gather premise)."""
+    import torch
+    d = I.make_config(1, m=300, n=768, k=900, seed=12)
+    A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+    ref = [N(x) for x in casc.casc_i8_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo)]
+    pa = casc.casc_i8_pack(A_hi, A_lo, False)
+    pb = casc.casc_i8_pack(B_hi, B_lo, True)
+    got = [N(x) for x in casc.casc_i8_gemm_packed(300, 768, 900, pa, pb)]
+    assert all(np.array_equal(x, z) for x, z in zip(ref, got))
+    blk = casc.casc_i8_packed_block_bytes(900)
+    assert pb.numel() == 6 * blk
+    slab = casc.casc_i8_pack(B_hi[:, 256:512].contiguous(), B_lo[:, 256:512].contiguous(), True)
+    assert slab.numel() == 2 * blk
+    # chunks and exponents identical; the u64 max scratch is part of each block too
+    assert torch.equal(slab, pb[2 * blk:4 * blk])
