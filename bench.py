@@ -64,6 +64,81 @@ def load_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_int8_peak():
+    """INT8 dense tensor peak: MEASURED_PEAKS.json's sustained bf16 figure x the
+    guide's nominal int8:bf16 ratio of 2 (4.5 vs 2.25 PFLOP/s dense).  The kernel
+    is timed inside a long step, hence the sustained figure."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return 2.0 * d["bf16_tflops_sustained"], 2.0 * d["bf16_tflops"], \
+            "MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal int8:bf16 ratio)"
+    except Exception:
+        return 4500.0, 4500.0, "fallback: nominal 4.5 POPS dense int8"
+
+
+def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, y=14):
+    """NEXT-3: the INT8 cascade (casc_i8_pack x2 + casc_i8_gemm_packed) on the
+    same device-resident workload, phases timed with CUDA events."""
+    import torch
+    dev = A_hi.device
+    pa = torch.empty(casc.casc_i8_packed_bytes(m, k, y), dtype=torch.uint8, device=dev)
+    pb = torch.empty(casc.casc_i8_packed_bytes(n, k, y), dtype=torch.uint8, device=dev)
+    ws = torch.empty(casc.casc_i8_gemm_ws_bytes(m, n), dtype=torch.uint8, device=dev)
+    C_hi = torch.empty((m, n), dtype=torch.float64, device=dev)
+    C_lo = torch.empty_like(C_hi)
+    fl = torch.empty((m, n), dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record()
+        casc.casc_i8_pack(A_hi, A_lo, False, y, packed=pa)
+        if ev:
+            ev[1].record()
+        casc.casc_i8_pack(B_hi, B_lo, True, y, packed=pb)
+        if ev:
+            ev[2].record()
+        casc.casc_i8_gemm_packed(m, n, k, pa, pb, y, C_hi=C_hi, C_lo=C_lo, flags=fl, ws=ws)
+        if ev:
+            ev[3].record()
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    with ClockSampler(None) as cs:
+        for s_ in range(steps):
+            step(evs[s_])
+        torch.cuda.synchronize()
+    ph = {"pack_a": 0.0, "pack_b": 0.0, "gemm": 0.0}
+    for e in evs:
+        ph["pack_a"] += e[0].elapsed_time(e[1]) / steps
+        ph["pack_b"] += e[1].elapsed_time(e[2]) / steps
+        ph["gemm"] += e[2].elapsed_time(e[3]) / steps
+    total = sum(ph.values())
+    prods = y * (y + 1) // 2
+    ops = 2.0 * prods * m * n * k
+    peak_sus, peak_burst, src = load_int8_peak()
+    achieved = ops / (ph["gemm"] * 1e-3) / 1e12
+    del pa, pb, ws, C_hi, C_lo, fl
+    return {
+        "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3756), y=%d slices, "
+                  "%d int8 products per k panel of 8192; readings R22-R26" % (y, prods),
+        "value": 2.0 * m * n * k / (total * 1e-3) / 1e9, "unit": UNIT,
+        "ms_per_step": total, "phases_ms": ph,
+        "parity": "bit-exact vs oracle/casc_i8_oracle.c (tests/test_gpu_i8.py)",
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
+                     "unit": "TOP/s (int8)", "frac": achieved / peak_sus, "traffic": None,
+                     "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
+                               "combine)",
+                     "peak_source": f"{src} (burst {peak_burst:.0f}); own probe with random "
+                                    "operands: 3668 sustained / 4210 burst "
+                                    "(profiles/r01d/i8_pair_probe_rand.json)",
+                     "algorithmic_ops_per_launch": ops},
+        "clocks": cs.summary(),
+    }
+
+
 def load_ncu_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
     try:
@@ -216,6 +291,8 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-int8", action="store_true",
+                    help="skip the NEXT-3 INT8-cascade measurement on the same workload")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -391,6 +468,13 @@ def main():
         except Exception:
             dgemm_ratio = None
 
+    int8 = None
+    if world == 1 and not args.no_int8:
+        try:
+            int8 = measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, args.steps, args.warmup)
+        except Exception as ex:  # reported, never silently replaced
+            int8 = {"error": repr(ex)}
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo)
@@ -413,6 +497,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
+        "next3_int8_cascade": int8,
     }
     print(json.dumps(out), flush=True)
     if world > 1:
