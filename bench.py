@@ -122,7 +122,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, y=14):
     achieved = ops / (ph["gemm"] * 1e-3) / 1e12
     del pa, pb, ws, C_hi, C_lo, fl
     return {
-        "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3756), y=%d slices, "
+        "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3754), y=%d slices, "
                   "%d int8 products per k panel of 8192; readings R22-R26" % (y, prods),
         "value": 2.0 * m * n * k / (total * 1e-3) / 1e9, "unit": UNIT,
         "ms_per_step": total, "phases_ms": ph,

@@ -239,12 +239,12 @@ int casc_slice_product(int64_t m, int64_t n, int64_t k,
                        int sa, int sb, int64_t panel, double* out, casc_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
-/* NEXT-3: the INT8 cascade (paper §6 "FP64x2 in terms of INT8", P:L3753-3756) */
+/* NEXT-3: the INT8 cascade (paper §6 "FP64x2 in terms of INT8", P:L3753-3754) */
 /* ------------------------------------------------------------------------ */
 /* The same product C := A B (FP64x2) computed from y int8 slices per operand
  * with the y(y+1)/2 products A_i B_j, i + j < y ("14 to 15 INT8 splits and
  * about 105 to 120 INT8 multiplies") on the INT8 tensor cores
- * (tcgen05.mma kind::i8, int32 accumulation in tensor memory, P:L3750-3751).
+ * (tcgen05.mma kind::i8, int32 accumulation in tensor memory, P:L3749-3751).
  * DESIGN.md readings R22-R26 fix what the paper leaves open:
  *   R22 k panel 8192; scale exponent per (row, panel) / (column, panel);
  *   R23 X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)), F = 6 + 8(y-1), slices = the
@@ -304,8 +304,9 @@ size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y);
  * `packed` (casc_i8_packed_bytes(rows, k, y) bytes, 256-byte aligned). */
 int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
                  int is_b, int y, void* packed, casc_stream_t stream);
-/* Bytes of the GEMM's own scratch: 4 x 128 x 128 doubles per CTA (the FP64x2
- * panel sum T and the C accumulator of the tile in flight). */
+/* Bytes of the GEMM's own scratch: 5 x 128 x 128 x 8 bytes per CTA (the FP64x2
+ * panel sum T, the C accumulator and the exact group values of the tile in
+ * flight), then a wave-synchronisation counter. */
 size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
 /* Phases 2-3 (R24-R26) from packed operands of the same m, n, k, y: the fused
  * tcgen05 kernel on CTA pairs.  ws: >= casc_i8_gemm_ws_bytes(m, n) bytes of

@@ -1,7 +1,7 @@
 /*
  * casc_i8_oracle.c — CPU ORACLE for the INT8 cascade of an FP64x2 GEMM
  * (NEXT-3; arXiv 2303.04353 §6 "FP64x2 in terms of INT8",
- * P:L3753-3756, and "FP64 in terms of INT8").
+ * P:L3753-3754, and "FP64 in terms of INT8").
  *
  * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs may load or call this library. The
@@ -9,10 +9,10 @@
  * shares no code, header, table or constant generator with it.
  *
  * The paper only sketches this variant: the FP64x2 matrix is "converted into
- * fixed point numbers which can be stored in integers" (P:L3750), cascaded into
+ * fixed point numbers which can be stored in integers" (P:L3749), cascaded into
  * "approximately 14 to 15 INT8 splits" with "about 105 to 120 INT8 multiplies"
  * (P:L3754), i.e. the y(y+1)/2 products A_i B_j with i + j < y, and "32-bit
- * accumulation" (P:L3750-3751) plays the role the 2^53 budget plays for the
+ * accumulation" (P:L3749-3751) plays the role the 2^53 budget plays for the
  * FP64 cascade.  Everything the paper leaves open is fixed by the readings
  * R22-R26 in DESIGN.md §3; this file follows them step by step:
  *

@@ -1,9 +1,9 @@
 // casc_i8.cu — NEXT-3: the FP64x2 GEMM C := A B as a cascade
 // of INT8 tensor-core GEMMs, the variant the paper proposes in §6 "FP64x2 in
-// terms of INT8" (P:L3753-3756): the matrices are "converted into fixed point
-// numbers which can be stored in integers" (P:L3750), cascaded into ~14-15
+// terms of INT8" (P:L3753-3754): the matrices are "converted into fixed point
+// numbers which can be stored in integers" (P:L3749), cascaded into ~14-15
 // int8 splits, multiplied with the y(y+1)/2 products of the triangle i + j < y
-// (P:L3754) and accumulated in 32-bit integers (P:L3750-3751).  DESIGN.md
+// (P:L3754) and accumulated in 32-bit integers (P:L3749-3751).  DESIGN.md
 // readings R22-R26 fix what the paper leaves open (the CPU oracle
 // oracle/casc_i8_oracle.c follows the same readings with its own code):
 //   R22  k panel of 8192; per (row, panel) / (column, panel) scale exponent e
@@ -35,9 +35,9 @@
 //              A_top .. A_s, B_0, A_(s-1), B_1, ... so each B_j meets its (up to)
 //              four A_i partners while they sit in smem: every chunk is loaded
 //              once per k block and feeds up to four MMAs;
-//   warp 2     TMEM allocator (512 columns);
-//   warps 4-11 epilogue: tcgen05.ld of the int32 bins (warp w reads TMEM lane
-//              quarter w%4, column half (w-4)/4), exact group value, FP64x2
+//   warp 1 also allocates TMEM (512 columns);
+//   warps 2-9  epilogue: tcgen05.ld of the int32 bins (warp w reads TMEM lane
+//              quarter w%4, column half (w-2)/4), exact group value, FP64x2
 //              panel sum T and C in a per-CTA workspace (L2-resident), detector,
 //              final store of C and the flags.
 #include <cuda.h>
@@ -64,8 +64,15 @@ constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
 constexpr int NSA = 8, NSB = 8;    // smem ring slots (A: 16 KB, B: 8 KB half chunks)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
-constexpr int THREADS = 384;
-constexpr int EPI_WARP0 = 4, EPI_THREADS = 256;
+// warp 0 TMA producer, warp 1 MMA issuer + TMEM allocator, warps 2-9 epilogue
+// (320 threads: up to 204 registers each, room for the epilogue's 64 exact
+// group values)
+constexpr int THREADS = 320;
+constexpr int EPI_WARP0 = 2, EPI_THREADS = 256;
+#ifndef CASC_I8_EPI_SUB
+#define CASC_I8_EPI_SUB 8
+#endif
+constexpr int EPI_SUB = CASC_I8_EPI_SUB;  // elements per phase-2 step of the epilogue
 #ifndef CASC_I8_GROUP_M
 #define CASC_I8_GROUP_M 12
 #endif
@@ -284,7 +291,8 @@ struct GemmArgs {
   double* C_lo;
   int64_t ldc;
   uint8_t* flags;
-  double* ws;           // per CTA: T hi, T lo, C hi, C lo (4 x 16384 doubles)
+  double* ws;           // per CTA: T hi, T lo, C hi, C lo, V (5 x 16384 x 8 bytes)
+  unsigned int* sync;   // wave-sync counter (zeroed before the launch) or null
   int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
   int64_t dbg_panel;
 };
@@ -447,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(tempty, 2 * EPI_THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -486,14 +494,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                      leader ? 2 * BHALF : 0);
       ++bseq;
     };
+    const int full_waves = tiles / npairs;  // waves in which every pair has a tile
+    uint32_t sweep = 0;
     for (int tile = pair; tile < tiles; tile += npairs) {
       int64_t rp, cb;
       tile_of(tile, RP, RB, rp, cb);
       const int64_t rb = 2 * rp + rank;
+      const bool synced = p.sync && (tile / npairs) < full_waves;
       for (int q = 0; q < P; ++q) {
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
         for (int grp = 0; grp < ngroups; ++grp) {
           const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+          if (synced) {
+            // Soft wave synchronisation: the producers of all CTAs start each
+            // (panel, group) sweep of a full tile wave together, so the tiles in
+            // flight stream the same slice chunks at the same time and hit them in
+            // L2 (bounded wait: never a hang, at worst an unsynchronised sweep).
+            ++sweep;
+            if (lane == 0) {
+              atomicAdd(p.sync, 1u);
+              const unsigned int target = sweep * gridDim.x;
+              unsigned int v;
+              for (int spin = 0; spin < 20000; ++spin) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+              }
+            }
+            __syncwarp();
+          }
           for (int64_t kb = kb0; kb < kb1; ++kb) {
             for (int i = top; i >= s; --i) loadA(i, rb, kb);
             loadB(0, cb, kb);
@@ -566,10 +595,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int lr = quarter * 32 + lane;       // tile row = TMEM lane
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const uint32_t tempty_leader = leader_addr(tempty);
-    double* Th = p.ws + (int64_t)blockIdx.x * 4 * (TR * TR);
+    double* Th = p.ws + (int64_t)blockIdx.x * 5 * (TR * TR);
     double* Tl = Th + TR * TR;
     double* Ch = Tl + TR * TR;
     double* Cl = Ch + TR * TR;
+    long long* Vw = reinterpret_cast<long long*>(Cl + TR * TR);  // exact group values
     uint32_t gcount = 0;
     for (int tile = pair; tile < tiles; tile += npairs) {
       int64_t rp, cb;
@@ -594,6 +624,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           mbar_wait(tfull, gcount & 1);
 #endif
           tc_fence_after();
+          // Phase 1: drain this warp's part of TMEM into the exact group values
+          // V = sum_u bin_(s+u) 2^(8(nb-1-u)) (int64, |V| < 2^56; R25), then
+          // release TMEM so that the MMAs of the next group start at once.
+#pragma unroll 2
           for (int cc = 0; cc < 8; ++cc) {
             const int c0 = half * 64 + cc * 8;
             uint32_t r0[8], r1[8], r2[8], r3[8];
@@ -601,67 +635,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (nb > 1) tmem_ld8(trow + 1 * 128 + c0, r1);
             if (nb > 2) tmem_ld8(trow + 2 * 128 + c0, r2);
             if (nb > 3) tmem_ld8(trow + 3 * 128 + c0, r3);
-            // the running panel sum T and C of these 8 elements (independent loads,
-            // issued together while the TMEM loads are in flight)
-            double xth[8], xtl[8], xch[8], xcl[8];
-            if (!DBG && needT) {
+            tmem_wait_ld();
+            if (DBG && q == p.dbg_panel) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
+                const int64_t gj = cb * TR + c0 + i;
+                if (gi < p.m && gj < p.n) {
+                  const int64_t mn = p.m * p.n, o = gi * p.n + gj;
+                  p.dbg[(int64_t)(s + 0) * mn + o] = (int32_t)r0[i];
+                  if (nb > 1) p.dbg[(int64_t)(s + 1) * mn + o] = (int32_t)r1[i];
+                  if (nb > 2) p.dbg[(int64_t)(s + 2) * mn + o] = (int32_t)r2[i];
+                  if (nb > 3) p.dbg[(int64_t)(s + 3) * mn + o] = (int32_t)r3[i];
+                }
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              long long v = (int32_t)r0[i];
+              if (nb > 1) v = v * 256 + (int32_t)r1[i];
+              if (nb > 2) v = v * 256 + (int32_t)r2[i];
+              if (nb > 3) v = v * 256 + (int32_t)r3[i];
+              Vw[(c0 + i) * TR + lr] = v;
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader);
+          if (DBG) continue;
+#ifdef CASC_I8_NO_EPI
+          continue;
+#endif
+          // Phase 2 (overlaps the next group's MMAs): FP64x2 panel sum T,
+          // detector and C, EPI_SUB elements at a time
+#pragma unroll
+          for (int cc = 0; cc < 64 / EPI_SUB; ++cc) {
+            const int c0 = half * 64 + cc * EPI_SUB;
+            double xth[EPI_SUB], xtl[EPI_SUB], xch[EPI_SUB], xcl[EPI_SUB];
+            long long xv[EPI_SUB];
+#pragma unroll
+            for (int i = 0; i < EPI_SUB; ++i) xv[i] = Vw[(c0 + i) * TR + lr];
+            if (needT) {
+#pragma unroll
+              for (int i = 0; i < EPI_SUB; ++i) {
                 xth[i] = Th[(c0 + i) * TR + lr];
                 xtl[i] = Tl[(c0 + i) * TR + lr];
               }
             }
-            if (!DBG && needC) {
+            if (needC) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
+              for (int i = 0; i < EPI_SUB; ++i) {
                 xch[i] = Ch[(c0 + i) * TR + lr];
                 xcl[i] = Cl[(c0 + i) * TR + lr];
               }
             }
-            tmem_wait_ld();
-            if (cc == 7) {  // this warp's part of TMEM is read: the next group may start
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive_cluster(tempty_leader);
-            }
-#ifdef CASC_I8_NO_EPI
-            if (r0[0] == 0x7fffffffu && r1[1] == 0x7fffffffu) p.C_hi[0] = 1.0;  // keep the loads
-            continue;
-#endif
-            if (DBG) {
-              if (q == p.dbg_panel) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const int64_t gj = cb * TR + c0 + i;
-                  if (gi < p.m && gj < p.n) {
-                    const int64_t mn = p.m * p.n, o = gi * p.n + gj;
-                    p.dbg[(int64_t)(s + 0) * mn + o] = (int32_t)r0[i];
-                    if (nb > 1) p.dbg[(int64_t)(s + 1) * mn + o] = (int32_t)r1[i];
-                    if (nb > 2) p.dbg[(int64_t)(s + 2) * mn + o] = (int32_t)r2[i];
-                    if (nb > 3) p.dbg[(int64_t)(s + 3) * mn + o] = (int32_t)r3[i];
-                  }
-                }
-              }
-              continue;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < EPI_SUB; ++i) {
               const int lc = c0 + i;
               const int fj = sF[lc];
-              // R25: exact group value (hi = RN(V), lo = V - hi)
-              double gh, gl;
-              const double b0 = (double)(int32_t)r0[i];
-              if (nb == 4) {
-                const double P1 = __dadd_rn(__dmul_rn(b0, 256.0), (double)(int32_t)r1[i]);
-                const double P2 =
-                    __dadd_rn(__dmul_rn((double)(int32_t)r2[i], 256.0), (double)(int32_t)r3[i]);
-                two_sum(__dmul_rn(P1, 65536.0), P2, gh, gl);
-              } else {
-                gh = b0;
-                if (nb > 1) gh = __dadd_rn(__dmul_rn(gh, 256.0), (double)(int32_t)r1[i]);
-                if (nb > 2) gh = __dadd_rn(__dmul_rn(gh, 256.0), (double)(int32_t)r2[i]);
-                gl = 0.0;
-              }
+              // R25: G = (RN(V), V - RN(V)), exact
+              const long long v = xv[i];
+              double gh = __ll2double_rn(v);
+              double gl = __ll2double_rn(v - __double2ll_rn(gh));
               const int w = ei + fj - 12 - 8 * (s + nb - 1);
               gh = mulp2(gh, w);
               gl = mulp2(gl, w);
@@ -697,7 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   cluster_sync_all();
-  if (warp == 2) {
+  if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -735,7 +769,8 @@ int grid_for(int64_t m, int64_t n, int sms) {  // CTAs: 2 per pair, one pair per
   const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
   return (int)(2 * pairs);
 }
-size_t cta_ws_bytes(int grid) { return (size_t)grid * 4 * TR * TR * sizeof(double); }
+// per-CTA T / C scratch, then the wave-sync counter
+size_t cta_ws_bytes(int grid) { return (size_t)grid * 5 * TR * TR * sizeof(double) + 256; }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -784,6 +819,13 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   a.ws = ws;
   a.dbg = dbg;
   a.dbg_panel = dbg_panel;
+  const char* env = getenv("CASC_I8_WAVE_SYNC");  // "0": off (timing studies)
+  if (!(env && env[0] == '0')) {
+    a.sync = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(ws) +
+                                             (size_t)grid * 5 * TR * TR * sizeof(double));
+    cudaError_t e0 = cudaMemsetAsync(a.sync, 0, sizeof(unsigned int), st);
+    if (e0 != cudaSuccess) return e0;
+  }
   CUtensorMap mA, mB;
   cudaError_t e = slice_map(&mA, pa, a.ga, TR);
   if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TR / 2);
