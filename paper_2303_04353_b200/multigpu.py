@@ -16,6 +16,10 @@ k is never split, so there is no reduction and every element is computed by
 exactly the same arithmetic as on one GPU: C is bitwise independent of W
 (P-invariance).
 
+The INT8 cascade (NEXT-3) shards the same way: its packed B is also
+column-block major (128-column blocks, counted in pairs), so a 256-multiple
+slab is a byte range of the full packed B (`i8_cuda_ops`, block = 256).
+
 `ops` makes the kernels injectable so the host-side plumbing (sharding,
 padding, gather order) is testable on CPU with the gloo backend.
 """
@@ -27,7 +31,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-BLOCK = 64  # packed column-block width (casc_layout.cuh TN)
+BLOCK = 64  # packed column-block width of the FP64 cascade (casc_layout.cuh TN)
+I8_BLOCK = 256  # slab granularity of the INT8 cascade (two 128-column packed blocks)
 
 
 def row_shard(m: int, world: int, rank: int):
@@ -35,13 +40,13 @@ def row_shard(m: int, world: int, rank: int):
     return (rank * m) // world, ((rank + 1) * m) // world
 
 
-def col_slab(n: int, world: int, rank: int):
-    """Columns [c0, c1) of B packed by `rank`: equal 64-multiple slabs so every
-    rank contributes the same number of packed blocks to the all-gather."""
-    nb = -(-n // BLOCK)
+def col_slab(n: int, world: int, rank: int, block: int = BLOCK):
+    """Columns [c0, c1) of B packed by `rank`: equal block-multiple slabs so
+    every rank contributes the same number of packed blocks to the all-gather."""
+    nb = -(-n // block)
     per = -(-nb // world)
-    c0 = min(n, rank * per * BLOCK)
-    c1 = min(n, (rank + 1) * per * BLOCK)
+    c0 = min(n, rank * per * block)
+    c1 = min(n, (rank + 1) * per * block)
     return c0, c1, per
 
 
@@ -62,20 +67,41 @@ def cuda_ops() -> Ops:
                launch_count=casc.casc_last_launch_count)
 
 
+def i8_cuda_ops(y: int = 14) -> Ops:
+    """The INT8 cascade's entry points with the Ops contracts (block = 256 columns)."""
+    import paper_2303_04353_b200 as casc
+
+    def pack_a(A_hi, A_lo, packed=None):
+        return casc.casc_i8_pack(A_hi, A_lo, False, y, packed=packed)
+
+    def pack_b(B_hi, B_lo, packed):
+        return casc.casc_i8_pack(B_hi, B_lo, True, y, packed=packed)
+
+    def gemm_packed(m, n, k, pa, pb, C_hi=None, C_lo=None, flags=None):
+        return casc.casc_i8_gemm_packed(m, n, k, pa, pb, y, C_hi=C_hi, C_lo=C_lo, flags=flags)
+
+    return Ops(pack_a=pack_a, pack_b=pack_b, gemm_packed=gemm_packed,
+               packed_b_block_bytes=lambda k: 2 * casc.casc_i8_packed_block_bytes(k, y),
+               launch_count=casc.casc_last_launch_count)
+
+
 class ShardedCascGemm:
     """Row-sharded cascaded FP64x2 GEMM for one (m, n, k) problem.  Buffers are
     allocated once and reused across calls (bench steps)."""
 
     def __init__(self, m: int, n: int, k: int, group=None, ops: Ops | None = None,
-                 device=None):
+                 device=None, block: int = BLOCK):
+        """block: slab granularity (columns) of the packed B: 64 for the FP64
+        cascade, I8_BLOCK with i8_cuda_ops()."""
         self.m, self.n, self.k = m, n, k
+        self.block = block
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.ops = ops or cuda_ops()
         self.device = device if device is not None else torch.device("cuda")
         self.r0, self.r1 = row_shard(m, self.world, self.rank)
-        self.c0, self.c1, self.blocks_per_rank = col_slab(n, self.world, self.rank)
+        self.c0, self.c1, self.blocks_per_rank = col_slab(n, self.world, self.rank, block)
         blk = self.ops.packed_b_block_bytes(k)
         self.chunk = self.blocks_per_rank * blk
         self.packed_b_local = torch.zeros(self.chunk, dtype=torch.uint8, device=self.device)
@@ -96,7 +122,7 @@ class ShardedCascGemm:
         rec = (lambda i: events[i].record()) if events else (lambda i: None)
         rec(0)
         if self.c1 > self.c0:
-            used = -(-(self.c1 - self.c0) // BLOCK) * self.ops.packed_b_block_bytes(self.k)
+            used = -(-(self.c1 - self.c0) // self.block) * self.ops.packed_b_block_bytes(self.k)
             self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])
             self.launches += count()
         rec(1)

@@ -43,43 +43,51 @@ def test_shard_arithmetic():
 
 class _CpuOps:
     """CPU stand-ins with the same contracts as the CUDA entry points: packed B
-    is 64-column-block major (each block = raw hi | lo of k x 64, zero-padded)."""
+    is column-block major (each block = raw hi | lo of k x W, zero-padded; W =
+    64 for the FP64 cascade, 256 for the INT8 cascade's slab unit), and the
+    product is the matching oracle."""
 
-    def __init__(self, k):
+    def __init__(self, k, W=64, i8=False):
         self.k = k
+        self.W = W
+        self.i8 = i8
 
     def packed_b_block_bytes(self, k):
-        return 2 * k * 64 * 8
+        return 2 * k * self.W * 8
 
     def pack_a(self, A_hi, A_lo, packed=None):
         return (A_hi.clone(), A_lo.clone())
 
     def pack_b(self, B_hi, B_lo, packed):
         k, w = B_hi.shape
-        nb = -(-w // 64)
-        buf = packed.view(torch.float64).view(nb, 2, k, 64)
+        W = self.W
+        nb = -(-w // W)
+        buf = packed.view(torch.float64).view(nb, 2, k, W)
         buf.zero_()
         for j in range(nb):
-            c = B_hi[:, 64 * j:64 * (j + 1)]
+            c = B_hi[:, W * j:W * (j + 1)]
             buf[j, 0, :, :c.shape[1]] = c
-            buf[j, 1, :, :c.shape[1]] = B_lo[:, 64 * j:64 * (j + 1)]
+            buf[j, 1, :, :c.shape[1]] = B_lo[:, W * j:W * (j + 1)]
         return packed
 
     def gemm_packed(self, m, n, k, pa, pb, C_hi=None, C_lo=None, flags=None):
         import oracle
-        nb = -(-n // 64)
-        blocks = pb.view(torch.float64)[:nb * 2 * k * 64].view(nb, 2, k, 64)
+        W = self.W
+        nb = -(-n // W)
+        blocks = pb.view(torch.float64)[:nb * 2 * k * W].view(nb, 2, k, W)
         B_hi = torch.cat([blocks[j, 0] for j in range(nb)], dim=1)[:, :n].numpy()
         B_lo = torch.cat([blocks[j, 1] for j in range(nb)], dim=1)[:, :n].numpy()
-        h, l, f = oracle.casc_gemm(pa[0].numpy(), pa[1].numpy(), B_hi, B_lo)
+        fn = oracle.i8_casc_gemm if self.i8 else oracle.casc_gemm
+        h, l, f = fn(pa[0].numpy(), pa[1].numpy(), B_hi, B_lo)
         return torch.from_numpy(h), torch.from_numpy(l), torch.from_numpy(f)
 
 
-def _worker(rank, world, port, m, n, k, out):
+def _worker(rank, world, port, m, n, k, out, i8=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2303_04353_b200.multigpu import ShardedCascGemm
-    op = ShardedCascGemm(m, n, k, ops=_CpuOps(k), device=torch.device("cpu"))
+    from paper_2303_04353_b200.multigpu import I8_BLOCK, ShardedCascGemm
+    W = I8_BLOCK if i8 else 64
+    op = ShardedCascGemm(m, n, k, ops=_CpuOps(k, W, i8), device=torch.device("cpu"), block=W)
     d = I.make_config(1, m=m, n=n, k=k, seed=21, rows=slice(op.r0, op.r1))
     A_hi, A_lo = torch.from_numpy(d["A_hi"]), torch.from_numpy(d["A_lo"])
     B_hi = torch.from_numpy(d["B_hi"][:, op.c0:op.c1].copy())
@@ -98,6 +106,26 @@ def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k):
              join=True)
     d = I.make_config(1, m=m, n=n, k=k, seed=21)
     ref_hi, ref_lo, ref_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    rows = 0
+    for r in range(world):
+        z = np.load(tmp_path / f"r{r}.npz")
+        r0, r1 = int(z["r0"]), int(z["r1"])
+        assert np.array_equal(z["C_hi"], ref_hi[r0:r1])
+        assert np.array_equal(z["C_lo"], ref_lo[r0:r1])
+        assert np.array_equal(z["fl"], ref_fl[r0:r1])
+        rows += r1 - r0
+    assert rows == m
+
+
+@pytest.mark.parametrize("m,n,k", [(9, 600, 70), (4, 256, 33)])
+def test_gloo_world2_i8_p_invariance(tmp_path, orc, m, n, k):
+    """The INT8 cascade's sharding (256-column slabs, NEXT-3): the gathered
+    result equals the single-process oracle bit for bit."""
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), True), nprocs=world,
+             join=True)
+    d = I.make_config(1, m=m, n=n, k=k, seed=21)
+    ref_hi, ref_lo, ref_fl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
     rows = 0
     for r in range(world):
         z = np.load(tmp_path / f"r{r}.npz")
