@@ -182,11 +182,58 @@ __device__ __forceinline__ int scale_exp(unsigned long long bits) {
   return e;
 }
 
-// Digits (R23) of 32 consecutive k of one vector, written as two 16-byte units
-// per slice.  COLS = false: A rows (element (r, p) at hi[r*ld + p]); block =
-// 64 rows x 128 k.  COLS = true: B columns (element (p, j) at hi[p*ld + j]);
-// block = 128 columns x 128 k.  Padding rows / k are written as zero digits,
-// so the packed operand is fully defined.
+// 128-bit two's-complement integer as four 32-bit words (w[0] least significant)
+struct U128 {
+  uint32_t w[4];
+};
+// exact conversion of an integer-valued double (|x| < 2^113) to 128 bits
+__device__ __forceinline__ U128 dbl_to_u128(double x) {
+  U128 r{{0u, 0u, 0u, 0u}};
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const int be = (int)((b >> 52) & 0x7ff);
+  if (be == 0) return r;  // +-0 (an integer-valued double is never subnormal here)
+  const int sh = be - 1075;  // value = mant * 2^sh, mant in [2^52, 2^53)
+  unsigned long long mant = (b & 0xfffffffffffffull) | 0x10000000000000ull;
+  unsigned long long lo, hi;
+  if (sh <= 0) {
+    lo = mant >> (-sh);  // exact: x is an integer
+    hi = 0;
+  } else if (sh < 64) {
+    lo = mant << sh;
+    hi = sh > 11 ? mant >> (64 - sh) : 0ull;
+  } else {
+    lo = 0;
+    hi = mant << (sh - 64);
+  }
+  if (b >> 63) {  // negate (two's complement)
+    lo = ~lo + 1ull;
+    hi = ~hi + (lo == 0 ? 1ull : 0ull);
+  }
+  r.w[0] = (uint32_t)lo;
+  r.w[1] = (uint32_t)(lo >> 32);
+  r.w[2] = (uint32_t)hi;
+  r.w[3] = (uint32_t)(hi >> 32);
+  return r;
+}
+__device__ __forceinline__ U128 add_u128(const U128& a, const U128& b) {
+  U128 r;
+  asm("add.cc.u32 %0, %4, %8;\n\taddc.cc.u32 %1, %5, %9;\n\taddc.cc.u32 %2, %6, %10;\n\t"
+      "addc.u32 %3, %7, %11;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]),
+        "r"(b.w[2]), "r"(b.w[3]));
+  return r;
+}
+
+// Digits (R23) of 16 consecutive k of one vector, one 16-byte unit per slice.
+// X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)) exactly (128-bit); with K = 0x80 in
+// each of the y-1 lowest byte positions, U = (X + K) xor K has the balanced
+// base-256 digits of X as its bytes: d_t = byte (y-1-t) of U (adding 128 to a
+// digit in [-128, 127] cannot carry; the top digit d_0 in [-64, 64] is the
+// sign-extended remainder).  COLS = false: A rows (element (r, p) at
+// hi[r*ld + p]); block = 32 rows x 128 k.  COLS = true: B columns (element (p, j)
+// at hi[p*ld + j]); block = 128 columns x 32 k.  Padding rows / k get zero
+// digits, so the packed operand is fully defined.
 template <bool COLS>
 __global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict__ hi,
                                                         const double* __restrict__ lo, int64_t ld,
@@ -195,35 +242,42 @@ __global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict
   const int t = threadIdx.x;
   const int64_t kb = blockIdx.y;
   int64_t r;
-  int cs[2];
-  int ncs;
+  int u0, du, nu;
   if (COLS) {
     r = (int64_t)blockIdx.x * 128 + (t & 127);
-    cs[0] = t >> 7;
-    cs[1] = (t >> 7) + 2;
-    ncs = 2;
+    u0 = 2 * blockIdx.z + (t >> 7);  // 16-k unit: grid.z = 4 pairs of units
+    du = 0;
+    nu = 1;
   } else {
-    r = (int64_t)blockIdx.x * 64 + (t >> 2);
-    cs[0] = t & 3;
-    ncs = 1;
+    r = (int64_t)blockIdx.x * 32 + (t >> 3);
+    u0 = t & 7;
+    du = 8;
+    nu = 1;
   }
   if (r >= g.R * TR) return;
   const int64_t q = kb / KBP;
   const int e =
       r < rows ? scale_exp(*reinterpret_cast<const unsigned long long*>(packed + max_at(g, r, q)))
                : 0;
-  if ((kb % KBP) == 0 && cs[0] == 0) *reinterpret_cast<int32_t*>(packed + exp_at(g, r, q)) = e;
-  const int F = 6 + 8 * (g.y - 1);
+  if ((kb % KBP) == 0 && (COLS ? u0 : t & 7) == 0)
+    *reinterpret_cast<int32_t*>(packed + exp_at(g, r, q)) = e;
+  const int y = g.y;
+  const int F = 6 + 8 * (y - 1);
   const int s1 = min(F - e, 1023), s2 = F - e - s1;
   const double sc1 = p2(s1), sc2 = p2(s2);
+  // K: 0x80 in byte positions 0 .. y-2
+  U128 K{{0u, 0u, 0u, 0u}};
+#pragma unroll
+  for (int pos = 0; pos < 16; ++pos)
+    if (pos < y - 1) K.w[pos >> 2] |= 0x80u << (8 * (pos & 3));
   const int rl = (int)(r % TR);
   const int64_t rb = r / TR;
-  for (int u = 0; u < ncs; ++u) {
-    const int c = cs[u];
-    const int64_t p0 = kb * KB + c * 32;
-    __int128 X[32];
+  for (int iu = 0; iu < nu; ++iu) {
+    const int u = u0 + iu * du;
+    const int64_t p0 = kb * KB + u * 16;
+    U128 U[16];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 16; ++i) {
       const int64_t p = p0 + i;
       double h = 0.0, l = 0.0;
       if (r < rows && p < k) {
@@ -231,28 +285,32 @@ __global__ void __launch_bounds__(256) i8_digits_kernel(const double* __restrict
         h = __ldg(hi + idx);
         l = __ldg(lo + idx);
       }
-      X[i] = to_i128(rint(__dmul_rn(__dmul_rn(h, sc1), sc2))) +
-             to_i128(rint(__dmul_rn(__dmul_rn(l, sc1), sc2)));
+      U128 x = add_u128(dbl_to_u128(rint(__dmul_rn(__dmul_rn(h, sc1), sc2))),
+                        dbl_to_u128(rint(__dmul_rn(__dmul_rn(l, sc1), sc2))));
+      x = add_u128(x, K);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) x.w[w] ^= K.w[w];
+      U[i] = x;
     }
-    const uint32_t o0 = sw128(rl, c * 32), o1 = sw128(rl, c * 32 + 16);
-    for (int s = g.y - 1; s >= 0; --s) {
-      uint32_t w[8];
+    const uint32_t off = sw128(rl, u * 16);
 #pragma unroll
-      for (int v = 0; v < 8; ++v) w[v] = 0;
+    for (int pos = 0; pos < 16; ++pos) {  // byte position pos holds slice y-1-pos
+      if (pos >= y) break;
+      const int sl = y - 1 - pos;
+      const int wi = pos >> 2;
+      const uint32_t sel = (uint32_t)(pos & 3);
+      // gather byte `pos` of the 16 elements into 4 words (PRMT)
+      uint32_t o[4];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        int d;
-        if (s > 0) {
-          d = (int)(int8_t)(uint8_t)((unsigned long long)X[i] & 0xffull);
-          X[i] = (X[i] - d) >> 8;
-        } else {
-          d = (int)(long long)X[i];
-        }
-        w[i >> 2] |= (uint32_t)(uint8_t)d << (8 * (i & 3));
+      for (int v = 0; v < 4; ++v) {
+        const uint32_t a0 = U[4 * v + 0].w[wi], a1 = U[4 * v + 1].w[wi];
+        const uint32_t a2 = U[4 * v + 2].w[wi], a3 = U[4 * v + 3].w[wi];
+        const uint32_t lo2 = __byte_perm(a0, a1, sel | ((sel + 4) << 4));
+        const uint32_t hi2 = __byte_perm(a2, a3, sel | ((sel + 4) << 4));
+        o[v] = __byte_perm(lo2, hi2, 0x5410);
       }
-      uint8_t* base = packed + chunk_off(g, s, rb, kb);
-      *reinterpret_cast<uint4*>(base + o0) = make_uint4(w[0], w[1], w[2], w[3]);
-      *reinterpret_cast<uint4*>(base + o1) = make_uint4(w[4], w[5], w[6], w[7]);
+      *reinterpret_cast<uint4*>(packed + chunk_off(g, sl, rb, kb) + off) =
+          make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
@@ -746,12 +804,12 @@ cudaError_t pack(const double* hi, const double* lo, int64_t ld, int64_t rows, i
   if (cols) {
     i8_colmax_kernel<<<dim3((unsigned)((rows + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0,
                        st>>>(hi, ld, rows, k, g, pk);
-    i8_digits_kernel<true><<<dim3((unsigned)g.R, (unsigned)g.KBn), 256, 0, st>>>(hi, lo, ld, rows,
-                                                                                k, g, pk);
+    i8_digits_kernel<true><<<dim3((unsigned)g.R, (unsigned)g.KBn, 4), 256, 0, st>>>(
+        hi, lo, ld, rows, k, g, pk);
   } else {
     i8_rowmax_kernel<<<dim3((unsigned)((rows + 7) / 8), (unsigned)((k + 1023) / 1024)), 256, 0,
                        st>>>(hi, ld, rows, k, g, pk);
-    i8_digits_kernel<false><<<dim3((unsigned)(g.R * 2), (unsigned)g.KBn), 256, 0, st>>>(
+    i8_digits_kernel<false><<<dim3((unsigned)(g.R * 4), (unsigned)g.KBn), 256, 0, st>>>(
         hi, lo, ld, rows, k, g, pk);
   }
   return cudaGetLastError();
