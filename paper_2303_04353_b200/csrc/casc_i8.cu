@@ -69,6 +69,9 @@ constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
 // group values)
 constexpr int THREADS = 320;
 constexpr int EPI_WARP0 = 2, EPI_THREADS = 256;
+#ifndef CASC_I8_SUSPEND_NS
+#define CASC_I8_SUSPEND_NS 1000000
+#endif
 #ifndef CASC_I8_EPI_SUB
 #define CASC_I8_EPI_SUB 8
 #endif
@@ -397,6 +400,23 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Blocking wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint elapses) instead of spinning, so waiting warps do not
+// steal issue slots from the MMA warp or burn power.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_S:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE_S;\nbra WAIT_S;\nDONE_S:\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(CASC_I8_SUSPEND_NS)
+      : "memory");
+}
+// warp-uniform wait: the loop condition is a warp vote, so control flow stays
+// provably uniform and the scalar state can live in the uniform datapath
+__device__ __forceinline__ void mbar_wait_uniform(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
+  }
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
                : "memory");
@@ -424,17 +444,18 @@ __device__ __forceinline__ void tma_pair_elect(void* dst, const CUtensorMap* map
 // acc == 0: the first overwrites the accumulator.
 __device__ __forceinline__ void mma_i8_x4(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
-      "{\n.reg .pred e, p, t;\n"
+      "{\n.reg .pred e, p, t;\n.reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "add.s64 a1, %1, 2;\nadd.s64 a2, %1, 4;\nadd.s64 a3, %1, 6;\n"
+      "add.s64 b1, %2, 2;\nadd.s64 b2, %2, 4;\nadd.s64 b3, %2, 6;\n"
       "elect.sync _|e, 0xffffffff;\n"
       "setp.ne.b32 p, %3, 0;\n"
       "setp.eq.b32 t, 0, 0;\n"
       "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %4, p;\n"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %5, %6, %4, t;\n"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %7, %8, %4, t;\n"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %9, %10, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a1, b1, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a2, b2, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a3, b3, %4, t;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(acc), "n"(IDESC), "l"(a + 2), "l"(b + 2), "l"(a + 4), "l"(b + 4),
-      "l"(a + 6), "l"(b + 6));
+      "l"(a), "l"(b), "r"(acc), "n"(IDESC));
 }
 // tcgen05.commit (multicast to both CTAs of the pair) to one / two mbarriers
 __device__ __forceinline__ void mma_commit1(uint64_t* bar) {
@@ -454,6 +475,62 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
       " [%1], %2;\n}\n" ::"r"(smem_u32(bar0)),
       "r"(smem_u32(bar1)), "h"((uint16_t)3)
       : "memory");
+}
+
+// The MMAs of one 128-byte k block of a group (bins S .. S+NB-1), chain
+// order: for B_j (j = 0 .. top) its partners A_i, i = top-j .. max(0, S-j).
+// Everything except the ring positions is a compile-time constant.
+template <int S, int NB>
+__device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_t& bseq,
+                                          uint32_t tmem, uint32_t a0, uint32_t b0,
+                                          uint64_t* fullA, uint64_t* emptyA, uint64_t* fullB,
+                                          uint64_t* emptyB) {
+  constexpr int TOP = S + NB - 1;
+  const uint32_t abase = aseq;
+#pragma unroll
+  for (int j = 0; j <= TOP; ++j) {
+    const uint32_t bq = bseq + j;
+    const uint32_t bs = bq % NSB;
+    mbar_wait_uniform(&fullB[bs], (bq / NSB) & 1);
+    // A operands first used at this step: A_top..A_S at j = 0, A_(S-j) after
+    if (j == 0) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) mbar_wait_uniform(&fullA[(abase + i) % NSA], ((abase + i) / NSA) & 1);
+    } else if (S - j >= 0) {
+      const uint32_t aq = abase + NB + (j - 1);
+      mbar_wait_uniform(&fullA[aq % NSA], (aq / NSA) & 1);
+    }
+    tc_fence_after();
+    const uint64_t bd = sdesc(b0 + bs * BHALF);
+#pragma unroll
+    for (int i = TOP - j; i >= (S - j > 0 ? S - j : 0); --i) {
+      const uint32_t aq = i >= S ? abase + (TOP - i) : abase + NB + (S - 1 - i);
+      const uint64_t ad = sdesc(a0 + (aq % NSA) * CHUNK);
+      // at the panel's first k block, every bin is first written at j = 0
+      mma_i8_x4(tmem + (i + j - S) * 128, ad, bd, (first_kb && j == 0) ? 0u : 1u);
+    }
+    // B_j is done; A_(TOP-j) has met its last partner
+    const uint32_t rq = (TOP - j) >= S ? abase + j : abase + NB + (S - 1 - (TOP - j));
+    mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
+  }
+  aseq = abase + (uint32_t)(S + NB);
+  bseq += (uint32_t)(TOP + 1);
+}
+
+__device__ __forceinline__ void mma_kblock(int s, int nb, bool first_kb, uint32_t& aseq,
+                                           uint32_t& bseq, uint32_t tmem, uint32_t a0,
+                                           uint32_t b0, uint64_t* fullA, uint64_t* emptyA,
+                                           uint64_t* fullB, uint64_t* emptyB) {
+#define CASC_I8_CHAIN(SS, NN)                                                             \
+  if (s == SS && nb == NN) {                                                              \
+    mma_chain<SS, NN>(first_kb, aseq, bseq, tmem, a0, b0, fullA, emptyA, fullB, emptyB); \
+    return;                                                                               \
+  }
+  CASC_I8_CHAIN(0, 4) CASC_I8_CHAIN(4, 4) CASC_I8_CHAIN(8, 4) CASC_I8_CHAIN(12, 2)
+  CASC_I8_CHAIN(0, 3) CASC_I8_CHAIN(4, 1) CASC_I8_CHAIN(4, 2) CASC_I8_CHAIN(4, 3)
+  CASC_I8_CHAIN(8, 1) CASC_I8_CHAIN(8, 2) CASC_I8_CHAIN(8, 3) CASC_I8_CHAIN(12, 1)
+  CASC_I8_CHAIN(12, 3)
+#undef CASC_I8_CHAIN
 }
 
 // named barrier 1 over the 256 epilogue threads
@@ -538,7 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint32_t aseq = 0, bseq = 0;
     auto loadA = [&](int i, int64_t rb, int64_t kb) {
       const uint32_t s = aseq % NSA;
-      mbar_wait(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
+      mbar_wait_sleep(&emptyA[s], ((aseq / NSA) & 1) ^ 1);
       const int row = (int)(chunk_off(p.ga, i, rb, kb) / KB);
       tma_pair_elect(sA + s * CHUNK, &mapA, row, &fullA[s], leader_addr(&fullA[s]),
                      leader ? 2 * CHUNK : 0);
@@ -546,7 +623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     auto loadB = [&](int j, int64_t cb, int64_t kb) {
       const uint32_t s = bseq % NSB;
-      mbar_wait(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
+      mbar_wait_sleep(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
       const int row = (int)(chunk_off(p.gb, j, cb, kb) / KB + rank * (TR / 2));
       tma_pair_elect(sB + s * BHALF, &mapB, row, &fullB[s], leader_addr(&fullB[s]),
                      leader ? 2 * BHALF : 0);
@@ -607,40 +684,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
             mbar_wait_cluster(tempty, (gcount & 1) ^ 1);
             tc_fence_after();
-            uint32_t touched = 0;
-            for (int kb = kb0; kb < kb1; ++kb) {
-              const uint32_t abase = aseq;
-              for (int j = 0; j <= top; ++j) {
-                const uint32_t bs = bseq % NSB;
-                mbar_wait(&fullB[bs], (bseq / NSB) & 1);
-                // A operands first used at this step: A_top..A_s at j = 0, A_(s-j) after
-                if (j == 0) {
-                  for (int i = 0; i < nb; ++i) {
-                    const uint32_t aq = abase + i;
-                    mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
-                  }
-                } else if (s - j >= 0) {
-                  const uint32_t aq = abase + nb + (j - 1);
-                  mbar_wait(&fullA[aq % NSA], (aq / NSA) & 1);
-                }
-                tc_fence_after();
-                const uint64_t bd = sdesc(b_base_addr + bs * BHALF);
-                const int ilo = max(0, s - j), ihi = top - j;
-                for (int i = ihi; i >= ilo; --i) {
-                  const uint32_t aq = i >= s ? abase + (top - i) : abase + nb + (s - 1 - i);
-                  const uint64_t ad = sdesc(a_base_addr + (aq % NSA) * CHUNK);
-                  const int b = i + j - s;
-                  const uint32_t acc = (kb == kb0 && !((touched >> b) & 1)) ? 0u : 1u;
-                  mma_i8_x4(tmem + b * 128, ad, bd, acc);
-                  touched |= 1u << b;
-                }
-                // B_j is done; A_(top-j) has met its last partner
-                const uint32_t rq = (top - j) >= s ? abase + j : abase + nb + (s - 1 - (top - j));
-                mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
-                ++bseq;
-              }
-              aseq = abase + (uint32_t)(s + nb);
-            }
+            for (int kb = kb0; kb < kb1; ++kb)
+              mma_kblock(s, nb, kb == kb0, aseq, bseq, tmem, a_base_addr, b_base_addr, fullA,
+                         emptyA, fullB, emptyB);
             mma_commit1(tfull);
           }
         }
@@ -676,11 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
           const int s = grp * NBIN, nb = min(NBIN, y - s);
           const bool needT = grp > 0, lastg = grp + 1 == ngroups, needC = lastg && q > 0;
-#ifdef CASC_I8_EPI_SLEEP
-          while (!mbar_try(tfull, gcount & 1)) __nanosleep(CASC_I8_EPI_SLEEP);
-#else
-          mbar_wait(tfull, gcount & 1);
-#endif
+          mbar_wait_sleep(tfull, gcount & 1);
           tc_fence_after();
           // Phase 1: drain this warp's part of TMEM into the exact group values
           // V = sum_u bin_(s+u) 2^(8(nb-1-u)) (int64, |V| < 2^56; R25), then

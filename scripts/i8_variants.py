@@ -5,9 +5,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
-    "sleep": ["CASC_I8_EPI_SLEEP=200"],
+    "susp0": ["CASC_I8_SUSPEND_NS=0"],
+    "susp10k": ["CASC_I8_SUSPEND_NS=10000"],
     "g4": ["CASC_I8_GROUP_M=4"],
-    "g32": ["CASC_I8_GROUP_M=32"],
+    "g8": ["CASC_I8_GROUP_M=8"],
 }
 if sys.argv[1] == "build":
     import importlib.util
