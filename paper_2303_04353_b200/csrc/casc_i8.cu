@@ -25,21 +25,28 @@
 //        (r/8)*1024 + (r%8)*128, 16-byte unit u at u ^ (r%8)), so the GEMM
 //        moves every operand tile with ONE cp.async.bulk and points the MMA
 //        descriptor at it.
-// Phase 2+3: i8_gemm_kernel, persistent (one CTA per SM), 384 threads:
-//   warp 0     TMA producer: 16 KB chunks into an A ring (8 slots) and a B ring
-//              (4 slots), mbarrier complete_tx;
-//   warp 1     MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::i8,
-//              M = N = 128, K = 32, s8 x s8 -> s32; the four bins of a group
-//              accumulate in tensor memory (4 x 128 of the 512 columns).  Per
-//              128-byte k block the operands of a group are streamed as a chain
-//              A_top .. A_s, B_0, A_(s-1), B_1, ... so each B_j meets its (up to)
-//              four A_i partners while they sit in smem: every chunk is loaded
-//              once per k block and feeds up to four MMAs;
-//   warp 1 also allocates TMEM (512 columns);
-//   warps 2-9  epilogue: tcgen05.ld of the int32 bins (warp w reads TMEM lane
-//              quarter w%4, column half (w-2)/4), exact group value, FP64x2
-//              panel sum T and C in a per-CTA workspace (L2-resident), detector,
-//              final store of C and the flags.
+// Phase 2+3: i8_gemm_kernel, persistent CTA pairs (cluster of 2, one pair per
+// two SMs, 320 threads each); the pair computes a 256 x 128 C tile:
+//   warp 8     TMA producer (both CTAs): 2-SM tensor copies
+//              (cp.async.bulk.tensor.2d.cta_group::2) of the CTA's half of each
+//              operand chunk (A: its 128 rows, 16 KB; B: its 64 of the chunk's
+//              128 columns, 8 KB) into rings of 8 + 8 slots, completing on the
+//              leader CTA's mbarriers; a soft wave synchronisation aligns the
+//              producers of all CTAs at every (panel, group) sweep (L2 reuse);
+//   warp 9     MMA issuer (leader CTA; also allocates TMEM): tcgen05.mma
+//              .cta_group::2.kind::i8, M = 256, N = 128, K = 32, s8 x s8 -> s32,
+//              the four bins of a group in tensor memory (4 x 128 = all 512
+//              columns of each CTA); per 128-byte k block the group's operands
+//              stream as a chain A_top .. A_s, B_0, A_(s-1), B_1, ... so every
+//              chunk is loaded once and meets all (up to four) partners while
+//              resident; commits are multicast to both CTAs;
+//   warps 0-7  epilogue (both CTAs): tcgen05.ld of the int32 bins of the CTA's
+//              128 rows (warp w reads TMEM lane quarter w%4, column half w/4)
+//              into exact int64 group values (then TMEM is released), then the
+//              FP64x2 panel sum T and C in a per-CTA workspace, the detector, and
+//              the final store of C and the flags.
+// Producer and MMA warps have the highest warp ids: the sub-partition scheduler
+// favours them over the epilogue warps they share an issue slot with.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -64,11 +71,14 @@ constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
 constexpr int NSA = 8, NSB = 8;    // smem ring slots (A: 16 KB, B: 8 KB half chunks)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
-// warp 0 TMA producer, warp 1 MMA issuer + TMEM allocator, warps 2-9 epilogue
 // (320 threads: up to 204 registers each, room for the epilogue's 64 exact
 // group values)
 constexpr int THREADS = 320;
-constexpr int EPI_WARP0 = 2, EPI_THREADS = 256;
+// warps 0-7 epilogue, warp 8 TMA producer, warp 9 MMA issuer + TMEM allocator.
+// The warp scheduler of a sub-partition (warp id % 4) favours the highest warp
+// id, so the producer and the MMA issuer win the issue slot over the epilogue
+// warps they share a sub-partition with.
+constexpr int PRODUCER_WARP = 8, MMA_WARP = 9, EPI_THREADS = 256;
 #ifndef CASC_I8_SUSPEND_NS
 #define CASC_I8_SUSPEND_NS 1000000
 #endif
@@ -477,6 +487,11 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
       : "memory");
 }
 
+#ifdef CASC_I8_NOWAIT  // timing study only: MMA issue rate without data waits (wrong results)
+#define CASC_I8_WAITS_ON 0
+#else
+#define CASC_I8_WAITS_ON 1
+#endif
 // The MMAs of one 128-byte k block of a group (bins S .. S+NB-1), chain
 // order: for B_j (j = 0 .. top) its partners A_i, i = top-j .. max(0, S-j).
 // Everything except the ring positions is a compile-time constant.
@@ -491,12 +506,14 @@ __device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_
   for (int j = 0; j <= TOP; ++j) {
     const uint32_t bq = bseq + j;
     const uint32_t bs = bq % NSB;
+#ifndef CASC_I8_NOWAIT
     mbar_wait_uniform(&fullB[bs], (bq / NSB) & 1);
+#endif
     // A operands first used at this step: A_top..A_S at j = 0, A_(S-j) after
-    if (j == 0) {
+    if (CASC_I8_WAITS_ON && j == 0) {
 #pragma unroll
       for (int i = 0; i < NB; ++i) mbar_wait_uniform(&fullA[(abase + i) % NSA], ((abase + i) / NSA) & 1);
-    } else if (S - j >= 0) {
+    } else if (CASC_I8_WAITS_ON && S - j >= 0) {
       const uint32_t aq = abase + NB + (j - 1);
       mbar_wait_uniform(&fullA[aq % NSA], (aq / NSA) & 1);
     }
@@ -590,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(tempty, 2 * EPI_THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -608,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int tiles = (int)(RP * RB);
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
-  if (warp == 0) {
+  if (warp == PRODUCER_WARP) {
     // ============================ TMA producer (both CTAs) ============================
     // all lanes run the loop; one elected lane arms / issues; the data of both
     // CTAs completes on the leader's full barriers
@@ -669,7 +686,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == MMA_WARP) {
     if (leader) {
       // ============================ MMA issuer (leader CTA) ============================
       // All 32 lanes run the loop (warp-uniform control flow, so the scalar state
@@ -682,7 +699,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
           for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
             const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+#ifndef CASC_I8_NOWAIT
             mbar_wait_cluster(tempty, (gcount & 1) ^ 1);
+#endif
             tc_fence_after();
             for (int kb = kb0; kb < kb1; ++kb)
               mma_kblock(s, nb, kb == kb0, aseq, bseq, tmem, a_base_addr, b_base_addr, fullA,
@@ -692,9 +711,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  } else {
     // ============================ epilogue (both CTAs) ============================
-    const int ew = warp - EPI_WARP0;
+    const int ew = warp;  // 0..7
     const int quarter = warp & 3, half = ew >> 2;
     const int lr = quarter * 32 + lane;       // tile row = TMEM lane
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
@@ -831,7 +850,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   cluster_sync_all();
-  if (warp == 1) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }

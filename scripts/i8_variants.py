@@ -5,9 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
-    "susp0": ["CASC_I8_SUSPEND_NS=0"],
-    "susp10k": ["CASC_I8_SUSPEND_NS=10000"],
-    "g4": ["CASC_I8_GROUP_M=4"],
+    "nowait": ["CASC_I8_NOWAIT"],
+    "nowait_noepi": ["CASC_I8_NOWAIT", "CASC_I8_NO_EPI"],
     "g8": ["CASC_I8_GROUP_M=8"],
 }
 if sys.argv[1] == "build":
