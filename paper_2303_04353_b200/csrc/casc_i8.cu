@@ -52,6 +52,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "../../include/casc.h"
 #include "casc_dd.cuh"
@@ -550,6 +551,25 @@ __device__ __forceinline__ void mma_kblock(int s, int nb, bool first_kb, uint32_
 #undef CASC_I8_CHAIN
 }
 
+// epilogue workspace loads: coherent, no L1 allocation (keeps L1 / shared
+// memory bandwidth for the tensor cores' operand reads)
+template <typename T>
+__device__ __forceinline__ T ld_na(const T* p) {
+#ifdef CASC_I8_LD_PLAIN
+  return *p;
+#else
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long v;
+    asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    T r;
+    memcpy(&r, &v, 8);
+    return r;
+  } else {
+    return *p;
+  }
+#endif
+}
+
 // named barrier 1 over the 256 epilogue threads
 __device__ __forceinline__ void epi_bar_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
@@ -792,19 +812,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             double xth[EPI_SUB], xtl[EPI_SUB], xch[EPI_SUB], xcl[EPI_SUB];
             long long xv[EPI_SUB];
 #pragma unroll
-            for (int i = 0; i < EPI_SUB; ++i) xv[i] = Vw[(c0 + i) * TR + lr];
+            for (int i = 0; i < EPI_SUB; ++i) xv[i] = ld_na(&Vw[(c0 + i) * TR + lr]);
             if (needT) {
 #pragma unroll
               for (int i = 0; i < EPI_SUB; ++i) {
-                xth[i] = Th[(c0 + i) * TR + lr];
-                xtl[i] = Tl[(c0 + i) * TR + lr];
+                xth[i] = ld_na(&Th[(c0 + i) * TR + lr]);
+                xtl[i] = ld_na(&Tl[(c0 + i) * TR + lr]);
               }
             }
             if (needC) {
 #pragma unroll
               for (int i = 0; i < EPI_SUB; ++i) {
-                xch[i] = Ch[(c0 + i) * TR + lr];
-                xcl[i] = Cl[(c0 + i) * TR + lr];
+                xch[i] = ld_na(&Ch[(c0 + i) * TR + lr]);
+                xcl[i] = ld_na(&Cl[(c0 + i) * TR + lr]);
               }
             }
 #pragma unroll

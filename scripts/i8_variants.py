@@ -5,8 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
-    "nowait": ["CASC_I8_NOWAIT"],
-    "nowait_noepi": ["CASC_I8_NOWAIT", "CASC_I8_NO_EPI"],
+    "ldplain": ["CASC_I8_LD_PLAIN"],
     "g8": ["CASC_I8_GROUP_M=8"],
 }
 if sys.argv[1] == "build":
