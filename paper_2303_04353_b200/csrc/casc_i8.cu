@@ -88,7 +88,7 @@ constexpr int PRODUCER_WARP = 8, MMA_WARP = 9, EPI_THREADS = 256;
 #endif
 constexpr int EPI_SUB = CASC_I8_EPI_SUB;  // elements per phase-2 step of the epilogue
 #ifndef CASC_I8_GROUP_M
-#define CASC_I8_GROUP_M 12
+#define CASC_I8_GROUP_M 6
 #endif
 constexpr int GROUP_M = CASC_I8_GROUP_M;  // tile raster: GROUP_M row-pair blocks sweep the columns
 constexpr size_t SMEM = (size_t)NSA * CHUNK + (size_t)NSB * (CHUNK / 2) + 1024 + 1024;

@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
-    "ldplain": ["CASC_I8_LD_PLAIN"],
+    "g6": ["CASC_I8_GROUP_M=6"],
+    "g5": ["CASC_I8_GROUP_M=5"],
     "g8": ["CASC_I8_GROUP_M=8"],
 }
 if sys.argv[1] == "build":
