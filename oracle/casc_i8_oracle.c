@@ -27,8 +27,10 @@
  *                  slice t is d_t 2^(e - 6 - 8t).
  *   R24 products   bin_s = sum_p sum_(i+j=s) dA_i dB_j for s = 0 .. y-1 (the
  *                  paper's triangle of y(y+1)/2 products), exact.
- *   R25 combine    bins four at a time, most significant group first: the
- *                  group value V = sum_u bin_(s+u) 2^(8(nb-1-u)) is exact in
+ *   R25 combine    bins in groups of four aligned at the least significant bin
+ *                  (the first group is bins 0 .. r-1, r = (y-1) % 4 + 1, e.g.
+ *                  {0,1} {2-5} {6-9} {10-13} for y = 14), most significant group
+ *                  first: the group value V = sum_u bin_(s+u) 2^(8(nb-1-u)) is exact in
  *                  int64; G = (RN(V), V - RN(V)) scaled by 2^(e+f-12-8(s+nb-1));
  *                  the panel value T = DDadd over the groups, then C = DDadd(C, T)
  *                  over panels in ascending order (FP64x2; the FP64
@@ -159,10 +161,13 @@ void orc_i8_casc_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const 
           }
           b[s] = acc;
         }
-        /* reading R25: groups of four, most significant first -> panel value T */
+        /* reading R25: groups of four aligned at the least significant bin (the
+         * first group holds bins 0 .. r-1, r = (y-1) % 4 + 1), most significant
+         * group first -> panel value T */
         double th = 0.0, tl = 0.0;
-        for (int s = 0; s < y; s += 4) {
-          const int nb = (y - s < 4) ? y - s : 4;
+        const int r0 = (y - 1) % 4 + 1;
+        for (int s = 0; s < y; s = (s == 0 ? r0 : s + 4)) {
+          const int nb = (s == 0) ? r0 : 4;
           double gh, gl;
           orc_i8_group_value(b + s, nb, &gh, &gl);
           const int w = e[i] + f[j] - 12 - 8 * (s + nb - 1);

@@ -11,7 +11,8 @@
 //   R23  X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)), F = 6 + 8(y-1); slices = the
 //        balanced base-256 digits of X (d_0 in [-64, 64], others [-128, 127]).
 //   R24  bin_s = sum_p sum_(i+j=s) dA_i dB_j, s < y.
-//   R25  groups of four bins -> exact FP64x2 group value G, scaled by
+//   R25  groups of four bins aligned at the least significant bin (bins
+//        0 .. r-1, r = (y-1) % 4 + 1, first) -> exact FP64x2 group value G, scaled by
 //        2^(e+f-12-8(s+nb-1)); panel value T = FP64x2 sum of the groups, most
 //        significant first; C = C (+) T over panels.
 //   R26  flag |= |T.hi| <= kp 2^(e+f-50).
@@ -544,10 +545,11 @@ __device__ __forceinline__ void mma_kblock(int s, int nb, bool first_kb, uint32_
     mma_chain<SS, NN>(first_kb, aseq, bseq, tmem, a0, b0, fullA, emptyA, fullB, emptyB); \
     return;                                                                               \
   }
-  CASC_I8_CHAIN(0, 4) CASC_I8_CHAIN(4, 4) CASC_I8_CHAIN(8, 4) CASC_I8_CHAIN(12, 2)
-  CASC_I8_CHAIN(0, 3) CASC_I8_CHAIN(4, 1) CASC_I8_CHAIN(4, 2) CASC_I8_CHAIN(4, 3)
-  CASC_I8_CHAIN(8, 1) CASC_I8_CHAIN(8, 2) CASC_I8_CHAIN(8, 3) CASC_I8_CHAIN(12, 1)
-  CASC_I8_CHAIN(12, 3)
+  // (first bin, bins) of the R25 groups for y = 3 .. 15
+  CASC_I8_CHAIN(0, 1) CASC_I8_CHAIN(0, 2) CASC_I8_CHAIN(0, 3) CASC_I8_CHAIN(0, 4)
+  CASC_I8_CHAIN(1, 4) CASC_I8_CHAIN(2, 4) CASC_I8_CHAIN(3, 4) CASC_I8_CHAIN(4, 4)
+  CASC_I8_CHAIN(5, 4) CASC_I8_CHAIN(6, 4) CASC_I8_CHAIN(7, 4) CASC_I8_CHAIN(8, 4)
+  CASC_I8_CHAIN(9, 4) CASC_I8_CHAIN(10, 4) CASC_I8_CHAIN(11, 4)
 #undef CASC_I8_CHAIN
 }
 
@@ -638,7 +640,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tslot;
 
   const int y = p.ga.y;
-  const int ngroups = (y + NBIN - 1) / NBIN;
+  // R25 groups: bins 0 .. r0-1, then fours (aligned at the least significant bin)
+  const int r0 = (y - 1) % NBIN + 1;
+  const int ngroups = 1 + (y - r0) / NBIN;
   const int64_t RA = p.ga.R, RB = p.gb.R, KBn = p.ga.KBn;
   const int64_t RP = RA / 2;
   const int P = (int)p.ga.P;
@@ -676,7 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int q = 0; q < P; ++q) {
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
         for (int grp = 0; grp < ngroups; ++grp) {
-          const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+          const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
           if (synced) {
             // Soft wave synchronisation: the producers of all CTAs start each
             // (panel, group) sweep of a full tile wave together, so the tiles in
@@ -718,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int q = 0; q < P; ++q) {
           const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
           for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
-            const int s = grp * NBIN, nb = min(NBIN, y - s), top = s + nb - 1;
+            const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
 #ifndef CASC_I8_NOWAIT
             mbar_wait_cluster(tempty, (gcount & 1) ^ 1);
 #endif
@@ -759,7 +763,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, cb * TR + ew * 32 + lane, q));
         epi_bar_sync();
         for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
-          const int s = grp * NBIN, nb = min(NBIN, y - s);
+          const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
           const bool needT = grp > 0, lastg = grp + 1 == ngroups, needC = lastg && q > 0;
           mbar_wait_sleep(tfull, gcount & 1);
           tc_fence_after();
