@@ -137,7 +137,9 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, y=14):
         "ms_per_step": total, "phases_ms": ph,
         "parity": "bit-exact vs oracle/casc_i8_oracle.c (tests/test_gpu_i8.py)",
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
-                     "unit": "TOP/s (int8)", "frac": achieved / peak_sus, "traffic": None,
+                     "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
+                     "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
+                     if (m, n, k) == (16384, 16384, 16384) else None,
                      "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
                                "combine)",
                      "peak_source": f"{src}, sustained (burst {peak_burst:.0f}); "

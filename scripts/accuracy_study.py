@@ -2,7 +2,8 @@
 
 For uniform, wide-range and ill-conditioned (t = 1e-9, 1e-14, 1e-19) inputs and
 a sweep of square sizes, compare the componentwise relative error of
-  * the cascaded GEMM on the GPU (casc_gemm_fp64x2), and
+  * the cascaded GEMM on the GPU (casc_gemm_fp64x2),
+  * the INT8 cascade on the GPU (casc_i8_gemm_fp64x2, NEXT-3, y = 14), and
   * the plain triple-loop FP64x2 GEMM (ORACLE-DD, the paper's comparator),
 against the EXACT product (superaccumulator; the paper used FP128x2).
 Reports max / median relative error, the ratio max_DD / max_cascade (the
@@ -43,8 +44,12 @@ def run_case(d, casc, torch):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     g_hi, g_lo, fl = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]))
     g_hi, g_lo, fl = g_hi.cpu().numpy(), g_lo.cpu().numpy(), fl.cpu().numpy()
+    i_hi, i_lo, ifl = casc.casc_i8_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                               T(d["B_lo"]))
+    i_hi, i_lo, ifl = i_hi.cpu().numpy(), i_lo.cpu().numpy(), ifl.cpu().numpy()
     o_hi, o_lo = oracle.dd_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
     rc, r = rel_errors(d, g_hi, g_lo)
+    ri, ri_r = rel_errors(d, i_hi, i_lo)
     rd, _ = rel_errors(d, o_hi, o_lo)
     bound = oracle.north_star_bound(d["k"], r["absab"]).reshape(rc.shape)
     abs_c = np.abs(r["err"]).reshape(rc.shape)
@@ -53,7 +58,11 @@ def run_case(d, casc, torch):
                 ratio_max_dd_over_cascade=float(rd.max() / rc.max()) if rc.max() > 0 else None,
                 flags=int(fl.sum()), within_north_star_bound=bool(np.all(abs_c <= bound)),
                 frac_elements_cascade_better=float(np.mean(rc < rd)),
-                frac_elements_cascade_not_worse=float(np.mean(rc <= rd))), rc, rd
+                frac_elements_cascade_not_worse=float(np.mean(rc <= rd)),
+                max_rel_int8=float(ri.max()), median_rel_int8=float(np.median(ri)),
+                flags_int8=int(ifl.sum()),
+                int8_within_north_star_bound=bool(np.all(np.abs(ri_r["err"]).reshape(rc.shape)
+                                                         <= bound))), rc, rd
 
 
 def main():

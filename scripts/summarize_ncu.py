@@ -24,6 +24,9 @@ KEYS = [
     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__cycles_elapsed.avg.per_second", "lts__t_sector_hit_rate.pct",
+    "l1tex__m_xbar2l1tex_read_bytes.sum",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -101,13 +104,26 @@ def summarize_launches(path, out):
             d = dict(zip(hdr, r))
             name = d["Kernel Name"].split("(")[0]
             per[name].append(float(d["Metric Value"]))
-    ours = {k: v for k, v in per.items() if k.startswith("casc::")}
-    step = sum(sum(v) / len(v) for v in ours.values())
-    lines = ["kernel | launches | mean ms | share of step (our kernels)"]
+    # two steps share the launch list: the north star's FP64 cascade (casc::) and
+    # the NEXT-3 INT8 cascade (i8::); shares are within each step
+    def step_of(k):
+        base = k.replace("void ", "")
+        if "i8::" in base or base.startswith("i8_"):
+            return "int8"
+        if "casc::" in base or base.startswith("casc_") or base.startswith("split_"):
+            return "fp64"
+        return None
+    steps = defaultdict(float)
+    for k, v in per.items():
+        if step_of(k):
+            steps[step_of(k)] += sum(v) / len(v)
+    lines = ["kernel | launches | mean ms | step | share of its step (our kernels)"]
     for k, v in sorted(per.items(), key=lambda x: -sum(x[1])):
         mean = sum(v) / len(v) / 1e6
-        share = (sum(v) / len(v)) / step if k in ours else None
-        lines.append(f"{k} | {len(v)} | {mean:.3f} | {'' if share is None else f'{100 * share:.2f}%'}")
+        st = step_of(k)
+        share = (sum(v) / len(v)) / steps[st] if st else None
+        lines.append(f"{k} | {len(v)} | {mean:.3f} | {st or ''} | "
+                     f"{'' if share is None else f'{100 * share:.2f}%'}")
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
 
