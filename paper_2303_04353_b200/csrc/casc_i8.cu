@@ -497,43 +497,117 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
 // The MMAs of one 128-byte k block of a group (bins S .. S+NB-1), chain
 // order: for B_j (j = 0 .. top) its partners A_i, i = top-j .. max(0, S-j).
 // Everything except the ring positions is a compile-time constant.
+// One 32-byte k step (kk) of A_i against its P partners B_j, issued by one
+// elected lane: the A operand is read from shared memory once and held in the
+// tensor core's A collector (collector::a::fill / use / lastuse) for the other
+// P-1 MMAs.  d[u]: accumulator column of partner u; acc == 0: the MMAs
+// overwrite (first k step of the panel).
+template <int P>
+__device__ __forceinline__ void mma_i8_astat(const uint32_t (&d)[4], uint64_t a,
+                                             const uint64_t (&b)[4], uint32_t acc) {
+  if constexpr (P == 1) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %3, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %4, p;\n}\n" ::"r"(d[0]),
+        "l"(a), "l"(b[0]), "r"(acc), "n"(IDESC));
+  } else if constexpr (P == 2) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %5, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %2, %3, %6, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%1], %2, %4, %6, p;\n}\n" ::"r"(
+            d[0]),
+        "r"(d[1]), "l"(a), "l"(b[0]), "l"(b[1]), "r"(acc), "n"(IDESC));
+  } else if constexpr (P == 3) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %7, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %3, %4, %8, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::use [%1], %3, %5, %8, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%2], %3, %6, %8, p;\n}\n" ::"r"(
+            d[0]),
+        "r"(d[1]), "r"(d[2]), "l"(a), "l"(b[0]), "l"(b[1]), "l"(b[2]), "r"(acc), "n"(IDESC));
+  } else {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %9, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::fill [%0], %4, %5, %10, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::use [%1], %4, %6, %10, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::use [%2], %4, %7, %10, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::i8.collector::a::lastuse [%3], %4, %8, %10, p;\n}\n" ::"r"(
+            d[0]),
+        "r"(d[1]), "r"(d[2]), "r"(d[3]), "l"(a), "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]),
+        "r"(acc), "n"(IDESC));
+  }
+}
+
+// The MMAs of one 128-byte k block of a group (bins S .. S+NB-1, TOP = S+NB-1),
+// A-stationary chain order: A_i for i = 0 .. TOP meets its partners B_j,
+// j = TOP-i .. max(0, S-i), while they sit in shared memory (a window of up to
+// four B chunks: B_TOP .. B_S first, then one new B_(S-i) per A_i), and for
+// each 32-byte k step the A operand is fetched once into the collector.  The
+// producer streams B_TOP .. B_S, A_0, B_(S-1), A_1, B_(S-2), A_2, ...
+// Everything except the ring positions is a compile-time constant.
 template <int S, int NB>
 __device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_t& bseq,
                                           uint32_t tmem, uint32_t a0, uint32_t b0,
                                           uint64_t* fullA, uint64_t* emptyA, uint64_t* fullB,
                                           uint64_t* emptyB) {
   constexpr int TOP = S + NB - 1;
-  const uint32_t abase = aseq;
+  const uint32_t bbase = bseq;
 #pragma unroll
-  for (int j = 0; j <= TOP; ++j) {
-    const uint32_t bq = bseq + j;
-    const uint32_t bs = bq % NSB;
-#ifndef CASC_I8_NOWAIT
-    mbar_wait_uniform(&fullB[bs], (bq / NSB) & 1);
-#endif
-    // A operands first used at this step: A_top..A_S at j = 0, A_(S-j) after
-    if (CASC_I8_WAITS_ON && j == 0) {
+  for (int i = 0; i <= TOP; ++i) {
+    const uint32_t aq = aseq + i;
+    const uint32_t as = aq % NSA;
+    // B operands first used at this step: B_TOP..B_S at i = 0, B_(S-i) after
+    if (i == 0) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) mbar_wait_uniform(&fullA[(abase + i) % NSA], ((abase + i) / NSA) & 1);
-    } else if (CASC_I8_WAITS_ON && S - j >= 0) {
-      const uint32_t aq = abase + NB + (j - 1);
-      mbar_wait_uniform(&fullA[aq % NSA], (aq / NSA) & 1);
+      for (int u = 0; u < NB; ++u)
+        mbar_wait_uniform(&fullB[(bbase + u) % NSB], ((bbase + u) / NSB) & 1);
+    } else if (S - i >= 0) {
+      const uint32_t bq = bbase + NB + (i - 1);
+      mbar_wait_uniform(&fullB[bq % NSB], (bq / NSB) & 1);
     }
+    mbar_wait_uniform(&fullA[as], (aq / NSA) & 1);
     tc_fence_after();
-    const uint64_t bd = sdesc(b0 + bs * BHALF);
+    constexpr int JHI_ = TOP;  // (per i below)
+    (void)JHI_;
+    const int jhi = TOP - i, jlo = (S - i > 0 ? S - i : 0);
+    constexpr int PMAX = 4;
+    uint32_t d[PMAX];
+    uint64_t bd[PMAX];
 #pragma unroll
-    for (int i = TOP - j; i >= (S - j > 0 ? S - j : 0); --i) {
-      const uint32_t aq = i >= S ? abase + (TOP - i) : abase + NB + (S - 1 - i);
-      const uint64_t ad = sdesc(a0 + (aq % NSA) * CHUNK);
-      // at the panel's first k block, every bin is first written at j = 0
-      mma_i8_x4(tmem + (i + j - S) * 128, ad, bd, (first_kb && j == 0) ? 0u : 1u);
+    for (int u = 0; u < PMAX; ++u) {
+      const int j = jhi - u;
+      if (j >= jlo) {
+        const uint32_t bq = j >= S ? bbase + (TOP - j) : bbase + NB + (S - 1 - j);
+        bd[u] = sdesc(b0 + (bq % NSB) * BHALF);
+        d[u] = tmem + (i + j - S) * 128;
+      } else {
+        bd[u] = 0;
+        d[u] = 0;
+      }
     }
-    // B_j is done; A_(TOP-j) has met its last partner
-    const uint32_t rq = (TOP - j) >= S ? abase + j : abase + NB + (S - 1 - (TOP - j));
-    mma_commit2(&emptyB[bs], &emptyA[rq % NSA]);
+    const uint64_t ad = sdesc(a0 + as * CHUNK);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      // at the panel's first k block every bin is first written at i = 0, kk = 0
+      const uint32_t acc = (first_kb && i == 0 && kk == 0) ? 0u : 1u;
+      const uint64_t bk[4] = {bd[0] + 2 * kk, bd[1] + 2 * kk, bd[2] + 2 * kk, bd[3] + 2 * kk};
+      const int np = jhi - jlo + 1;
+      if (np == 4)
+        mma_i8_astat<4>(d, ad + 2 * kk, bk, acc);
+      else if (np == 3)
+        mma_i8_astat<3>(d, ad + 2 * kk, bk, acc);
+      else if (np == 2)
+        mma_i8_astat<2>(d, ad + 2 * kk, bk, acc);
+      else
+        mma_i8_astat<1>(d, ad + 2 * kk, bk, acc);
+    }
+    // A_i is done; B_(TOP-i) has met its last partner
+    const int jr = TOP - i;
+    const uint32_t rq = jr >= S ? bbase + i : bbase + NB + (S - 1 - jr);
+    mma_commit2(&emptyA[as], &emptyB[rq % NSB]);
   }
-  aseq = abase + (uint32_t)(S + NB);
-  bseq += (uint32_t)(TOP + 1);
+  aseq += (uint32_t)(TOP + 1);
+  bseq = bbase + (uint32_t)(S + NB);
 }
 
 __device__ __forceinline__ void mma_kblock(int s, int nb, bool first_kb, uint32_t& aseq,
@@ -700,11 +774,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             __syncwarp();
           }
           for (int64_t kb = kb0; kb < kb1; ++kb) {
-            for (int i = top; i >= s; --i) loadA(i, rb, kb);
-            loadB(0, cb, kb);
-            for (int j = 1; j <= top; ++j) {
-              if (s - j >= 0) loadA(s - j, rb, kb);
-              loadB(j, cb, kb);
+            // A-stationary chain (mma_chain): B_top .. B_s, A_0, B_(s-1), A_1, ...
+            for (int j = top; j >= s; --j) loadB(j, cb, kb);
+            loadA(0, rb, kb);
+            for (int i = 1; i <= top; ++i) {
+              if (s - i >= 0) loadB(s - i, cb, kb);
+              loadA(i, rb, kb);
             }
           }
         }
