@@ -195,3 +195,63 @@ def test_i8_packed_interface_and_slab_contiguity(casc, orc):
     assert slab.numel() == 2 * blk
     # chunks and exponents identical; the u64 max scratch is part of each block too
     assert torch.equal(slab, pb[2 * blk:4 * blk])
+
+
+@pytest.mark.parametrize("cfg,variant", [(2, "a"), (3, "a"), (3, "b"), (4, "a")])
+def test_i8_full_size_configs_sampled(casc, orc, cfg, variant):
+    """BASELINE configs 2, 3 and 4 at FULL size through casc_i8_gemm_fp64x2 (the
+    kernels and launch configuration bench.py times): a rows x 96-column block
+    bit-exact against the INT8 oracle (rows and columns are independent: per-row
+    and per-column scales), sampled entries within the north-star bound of the
+    exact product (except where flagged: 3b cancels by design)."""
+    import torch
+    d = I.make_config(cfg, variant=variant)
+    m, n, k = d["m"], d["n"], d["k"]
+    C_hi, C_lo, fl = casc.casc_i8_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                              T(d["B_lo"]))
+    torch.cuda.synchronize()
+    C_hi, C_lo, fl = N(C_hi), N(C_lo), N(fl)
+    rows = [0, m // 2, m - 1]
+    c0, c1 = n - 96, n
+    o_hi, o_lo, o_fl = orc.i8_casc_gemm(d["A_hi"][rows], d["A_lo"][rows],
+                                        d["B_hi"][:, c0:c1].copy(), d["B_lo"][:, c0:c1].copy())
+    assert bitwise(C_hi[rows, c0:c1], o_hi) and bitwise(C_lo[rows, c0:c1], o_lo)
+    assert np.array_equal(fl[rows, c0:c1], o_fl)
+    if variant == "b":
+        assert fl.all()
+        return
+    rng = np.random.default_rng(cfg)
+    ii = np.concatenate([rng.integers(0, m, 100), [0, m - 1]])
+    jj = np.concatenate([rng.integers(0, n, 100), [n - 1, 0]])
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii, jj, C_hi, C_lo)
+    assert np.max(np.abs(r["err"]) / orc.north_star_bound(k, r["absab"])) <= 1.0
+    assert fl.sum() == 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_i8_p_invariance_emulated_ranks(casc, world):
+    """The INT8 multi-GPU data path rank by rank on one GPU: rank r packs its
+    rows of A and its 256-column slab of B; the slabs concatenated in rank order
+    are the all-gathered buffer; C is bitwise the single-call result."""
+    import torch
+    from paper_2303_04353_b200.multigpu import I8_BLOCK, col_slab, row_shard
+    m, n, k = 300, 700, 530
+    d = I.make_config(1, m=m, n=n, k=k, seed=13)
+    A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+    ref = [N(x) for x in casc.casc_i8_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo)]
+    blk = 2 * casc.casc_i8_packed_block_bytes(k)
+    chunks = []
+    for r in range(world):
+        c0, c1, per = col_slab(n, world, r, I8_BLOCK)
+        buf = torch.zeros(per * blk, dtype=torch.uint8, device="cuda")
+        if c1 > c0:
+            used = -(-(c1 - c0) // I8_BLOCK) * blk
+            casc.casc_i8_pack(B_hi[:, c0:c1].contiguous(), B_lo[:, c0:c1].contiguous(), True,
+                              packed=buf[:used])
+        chunks.append(buf)
+    pb = torch.cat(chunks)
+    for r in range(world):
+        r0, r1 = row_shard(m, world, r)
+        pa = casc.casc_i8_pack(A_hi[r0:r1].contiguous(), A_lo[r0:r1].contiguous(), False)
+        got = [N(x) for x in casc.casc_i8_gemm_packed(r1 - r0, n, k, pa, pb)]
+        assert all(np.array_equal(g, x[r0:r1]) for g, x in zip(got, ref))
