@@ -81,6 +81,9 @@ constexpr int THREADS = 320;
 // id, so the producer and the MMA issuer win the issue slot over the epilogue
 // warps they share a sub-partition with.
 constexpr int PRODUCER_WARP = 8, MMA_WARP = 9, EPI_THREADS = 256;
+#ifndef CASC_I8_SYNC_KB
+#define CASC_I8_SYNC_KB 64  // k blocks between wave synchronisations (64 = once per sweep)
+#endif
 #ifndef CASC_I8_SUSPEND_NS
 #define CASC_I8_SUSPEND_NS 1000000
 #endif
@@ -755,25 +758,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
         for (int grp = 0; grp < ngroups; ++grp) {
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
-          if (synced) {
-            // Soft wave synchronisation: the producers of all CTAs start each
-            // (panel, group) sweep of a full tile wave together, so the tiles in
-            // flight stream the same slice chunks at the same time and hit them in
-            // L2 (bounded wait: never a hang, at worst an unsynchronised sweep).
-            ++sweep;
-            if (lane == 0) {
-              atomicAdd(p.sync, 1u);
-              const unsigned int target = sweep * gridDim.x;
-              unsigned int v;
-              for (int spin = 0; spin < 20000; ++spin) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
-                if (v >= target) break;
-                __nanosleep(64);
-              }
-            }
-            __syncwarp();
-          }
           for (int64_t kb = kb0; kb < kb1; ++kb) {
+            if (synced && (kb - kb0) % CASC_I8_SYNC_KB == 0) {
+              // Soft wave synchronisation: the producers of all CTAs start each
+              // (panel, group) sweep of a full tile wave, and every
+              // CASC_I8_SYNC_KB k blocks of it, together, so the tiles in flight
+              // stream the same slice chunks at the same time and hit them in L2
+              // (bounded wait: never a hang, at worst an unsynchronised stretch).
+              ++sweep;
+              if (lane == 0) {
+                atomicAdd(p.sync, 1u);
+                const unsigned int target = sweep * gridDim.x;
+                unsigned int v;
+                for (int spin = 0; spin < 20000; ++spin) {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
+                  if (v >= target) break;
+                  __nanosleep(64);
+                }
+              }
+              __syncwarp();
+            }
             // A-stationary chain (mma_chain): B_top .. B_s, A_0, B_(s-1), A_1, ...
             for (int j = top; j >= s; --j) loadB(j, cb, kb);
             loadA(0, rb, kb);

@@ -5,9 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
-    "g6": ["CASC_I8_GROUP_M=6"],
-    "g5": ["CASC_I8_GROUP_M=5"],
-    "g8": ["CASC_I8_GROUP_M=8"],
+    "skb32": ["CASC_I8_SYNC_KB=32"],
+    "skb16": ["CASC_I8_SYNC_KB=16"],
+    "skb8": ["CASC_I8_SYNC_KB=8"],
 }
 if sys.argv[1] == "build":
     import importlib.util
