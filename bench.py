@@ -86,60 +86,59 @@ def load_int8_peak():
         return 4500.0, 4500.0, "fallback: nominal 4.5 POPS dense int8"
 
 
-def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, y=14):
-    """NEXT-3: the INT8 cascade (casc_i8_pack x2 + casc_i8_gemm_packed) on the
-    same device-resident workload, phases timed with CUDA events."""
+def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, y=14,
+                 barrier=None, max_over_ranks=None):
+    """NEXT-3: the INT8 cascade on the same device-resident workload through the
+    multi-GPU layer (paper_2303_04353_b200/multigpu.py with i8_cuda_ops): each
+    rank packs its rows of A (casc_i8_pack) and its 256-column slab of B, the
+    packed slabs are all-gathered (NCCL, N > 1), and casc_i8_gemm_packed runs
+    on the rank's rows.  A_*: this rank's rows; B_*: this rank's INT8 slab.
+    Phases timed with CUDA events, the step time is the max over ranks."""
     import torch
+    from paper_2303_04353_b200.multigpu import I8_BLOCK, ShardedCascGemm, i8_cuda_ops
     dev = A_hi.device
-    pa = torch.empty(casc.casc_i8_packed_bytes(m, k, y), dtype=torch.uint8, device=dev)
-    pb = torch.empty(casc.casc_i8_packed_bytes(n, k, y), dtype=torch.uint8, device=dev)
-    ws = torch.empty(casc.casc_i8_gemm_ws_bytes(m, n), dtype=torch.uint8, device=dev)
-    C_hi = torch.empty((m, n), dtype=torch.float64, device=dev)
+    op = ShardedCascGemm(m, n, k, ops=i8_cuda_ops(y), device=dev, block=I8_BLOCK)
+    mloc = op.r1 - op.r0
+    C_hi = torch.empty((mloc, n), dtype=torch.float64, device=dev)
     C_lo = torch.empty_like(C_hi)
-    fl = torch.empty((m, n), dtype=torch.uint8, device=dev)
+    fl = torch.empty((mloc, n), dtype=torch.uint8, device=dev)
 
     def step(ev=None):
-        if ev:
-            ev[0].record()
-        casc.casc_i8_pack(A_hi, A_lo, False, y, packed=pa)
-        if ev:
-            ev[1].record()
-        casc.casc_i8_pack(B_hi, B_lo, True, y, packed=pb)
-        if ev:
-            ev[2].record()
-        casc.casc_i8_gemm_packed(m, n, k, pa, pb, y, C_hi=C_hi, C_lo=C_lo, flags=fl, ws=ws)
-        if ev:
-            ev[3].record()
+        op(A_hi, A_lo, B_hi, B_lo, C_hi=C_hi, C_lo=C_lo, flags=fl, events=ev)
 
     for _ in range(warmup):
         step()
-    torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(steps)]
     with ClockSampler(None) as cs:
         for s_ in range(steps):
-            step(evs[s_])
-        torch.cuda.synchronize()
-    ph = {"pack_a": 0.0, "pack_b": 0.0, "gemm": 0.0}
+            evs[s_][0].record()
+            step(evs[s_][1:])
+        barrier()
+    ph = {"pack_a": 0.0, "pack_b": 0.0, "allgather": 0.0, "gemm": 0.0}
+    total = 0.0
     for e in evs:
         ph["pack_a"] += e[0].elapsed_time(e[1]) / steps
         ph["pack_b"] += e[1].elapsed_time(e[2]) / steps
-        ph["gemm"] += e[2].elapsed_time(e[3]) / steps
-    total = sum(ph.values())
+        ph["allgather"] += e[2].elapsed_time(e[3]) / steps
+        ph["gemm"] += e[3].elapsed_time(e[4]) / steps
+        total += e[0].elapsed_time(e[4]) / steps
+    total = max_over_ranks(total)
     prods = y * (y + 1) // 2
-    ops = 2.0 * prods * m * n * k
+    ops = 2.0 * prods * mloc * n * k
     peak_sus, peak_burst, src = load_int8_peak()
     achieved = ops / (ph["gemm"] * 1e-3) / 1e12
-    del pa, pb, ws, C_hi, C_lo, fl
+    del op, C_hi, C_lo, fl
     return {
         "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3754), y=%d slices, "
                   "%d int8 products per k panel of 8192; readings R22-R26" % (y, prods),
         "value": 2.0 * m * n * k / (total * 1e-3) / 1e9, "unit": UNIT,
-        "ms_per_step": total, "phases_ms": ph,
+        "n_gpus": world, "ms_per_step": total, "phases_ms_rank0": ph,
         "parity": "bit-exact vs oracle/casc_i8_oracle.c (tests/test_gpu_i8.py)",
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
                      "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
                      "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
-                     if (m, n, k) == (16384, 16384, 16384) else None,
+                     if (mloc, n, k) == (16384, 16384, 16384) else None,
                      "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
                                "combine)",
                      "peak_source": f"{src}, sustained (burst {peak_burst:.0f}); "
@@ -453,6 +452,41 @@ def main():
     split_bytes = 48.0 * mloc * k + 72.0 * (c1 - c0) * k
     split_ms = phases["split_a"] + phases["split_b"]
 
+    # ---- NEXT-3: the INT8 cascade on the same workload (all ranks; N > 1 shards it)
+    int8 = None
+    if not args.no_int8:
+        from paper_2303_04353_b200.multigpu import I8_BLOCK
+        ok = 1
+        try:
+            i0, i1, _ = col_slab(n, world, rank, I8_BLOCK)
+            if world == 1:
+                Bi_hi, Bi_lo = B_hi, B_lo
+            else:  # this rank's 256-column slab (the FP64 path's slab is 64-aligned)
+                sl = I.make_config(args.config, rows=slice(0, 1), cols=slice(i0, i1))
+                Bi_hi = torch.from_numpy(np.ascontiguousarray(sl["B_hi"])).to(dev)
+                Bi_lo = torch.from_numpy(np.ascontiguousarray(sl["B_lo"])).to(dev)
+                del sl
+        except Exception as ex:
+            ok, int8 = 0, {"error": repr(ex)}
+        if world > 1:  # every rank enters the collectives or none does
+            okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            ok = int(okt.item())
+
+        def mx(v):
+            tt = torch.tensor([v], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return tt.item()
+        if ok:
+            try:
+                int8 = measure_int8(casc, A_hi, A_lo, Bi_hi, Bi_lo, m, n, k, args.steps,
+                                    args.warmup, world=world, barrier=barrier,
+                                    max_over_ranks=mx)
+            except Exception as ex:  # reported, never silently replaced
+                int8 = {"error": repr(ex)}
+            del Bi_hi, Bi_lo
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -477,13 +511,6 @@ def main():
             del x, y
         except Exception:
             dgemm_ratio = None
-
-    int8 = None
-    if world == 1 and not args.no_int8:
-        try:
-            int8 = measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, args.steps, args.warmup)
-        except Exception as ex:  # reported, never silently replaced
-            int8 = {"error": repr(ex)}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
