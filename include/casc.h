@@ -304,9 +304,9 @@ size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y);
  * `packed` (casc_i8_packed_bytes(rows, k, y) bytes, 256-byte aligned). */
 int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
                  int is_b, int y, void* packed, casc_stream_t stream);
-/* Bytes of the GEMM's own scratch: 5 x 128 x 128 x 8 bytes per CTA (the FP64x2
- * panel sum T, the C accumulator and the exact group values of the tile in
- * flight), then a wave-synchronisation counter. */
+/* Bytes of the GEMM's own scratch: 6 x 128 x 128 x 8 bytes per CTA (the FP64x2
+ * C accumulator and the exact group values of the tile in flight), then a
+ * wave-synchronisation counter. */
 size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
 /* Phases 2-3 (R24-R26) from packed operands of the same m, n, k, y: the fused
  * tcgen05 kernel on CTA pairs.  ws: >= casc_i8_gemm_ws_bytes(m, n) bytes of

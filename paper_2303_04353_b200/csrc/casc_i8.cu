@@ -73,6 +73,8 @@ constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
 constexpr int NSA = 8, NSB = 8;    // smem ring slots (A: 16 KB, B: 8 KB half chunks)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
+constexpr int NGMAX = (YMAX + NBIN - 1) / NBIN;  // groups per panel, at most
+constexpr int64_t WS_PER_CTA = (2 + NGMAX) * 128 * 128;  // doubles / int64 per CTA
 // (320 threads: up to 204 registers each, room for the epilogue's 64 exact
 // group values)
 constexpr int THREADS = 320;
@@ -88,7 +90,7 @@ constexpr int PRODUCER_WARP = 8, MMA_WARP = 9, EPI_THREADS = 256;
 #define CASC_I8_SUSPEND_NS 1000000
 #endif
 #ifndef CASC_I8_EPI_SUB
-#define CASC_I8_EPI_SUB 8
+#define CASC_I8_EPI_SUB 4
 #endif
 constexpr int EPI_SUB = CASC_I8_EPI_SUB;  // elements per phase-2 step of the epilogue
 #ifndef CASC_I8_GROUP_M
@@ -367,7 +369,7 @@ struct GemmArgs {
   double* C_lo;
   int64_t ldc;
   uint8_t* flags;
-  double* ws;           // per CTA: T hi, T lo, C hi, C lo, V (5 x 16384 x 8 bytes)
+  double* ws;           // per CTA: C hi, C lo, V[NGMAX] (WS_PER_CTA doubles)
   unsigned int* sync;   // wave-sync counter (zeroed before the launch) or null
   int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
   int64_t dbg_panel;
@@ -821,11 +823,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int lr = quarter * 32 + lane;       // tile row = TMEM lane
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
     const uint32_t tempty_leader = leader_addr(tempty);
-    double* Th = p.ws + (int64_t)blockIdx.x * 5 * (TR * TR);
-    double* Tl = Th + TR * TR;
-    double* Ch = Tl + TR * TR;
+    // per-CTA workspace: C accumulator (hi, lo) of the tile, then the exact
+    // group values V of the panel's groups [NGMAX][128 x 128]
+    double* Ch = p.ws + (int64_t)blockIdx.x * WS_PER_CTA;
     double* Cl = Ch + TR * TR;
-    long long* Vw = reinterpret_cast<long long*>(Cl + TR * TR);  // exact group values
+    long long* Vw = reinterpret_cast<long long*>(Cl + TR * TR);
     uint32_t gcount = 0;
     for (int tile = pair; tile < tiles; tile += npairs) {
       int64_t rp, cb;
@@ -843,7 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         epi_bar_sync();
         for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
-          const bool needT = grp > 0, lastg = grp + 1 == ngroups, needC = lastg && q > 0;
+          const bool lastg = grp + 1 == ngroups;
           mbar_wait_sleep(tfull, gcount & 1);
           tc_fence_after();
           // Phase 1: drain this warp's part of TMEM into the exact group values
@@ -877,7 +879,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (nb > 1) v = v * 256 + (int32_t)r1[i];
               if (nb > 2) v = v * 256 + (int32_t)r2[i];
               if (nb > 3) v = v * 256 + (int32_t)r3[i];
-              Vw[(c0 + i) * TR + lr] = v;
+              Vw[(int64_t)grp * TR * TR + (c0 + i) * TR + lr] = v;
             }
           }
           tc_fence_before();
@@ -887,62 +889,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef CASC_I8_NO_EPI
           continue;
 #endif
-          // Phase 2 (overlaps the next group's MMAs): FP64x2 panel sum T,
-          // detector and C, EPI_SUB elements at a time
-#pragma unroll
+          if (!lastg) continue;
+          // Phase 2, once per panel after its last group (overlaps the MMAs of
+          // the next panel / tile): the FP64x2 panel sum T over the groups' exact
+          // values, most significant first (R25), the detector (R26) and C.
+#pragma unroll 1
           for (int cc = 0; cc < 64 / EPI_SUB; ++cc) {
             const int c0 = half * 64 + cc * EPI_SUB;
-            double xth[EPI_SUB], xtl[EPI_SUB], xch[EPI_SUB], xcl[EPI_SUB];
-            long long xv[EPI_SUB];
-#pragma unroll
-            for (int i = 0; i < EPI_SUB; ++i) xv[i] = ld_na(&Vw[(c0 + i) * TR + lr]);
-            if (needT) {
-#pragma unroll
-              for (int i = 0; i < EPI_SUB; ++i) {
-                xth[i] = ld_na(&Th[(c0 + i) * TR + lr]);
-                xtl[i] = ld_na(&Tl[(c0 + i) * TR + lr]);
-              }
-            }
-            if (needC) {
+            double th[EPI_SUB], tl[EPI_SUB], xch[EPI_SUB], xcl[EPI_SUB];
+            if (q > 0) {
 #pragma unroll
               for (int i = 0; i < EPI_SUB; ++i) {
                 xch[i] = ld_na(&Ch[(c0 + i) * TR + lr]);
                 xcl[i] = ld_na(&Cl[(c0 + i) * TR + lr]);
               }
             }
+            for (int g2 = 0; g2 < ngroups; ++g2) {
+              const int s2 = g2 ? r0 + (g2 - 1) * NBIN : 0, nb2 = g2 ? NBIN : r0;
+              long long xv[EPI_SUB];
+#pragma unroll
+              for (int i = 0; i < EPI_SUB; ++i)
+                xv[i] = ld_na(&Vw[(int64_t)g2 * TR * TR + (c0 + i) * TR + lr]);
+#pragma unroll
+              for (int i = 0; i < EPI_SUB; ++i) {
+                const int fj = sF[c0 + i];
+                // R25: G = (RN(V), V - RN(V)), exact
+                const long long v = xv[i];
+                double gh = __ll2double_rn(v);
+                double gl = __ll2double_rn(v - __double2ll_rn(gh));
+                const int w = ei + fj - 12 - 8 * (s2 + nb2 - 1);
+                gh = mulp2(gh, w);
+                gl = mulp2(gl, w);
+                if (g2 == 0) {
+                  th[i] = gh;
+                  tl[i] = gl;
+                } else {
+                  dd_add(th[i], tl[i], gh, gl, th[i], tl[i]);
+                }
+              }
+            }
 #pragma unroll
             for (int i = 0; i < EPI_SUB; ++i) {
               const int lc = c0 + i;
               const int fj = sF[lc];
-              // R25: G = (RN(V), V - RN(V)), exact
-              const long long v = xv[i];
-              double gh = __ll2double_rn(v);
-              double gl = __ll2double_rn(v - __double2ll_rn(gh));
-              const int w = ei + fj - 12 - 8 * (s + nb - 1);
-              gh = mulp2(gh, w);
-              gl = mulp2(gl, w);
               const int widx = lc * TR + lr;
-              double th = gh, tl = gl;
-              if (needT) dd_add(xth[i], xtl[i], gh, gl, th, tl);
-              if (!lastg) {
-                Th[widx] = th;
-                Tl[widx] = tl;
+              // R26 detector, then C (+)= T
+              if (fabs(th[i]) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * 64);
+              double ch = th[i], cl = tl[i];
+              if (q > 0) dd_add(xch[i], xcl[i], th[i], tl[i], ch, cl);
+              if (q + 1 < P) {
+                Ch[widx] = ch;
+                Cl[widx] = cl;
               } else {
-                // R26 detector, then C (+)= T
-                if (fabs(th) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * 64);
-                double ch = th, cl = tl;
-                if (needC) dd_add(xch[i], xcl[i], th, tl, ch, cl);
-                if (q + 1 < P) {
-                  Ch[widx] = ch;
-                  Cl[widx] = cl;
-                } else {
-                  const int64_t gj = cb * TR + lc;
-                  if (gi < p.m && gj < p.n) {
-                    p.C_hi[gi * p.ldc + gj] = ch;
-                    p.C_lo[gi * p.ldc + gj] = cl;
-                    if (p.flags)
-                      p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
-                  }
+                const int64_t gj = cb * TR + lc;
+                if (gi < p.m && gj < p.n) {
+                  p.C_hi[gi * p.ldc + gj] = ch;
+                  p.C_lo[gi * p.ldc + gj] = cl;
+                  if (p.flags) p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
                 }
               }
             }
@@ -992,7 +995,7 @@ int grid_for(int64_t m, int64_t n, int sms) {  // CTAs: 2 per pair, one pair per
   return (int)(2 * pairs);
 }
 // per-CTA T / C scratch, then the wave-sync counter
-size_t cta_ws_bytes(int grid) { return (size_t)grid * 5 * TR * TR * sizeof(double) + 256; }
+size_t cta_ws_bytes(int grid) { return (size_t)grid * WS_PER_CTA * sizeof(double) + 256; }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1044,7 +1047,7 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   const char* env = getenv("CASC_I8_WAVE_SYNC");  // "0": off (timing studies)
   if (!(env && env[0] == '0')) {
     a.sync = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(ws) +
-                                             (size_t)grid * 5 * TR * TR * sizeof(double));
+                                             (size_t)grid * WS_PER_CTA * sizeof(double));
     cudaError_t e0 = cudaMemsetAsync(a.sync, 0, sizeof(unsigned int), st);
     if (e0 != cudaSuccess) return e0;
   }
