@@ -220,27 +220,30 @@ def _num(s):
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0):
-    """ORACLE-CASCADE (as it stands) on a bounded sample of the workload:
-    the first R rows x first C columns of C with the full k.  R is calibrated
-    so the run takes ~target_s seconds on this host's cores."""
+def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=512):
+    """ORACLE-CASCADE (as it stands; ORACLE-I8CASCADE with int8=True) on a
+    bounded sample of the workload: the first R rows x first C columns of C
+    with the full k.  R is calibrated so the run takes ~target_s seconds on
+    this host's cores."""
     import oracle
     oracle.build()
     m, k = A_hi.shape
     n = B_hi.shape[1]
-    C = min(n, 512)
+    C = min(n, cols)
     Bh, Bl = B_hi[:, :C].copy(), B_lo[:, :C].copy()
     R = min(m, 8)
+    fn = oracle.i8_casc_gemm if int8 else oracle.casc_gemm
+    name = "ORACLE-I8CASCADE" if int8 else "ORACLE-CASCADE"
     while True:
         t0 = time.perf_counter()
-        oracle.casc_gemm(A_hi[:R], A_lo[:R], Bh, Bl)
+        fn(A_hi[:R], A_lo[:R], Bh, Bl)
         t = time.perf_counter() - t0
         if t >= 0.5 * target_s or R >= m:
             break
         R = int(min(m, max(2 * R, R * 0.8 * target_s / max(t, 1e-3))))
     return {"value": 2.0 * R * C * k / t / 1e9, "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": f"ORACLE-CASCADE on rows 0..{R - 1} x cols 0..{C - 1} of C, full k={k} "
+            "sample": f"{name} on rows 0..{R - 1} x cols 0..{C - 1} of C, full k={k} "
                       f"({t:.2f} s wall)", "seconds": t}
 
 
@@ -516,6 +519,11 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo)
         cpu.pop("seconds", None)
+        if isinstance(int8, dict) and "value" in int8:
+            c8 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=6.0,
+                                   int8=True, cols=64)
+            c8.pop("seconds", None)
+            int8["cpu_baseline"] = c8
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
