@@ -220,7 +220,7 @@ def _num(s):
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=512):
+def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=512, nthreads=0):
     """ORACLE-CASCADE (as it stands; ORACLE-I8CASCADE with int8=True) on a
     bounded sample of the workload: the first R rows x first C columns of C
     with the full k.  R is calibrated so the run takes ~target_s seconds on
@@ -236,12 +236,13 @@ def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=51
     name = "ORACLE-I8CASCADE" if int8 else "ORACLE-CASCADE"
     while True:
         t0 = time.perf_counter()
-        fn(A_hi[:R], A_lo[:R], Bh, Bl)
+        fn(A_hi[:R], A_lo[:R], Bh, Bl, nthreads=nthreads)
         t = time.perf_counter() - t0
         if t >= 0.5 * target_s or R >= m:
             break
         R = int(min(m, max(2 * R, R * 0.8 * target_s / max(t, 1e-3))))
-    return {"value": 2.0 * R * C * k / t / 1e9, "unit": UNIT, "cores": oracle.num_threads(),
+    return {"value": 2.0 * R * C * k / t / 1e9, "unit": UNIT,
+            "cores": nthreads if nthreads > 0 else oracle.num_threads(),
             "kind": "oracle",
             "sample": f"{name} on rows 0..{R - 1} x cols 0..{C - 1} of C, full k={k} "
                       f"({t:.2f} s wall)", "seconds": t}
@@ -519,6 +520,10 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo)
         cpu.pop("seconds", None)
+        # one host core, beside the paper's single-core context
+        c1 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=3.0, cols=64,
+                               nthreads=1)
+        cpu["one_core"] = {"value": c1["value"], "unit": UNIT, "sample": c1["sample"]}
         if isinstance(int8, dict) and "value" in int8:
             c8 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=6.0,
                                    int8=True, cols=64)
