@@ -255,3 +255,29 @@ def test_i8_p_invariance_emulated_ranks(casc, world):
         pa = casc.casc_i8_pack(A_hi[r0:r1].contiguous(), A_lo[r0:r1].contiguous(), False)
         got = [N(x) for x in casc.casc_i8_gemm_packed(r1 - r0, n, k, pa, pb)]
         assert all(np.array_equal(g, x[r0:r1]) for g, x in zip(got, ref))
+
+
+@pytest.mark.parametrize("m,n,k", [(600, 1, 300), (1, 700, 300), (257, 129, 8192),
+                                   (70, 40, 16384 + 1)])
+def test_i8_skinny_and_panel_edges(casc, orc, m, n, k):
+    """One-column / one-row problems (raster with a single tile row or column),
+    exactly one full 8192 panel, and two full panels plus one k."""
+    d = I.make_config(1, m=m, n=n, k=k, seed=m + n)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
+
+
+def test_i8_extreme_exponents(casc, orc):
+    """Rows of A scaled by 2^-700 and columns of B by 2^-300 (the products sit
+    near 2^-1000, the FP64x2 tails are subnormal; the 2^w scaling takes the
+    two-step path): still bit-exact with the oracle's ldexp."""
+    d = I.make_config(1, m=90, n=70, k=500, seed=31)
+    for x in ("A_hi", "A_lo"):
+        d[x] = np.ldexp(d[x], -700)
+    for x in ("B_hi", "B_lo"):
+        d[x] = np.ldexp(d[x], -300)
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
+    assert np.all(np.abs(C_hi) < 2.0**-990) and np.any(C_hi != 0)
