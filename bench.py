@@ -87,7 +87,7 @@ def load_int8_peak():
 
 
 def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, y=14,
-                 barrier=None, max_over_ranks=None):
+                 barrier=None, max_over_ranks=None, host=None):
     """NEXT-3: the INT8 cascade on the same device-resident workload through the
     multi-GPU layer (paper_2303_04353_b200/multigpu.py with i8_cuda_ops): each
     rank packs its rows of A (casc_i8_pack) and its 256-column slab of B, the
@@ -124,6 +124,33 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         ph["gemm"] += e[3].elapsed_time(e[4]) / steps
         total += e[0].elapsed_time(e[4]) / steps
     total = max_over_ranks(total)
+    e2e = None
+    if host is not None:  # H2D of the inputs, the calls, D2H of C and flags, every step
+        hA_hi, hA_lo, hB_hi, hB_lo = host
+        oC_hi = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
+        oC_lo = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
+        oF = torch.empty((mloc, n), dtype=torch.uint8).pin_memory()
+        e2e_steps = max(1, min(steps, 2))
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(e2e_steps):
+            A_hi.copy_(hA_hi, non_blocking=True)
+            A_lo.copy_(hA_lo, non_blocking=True)
+            B_hi.copy_(hB_hi, non_blocking=True)
+            B_lo.copy_(hB_lo, non_blocking=True)
+            step()
+            oC_hi.copy_(C_hi, non_blocking=True)
+            oC_lo.copy_(C_lo, non_blocking=True)
+            oF.copy_(fl, non_blocking=True)
+        e1.record()
+        barrier()
+        te = e0.elapsed_time(e1) / e2e_steps
+        e2e = {"value": 2.0 * m * n * k / (te * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 16 * (mloc * k + k * B_hi.shape[1]),
+               "d2h_bytes_per_step": 17 * mloc * n, "ms_per_step": te, "steps": e2e_steps,
+               "api": "paper_2303_04353_b200 C ABI (casc_i8_pack x2 / casc_i8_gemm_packed)"}
     prods = y * (y + 1) // 2
     ops = 2.0 * prods * mloc * n * k
     peak_sus, peak_burst, src = load_int8_peak()
@@ -135,6 +162,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         "value": 2.0 * m * n * k / (total * 1e-3) / 1e9, "unit": UNIT,
         "n_gpus": world, "ms_per_step": total, "phases_ms_rank0": ph,
         "parity": "bit-exact vs oracle/casc_i8_oracle.c (tests/test_gpu_i8.py)",
+        "e2e": e2e,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
                      "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
                      "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
@@ -486,7 +514,9 @@ def main():
             try:
                 int8 = measure_int8(casc, A_hi, A_lo, Bi_hi, Bi_lo, m, n, k, args.steps,
                                     args.warmup, world=world, barrier=barrier,
-                                    max_over_ranks=mx)
+                                    max_over_ranks=mx,
+                                    host=(hA_hi, hA_lo, hB_hi, hB_lo)
+                                    if world == 1 and not args.no_e2e else None)
             except Exception as ex:  # reported, never silently replaced
                 int8 = {"error": repr(ex)}
             del Bi_hi, Bi_lo
