@@ -261,6 +261,9 @@ def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=51
     Bh, Bl = B_hi[:, :C].copy(), B_lo[:, :C].copy()
     R = min(m, 8)
     fn = oracle.i8_casc_gemm if int8 else oracle.casc_gemm
+    if nthreads <= 0:  # all host cores (explicit: the oracle's OpenMP setting is global)
+        nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else \
+            (os.cpu_count() or 1)
     name = "ORACLE-I8CASCADE" if int8 else "ORACLE-CASCADE"
     while True:
         t0 = time.perf_counter()
@@ -269,8 +272,7 @@ def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=51
         if t >= 0.5 * target_s or R >= m:
             break
         R = int(min(m, max(2 * R, R * 0.8 * target_s / max(t, 1e-3))))
-    return {"value": 2.0 * R * C * k / t / 1e9, "unit": UNIT,
-            "cores": nthreads if nthreads > 0 else oracle.num_threads(),
+    return {"value": 2.0 * R * C * k / t / 1e9, "unit": UNIT, "cores": nthreads,
             "kind": "oracle",
             "sample": f"{name} on rows 0..{R - 1} x cols 0..{C - 1} of C, full k={k} "
                       f"({t:.2f} s wall)", "seconds": t}
@@ -550,15 +552,15 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo)
         cpu.pop("seconds", None)
-        # one host core, beside the paper's single-core context (BASELINE.md §1)
-        c1 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=3.0, cols=64,
-                               nthreads=1)
-        cpu["one_core"] = {"value": c1["value"], "unit": UNIT, "sample": c1["sample"]}
         if isinstance(int8, dict) and "value" in int8:
             c8 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=6.0,
                                    int8=True, cols=64)
             c8.pop("seconds", None)
             int8["cpu_baseline"] = c8
+        # one host core, beside the paper's single-core context (BASELINE.md §1)
+        c1 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=3.0, cols=64,
+                               nthreads=1)
+        cpu["one_core"] = {"value": c1["value"], "unit": UNIT, "sample": c1["sample"]}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
