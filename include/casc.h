@@ -265,7 +265,10 @@ int casc_slice_product(int64_t m, int64_t n, int64_t k,
  * Arguments, aliasing rules, k == 0 / m == 0 / n == 0 behaviour and errors as
  * casc_gemm_fp64x2 (flags semantics: R26 above).  Uses a library-owned device
  * workspace of casc_i8_workspace_bytes(m, n, k, y) bytes (allocated with a
- * host-synchronising cudaMalloc on first use or growth; casc_i8_finalize frees it). */
+ * host-synchronising cudaMalloc on first use or growth; casc_i8_finalize frees it).
+ * Not re-entrant across host threads or concurrent streams on the same device
+ * (the workspace also holds the kernel's wave-synchronisation counter): use
+ * casc_i8_gemm_fp64x2_ws with one workspace per concurrent call. */
 int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
                         const double* A_hi, const double* A_lo, int64_t lda,
                         const double* B_hi, const double* B_lo, int64_t ldb,
