@@ -318,7 +318,8 @@ def _cfg4_block(I, rows):
 def _config(args, world):
     m, n, k = CONFIGS[args.config]
     return {"workload": CONFIG_TEXT[args.config], "m": m, "n": n, "k": k,
-            "parallelism": f"C row-sharded x{world}, packed B slabs all-gathered (NCCL)"
+            "parallelism": f"C row-sharded x{world}, FP64x2 B slabs all-gathered (NCCL) and "
+                           "split on every rank; INT8 path: packed slabs all-gathered"
             if world > 1 else "single B200",
             "l2": "inputs (16 B/elt x (mk+kn)) larger than the 126 MB L2; no flush",
             "k_panel": 256, "widths": [22, 21, 21] if k >= 256 else None}
@@ -377,7 +378,10 @@ def main():
     C_hi = torch.empty((mloc, n), dtype=torch.float64, device=dev)
     C_lo = torch.empty_like(C_hi)
     flags = torch.empty((mloc, n), dtype=torch.uint8, device=dev)
-    op = ShardedCascGemm(m, n, k, device=dev)
+    # N > 1: the FP64x2 slabs of B are all-gathered (16 B / element) and every
+    # rank splits all of B locally: fewer NVLink bytes than gathering the
+    # 56 B / element packed slices
+    op = ShardedCascGemm(m, n, k, device=dev, gather="raw")
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -413,13 +417,11 @@ def main():
             t_end.record(stream)
             barrier()
         total_ms = t_start.elapsed_time(t_end)
-        ph = {"split_a": 0.0, "split_b": 0.0, "allgather": 0.0, "gemm": 0.0}
+        ph = {name: 0.0 for name in op.phase_names}
         for s in range(args.steps):
             e = ev[s]
-            ph["split_a"] += e[0].elapsed_time(e[1])
-            ph["split_b"] += e[1].elapsed_time(e[2])
-            ph["allgather"] += e[2].elapsed_time(e[3])
-            ph["gemm"] += e[3].elapsed_time(e[4])
+            for i, name in enumerate(op.phase_names):
+                ph[name] += e[i].elapsed_time(e[i + 1])
         ph = {key: v / args.steps for key, v in ph.items()}
         return total_ms, ph, cs.summary(), launches
 
@@ -483,7 +485,7 @@ def main():
                 "peak_source": f"{peak_src}: DMMA microbenchmark, sustained (burst {peak_burst})",
                 "algorithmic_flops_per_launch": gemm_flops}
     hbm_peak, hbm_src = load_hbm_peak()
-    split_bytes = 48.0 * mloc * k + 72.0 * (c1 - c0) * k
+    split_bytes = 48.0 * mloc * k + 72.0 * (n if op.raw else (c1 - c0)) * k
     split_ms = phases["split_a"] + phases["split_b"]
 
     # ---- NEXT-3: the INT8 cascade on the same workload (all ranks; N > 1 shards it)

@@ -90,11 +90,20 @@ class ShardedCascGemm:
     allocated once and reused across calls (bench steps)."""
 
     def __init__(self, m: int, n: int, k: int, group=None, ops: Ops | None = None,
-                 device=None, block: int = BLOCK):
+                 device=None, block: int = BLOCK, gather: str = "packed"):
         """block: slab granularity (columns) of the packed B: 64 for the FP64
-        cascade, I8_BLOCK with i8_cuda_ops()."""
+        cascade, I8_BLOCK with i8_cuda_ops().
+        gather: what the ranks exchange (N > 1).  "packed": each rank splits its
+        column slab of B and the packed slabs are all-gathered (FP64 cascade:
+        56 B per element of B; INT8 cascade: ~14 B).  "raw": the FP64x2 slabs
+        themselves are all-gathered (16 B per element) and every rank splits all
+        of B locally, slab by slab into the packed layout (the byte-cheaper
+        choice for the FP64 cascade).  Bitwise the same result."""
+        if gather not in ("packed", "raw"):
+            raise ValueError("gather must be 'packed' or 'raw'")
         self.m, self.n, self.k = m, n, k
         self.block = block
+        self.gather = gather
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -108,6 +117,17 @@ class ShardedCascGemm:
         self.packed_b_full = (torch.empty(self.chunk * self.world, dtype=torch.uint8,
                                           device=self.device) if self.world > 1 else None)
         self.packed_a = None
+        self.raw = self.gather == "raw" and self.world > 1
+        if self.raw:  # [rank][hi | lo][k][slab width padded to whole blocks]
+            self.wpad = self.blocks_per_rank * block
+            self.raw_local = torch.zeros((2, k, self.wpad), dtype=torch.float64,
+                                         device=self.device)
+            self.raw_full = torch.empty((self.world, 2, k, self.wpad), dtype=torch.float64,
+                                        device=self.device)
+            self.slabs = [col_slab(n, self.world, r, block)[:2] for r in range(self.world)]
+        # names of the intervals between the 4 events of __call__ (bench phases)
+        self.phase_names = (["split_a", "allgather_raw", "split_b", "gemm"] if self.raw else
+                            ["split_a", "split_b", "allgather", "gemm"])
 
     def __call__(self, A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi=None, C_lo=None,
                  flags=None, events=None):
@@ -121,6 +141,32 @@ class ShardedCascGemm:
         self.launches += count()
         rec = (lambda i: events[i].record()) if events else (lambda i: None)
         rec(0)
+        if self.raw:
+            w = self.c1 - self.c0
+            if w > 0:
+                self.raw_local[0, :, :w].copy_(B_hi_slab)
+                self.raw_local[1, :, :w].copy_(B_lo_slab)
+            if dist.get_backend(self.group) == "gloo":  # CPU plumbing tests
+                dist.all_gather(list(self.raw_full.unbind(0)), self.raw_local, group=self.group)
+            else:  # NCCL over NVLink / NVSwitch
+                dist.all_gather_into_tensor(self.raw_full.view(-1), self.raw_local.view(-1),
+                                            group=self.group)
+            rec(1)
+            blk = self.ops.packed_b_block_bytes(self.k)
+            for r, (a0, a1) in enumerate(self.slabs):
+                if a1 > a0:
+                    used = -(-(a1 - a0) // self.block) * blk
+                    base = r * self.chunk
+                    self.ops.pack_b(self.raw_full[r, 0, :, :a1 - a0],
+                                    self.raw_full[r, 1, :, :a1 - a0],
+                                    packed=self.packed_b_full[base:base + used])
+                    self.launches += count()
+            rec(2)
+            out = self.ops.gemm_packed(mloc, self.n, self.k, self.packed_a, self.packed_b_full,
+                                       C_hi=C_hi, C_lo=C_lo, flags=flags)
+            self.launches += count()
+            rec(3)
+            return out
         if self.c1 > self.c0:
             used = -(-(self.c1 - self.c0) // self.block) * self.ops.packed_b_block_bytes(self.k)
             self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])

@@ -82,12 +82,13 @@ class _CpuOps:
         return torch.from_numpy(h), torch.from_numpy(l), torch.from_numpy(f)
 
 
-def _worker(rank, world, port, m, n, k, out, i8=False):
+def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2303_04353_b200.multigpu import I8_BLOCK, ShardedCascGemm
     W = I8_BLOCK if i8 else 64
-    op = ShardedCascGemm(m, n, k, ops=_CpuOps(k, W, i8), device=torch.device("cpu"), block=W)
+    op = ShardedCascGemm(m, n, k, ops=_CpuOps(k, W, i8), device=torch.device("cpu"), block=W,
+                         gather=gather)
     d = I.make_config(1, m=m, n=n, k=k, seed=21, rows=slice(op.r0, op.r1))
     A_hi, A_lo = torch.from_numpy(d["A_hi"]), torch.from_numpy(d["A_lo"])
     B_hi = torch.from_numpy(d["B_hi"][:, op.c0:op.c1].copy())
@@ -99,11 +100,14 @@ def _worker(rank, world, port, m, n, k, out, i8=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,n,k", [(10, 150, 300), (7, 64, 40)])
-def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k):
+@pytest.mark.parametrize("m,n,k,gather", [(10, 150, 300, "packed"), (7, 64, 40, "packed"),
+                                          (10, 150, 300, "raw"), (5, 200, 70, "raw")])
+def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k, gather):
+    """gather="raw" exchanges the FP64x2 slabs and packs all of B on every rank
+    (SURVEY §8(e) byte-cheaper alternative): the same bits."""
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path)), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), False, gather),
+             nprocs=world, join=True)
     d = I.make_config(1, m=m, n=n, k=k, seed=21)
     ref_hi, ref_lo, ref_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
     rows = 0
