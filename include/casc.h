@@ -285,6 +285,20 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                            uint8_t* flags, int y, void* workspace, size_t workspace_bytes,
                            casc_stream_t stream);
 
+/* NEXT-4 on the INT8 cascade: C := alpha (x) op(A) op(B) (+) beta (x) C with the
+ * semantics, argument layout and errors of casc_gemm_fp64x2_ex (reading R21),
+ * the product computed through y int8 slices (bitwise the casc_i8_gemm_fp64x2
+ * product of the same op(A), op(B)).  workspace: NULL (temporary stream-ordered
+ * allocation) or >= casc_i8_workspace_bytes(m, n, k, y) bytes. */
+int casc_i8_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                           double alpha_hi, double alpha_lo,
+                           const double* A_hi, const double* A_lo, int64_t lda,
+                           const double* B_hi, const double* B_lo, int64_t ldb,
+                           double beta_hi, double beta_lo,
+                           double* C_hi, double* C_lo, int64_t ldc,
+                           uint8_t* flags, int y, void* workspace, size_t workspace_bytes,
+                           casc_stream_t stream);
+
 /* Workspace bytes: packed A + packed B + casc_i8_gemm_ws_bytes(m, n) (each
  * part 256-byte aligned).  0 for empty problems or y out of range. */
 size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y);

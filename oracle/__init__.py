@@ -96,6 +96,9 @@ def _setup(L):
     L.orc_i8_group_value.argtypes = [_pi64, ctypes.c_int, _pd, _pd]
     L.orc_i8_casc_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64,
                                    ctypes.c_int, _pd, _pd, _i64, _pu8, ctypes.c_int]
+    L.orc_i8_casc_gemm_ex.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, _d, _d,
+                                      _pd, _pd, _i64, _pd, _pd, _i64, _d, _d, _pd, _pd, _i64,
+                                      _pu8, ctypes.c_int, ctypes.c_int]
 
 
 def _p(a, ptr=_pd):
@@ -371,4 +374,22 @@ def i8_casc_gemm(A_hi, A_lo, B_hi, B_lo, y: int = 14, nthreads: int = 0):
     flags = np.empty((m, n), dtype=np.uint8)
     lib().orc_i8_casc_gemm(m, n, k, _p(A_hi), _p(A_lo), k, _p(B_hi), _p(B_lo), n, int(y),
                            _p(C_hi), _p(C_lo), n, _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags
+
+
+def i8_casc_gemm_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, y: int = 14,
+                    nthreads: int = 0):
+    """NEXT-4 on the INT8 cascade: C := alpha (x) op(A) op(B) (+) beta (x) C
+    (reading R21).  A, B are the STORED matrices; alpha, beta (hi, lo).
+    Returns new (C_hi, C_lo, flags)."""
+    ta, tb = int(transa in ("T", 1, True)), int(transb in ("T", 1, True))
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    C_hi, C_lo = _c64(C_hi).copy(), _c64(C_lo).copy()
+    m, n = C_hi.shape
+    k = A_hi.shape[0] if ta else A_hi.shape[1]
+    flags = np.zeros((m, n), dtype=np.uint8)
+    lib().orc_i8_casc_gemm_ex(ta, tb, m, n, k, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                              A_hi.shape[1] if A_hi.size else 1, _p(B_hi), _p(B_lo),
+                              B_hi.shape[1] if B_hi.size else 1, beta[0], beta[1], _p(C_hi),
+                              _p(C_lo), n, _p(flags, _pu8), int(y), nthreads)
     return C_hi, C_lo, flags

@@ -187,3 +187,68 @@ void orc_i8_casc_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const 
     free(f);
   }
 }
+
+/* NEXT-4 on the INT8 cascade: C := (alpha (x) P) (+) (beta (x) C), P = op(A) op(B)
+ * through the INT8 cascade (reading R21; the same update sequence as the FP64
+ * cascade's orc_casc_gemm_ex).  A stored m x k (transa = 0, lda) or k x m
+ * (transa = 1); B stored k x n (transb = 0, ldb) or n x k (transb = 1).
+ * beta == 0: C is not read; k == 0 or alpha == 0: C := beta (x) C, flags := 0. */
+void orc_dd_mul(double xh, double xl, double yh, double yl, double* rh, double* rl);
+void orc_i8_casc_gemm_ex(int transa, int transb, int64_t m, int64_t n, int64_t k, double ah,
+                         double al, const double* Ahi, const double* Alo, int64_t lda,
+                         const double* Bhi, const double* Blo, int64_t ldb, double bh, double bl,
+                         double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int y,
+                         int nthreads) {
+  const int use_beta = !(bh == 0.0 && bl == 0.0);
+  if (k == 0 || (ah == 0.0 && al == 0.0)) {
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double rh = 0.0, rl = 0.0;
+        if (use_beta) orc_dd_mul(bh, bl, Chi[i * ldc + j], Clo[i * ldc + j], &rh, &rl);
+        Chi[i * ldc + j] = rh;
+        Clo[i * ldc + j] = rl;
+        if (flags) flags[i * n + j] = 0;
+      }
+    return;
+  }
+  double* a_h = (double*)calloc((size_t)(m * k), sizeof(double));
+  double* a_l = (double*)calloc((size_t)(m * k), sizeof(double));
+  double* b_h = (double*)calloc((size_t)(k * n), sizeof(double));
+  double* b_l = (double*)calloc((size_t)(k * n), sizeof(double));
+  double* p_h = (double*)calloc((size_t)(m * n), sizeof(double));
+  double* p_l = (double*)calloc((size_t)(m * n), sizeof(double));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t p = 0; p < k; ++p) {
+      const int64_t s = transa ? p * lda + i : i * lda + p;
+      a_h[i * k + p] = Ahi[s];
+      a_l[i * k + p] = Alo[s];
+    }
+  for (int64_t p = 0; p < k; ++p)
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t s = transb ? j * ldb + p : p * ldb + j;
+      b_h[p * n + j] = Bhi[s];
+      b_l[p * n + j] = Blo[s];
+    }
+  orc_i8_casc_gemm(m, n, k, a_h, a_l, k, b_h, b_l, n, y, p_h, p_l, n, flags, nthreads);
+  const int unit_alpha = (ah == 1.0 && al == 0.0);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double th = p_h[i * n + j], tl = p_l[i * n + j];
+      if (!unit_alpha || use_beta) {
+        orc_dd_mul(ah, al, th, tl, &th, &tl);
+        if (use_beta) {
+          double uh, ul;
+          orc_dd_mul(bh, bl, Chi[i * ldc + j], Clo[i * ldc + j], &uh, &ul);
+          orc_dd_add(th, tl, uh, ul, &th, &tl);
+        }
+      }
+      Chi[i * ldc + j] = th;
+      Clo[i * ldc + j] = tl;
+    }
+  free(a_h);
+  free(a_l);
+  free(b_h);
+  free(b_l);
+  free(p_h);
+  free(p_l);
+}

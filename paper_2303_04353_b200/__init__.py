@@ -71,7 +71,7 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_gemm_fp64x2", "casc_i8_gemm_fp64x2_ws", "casc_i8_workspace_bytes",
             "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
-            "casc_i8_gemm_packed"]
+            "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -97,11 +97,31 @@ _sig("casc_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctype
 CASC_OP_N, CASC_OP_T = 0, 1
 
 
+_sig("casc_i8_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,
+                                ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
+                                ctypes.c_double, _vp, _vp, _i64, _vp, ctypes.c_int, _vp, _sz,
+                                _vp])
+
+
 def casc_gemm_fp64x2_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo,
                         flags=None, workspace=None, stream=None):
     """C := alpha op(A) op(B) + beta C (FP64x2; NEXT-4).  transa/transb in
     {'N', 'T', 0, 1}; alpha, beta are (hi, lo) pairs or floats.  C_hi / C_lo
     (m x n) are updated in place; returns (C_hi, C_lo, flags)."""
+    return _gemm_ex(None, transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo,
+                    flags, workspace, stream)
+
+
+def casc_i8_gemm_fp64x2_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo,
+                           flags=None, y: int = 14, workspace=None, stream=None):
+    """casc_gemm_fp64x2_ex on the INT8 cascade (NEXT-3 + NEXT-4): the product
+    op(A) op(B) through y int8 slices (readings R21-R26)."""
+    return _gemm_ex(int(y), transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo,
+                    flags, workspace, stream)
+
+
+def _gemm_ex(y, transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, flags,
+             workspace, stream):
     ta = 1 if transa in ("T", "t", 1, True) else 0
     tb = 1 if transb in ("T", "t", 1, True) else 0
     ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
@@ -118,12 +138,13 @@ def casc_gemm_fp64x2_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_h
         k = 0
     if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (m, n)):
         raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
-    _check(_lib.casc_gemm_fp64x2_ex(ta, tb, m, n, k, float(ah), float(al), _ptr(A_hi),
-                                    _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo), ldb, float(bh),
-                                    float(bl), _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
-                                    _ptr(workspace), 0 if workspace is None else workspace.numel(),
-                                    _stream(stream)),
-           "casc_gemm_fp64x2_ex")
+    head = (ta, tb, m, n, k, float(ah), float(al), _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+            _ptr(B_lo), ldb, float(bh), float(bl), _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags))
+    tail = (_ptr(workspace), 0 if workspace is None else workspace.numel(), _stream(stream))
+    if y is None:
+        _check(_lib.casc_gemm_fp64x2_ex(*head, *tail), "casc_gemm_fp64x2_ex")
+    else:
+        _check(_lib.casc_i8_gemm_fp64x2_ex(*head, y, *tail), "casc_i8_gemm_fp64x2_ex")
     return C_hi, C_lo, flags
 
 

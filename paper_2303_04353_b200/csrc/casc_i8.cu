@@ -373,6 +373,8 @@ struct GemmArgs {
   unsigned int* sync;   // wave-sync counter (zeroed before the launch) or null
   int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
   int64_t dbg_panel;
+  int ab;               // NEXT-4 update at the final store: 0 none, 1 alpha, 2 alpha and beta
+  double ah, al, bh, bl;
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
@@ -943,8 +945,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               } else {
                 const int64_t gj = cb * TR + lc;
                 if (gi < p.m && gj < p.n) {
-                  p.C_hi[gi * p.ldc + gj] = ch;
-                  p.C_lo[gi * p.ldc + gj] = cl;
+                  double* oh = p.C_hi + gi * p.ldc + gj;
+                  double* ol = p.C_lo + gi * p.ldc + gj;
+                  // NEXT-4 (reading R21): C := alpha (x) P (+) beta (x) C
+                  if (p.ab)
+                    apply_alpha_beta(ch, cl, p.ah, p.al, p.bh, p.bl, p.ab == 2 ? *oh : 0.0,
+                                     p.ab == 2 ? *ol : 0.0, p.ab == 2);
+                  *oh = ch;
+                  *ol = cl;
                   if (p.flags) p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
                 }
               }
@@ -1028,8 +1036,14 @@ cudaError_t slice_map(CUtensorMap* map, const void* packed, const Pack& g, uint3
 
 cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
                  double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
-                 int32_t* dbg, int64_t dbg_panel, cudaStream_t st) {
+                 int32_t* dbg, int64_t dbg_panel, cudaStream_t st, int ab = 0, double ah = 1.0,
+                 double al = 0.0, double bh = 0.0, double bl = 0.0) {
   GemmArgs a{};
+  a.ab = ab;
+  a.ah = ah;
+  a.al = al;
+  a.bh = bh;
+  a.bl = bl;
   a.pa = static_cast<const uint8_t*>(pa);
   a.pb = static_cast<const uint8_t*>(pb);
   a.ga = pack_of(m, k, y);
@@ -1072,6 +1086,9 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
 
 // ====================================================================== C ABI
 namespace casc {
+cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
+                           double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
+                           cudaStream_t st);
 namespace host {
 int device_check(int* sms);
 int validate_gemm(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
@@ -1182,6 +1199,65 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
   if (e == cudaSuccess)
     e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, ws, i8::grid_for(m, n, sms), nullptr,
                  0, st);
+  if (e == cudaSuccess) host::set_launches(7);
+  return st8(e);
+}
+
+int casc_i8_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                           double alpha_hi, double alpha_lo, const double* A_hi,
+                           const double* A_lo, int64_t lda, const double* B_hi,
+                           const double* B_lo, int64_t ldb, double beta_hi, double beta_lo,
+                           double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int y,
+                           void* workspace, size_t workspace_bytes, casc_stream_t stream) {
+  host::set_launches(0);
+  if ((transa != CASC_OP_N && transa != CASC_OP_T) || (transb != CASC_OP_N && transb != CASC_OP_T))
+    return CASC_ERR_INVALID;
+  if (m < 0 || n < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  // stored shapes: op(A) is m x k (A stored k x m if transposed), op(B) is k x n
+  const int64_t ar = transa ? k : m, ac = transa ? m : k;
+  const int64_t br = transb ? n : k, bc = transb ? k : n;
+  const bool no_product = (k == 0) || (alpha_hi == 0.0 && alpha_lo == 0.0);
+  int r;
+  if (!no_product) {
+    if ((r = host::check_mat(A_hi, ar, ac, lda)) || (r = host::check_mat(A_lo, ar, ac, lda)))
+      return r;
+    if ((r = host::check_mat(B_hi, br, bc, ldb)) || (r = host::check_mat(B_lo, br, bc, ldb)))
+      return r;
+  }
+  if ((r = host::check_mat(C_hi, m, n, ldc)) || (r = host::check_mat(C_lo, m, n, ldc))) return r;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  const bool use_beta = !(beta_hi == 0.0 && beta_lo == 0.0);
+  if (no_product) {  // C := beta C (BLAS: A and B are not referenced)
+    const cudaError_t e =
+        casc::launch_scale_c(m, n, beta_hi, beta_lo, use_beta, C_hi, C_lo, ldc, flags, sms, st);
+    if (e == cudaSuccess) host::set_launches(1);
+    return st8(e);
+  }
+  const size_t need = casc_i8_workspace_bytes(m, n, k, y);
+  void* ws = workspace;
+  bool owned = false;
+  if (!ws) {
+    if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+    owned = true;
+  } else if (workspace_bytes < need) {
+    return CASC_ERR_INVALID;
+  }
+  uint8_t* pa = static_cast<uint8_t*>(ws);
+  uint8_t* pb = pa + al256h(casc_i8_packed_bytes(m, k, y));
+  double* gws = reinterpret_cast<double*>(pb + al256h(casc_i8_packed_bytes(n, k, y)));
+  // rows of op(A) are columns of a transposed A; columns of op(B) are rows of a
+  // transposed B: the split kernels read either orientation directly
+  cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, transa == CASC_OP_T, pa, st);
+  if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, transb != CASC_OP_T, pb, st);
+  const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
+  const int ab = use_beta ? 2 : (unit_alpha ? 0 : 1);
+  if (e == cudaSuccess)
+    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, gws, i8::grid_for(m, n, sms),
+                 nullptr, 0, st, ab, alpha_hi, alpha_lo, beta_hi, beta_lo);
+  if (owned) cudaFreeAsync(ws, st);
   if (e == cudaSuccess) host::set_launches(7);
   return st8(e);
 }

@@ -281,3 +281,64 @@ def test_i8_extreme_exponents(casc, orc):
     o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
     assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
     assert np.all(np.abs(C_hi) < 2.0**-990) and np.any(C_hi != 0)
+
+
+# ------------------------------------------------------------------ BLAS-style (NEXT-4)
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_i8_blas_ex_bit_exact(casc, orc, ta, tb):
+    """casc_i8_gemm_fp64x2_ex: transposed operands, alpha / beta (reading R21)
+    bit-exact with oracle.i8_casc_gemm_ex, including a two-panel k and ragged tiles."""
+    import torch
+    m, n, k = 130, 257, 8192 + 300
+    d = I.make_config(1, m=m, n=n, k=k, seed=41)
+    A = (d["A_hi"].T.copy(), d["A_lo"].T.copy()) if ta == "T" else (d["A_hi"], d["A_lo"])
+    B = (d["B_hi"].T.copy(), d["B_lo"].T.copy()) if tb == "T" else (d["B_hi"], d["B_lo"])
+    rng = np.random.default_rng(11)
+    C0h = rng.uniform(-1, 1, (m, n))
+    C0l = C0h * 2.0 ** -60 * rng.uniform(-1, 1, (m, n))
+    for al, be in [((1.0, 0.0), (0.0, 0.0)), ((1.0 / 3.0, 2.0 ** -56), (0.0, 0.0)),
+                   ((1.0, 0.0), (-0.7, 2.0 ** -60)), ((-4.0, 0.0), (1.5, 0.0))]:
+        nan = be == (0.0, 0.0)  # beta = 0: C is not read (NaN in, finite out)
+        C_hi = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda") if nan \
+            else T(C0h)
+        C_lo = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda") if nan \
+            else T(C0l)
+        fl = torch.empty((m, n), dtype=torch.uint8, device="cuda")
+        casc.casc_i8_gemm_fp64x2_ex(ta, tb, al, T(A[0]), T(A[1]), T(B[0]), T(B[1]), be,
+                                    C_hi, C_lo, flags=fl)
+        o_hi, o_lo, o_fl = orc.i8_casc_gemm_ex(ta, tb, al, A[0], A[1], B[0], B[1], be,
+                                               C0h.copy(), C0l.copy())
+        assert bitwise(N(C_hi), o_hi) and bitwise(N(C_lo), o_lo), (ta, tb, al, be)
+        assert np.array_equal(N(fl), o_fl)
+
+
+def test_i8_blas_ex_degenerate(casc, orc):
+    """k = 0 / alpha = 0: C := beta C and flags := 0 without reading A, B;
+    strided C (ldc > n); workspace given explicitly; bad arguments rejected."""
+    import torch
+    m, n, k = 70, 90, 200
+    rng = np.random.default_rng(5)
+    C0 = rng.uniform(-1, 1, (m, n))
+    be = (-0.7, 2.0 ** -60)
+    C_hi, C_lo = T(C0), T(np.zeros((m, n)))
+    fl = torch.full((m, n), 5, dtype=torch.uint8, device="cuda")
+    casc.casc_i8_gemm_fp64x2_ex("N", "N", 0.0, None, None, None, None, be, C_hi, C_lo, flags=fl)
+    o_hi, o_lo, _ = orc.i8_casc_gemm_ex("N", "N", (0.0, 0.0), np.zeros((m, 0)), np.zeros((m, 0)),
+                                        np.zeros((0, n)), np.zeros((0, n)), be, C0.copy(),
+                                        np.zeros((m, n)))
+    assert bitwise(N(C_hi), o_hi) and bitwise(N(C_lo), o_lo) and N(fl).sum() == 0
+    # strided C inside a wider buffer, explicit workspace, y = 8
+    d = I.make_config(2, m=m, n=n, k=k, seed=43)
+    big_h = T(np.tile(C0, (1, 2)))
+    big_l = T(np.zeros((m, 2 * n)))
+    ws = torch.empty(casc.casc_i8_workspace_bytes(m, n, k, 8), dtype=torch.uint8, device="cuda")
+    casc.casc_i8_gemm_fp64x2_ex("N", "N", 2.0, T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                T(d["B_lo"]), 1.0, big_h[:, :n], big_l[:, :n], y=8,
+                                workspace=ws)
+    o_hi, o_lo, _ = orc.i8_casc_gemm_ex("N", "N", (2.0, 0.0), d["A_hi"], d["A_lo"], d["B_hi"],
+                                        d["B_lo"], (1.0, 0.0), C0.copy(), np.zeros((m, n)), y=8)
+    assert bitwise(N(big_h[:, :n]).copy(), o_hi) and bitwise(N(big_l[:, :n]).copy(), o_lo)
+    assert np.array_equal(N(big_h[:, n:]), C0)  # untouched
+    with pytest.raises(casc.CascError):
+        casc.casc_i8_gemm_fp64x2_ex("N", "N", 1.0, T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                    T(d["B_lo"]), 0.0, T(C0), T(C0), y=2)

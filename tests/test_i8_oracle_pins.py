@@ -247,3 +247,33 @@ def test_i8_k_zero(orc):
     C_hi, C_lo, flags = orc.i8_casc_gemm(np.zeros((3, 0)), np.zeros((3, 0)), np.zeros((0, 2)),
                                          np.zeros((0, 2)))
     assert np.all(C_hi == 0) and np.all(C_lo == 0) and np.all(flags == 0)
+
+
+def test_i8_blas_ex_oracle(orc):
+    """NEXT-4 on the INT8 cascade (reading R21): transposed storage gives the
+    plain product bit for bit; alpha = 2^p scales exactly; alpha = 1, beta = 1
+    adds C within 2^-104 (exact rationals); k == 0 and alpha == 0 give
+    beta (x) C with no flags; beta == 0 never reads C (NaN C stays unread)."""
+    d = I.make_config(1, m=9, n=7, k=300, seed=41)
+    P = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    nanC = np.full((9, 7), np.nan)
+    r = orc.i8_casc_gemm_ex("T", "T", (1.0, 0.0), d["A_hi"].T, d["A_lo"].T, d["B_hi"].T,
+                            d["B_lo"].T, (0.0, 0.0), nanC, nanC)
+    assert all(np.array_equal(x, z) for x, z in zip(r, P))
+    r = orc.i8_casc_gemm_ex("N", "T", (2.0**-5, 0.0), d["A_hi"], d["A_lo"], d["B_hi"].T,
+                            d["B_lo"].T, (0.0, 0.0), nanC, nanC)
+    assert np.array_equal(r[0], P[0] * 2.0**-5) and np.array_equal(r[1], P[1] * 2.0**-5)
+    X_hi = np.array(d["A_hi"][:, :7])
+    X_lo = np.zeros_like(X_hi)
+    r = orc.i8_casc_gemm_ex("N", "N", (1.0, 0.0), d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"],
+                            (1.0, 0.0), X_hi, X_lo)
+    for i in range(9):
+        for j in range(7):
+            ex = fr(P[0][i, j]) + fr(P[1][i, j]) + fr(X_hi[i, j])
+            got = fr(r[0][i, j]) + fr(r[1][i, j])
+            assert abs(got - ex) <= F(2) ** -104 * (abs(fr(P[0][i, j])) + abs(fr(X_hi[i, j])))
+    for alpha, kk in (((1.0, 0.0), 0), ((0.0, 0.0), 300)):
+        A = d["A_hi"][:, :kk]
+        B = d["B_hi"][:kk]
+        r = orc.i8_casc_gemm_ex("N", "N", alpha, A, A, B, B, (2.0, 0.0), X_hi, X_lo)
+        assert np.array_equal(r[0], 2 * X_hi) and np.all(r[2] == 0)
