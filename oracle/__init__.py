@@ -94,6 +94,7 @@ def _setup(L):
     L.orc_i8_panel_bins.argtypes = [_i64, _i64, _i64, ctypes.c_int, _pi8, _pi8, ctypes.c_int,
                                     _pi64]
     L.orc_i8_group_value.argtypes = [_pi64, ctypes.c_int, _pd, _pd]
+    L.orc_i8_panel_value.argtypes = [_pi64, ctypes.c_int, ctypes.c_int, _pd, _pd]
     L.orc_i8_casc_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64,
                                    ctypes.c_int, _pd, _pd, _i64, _pu8, ctypes.c_int]
     L.orc_i8_casc_gemm_ex.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, _d, _d,
@@ -361,6 +362,13 @@ def i8_group_value(b):
     """Exact FP64x2 value of up to four consecutive bins (reading R25)."""
     b = np.ascontiguousarray(b, dtype=np.int64)
     return _pair(lib().orc_i8_group_value, _p(b, _pi64), b.size)
+
+
+def i8_panel_value(b, w0: int):
+    """Panel value T of one element (reading R25, rev. 2): the FP64x2 number
+    nearest x = sum_s b[s] 2^(w0 + 8(y-1-s)), y = len(b)."""
+    b = np.ascontiguousarray(b, dtype=np.int64)
+    return _pair(lib().orc_i8_panel_value, _p(b, _pi64), b.size, int(w0))
 
 
 def i8_casc_gemm(A_hi, A_lo, B_hi, B_lo, y: int = 14, nthreads: int = 0):

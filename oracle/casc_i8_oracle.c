@@ -27,14 +27,14 @@
  *                  slice t is d_t 2^(e - 6 - 8t).
  *   R24 products   bin_s = sum_p sum_(i+j=s) dA_i dB_j for s = 0 .. y-1 (the
  *                  paper's triangle of y(y+1)/2 products), exact.
- *   R25 combine    bins in groups of four aligned at the least significant bin
- *                  (the first group is bins 0 .. r-1, r = (y-1) % 4 + 1, e.g.
- *                  {0,1} {2-5} {6-9} {10-13} for y = 14), most significant group
- *                  first: the group value V = sum_u bin_(s+u) 2^(8(nb-1-u)) is exact in
- *                  int64; G = (RN(V), V - RN(V)) scaled by 2^(e+f-12-8(s+nb-1));
- *                  the panel value T = DDadd over the groups, then C = DDadd(C, T)
- *                  over panels in ascending order (FP64x2; the FP64
- *                  cascade's per-panel T of P:L3295).
+ *   R25 combine    (revised twice; DESIGN.md §3 R25) the panel value T is the
+ *                  FP64x2 number nearest the panel's exact product
+ *                  x = sum_s bin_s 2^(e+f-12-8s):  T.hi = RN(x), T.lo = RN(x - T.hi)
+ *                  (IEEE round to nearest even, subnormals included, RN(0) = +0);
+ *                  then C = T over the first panel and C = DDadd(C, T) over the
+ *                  following ones, in ascending order (FP64x2; the FP64
+ *                  cascade's per-panel T of P:L3295).  Evaluated here with a plain
+ *                  sign-magnitude big integer and ldexp of a <= 53-bit integer.
  *   R26 detector   flag |= (|T.hi| <= kp 2^(e+f-50)): the panel's exact-integer
  *                  product lost at least ~50 bits against its operand scale.
  *                  The paper's test "bin 0 is zero" asks whether the
@@ -119,6 +119,109 @@ void orc_i8_group_value(const int64_t* b, int nb, double* hi, double* lo) {
   *lo = (double)(V - (int64_t)h);
 }
 
+/* ---- Reading R25 (rev. 2): the FP64x2 number nearest an exact integer x 2^w.
+ * Magnitudes are little-endian base-2^32 limbs, NL of them (> 160 bits). */
+#define NL 8
+static int big_bit(const uint32_t* M, int i) {
+  return (i >= 0 && i < 32 * NL) ? (int)((M[i / 32] >> (i % 32)) & 1u) : 0;
+}
+static int big_bitlen(const uint32_t* M) { /* index of the top set bit + 1; 0 for M = 0 */
+  for (int i = 32 * NL - 1; i >= 0; --i)
+    if (big_bit(M, i)) return i + 1;
+  return 0;
+}
+static int big_cmp(const uint32_t* a, const uint32_t* b) {
+  for (int l = NL - 1; l >= 0; --l)
+    if (a[l] != b[l]) return a[l] < b[l] ? -1 : 1;
+  return 0;
+}
+static void big_sub(uint32_t* a, const uint32_t* b) { /* a -= b, requires a >= b */
+  int64_t borrow = 0;
+  for (int l = 0; l < NL; ++l) {
+    int64_t d = (int64_t)a[l] - (int64_t)b[l] - borrow;
+    borrow = d < 0;
+    a[l] = (uint32_t)(d + (borrow ? ((int64_t)1 << 32) : 0));
+  }
+}
+static void big_add_u64_shifted(uint32_t* a, uint64_t v, int sh) { /* a += v 2^sh */
+  for (int i = 0; i < 64; ++i)
+    if ((v >> i) & 1u) { /* add 2^(sh + i) */
+      int j = sh + i;
+      uint64_t carry = 1;
+      for (int l = j / 32; l < NL && carry; ++l) {
+        const uint64_t t = (uint64_t)a[l] + (carry << (l == j / 32 ? j % 32 : 0));
+        a[l] = (uint32_t)t;
+        carry = t >> 32;
+      }
+    }
+}
+
+/* RN(+-M 2^w) in IEEE double (ties to even; subnormals; overflow -> inf;
+ * RN(0) = +0).  *R / *rneg receive the exact remainder M 2^w - |RN| as a
+ * magnitude and a sign relative to the input's sign. */
+static double rn_big(const uint32_t* M, int w, int neg, uint32_t* R, int* rneg) {
+  memset(R, 0, sizeof(uint32_t) * NL);
+  *rneg = 0;
+  const int len = big_bitlen(M);
+  if (len == 0) return 0.0;
+  const int p = len - 1;                       /* x in [2^(p+w), 2^(p+w+1)) */
+  int c = p - 52;                              /* keep 53 significant bits ... */
+  if (c < -1074 - w) c = -1074 - w;            /* ... or the subnormal grid 2^-1074 */
+  uint64_t q = 0;
+  int up = 0;
+  if (c <= 0) {
+    for (int i = 0; i <= p; ++i) q |= (uint64_t)big_bit(M, i) << i; /* exact */
+  } else {
+    for (int i = c; i <= p; ++i) q |= (uint64_t)big_bit(M, i) << (i - c);
+    const int guard = big_bit(M, c - 1);
+    int sticky = 0;
+    for (int i = 0; i < c - 1; ++i) sticky |= big_bit(M, i);
+    up = guard && (sticky || (q & 1u));
+    /* remainder: the bits below c, or 2^c minus them when rounded up */
+    uint32_t low[NL];
+    memset(low, 0, sizeof low);
+    for (int i = 0; i < c && i < 32 * NL; ++i)
+      if (big_bit(M, i)) low[i / 32] |= 1u << (i % 32);
+    if (up) {
+      uint32_t two_c[NL];
+      memset(two_c, 0, sizeof two_c);
+      if (c < 32 * NL) two_c[c / 32] = 1u << (c % 32);
+      big_sub(two_c, low);
+      memcpy(R, two_c, sizeof two_c);
+      *rneg = 1;
+    } else {
+      memcpy(R, low, sizeof low);
+    }
+    q += (uint64_t)up;
+  }
+  const double v = ldexp((double)q, w + (c > 0 ? c : 0)); /* q <= 2^53: exact */
+  return neg ? -v : v;
+}
+
+/* T of one element: bins b[0..y-1] (exact), x = sum_s b[s] 2^(w0 + 8(y-1-s)). */
+void orc_i8_panel_value(const int64_t* b, int y, int w0, double* hi, double* lo) {
+  uint32_t P[NL], N[NL], R[NL];
+  memset(P, 0, sizeof P);
+  memset(N, 0, sizeof N);
+  for (int s = 0; s < y; ++s) {
+    if (b[s] > 0) big_add_u64_shifted(P, (uint64_t)b[s], 8 * (y - 1 - s));
+    if (b[s] < 0) big_add_u64_shifted(N, (uint64_t)(-b[s]), 8 * (y - 1 - s));
+  }
+  int neg = 0;
+  if (big_cmp(P, N) >= 0) {
+    big_sub(P, N);
+  } else {
+    big_sub(N, P);
+    memcpy(P, N, sizeof P);
+    neg = 1;
+  }
+  int rneg;
+  *hi = rn_big(P, w0, neg, R, &rneg);
+  uint32_t R2[NL];
+  int r2neg;
+  *lo = rn_big(R, w0, neg ^ rneg, R2, &r2neg);
+}
+
 /* ORACLE-I8CASCADE: C := A B (FP64x2) through y int8 slices per operand.
  * Row-major A (m x k, lda), B (k x n, ldb), C (m x n, ldc); flags m x n
  * (ld = n, nullable).  k == 0 gives C = 0, flags = 0. */
@@ -161,22 +264,14 @@ void orc_i8_casc_gemm(int64_t m, int64_t n, int64_t k, const double* Ahi, const 
           }
           b[s] = acc;
         }
-        /* reading R25: groups of four aligned at the least significant bin (the
-         * first group holds bins 0 .. r-1, r = (y-1) % 4 + 1), most significant
-         * group first -> panel value T */
-        double th = 0.0, tl = 0.0;
-        const int r0 = (y - 1) % 4 + 1;
-        for (int s = 0; s < y; s = (s == 0 ? r0 : s + 4)) {
-          const int nb = (s == 0) ? r0 : 4;
-          double gh, gl;
-          orc_i8_group_value(b + s, nb, &gh, &gl);
-          const int w = e[i] + f[j] - 12 - 8 * (s + nb - 1);
-          orc_dd_add(th, tl, ldexp(gh, w), ldexp(gl, w), &th, &tl);
-        }
+        /* reading R25 (rev. 2): T = the FP64x2 number nearest the exact panel
+         * product */
+        double th, tl;
+        orc_i8_panel_value(b, y, e[i] + f[j] - 12 - 8 * (y - 1), &th, &tl);
         /* reading R26 */
         if (flags && fabs(th) <= ldexp((double)kp, e[i] + f[j] - 50)) flags[i * n + j] = 1;
-        double ch = Chi[i * ldc + j], cl = Clo[i * ldc + j];
-        orc_dd_add(ch, cl, th, tl, &ch, &cl);
+        double ch = th, cl = tl; /* C = T_0, then C = DDadd(C, T_q) */
+        if (q > 0) orc_dd_add(Chi[i * ldc + j], Clo[i * ldc + j], th, tl, &ch, &cl);
         Chi[i * ldc + j] = ch;
         Clo[i * ldc + j] = cl;
       }

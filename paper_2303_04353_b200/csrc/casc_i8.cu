@@ -52,6 +52,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -186,6 +187,110 @@ __device__ __forceinline__ double mulp2(double x, int n) {
   const int h = n / 2;
   return __dmul_rn(__dmul_rn(x, p2(h)), p2(n - h));
 }
+// ---- Reading R25 (rev. 2) on the integer pipe.  The panel value T is the FP64x2
+// number nearest the exact panel product x = S 2^w (S an exact integer of up to
+// ~150 bits): T.hi = RN(x), T.lo = RN(x - T.hi).  All of it is integer work:
+// FP64 ALU instructions issued while the int8 MMAs run were measured ~5x slower
+// than on an idle SM (they share a datapath), the integer pipe is not.
+struct U192 {
+  unsigned long long l0, l1, l2;  // little-endian limbs
+};
+__device__ __forceinline__ U192 u192_add(U192 a, U192 b) {
+  U192 r;
+  r.l0 = a.l0 + b.l0;
+  const unsigned long long c0 = r.l0 < a.l0;
+  const unsigned long long t = a.l1 + b.l1;
+  const unsigned long long c1 = t < a.l1;
+  r.l1 = t + c0;
+  const unsigned long long c2 = c1 | (r.l1 < t);
+  r.l2 = a.l2 + b.l2 + c2;
+  return r;
+}
+__device__ __forceinline__ U192 u192_neg(U192 a) {
+  U192 r{~a.l0, ~a.l1, ~a.l2};
+  return u192_add(r, U192{1ull, 0ull, 0ull});
+}
+// V 2^(32 sh32), sign-extended to 192 bits (sh32 = 0 .. 3)
+__device__ __forceinline__ U192 u192_from_shifted(long long v, int sh32) {
+  const unsigned long long sx = v < 0 ? ~0ull : 0ull;
+  const unsigned long long u = (unsigned long long)v;
+  switch (sh32) {
+    case 0: return U192{u, sx, sx};
+    case 1: return U192{u << 32, (unsigned long long)(v >> 32), sx};
+    case 2: return U192{0ull, u, sx};
+    default: return U192{0ull, u << 32, (unsigned long long)(v >> 32)};
+  }
+}
+__device__ __forceinline__ int u192_bitlen(const U192& a) {
+  if (a.l2) return 192 - __clzll((long long)a.l2);
+  if (a.l1) return 128 - __clzll((long long)a.l1);
+  if (a.l0) return 64 - __clzll((long long)a.l0);
+  return 0;
+}
+// bits [c, c + 64) of a (c >= 0)
+__device__ __forceinline__ unsigned long long u192_shr64(const U192& a, int c) {
+  if (c >= 192) return 0ull;
+  const unsigned long long x = c < 64 ? a.l0 : c < 128 ? a.l1 : a.l2;
+  const unsigned long long z = c < 64 ? a.l1 : c < 128 ? a.l2 : 0ull;
+  const int b = c & 63;
+  return b ? (x >> b) | (z << (64 - b)) : x;
+}
+// a mod 2^c (c >= 0)
+__device__ __forceinline__ U192 u192_low(const U192& a, int c) {
+  auto mask = [](int bits) { return bits >= 64 ? ~0ull : bits <= 0 ? 0ull : (1ull << bits) - 1; };
+  return U192{a.l0 & mask(c), a.l1 & mask(c - 64), a.l2 & mask(c - 128)};
+}
+__device__ __forceinline__ bool u192_nonzero(const U192& a) { return (a.l0 | a.l1 | a.l2) != 0; }
+// the double +-q 2^e2 for an integer q <= 2^54 whose value is representable
+// (q 2^e2 on or above the 2^-1074 grid); overflow gives inf
+__device__ __forceinline__ double make_double(bool neg, unsigned long long q, int e2) {
+  unsigned long long bits = 0;
+  if (q) {
+    const int top = 63 - __clzll((long long)q);  // q in [2^top, 2^(top+1))
+    int sh = 52 - top;                          // normalise to [2^52, 2^53)
+    if (e2 - sh < -1074) sh = e2 + 1074;        // subnormal: e2 -> -1074
+    q = sh >= 0 ? q << sh : q >> (-sh);         // exact (q even when shifted right)
+    e2 -= sh;
+    if (q >= (1ull << 52)) {                    // normal
+      const int field = e2 + 1075;
+      bits = field >= 2047 ? 0x7ff0000000000000ull
+                           : ((unsigned long long)field << 52) | (q & 0xfffffffffffffull);
+    } else {
+      bits = q;                                 // subnormal (e2 == -1074)
+    }
+  }
+  if (neg) bits |= 0x8000000000000000ull;
+  return __longlong_as_double((long long)bits);
+}
+// RN(+-M 2^w) (ties to even, subnormals, RN(0) = +0); R, rneg: the exact
+// remainder M 2^w - |RN| as a magnitude and a sign relative to the input's
+__device__ __forceinline__ double rn_u192(const U192& M, int w, bool neg, U192& R, bool& rneg) {
+  R = U192{0ull, 0ull, 0ull};
+  rneg = false;
+  const int len = u192_bitlen(M);
+  if (len == 0) return 0.0;
+  int c = len - 53;
+  if (c < -1074 - w) c = -1074 - w;
+  if (c <= 0) return make_double(neg, M.l0, w);  // exact: M < 2^53
+  unsigned long long q = u192_shr64(M, c);
+  const U192 low = u192_low(M, c);
+  const bool guard = (u192_shr64(M, c - 1) & 1ull) != 0;
+  const bool sticky = u192_nonzero(u192_low(M, c - 1));
+  const bool up = guard && (sticky || (q & 1ull));
+  if (up) {  // remainder 2^c - low, opposite sign
+    U192 two_c{0ull, 0ull, 0ull};
+    if (c < 64) two_c.l0 = 1ull << c;
+    else if (c < 128) two_c.l1 = 1ull << (c - 64);
+    else if (c < 192) two_c.l2 = 1ull << (c - 128);
+    R = u192_add(two_c, u192_neg(low));
+    rneg = true;
+    ++q;
+  } else {
+    R = low;
+  }
+  return make_double(neg, q, w + c);
+}
+
 // exact conversion of an integer-valued double (|w| < 2^126) to int128
 __device__ __forceinline__ __int128 to_i128(double w) {
   if (fabs(w) < 9.0e18) return (__int128)__double2ll_rz(w);
@@ -496,7 +601,22 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar0, uint64_t* bar1) {
       : "memory");
 }
 
-#ifdef CASC_I8_NOWAIT  // timing study only: MMA issue rate without data waits (wrong results)
+// timing studies only (wrong results): CASC_I8_NOWAIT, the MMAs do not wait for
+// the epilogue to drain tensor memory; CASC_I8_NOTMA, no operand loads at all
+// (the MMA issue rate on stale shared memory)
+#ifdef CASC_I8_PROF  // timing study: MMA-issuer cycles spent in each kind of wait
+__device__ unsigned long long g_i8prof[1024][64];
+#define I8_PROF_WAIT(slot, stmt)                                    \
+  do {                                                              \
+    const long long t0_ = clock64();                                \
+    stmt;                                                           \
+    if ((threadIdx.x & 31) == 0)                                    \
+      g_i8prof[blockIdx.x][slot] += (unsigned long long)(clock64() - t0_); \
+  } while (0)
+#else
+#define I8_PROF_WAIT(slot, stmt) stmt
+#endif
+#ifdef CASC_I8_NOTMA
 #define CASC_I8_WAITS_ON 0
 #else
 #define CASC_I8_WAITS_ON 1
@@ -564,15 +684,16 @@ __device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_
     const uint32_t aq = aseq + i;
     const uint32_t as = aq % NSA;
     // B operands first used at this step: B_TOP..B_S at i = 0, B_(S-i) after
-    if (i == 0) {
+    if (!CASC_I8_WAITS_ON) {
+    } else if (i == 0) {
 #pragma unroll
       for (int u = 0; u < NB; ++u)
-        mbar_wait_uniform(&fullB[(bbase + u) % NSB], ((bbase + u) / NSB) & 1);
+        I8_PROF_WAIT(16 + S, mbar_wait_uniform(&fullB[(bbase + u) % NSB], ((bbase + u) / NSB) & 1));
     } else if (S - i >= 0) {
       const uint32_t bq = bbase + NB + (i - 1);
-      mbar_wait_uniform(&fullB[bq % NSB], (bq / NSB) & 1);
+      I8_PROF_WAIT(16 + S, mbar_wait_uniform(&fullB[bq % NSB], (bq / NSB) & 1));
     }
-    mbar_wait_uniform(&fullA[as], (aq / NSA) & 1);
+    if (CASC_I8_WAITS_ON) I8_PROF_WAIT(32 + S, mbar_wait_uniform(&fullA[as], (aq / NSA) & 1));
     tc_fence_after();
     constexpr int JHI_ = TOP;  // (per i below)
     (void)JHI_;
@@ -599,6 +720,9 @@ __device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_
       const uint32_t acc = (first_kb && i == 0 && kk == 0) ? 0u : 1u;
       const uint64_t bk[4] = {bd[0] + 2 * kk, bd[1] + 2 * kk, bd[2] + 2 * kk, bd[3] + 2 * kk};
       const int np = jhi - jlo + 1;
+#ifdef CASC_I8_NOMMA  // timing study only: no tensor-core work at all
+      if (np > 0) continue;
+#endif
       if (np == 4)
         mma_i8_astat<4>(d, ad + 2 * kk, bk, acc);
       else if (np == 3)
@@ -694,7 +818,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   int32_t* sF = reinterpret_cast<int32_t*>(tempty + 2);  // column exponents [128]
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches are
+  // uniform and the MMA issuer's descriptors can live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   if (threadIdx.x == 0) {
@@ -753,14 +879,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     const int full_waves = tiles / npairs;  // waves in which every pair has a tile
     uint32_t sweep = 0;
-    for (int tile = pair; tile < tiles; tile += npairs) {
+    for (int tile = CASC_I8_WAITS_ON ? pair : tiles; tile < tiles; tile += npairs) {
       int64_t rp, cb;
       tile_of(tile, RP, RB, rp, cb);
       const int64_t rb = 2 * rp + rank;
       const bool synced = p.sync && (tile / npairs) < full_waves;
       for (int q = 0; q < P; ++q) {
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
-        for (int grp = 0; grp < ngroups; ++grp) {
+        for (int go = 0; go < ngroups; ++go) {
+          const int grp = ngroups - 1 - go;  // most significant group first (see MMA loop)
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
           for (int64_t kb = kb0; kb < kb1; ++kb) {
             if (synced && (kb - kb0) % CASC_I8_SYNC_KB == 0) {
@@ -801,13 +928,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // issue blocks picks the one lane that issues each tcgen05 operation.
       uint32_t aseq = 0, bseq = 0, gcount = 0;
       const uint32_t a_base_addr = smem_u32(sA), b_base_addr = smem_u32(sB);
+#ifdef CASC_I8_PROF
+      const long long tstart = clock64();
+      if (lane == 0)
+        for (int x = 0; x < 64; ++x) g_i8prof[blockIdx.x][x] = 0;
+#endif
       for (int tile = pair; tile < tiles; tile += npairs) {
         for (int q = 0; q < P; ++q) {
           const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
-          for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+          // groups in decreasing order: the short least-significant group ends
+          // the panel, so the epilogue's once-per-panel phase 2 overlaps the
+          // longest group's MMAs instead of delaying the drain of the shortest
+          for (int go = 0; go < ngroups; ++go, ++gcount) {
+            const int grp = ngroups - 1 - go;
             const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
 #ifndef CASC_I8_NOWAIT
-            mbar_wait_cluster(tempty, (gcount & 1) ^ 1);
+            I8_PROF_WAIT(s, mbar_wait_cluster(tempty, (gcount & 1) ^ 1));
 #endif
             tc_fence_after();
             for (int kb = kb0; kb < kb1; ++kb)
@@ -817,6 +953,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
       }
+#ifdef CASC_I8_PROF
+      if (lane == 0 && (blockIdx.x % 16) == 0) {
+        const unsigned long long* g = g_i8prof[blockIdx.x];
+        printf("i8prof cta %d phase2 %llu x %llu | total %lld | tempty %llu %llu %llu %llu | fullB %llu %llu %llu %llu"
+               " | fullA %llu %llu %llu %llu\n", blockIdx.x, g[48], g[49], clock64() - tstart, g[0], g[2],
+               g[6], g[10], g[16], g[18], g[22], g[26], g[32], g[34], g[38], g[42]);
+      }
+#endif
     }
   } else {
     // ============================ epilogue (both CTAs) ============================
@@ -845,9 +989,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           sF[ew * 32 + lane] =
               *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, cb * TR + ew * 32 + lane, q));
         epi_bar_sync();
-        for (int grp = 0; grp < ngroups; ++grp, ++gcount) {
+        for (int go = 0; go < ngroups; ++go, ++gcount) {
+          const int grp = ngroups - 1 - go;  // the MMA issuer's group order
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
-          const bool lastg = grp + 1 == ngroups;
+          const bool lastg = go + 1 == ngroups;
           mbar_wait_sleep(tfull, gcount & 1);
           tc_fence_after();
           // Phase 1: drain this warp's part of TMEM into the exact group values
@@ -892,6 +1037,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           continue;
 #endif
           if (!lastg) continue;
+#ifdef CASC_I8_PROF
+          const long long tp2 = clock64();
+#endif
           // Phase 2, once per panel after its last group (overlaps the MMAs of
           // the next panel / tile): the FP64x2 panel sum T over the groups' exact
           // values, most significant first (R25), the detector (R26) and C.
@@ -906,29 +1054,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 xcl[i] = ld_na(&Cl[(c0 + i) * TR + lr]);
               }
             }
-            for (int g2 = 0; g2 < ngroups; ++g2) {
-              const int s2 = g2 ? r0 + (g2 - 1) * NBIN : 0, nb2 = g2 ? NBIN : r0;
-              long long xv[EPI_SUB];
+            // all of this block's group values in flight at once (memory-level
+            // parallelism: the loads are latency-bound under the operand traffic)
+            long long xv[NGMAX][EPI_SUB];
 #pragma unroll
-              for (int i = 0; i < EPI_SUB; ++i)
-                xv[i] = ld_na(&Vw[(int64_t)g2 * TR * TR + (c0 + i) * TR + lr]);
+            for (int g2 = 0; g2 < NGMAX; ++g2)
+              if (g2 < ngroups) {
 #pragma unroll
-              for (int i = 0; i < EPI_SUB; ++i) {
-                const int fj = sF[c0 + i];
-                // R25: G = (RN(V), V - RN(V)), exact
-                const long long v = xv[i];
-                double gh = __ll2double_rn(v);
-                double gl = __ll2double_rn(v - __double2ll_rn(gh));
-                const int w = ei + fj - 12 - 8 * (s2 + nb2 - 1);
-                gh = mulp2(gh, w);
-                gl = mulp2(gl, w);
-                if (g2 == 0) {
-                  th[i] = gh;
-                  tl[i] = gl;
-                } else {
-                  dd_add(th[i], tl[i], gh, gl, th[i], tl[i]);
-                }
+                for (int i = 0; i < EPI_SUB; ++i)
+                  xv[g2][i] = ld_na(&Vw[(int64_t)g2 * TR * TR + (c0 + i) * TR + lr]);
               }
+#pragma unroll
+            for (int i = 0; i < EPI_SUB; ++i) {
+              // R25 (rev. 2): S = sum_g V_g 2^(32 (ngroups-1-g)) exactly (the
+              // groups are aligned at the least significant bin), then
+              // T = (RN(S 2^w0), RN(S 2^w0 - T.hi)), w0 = e + f - 12 - 8(y-1)
+              U192 S{0ull, 0ull, 0ull};
+#pragma unroll
+              for (int g2 = 0; g2 < NGMAX; ++g2)
+                if (g2 < ngroups) S = u192_add(S, u192_from_shifted(xv[g2][i], ngroups - 1 - g2));
+              const bool neg = (long long)S.l2 < 0;
+              if (neg) S = u192_neg(S);
+              const int w0 = ei + sF[c0 + i] - 12 - 8 * (y - 1);
+              U192 R, R2;
+              bool rneg, r2neg;
+              th[i] = rn_u192(S, w0, neg, R, rneg);
+              tl[i] = rn_u192(R, w0, neg != rneg, R2, r2neg);
             }
 #pragma unroll
             for (int i = 0; i < EPI_SUB; ++i) {
@@ -958,6 +1109,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
             }
           }
+#ifdef CASC_I8_PROF
+          if (lane == 0 && ew == 1) g_i8prof[blockIdx.x][48] += clock64() - tp2;
+          if (lane == 0 && ew == 1) g_i8prof[blockIdx.x][49] += 1;
+#endif
         }
       }
     }

@@ -5,6 +5,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
+    "prof": ["CASC_I8_PROF"],
+    "prof8": ["CASC_I8_PROF", "CASC_I8_EPI_SUB=8"],
+    "sub8": ["CASC_I8_EPI_SUB=8"],
+    "prof_notma": ["CASC_I8_PROF", "CASC_I8_NOTMA"],
+    "prof_nomma": ["CASC_I8_PROF", "CASC_I8_NOTMA", "CASC_I8_NOMMA"],
+    "notma": ["CASC_I8_NOTMA", "CASC_I8_NOWAIT", "CASC_I8_NO_EPI"],
     "skb32": ["CASC_I8_SYNC_KB=32"],
     "skb16": ["CASC_I8_SYNC_KB=16"],
     "skb8": ["CASC_I8_SYNC_KB=8"],

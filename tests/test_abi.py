@@ -59,7 +59,7 @@ def test_library_is_sm100a_only(lib):
     # the product kernel (no debug export, no alpha/beta) and the split kernels
     # are spill-free
     funcs = re.split(r"\n\s*Function : ", sass)
-    main = [f for f in funcs if f.startswith("_ZN4casc16casc_gemm_kernelILb0ELb0E")]
+    main = [f for f in funcs if f.startswith("_ZN4casc16casc_gemm_kernelILb0ELb0ELb0E")]
     splits = [f for f in funcs if "split_a_kernel" in f[:60] or "split_b_kernel" in f[:60]]
     assert len(main) == 1 and len(splits) == 4
     for f in main + splits:

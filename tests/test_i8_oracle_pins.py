@@ -154,6 +154,54 @@ def test_i8_group_value_exact(orc):
         assert fr(h) + fr(l) == V and h == float(F(V))
 
 
+def _rn_pair_expected(bins, w0):
+    """T by exact rationals: hi = RN(x), lo = RN(x - hi) (Python's int / int is
+    correctly rounded, ties to even, subnormals included)."""
+    y = len(bins)
+    S = sum(int(b) << (8 * (y - 1 - s)) for s, b in enumerate(bins))
+    x = F(S) * F(2) ** w0
+    hi = float(x) if S else 0.0
+    r = x - F(hi)
+    lo = float(r) if r else 0.0
+    return hi, lo
+
+
+def _bits(v):
+    return np.float64(v).view(np.uint64)
+
+
+def test_i8_panel_value_exact_rounding(orc):
+    """Reading R25 (rev. 2): T.hi = RN(x), T.lo = RN(x - T.hi) for the exact panel
+    product x, against exact rationals: random bins, ties both ways, exact zeros,
+    cancelling bins and the subnormal range (bitwise, signed zeros included)."""
+    rng = random.Random(11)
+    cases = []
+    for _ in range(3000):
+        y = rng.randint(3, 15)
+        b = [rng.randint(-2**31 + 1, 2**31 - 1) for _ in range(y)]
+        for s in range(y):  # sparse / short / signed-mixed patterns
+            if rng.random() < 0.3:
+                b[s] = 0
+        cases.append((b, rng.randint(-300, 200)))
+    for _ in range(500):  # the subnormal range of hi and lo
+        y = rng.randint(3, 15)
+        b = [rng.randint(-2**31 + 1, 2**31 - 1) for _ in range(y)]
+        cases.append((b, rng.randint(-1250, -1000)))
+    for k in (3, 17, 40):  # ties: x = (q + 1/2) 2^k with q even and odd
+        for q in (2**53 - 2, 2**53 - 1, 2**52 + 1, 2**52 + 6):
+            S = (2 * q + 1) << (k - 1)
+            y = 15
+            digits = [(S >> (8 * (y - 1 - s))) & 0xff for s in range(y)]
+            assert sum(d << (8 * (y - 1 - s)) for s, d in enumerate(digits)) == S
+            cases += [(digits, 0), ([-d for d in digits], -7), (digits, -1074 - k - 20)]
+    cases += [([0] * 14, 0), ([1, -256] + [0] * 12, 5), ([0] * 13 + [1], -1080),
+              ([0] * 13 + [-1], -1080), ([0] * 13 + [-3], -1076)]
+    for b, w0 in cases:
+        h, l = orc.i8_panel_value(np.array(b), w0)
+        eh, el = _rn_pair_expected(b, w0)
+        assert _bits(h) == _bits(eh) and _bits(l) == _bits(el), (b, w0, h, l, eh, el)
+
+
 # ----------------------------------------------------------------- final C
 def _check_vs_exact(orc, d, C_hi, C_lo):
     m, n, k = d["m"], d["n"], d["k"]
