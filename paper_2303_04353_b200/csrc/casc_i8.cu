@@ -72,7 +72,13 @@ constexpr int KBP = KC8 / KB;      // k blocks per panel (64)
 constexpr int TR = 128;            // rows (A) / columns (B) per chunk = tile edge
 constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
-constexpr int NSA = 8, NSB = 8;    // smem ring slots (A: 16 KB, B: 8 KB half chunks)
+#ifndef CASC_I8_NSA
+#define CASC_I8_NSA 9
+#endif
+#ifndef CASC_I8_NSB
+#define CASC_I8_NSB 10
+#endif
+constexpr int NSA = CASC_I8_NSA, NSB = CASC_I8_NSB;  // smem ring slots (A: 16 KB, B: 8 KB halves)
 constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
 constexpr int NGMAX = (YMAX + NBIN - 1) / NBIN;  // groups per panel, at most
 constexpr int64_t WS_PER_CTA = (2 + NGMAX) * 128 * 128;  // doubles / int64 per CTA
@@ -887,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int q = 0; q < P; ++q) {
         const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
         for (int go = 0; go < ngroups; ++go) {
-          const int grp = ngroups - 1 - go;  // most significant group first (see MMA loop)
+          const int grp = ngroups - 1 - go;  // the MMA issuer's group order
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
           for (int64_t kb = kb0; kb < kb1; ++kb) {
             if (synced && (kb - kb0) % CASC_I8_SYNC_KB == 0) {
@@ -936,9 +942,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int tile = pair; tile < tiles; tile += npairs) {
         for (int q = 0; q < P; ++q) {
           const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
-          // groups in decreasing order: the short least-significant group ends
-          // the panel, so the epilogue's once-per-panel phase 2 overlaps the
-          // longest group's MMAs instead of delaying the drain of the shortest
+          // groups in reverse order (bins y-4 .. y-1 first): the short group
+          // 0 .. r-1 (most significant, fewest products) ends the panel, so the
+          // epilogue's once-per-panel phase 2 overlaps the longest group's MMAs
+          // instead of delaying the drain of the shortest one
           for (int go = 0; go < ngroups; ++go, ++gcount) {
             const int grp = ngroups - 1 - go;
             const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;

@@ -6,8 +6,13 @@ VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
     "prof": ["CASC_I8_PROF"],
-    "prof8": ["CASC_I8_PROF", "CASC_I8_EPI_SUB=8"],
+    "a10b8": ["CASC_I8_NSA=10"],
+    "a9b10": ["CASC_I8_NSA=9", "CASC_I8_NSB=10"],
+    "a8b12": ["CASC_I8_NSB=12"],
+    "a7b14": ["CASC_I8_NSA=7", "CASC_I8_NSB=14"],
+    "a8b11": ["CASC_I8_NSB=11"],
     "sub8": ["CASC_I8_EPI_SUB=8"],
+    "prof8": ["CASC_I8_PROF", "CASC_I8_EPI_SUB=8"],
     "prof_notma": ["CASC_I8_PROF", "CASC_I8_NOTMA"],
     "prof_nomma": ["CASC_I8_PROF", "CASC_I8_NOTMA", "CASC_I8_NOMMA"],
     "notma": ["CASC_I8_NOTMA", "CASC_I8_NOWAIT", "CASC_I8_NO_EPI"],
