@@ -134,23 +134,24 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        # one casc_i8_gemm_fp64x2_host call per step (blocks of C streamed: the
+        # copies of A and C overlap the GEMMs of other slabs)
+        import paper_2303_04353_b200 as casc
+        call = lambda: casc.casc_i8_gemm_fp64x2_host(hA_hi, hA_lo, hB_hi, hB_lo, y=y,
+                                                     C_hi=oC_hi, C_lo=oC_lo, flags=oF,
+                                                     sync=False)
+        call()  # warm-up: the stream-ordered pool reserves its buffers
+        barrier()
         e0.record()
         for _ in range(e2e_steps):
-            A_hi.copy_(hA_hi, non_blocking=True)
-            A_lo.copy_(hA_lo, non_blocking=True)
-            B_hi.copy_(hB_hi, non_blocking=True)
-            B_lo.copy_(hB_lo, non_blocking=True)
-            step()
-            oC_hi.copy_(C_hi, non_blocking=True)
-            oC_lo.copy_(C_lo, non_blocking=True)
-            oF.copy_(fl, non_blocking=True)
+            call()
         e1.record()
         barrier()
         te = e0.elapsed_time(e1) / e2e_steps
         e2e = {"value": 2.0 * m * n * k / (te * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 16 * (mloc * k + k * B_hi.shape[1]),
                "d2h_bytes_per_step": 17 * mloc * n, "ms_per_step": te, "steps": e2e_steps,
-               "api": "paper_2303_04353_b200 C ABI (casc_i8_pack x2 / casc_i8_gemm_packed)"}
+               "api": "paper_2303_04353_b200 C ABI casc_i8_gemm_fp64x2_host (blocks streamed)"}
     prods = y * (y + 1) // 2
     ops = 2.0 * prods * mloc * n * k
     peak_sus, peak_burst, src = load_int8_peak()
@@ -449,8 +450,20 @@ def main():
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        if world == 1:  # the host-operand entry point: copies overlap the kernels
+            import paper_2303_04353_b200 as casc
+            api = "paper_2303_04353_b200 C ABI casc_gemm_fp64x2_host (blocks streamed)"
+            call = lambda: casc.casc_gemm_fp64x2_host(hA_hi, hA_lo, hB_hi, hB_lo, C_hi=oC_hi,
+                                                      C_lo=oC_lo, flags=oF, stream=stream,
+                                                      sync=False)
+            call()  # warm-up: the stream-ordered pool reserves its buffers
+            barrier()
         e0.record(stream)
         for _ in range(e2e_steps):
+            if world == 1:
+                call()
+                continue
+            api = "paper_2303_04353_b200 C ABI (casc_pack_a/casc_pack_b/casc_gemm_packed)"
             A_hi.copy_(hA_hi, non_blocking=True)
             A_lo.copy_(hA_lo, non_blocking=True)
             B_hi.copy_(hB_hi, non_blocking=True)
@@ -468,8 +481,7 @@ def main():
         d2h = 17 * mloc * n
         e2e = {"value": 2.0 * m * n * k / (te.item() * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": te.item(), "steps": e2e_steps,
-               "api": "paper_2303_04353_b200 C ABI (casc_pack_a/casc_pack_b/casc_gemm_packed)"}
+               "ms_per_step": te.item(), "steps": e2e_steps, "api": api}
 
     # ---- roofline of the dominant kernel (fused GEMM): algorithmic 20 m n k flops
     peak_sus, peak_burst, peak_src = load_fp64_peak()

@@ -99,6 +99,32 @@ int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
  * casc_packed_a_bytes(m, k) + casc_packed_b_bytes(k, n). */
 size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k);
 
+/* casc_gemm_fp64x2 with HOST-resident operands (BASELINE north star's call,
+ * operands in host memory): A_hi/A_lo, B_hi/B_lo, C_hi/C_lo (row-major, lda /
+ * ldb / ldc in elements) and flags (m x n, ld = n, nullable) are host
+ * pointers; page-locked memory (cudaHostAlloc / cudaHostRegister) lets the
+ * copies overlap the kernels, pageable memory works but serialises them.
+ * Result: bitwise the casc_gemm_fp64x2 result of the same operands.
+ * Pipeline over blocks of C = row slabs of A (slab_rows rows) x column slabs
+ * of B (slab_cols columns; each 0 = 4096, rounded up to a multiple of 64), row slab
+ * outer: an internal H2D stream copies A_0, then the column slabs of B, then
+ * the next row slabs of A ahead of their use; the caller's stream splits each
+ * slab once and multiplies block after block; an internal D2H stream returns
+ * each block of C (and flags) as soon as it is done.  So only the first A and
+ * B slabs and the last C block are exposed.  Device memory (two staging slots
+ * for A, B and C blocks, the packed B, one packed A slab) comes from the
+ * device's stream-ordered pool and is returned at the end.  Stream-ordered:
+ * the call returns once everything is enqueued; the host buffers must stay
+ * valid and untouched until `stream` completes.  k == 0 synchronises `stream`
+ * and zeroes C and flags on the host.  Errors as casc_gemm_fp64x2
+ * (CASC_ERR_INVALID also for slab_rows or slab_cols < 0). */
+int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k,
+                          const double* A_hi, const double* A_lo, int64_t lda,
+                          const double* B_hi, const double* B_lo, int64_t ldb,
+                          double* C_hi, double* C_lo, int64_t ldc,
+                          uint8_t* flags, int64_t slab_rows, int64_t slab_cols,
+                          casc_stream_t stream);
+
 /* Same as casc_gemm_fp64x2 with a caller-owned device workspace of at least
  * casc_workspace_bytes(m, n, k) bytes (256-byte aligned).  No allocation, no
  * host synchronisation, re-entrant. */
@@ -284,6 +310,17 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                            double* C_hi, double* C_lo, int64_t ldc,
                            uint8_t* flags, int y, void* workspace, size_t workspace_bytes,
                            casc_stream_t stream);
+
+/* casc_gemm_fp64x2_host for the INT8 cascade: host-resident operands streamed
+ * in blocks (slab_rows, slab_cols: 0 = 4096, rounded up to multiples of 256), bitwise
+ * the casc_i8_gemm_fp64x2 result; memory, ordering and errors as
+ * casc_gemm_fp64x2_host (CASC_ERR_INVALID also for y outside [3, 15]). */
+int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k,
+                             const double* A_hi, const double* A_lo, int64_t lda,
+                             const double* B_hi, const double* B_lo, int64_t ldb,
+                             double* C_hi, double* C_lo, int64_t ldc,
+                             uint8_t* flags, int y, int64_t slab_rows, int64_t slab_cols,
+                             casc_stream_t stream);
 
 /* NEXT-4 on the INT8 cascade: C := alpha (x) op(A) op(B) (+) beta (x) C with the
  * semantics, argument layout and errors of casc_gemm_fp64x2_ex (reading R21),

@@ -71,7 +71,8 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_gemm_fp64x2", "casc_i8_gemm_fp64x2_ws", "casc_i8_workspace_bytes",
             "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
-            "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex"]
+            "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
+            "casc_i8_gemm_fp64x2_host"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -176,8 +177,17 @@ def _mat(t, name):
     return max(t.stride(0), 1) if t.size(0) > 1 else max(t.size(1), 1)
 
 
-def _ld_pair(hi, lo, name):
-    ldh, ldl = _mat(hi, name + "_hi"), _mat(lo, name + "_lo")
+def _hmat(t, name):
+    if t.dtype != torch.float64 or t.is_cuda or t.dim() != 2:
+        raise TypeError(f"{name} must be a 2-D float64 CPU (host) tensor")
+    if t.size(1) > 1 and t.stride(1) != 1:
+        raise TypeError(f"{name} must be row-major (unit column stride)")
+    return max(t.stride(0), 1) if t.size(0) > 1 else max(t.size(1), 1)
+
+
+def _ld_pair(hi, lo, name, host=False):
+    ldh = (_hmat if host else _mat)(hi, name + "_hi")
+    ldl = (_hmat if host else _mat)(lo, name + "_lo")
     if hi.shape != lo.shape or ldh != ldl:
         raise TypeError(f"{name}_hi and {name}_lo must have the same shape and layout")
     return ldh
@@ -215,6 +225,67 @@ def _outputs(m, n, device, C_hi, C_lo, flags, want_flags):
     if flags is not None and (flags.dtype != torch.uint8 or not flags.is_contiguous()
                               or tuple(flags.shape) != (m, n)):
         raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
+    return C_hi, C_lo, flags
+
+
+_sig("casc_gemm_fp64x2_host", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
+                               _vp, _i64, _i64, _vp])
+
+
+_sig("casc_i8_gemm_fp64x2_host", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                                  _i64, _vp, ctypes.c_int, _i64, _i64, _vp])
+
+
+def casc_gemm_fp64x2_host(A_hi, A_lo, B_hi, B_lo, C_hi=None, C_lo=None, flags=None,
+                          want_flags=True, slab_rows: int = 0, slab_cols: int = 0, stream=None,
+                          sync: bool = True):
+    """C := A B with HOST (CPU) tensors, streamed through the GPU in row slabs
+    (casc.h: casc_gemm_fp64x2_host; bitwise the device-resident result).
+    Pinned tensors (`.pin_memory()`) let the copies overlap the kernels.
+    Outputs are pinned CPU tensors unless given.  sync=False returns right after
+    enqueueing (the tensors must stay alive until `stream` completes)."""
+    return _host_call(None, A_hi, A_lo, B_hi, B_lo, C_hi, C_lo, flags, want_flags, slab_rows,
+                      slab_cols, stream, sync)
+
+
+def casc_i8_gemm_fp64x2_host(A_hi, A_lo, B_hi, B_lo, y: int = 14, C_hi=None, C_lo=None,
+                             flags=None, want_flags=True, slab_rows: int = 0, slab_cols: int = 0,
+                             stream=None, sync: bool = True):
+    """casc_gemm_fp64x2_host on the INT8 cascade (NEXT-3; casc_i8_gemm_fp64x2_host)."""
+    return _host_call(int(y), A_hi, A_lo, B_hi, B_lo, C_hi, C_lo, flags, want_flags, slab_rows,
+                      slab_cols, stream, sync)
+
+
+def _host_call(y, A_hi, A_lo, B_hi, B_lo, C_hi, C_lo, flags, want_flags, slab_rows, slab_cols,
+               stream, sync):
+    lda = _ld_pair(A_hi, A_lo, "A", host=True)
+    ldb = _ld_pair(B_hi, B_lo, "B", host=True)
+    m, k = A_hi.shape
+    k2, n = B_hi.shape
+    if k != k2:
+        raise ValueError("inner dimensions differ")
+    pin = lambda t: t.pin_memory() if torch.cuda.is_available() else t
+    if C_hi is None:
+        C_hi = pin(torch.empty((m, n), dtype=torch.float64))
+    if C_lo is None:
+        C_lo = pin(torch.empty((m, n), dtype=torch.float64))
+    if flags is None and want_flags:
+        flags = pin(torch.empty((m, n), dtype=torch.uint8))
+    if flags is not None and (flags.dtype != torch.uint8 or flags.is_cuda
+                              or not flags.is_contiguous() or tuple(flags.shape) != (m, n)):
+        raise TypeError("flags must be a contiguous (m, n) uint8 CPU tensor")
+    ldc = _ld_pair(C_hi, C_lo, "C", host=True)
+    head = (m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo), ldb, _ptr(C_hi),
+            _ptr(C_lo), ldc, _ptr(flags))
+    if y is None:
+        _check(_lib.casc_gemm_fp64x2_host(*head, int(slab_rows), int(slab_cols),
+                                          _stream(stream)), "casc_gemm_fp64x2_host")
+    else:
+        _check(_lib.casc_i8_gemm_fp64x2_host(*head, y, int(slab_rows), int(slab_cols),
+                                             _stream(stream)),
+               "casc_i8_gemm_fp64x2_host")
+    if sync:
+        (stream or torch.cuda.current_stream()).synchronize()
     return C_hi, C_lo, flags
 
 

@@ -4,10 +4,13 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "../../include/casc.h"
+#include "casc_host.cuh"
 #include "casc_layout.cuh"
 
 namespace casc {
@@ -376,6 +379,55 @@ int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k, const double* A_hi, const 
   }
   return casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
                              ws, need, stream);
+}
+
+// Host-resident operands (casc.h), the row-slab pipeline of casc_host.cuh.
+int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
+                          int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                          double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                          int64_t slab_rows, int64_t slab_cols, casc_stream_t stream) {
+  g_launches = 0;
+  int r = validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (slab_rows < 0 || slab_cols < 0) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  const cudaStream_t st = S(stream);
+  if (k == 0) return casc::hostpipe::zero_host_c(m, n, C_hi, C_lo, ldc, flags, st);
+  auto fit = [](int64_t v, int64_t blk, int64_t lim) {  // block multiple, at most lim rounded
+    v = (v + blk - 1) / blk * blk;
+    const int64_t l = (lim + blk - 1) / blk * blk;
+    return v < l ? v : l;
+  };
+  const int64_t sr = fit(slab_rows ? slab_rows : 4096, casc::TM, m);
+  const int64_t sc = fit(slab_cols ? slab_cols : 4096, casc::TN, n);
+  const casc::Widths w = widths_for(k);
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  int launches = 0;
+  auto pack_b = [&](const double* bh, const double* bl, int64_t cols, void* pb) {
+    const cudaError_t e = casc::launch_split_b(bh, bl, cols, k, cols, w, pb, st);
+    launches += e == cudaSuccess;
+    return cuda_status(e);
+  };
+  auto pack_a = [&](const double* ah, const double* al, int64_t rows, void* pa) {
+    const cudaError_t e = casc::launch_split_a(ah, al, k, rows, k, w, pa, st);
+    launches += e == cudaSuccess;
+    return cuda_status(e);
+  };
+  auto gemm = [&](int64_t rows, int64_t cols, const void* pa, const void* pb, double* ch,
+                  double* cl, uint8_t* fl) {
+    g_launches = 0;
+    const int rr =
+        gemm_packed_impl(rows, cols, k, pa, pb, ch, cl, cols, fl, sms, st, 0, nst, nullptr);
+    launches += g_launches;
+    return rr;
+  };
+  r = casc::hostpipe::run(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags, sr,
+                          sc, casc_packed_b_bytes(k, sc), casc_packed_a_bytes(sr, k), st, pack_b,
+                          pack_a, gemm);
+  g_launches = r == CASC_OK ? launches : 0;
+  return r;
 }
 
 int casc_finalize(void) {

@@ -58,6 +58,7 @@
 
 #include "../../include/casc.h"
 #include "casc_dd.cuh"
+#include "casc_host.cuh"
 #include "casc_ptx.cuh"
 
 // DBG instantiation: the combine below its early `continue` is unreachable by design
@@ -1363,6 +1364,60 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
                  0, st);
   if (e == cudaSuccess) host::set_launches(7);
   return st8(e);
+}
+
+// Host-resident operands (casc.h), the row-slab pipeline of casc_host.cuh; slab
+// starts are multiples of 256 rows (a CTA pair's tile).
+int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi,
+                             const double* A_lo, int64_t lda, const double* B_hi,
+                             const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                             int64_t ldc, uint8_t* flags, int y, int64_t slab_rows,
+                             int64_t slab_cols, casc_stream_t stream) {
+  host::set_launches(0);
+  int r = host::validate_gemm(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags);
+  if (r) return r;
+  if (y < i8::YMIN || y > i8::YMAX || slab_rows < 0 || slab_cols < 0) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  if (k == 0) return casc::hostpipe::zero_host_c(m, n, C_hi, C_lo, ldc, flags, st);
+  const int64_t blk = 2 * i8::TR;  // a CTA pair's rows; B slabs: two packed blocks
+  auto fit = [&](int64_t v, int64_t lim) {
+    v = (v + blk - 1) / blk * blk;
+    const int64_t l = (lim + blk - 1) / blk * blk;
+    return v < l ? v : l;
+  };
+  const int64_t sr = fit(slab_rows ? slab_rows : 4096, m);
+  const int64_t sc = fit(slab_cols ? slab_cols : 4096, n);
+  const int gmax = i8::grid_for(sr, sc, sms);
+  double* gws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&gws), i8::cta_ws_bytes(gmax), st) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  int launches = 0;
+  auto pack_b = [&](const double* bh, const double* bl, int64_t cols, void* pb) {
+    const cudaError_t e = i8::pack(bh, bl, cols, cols, k, y, true, pb, st);
+    launches += e == cudaSuccess ? 3 : 0;
+    return st8(e);
+  };
+  auto pack_a = [&](const double* ah, const double* al, int64_t rows, void* pa) {
+    const cudaError_t e = i8::pack(ah, al, k, rows, k, y, false, pa, st);
+    launches += e == cudaSuccess ? 3 : 0;
+    return st8(e);
+  };
+  auto gemm = [&](int64_t rows, int64_t cols, const void* pa, const void* pb, double* ch,
+                  double* cl, uint8_t* fl) {
+    const cudaError_t e = i8::gemm(pa, pb, rows, cols, k, y, ch, cl, cols, fl, gws,
+                                   i8::grid_for(rows, cols, sms), nullptr, 0, st);
+    launches += e == cudaSuccess;
+    return st8(e);
+  };
+  r = casc::hostpipe::run(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags, sr,
+                          sc, casc_i8_packed_bytes(sc, k, y), casc_i8_packed_bytes(sr, k, y), st,
+                          pack_b, pack_a, gemm);
+  cudaFreeAsync(gws, st);
+  host::set_launches(r == CASC_OK ? launches : 0);
+  return r;
 }
 
 int casc_i8_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,

@@ -268,19 +268,24 @@ def test_i8_skinny_and_panel_edges(casc, orc, m, n, k):
     assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
 
 
-def test_i8_extreme_exponents(casc, orc):
-    """Rows of A scaled by 2^-700 and columns of B by 2^-300 (the products sit
-    near 2^-1000, the FP64x2 tails are subnormal; the 2^w scaling takes the
-    two-step path): still bit-exact with the oracle's ldexp."""
-    d = I.make_config(1, m=90, n=70, k=500, seed=31)
+@pytest.mark.parametrize("sa,sb,k", [(-700, -300, 500), (-760, -300, 500),
+                                      (-775, -300, 8192 + 40), (-850, -300, 500)])
+def test_i8_extreme_exponents(casc, orc, sa, sb, k):
+    """Rows of A scaled by 2^sa and columns of B by 2^sb: products near 2^-1000
+    (subnormal FP64x2 tails), near 2^-1060 (T.hi itself subnormal), around
+    2^-1075 (partial underflow, two panels) and below 2^-1140 (everything rounds
+    to signed zeros): bit-exact with the oracle (R25 rev. 2 rounding on the
+    subnormal grid, signs of zero included)."""
+    d = I.make_config(1, m=90, n=70, k=k, seed=31)
     for x in ("A_hi", "A_lo"):
-        d[x] = np.ldexp(d[x], -700)
+        d[x] = np.ldexp(d[x], sa)
     for x in ("B_hi", "B_lo"):
-        d[x] = np.ldexp(d[x], -300)
+        d[x] = np.ldexp(d[x], sb)
     C_hi, C_lo, fl = gpu_gemm(casc, d)
     o_hi, o_lo, ofl = orc.i8_casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], 14)
     assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, ofl)
-    assert np.all(np.abs(C_hi) < 2.0**-990) and np.any(C_hi != 0)
+    if sa + sb > -1100:
+        assert np.all(np.abs(C_hi) < 2.0**(sa + sb + 20)) and np.any(C_hi != 0)
 
 
 # ------------------------------------------------------------------ BLAS-style (NEXT-4)
@@ -342,3 +347,22 @@ def test_i8_blas_ex_degenerate(casc, orc):
     with pytest.raises(casc.CascError):
         casc.casc_i8_gemm_fp64x2_ex("N", "N", 1.0, T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
                                     T(d["B_lo"]), 0.0, T(C0), T(C0), y=2)
+
+
+# ------------------------------------------------------------------ host operands
+@pytest.mark.parametrize("m,n,k,slab,scol,y", [(700, 300, 900, 256, 256, 14),
+                                               (300, 257, 8192 + 100, 0, 0, 14),
+                                               (513, 700, 640, 256, 256, 9)])
+def test_i8_host_operands_bitwise(casc, m, n, k, slab, scol, y):
+    """casc_i8_gemm_fp64x2_host (blocks of 256-multiple row and column slabs
+    streamed from pinned host memory): bitwise the device-resident
+    casc_i8_gemm_fp64x2 result."""
+    import torch
+    d = I.make_config(2, m=m, n=n, k=k, seed=61)
+    ref = gpu_gemm(casc, d, y=y)
+    P = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    C_hi, C_lo, fl = casc.casc_i8_gemm_fp64x2_host(P(d["A_hi"]), P(d["A_lo"]), P(d["B_hi"]),
+                                                   P(d["B_lo"]), y=y, slab_rows=slab,
+                                                   slab_cols=scol)
+    assert bitwise(C_hi.numpy(), ref[0]) and bitwise(C_lo.numpy(), ref[1])
+    assert np.array_equal(fl.numpy(), ref[2])
