@@ -234,6 +234,29 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
                         uint8_t* flags, void* workspace, size_t workspace_bytes,
                         casc_stream_t stream);
 
+/* NEXT-4, level-3 BLAS on the cascaded GEMM ("All Level-3 BLAS
+ * algorithms can be written in terms of GEMM"): symmetric rank-k update
+ *   C := alpha (x) op(A) op(A)^T (+) beta (x) C   on one triangle of C,
+ * op(A) = A (trans = CASC_OP_N, A stored n x k, lda >= max(1,k)) or A^T
+ * (CASC_OP_T, A stored k x n, lda >= max(1,n)); uplo = CASC_LOWER / CASC_UPPER
+ * selects the triangle (diagonal included) that is read (beta != 0) and
+ * written; the other triangle of C_hi / C_lo and of flags is not touched.
+ * The product is the cascaded GEMM of op(A) and op(A)^T: op(A) is split as the
+ * A and as the B operand and the fused kernel runs only the triangle's 64 x 64 tiles
+ * (half the work of the GEMM); every stored element is bitwise what
+ * casc_gemm_fp64x2_ex(trans, !trans, ..., A, A, ...) stores there.  alpha,
+ * beta, the update sequence (reading R21), k == 0 / alpha == 0, workspace
+ * (>= casc_workspace_bytes(n, n, k) or NULL), flags (n x n, ld = n) and
+ * errors as casc_gemm_fp64x2_ex. */
+typedef enum { CASC_LOWER = 0, CASC_UPPER = 1 } casc_uplo;
+int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
+                     double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda,
+                     double beta_hi, double beta_lo,
+                     double* C_hi, double* C_lo, int64_t ldc,
+                     uint8_t* flags, void* workspace, size_t workspace_bytes,
+                     casc_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* The paper's simple path (§4.2): phases as separate kernels.  */
 /* ------------------------------------------------------------------------ */

@@ -80,6 +80,8 @@ def _setup(L):
     L.orc_casc_gemm_ex.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, _d, _d, _pd,
                                    _pd, _i64, _pd, _pd, _i64, _d, _d, _pd, _pd, _i64, _pu8,
                                    ctypes.c_int]
+    L.orc_casc_syrk.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
+                                _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
     L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
                               _i64, ctypes.c_int]
     L.orc_exact_entries.argtypes = [_i64, _pd, _pd, _i64, _pd, _pd, _i64, _i64, _pi64, _pi64,
@@ -247,6 +249,24 @@ def casc_gemm_ex(transa, transb, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo
                            A_hi.shape[1] if A_hi.size else 1, _p(B_hi), _p(B_lo),
                            B_hi.shape[1] if B_hi.size else 1, beta[0], beta[1], _p(C_hi),
                            _p(C_lo), n, _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags
+
+
+def casc_syrk(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, nthreads: int = 0):
+    """NEXT-4 SYRK: the lower ('L') / upper ('U') triangle of
+    casc_gemm_ex(trans, not trans, alpha, A, A, beta, C); the other triangle
+    of C and flags is returned unchanged.  A is the STORED matrix (n x k for
+    trans 'N', k x n for 'T').  Returns new (C_hi, C_lo, flags)."""
+    lo = 0 if uplo in ("L", "l", 0) else 1
+    tr = int(trans in ("T", "t", 1, True))
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    C_hi, C_lo = _c64(C_hi).copy(), _c64(C_lo).copy()
+    n = C_hi.shape[0]
+    k = A_hi.shape[0] if tr else A_hi.shape[1]
+    flags = np.zeros((n, n), dtype=np.uint8) if flags is None else np.array(flags, np.uint8)
+    lib().orc_casc_syrk(lo, tr, n, k, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                        A_hi.shape[1] if A_hi.size else 1, beta[0], beta[1], _p(C_hi), _p(C_lo),
+                        n, _p(flags, _pu8), nthreads)
     return C_hi, C_lo, flags
 
 

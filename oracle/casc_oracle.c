@@ -613,3 +613,34 @@ int orc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* NEXT-4, level-3 BLAS on the cascaded GEMM ("All Level-3 BLAS
+ * algorithms can be written in terms of GEMM"): SYRK, C := alpha (x) op(A)
+ * op(A)^T (+) beta (x) C on the lower (uplo 0) or upper (uplo 1) triangle,
+ * diagonal included, by definition the triangle of orc_casc_gemm_ex with
+ * B = A read the other way round; the other triangle of C and flags (n x n,
+ * nullable) is left as it is.  A stored n x k (trans 0) or k x n (trans 1). */
+void orc_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, double al,
+                   const double* Ahi, const double* Alo, int64_t lda, double bh, double bl,
+                   double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int nthreads) {
+  double* Th = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  double* Tl = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  uint8_t* Tf = (uint8_t*)calloc((size_t)(n * n + 1), 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Th[i * n + j] = Chi[i * ldc + j];
+      Tl[i * n + j] = Clo[i * ldc + j];
+    }
+  orc_casc_gemm_ex(trans, !trans, n, n, k, ah, al, Ahi, Alo, lda, Ahi, Alo, lda, bh, bl, Th, Tl, n,
+                   Tf, nthreads);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      if (uplo == 0 ? j > i : j < i) continue;
+      Chi[i * ldc + j] = Th[i * n + j];
+      Clo[i * ldc + j] = Tl[i * n + j];
+      if (flags) flags[i * n + j] = Tf[i * n + j];
+    }
+  free(Th);
+  free(Tl);
+  free(Tf);
+}

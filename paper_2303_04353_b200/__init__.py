@@ -72,7 +72,7 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
-            "casc_i8_gemm_fp64x2_host"]
+            "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -96,6 +96,39 @@ _sig("casc_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctype
                              ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
                              ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _sz, _vp])
 CASC_OP_N, CASC_OP_T = 0, 1
+CASC_LOWER, CASC_UPPER = 0, 1
+_sig("casc_syrk_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double, ctypes.c_double,
+                          _vp, _vp, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp, _i64, _vp,
+                          _vp, _sz, _vp])
+
+
+def casc_syrk_fp64x2(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None,
+                     workspace=None, stream=None):
+    """SYRK on the cascaded GEMM (NEXT-4, casc.h): C := alpha op(A) op(A)^T +
+    beta C on the lower ('L') or upper ('U') triangle of the n x n C_hi / C_lo
+    (updated in place, the other triangle untouched).  A is the stored matrix:
+    n x k for trans 'N', k x n for 'T'; A_hi None means k = 0."""
+    lo = CASC_LOWER if uplo in ("L", "l", 0) else CASC_UPPER
+    if uplo not in ("L", "l", "U", "u", 0, 1):
+        raise ValueError("uplo must be 'L' or 'U'")
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
+    bh, bl = (beta, 0.0) if isinstance(beta, (int, float)) else beta
+    n = C_hi.shape[0]
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    if A_hi is None:
+        lda, k = 1, 0
+    else:
+        lda = _ld_pair(A_hi, A_lo, "A")
+        k = A_hi.shape[0] if tr else A_hi.shape[1]
+    if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (n, n)):
+        raise TypeError("flags must be a contiguous (n, n) uint8 CUDA tensor")
+    _check(_lib.casc_syrk_fp64x2(lo, tr, n, k, float(ah), float(al), _ptr(A_hi), _ptr(A_lo), lda,
+                                 float(bh), float(bl), _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
+                                 _ptr(workspace),
+                                 0 if workspace is None else workspace.numel(), _stream(stream)),
+           "casc_syrk_fp64x2")
+    return C_hi, C_lo, flags
 
 
 _sig("casc_i8_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctypes.c_double,

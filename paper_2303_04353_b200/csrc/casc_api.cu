@@ -18,6 +18,9 @@ cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
                                 const double* t_lo, const uint8_t* fbuf, double* C_hi,
                                 double* C_lo, int64_t ldc, uint8_t* flags, int ab, double ah,
                                 double al, double bh, double bl, int num_sms, cudaStream_t st);
+cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
+                                double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                                int num_sms, int uplo, cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -141,7 +144,7 @@ int current_sms() {
 int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb,
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
-                     const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr) {
+                     const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -169,8 +172,9 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.flags = flags;
   a.dbg = dbg;
   a.un_b2 = std::ldexp(1.0, w.c1 - w.c0);
+  a.tri = tri;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
-  const int P = (!dbg && st_begin == 0 && st_end == nst) ? split_plan(m, n, k, sms) : 0;
+  const int P = (!dbg && !tri && st_begin == 0 && st_end == nst) ? split_plan(m, n, k, sms) : 0;
   if (!P) {
     cudaError_t e = casc::launch_gemm(a, sms, st);
     if (e == cudaSuccess) ++g_launches;
@@ -588,6 +592,79 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
   g_launches = 0;
   r = (e == cudaSuccess) ? gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
                                             nst, nullptr, abv, ps)
+                         : CASC_ERR_CUDA;
+  if (owned) cudaFreeAsync(ws, st);
+  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------- SYRK (NEXT-4)
+// C := alpha op(A) op(A)^T + beta C on one triangle (level-3 BLAS
+// on the cascaded GEMM).  op(A) is split once as the A operand and, read
+// transposed, as the B operand; the fused kernel runs only the triangle's
+// tiles (half the work) and stores only the triangle's elements.
+int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda, double beta_hi,
+                     double beta_lo, double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                     void* workspace, size_t workspace_bytes, casc_stream_t stream) {
+  g_launches = 0;
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (trans != CASC_OP_N && trans != CASC_OP_T))
+    return CASC_ERR_INVALID;
+  if (n < 0 || k < 0) return CASC_ERR_INVALID;
+  const int64_t ar = trans ? k : n, ac = trans ? n : k;  // A as stored
+  const bool no_product = (k == 0) || (alpha_hi == 0.0 && alpha_lo == 0.0);
+  int r;
+  if (!no_product && ((r = check_mat(A_hi, ar, ac, lda)) || (r = check_mat(A_lo, ar, ac, lda))))
+    return r;
+  if ((r = check_mat(C_hi, n, n, ldc)) || (r = check_mat(C_lo, n, n, ldc))) return r;
+  if (!no_product) {
+    const size_t ea = extent(ar, ac, lda), ec = extent(n, n, ldc);
+    const void* ins[2] = {A_hi, A_lo};
+    void* outs[3] = {C_hi, C_lo, flags};
+    const size_t oute[3] = {ec, ec, flags ? (size_t)(n * n) : 0};
+    for (int o = 0; o < 3; ++o)
+      for (int i = 0; i < 2; ++i)
+        if (ranges_overlap(outs[o], oute[o], ins[i], ea)) return CASC_ERR_INVALID;
+  }
+  if (n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  cudaStream_t st = S(stream);
+  const bool use_beta = !(beta_hi == 0.0 && beta_lo == 0.0);
+  if (no_product) {  // C := beta C on the triangle
+    cudaError_t e = casc::launch_scale_c_uplo(n, n, beta_hi, beta_lo, use_beta, C_hi, C_lo, ldc,
+                                              flags, sms, uplo == CASC_LOWER ? 0 : 1, st);
+    if (e == cudaSuccess) g_launches = 1;
+    return cuda_status(e);
+  }
+  const size_t need = casc_workspace_bytes(n, n, k);
+  void* ws = workspace;
+  bool owned = false;
+  if (!ws) {
+    if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+    owned = true;
+  } else if (workspace_bytes < need) {
+    return CASC_ERR_INVALID;
+  }
+  uint8_t* pa = static_cast<uint8_t*>(ws);
+  uint8_t* pb = pa + (casc_packed_a_bytes(n, k) + 255) / 256 * 256;
+  const casc::Widths w = widths_for(k);
+  // op(A) (n x k) as the A operand; op(A)^T (k x n) as the B operand: stored as A
+  // itself, read transposed when trans == N
+  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, n, k, w, pa, st, trans == CASC_OP_T);
+  if (e == cudaSuccess)
+    e = casc::launch_split_b(A_hi, A_lo, lda, k, n, w, pb, st, trans == CASC_OP_N);
+  AlphaBeta abv;
+  abv.ab = use_beta ? 2 : ((alpha_hi == 1.0 && alpha_lo == 0.0) ? 0 : 1);  // as casc_gemm_fp64x2_ex
+  abv.ah = alpha_hi;
+  abv.al = alpha_lo;
+  abv.bh = beta_hi;
+  abv.bl = beta_lo;
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  g_launches = 0;
+  r = (e == cudaSuccess) ? gemm_packed_impl(n, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
+                                            nst, nullptr, abv, nullptr,
+                                            uplo == CASC_LOWER ? 1 : 2)
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 2 : 0;

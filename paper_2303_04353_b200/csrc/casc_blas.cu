@@ -10,14 +10,16 @@
 
 namespace casc {
 
+// uplo: -1 every element; 0 / 1 only the lower / upper triangle (SYRK)
 __global__ void __launch_bounds__(256) scale_c_kernel(int64_t m, int64_t n, double bh, double bl,
                                                       int use_beta, double* __restrict__ C_hi,
                                                       double* __restrict__ C_lo, int64_t ldc,
-                                                      uint8_t* __restrict__ flags) {
+                                                      uint8_t* __restrict__ flags, int uplo) {
   const int64_t mn = m * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / n, j = idx - (idx / n) * n;
+    if ((uplo == 0 && j > i) || (uplo == 1 && j < i)) continue;
     double* ch = C_hi + i * ldc + j;
     double* cl = C_lo + i * ldc + j;
     if (use_beta) {
@@ -75,15 +77,22 @@ cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
   return cudaGetLastError();
 }
 
-cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
-                           double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
-                           cudaStream_t st) {
+cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
+                                double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                                int num_sms, int uplo, cudaStream_t st) {
   const int64_t mn = m * n;
   if (mn == 0) return cudaSuccess;
   int64_t blocks = (mn + 255) / 256;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-  scale_c_kernel<<<(unsigned)blocks, 256, 0, st>>>(m, n, bh, bl, use_beta, C_hi, C_lo, ldc, flags);
+  scale_c_kernel<<<(unsigned)blocks, 256, 0, st>>>(m, n, bh, bl, use_beta, C_hi, C_lo, ldc, flags,
+                                                   uplo);
   return cudaGetLastError();
+}
+
+cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
+                           double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
+                           cudaStream_t st) {
+  return launch_scale_c_uplo(m, n, bh, bl, use_beta, C_hi, C_lo, ldc, flags, num_sms, -1, st);
 }
 
 }  // namespace casc

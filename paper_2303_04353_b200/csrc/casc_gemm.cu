@@ -75,9 +75,25 @@ __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, 
 // item per (tile, panel); its FP64x2 panel sum T_q goes to t_hi/t_lo[q] and a
 // reduce kernel adds T_0 (+) T_1 (+) ... in panel order (bitwise the same
 // sequence as the normal mode's C accumulation).
+// SYRK: tile t of the row-major lower triangle -> (mb, nb), nb <= mb; the
+// upper triangle is its transpose
+__device__ __forceinline__ void tri_coords(int t, int tri, int& mb, int& nb) {
+  int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  while (r * (r + 1) / 2 > t) --r;
+  const int c = t - r * (r + 1) / 2;
+  mb = tri == 2 ? c : r;
+  nb = tri == 2 ? r : c;
+}
+template <bool TRI>
 __device__ __forceinline__ void item_coords(const GemmArgs& p, int split_p, int item, int& mb,
                                             int& nb, int& s0, int& s1, int& q0) {
-  if (split_p) {
+  if (TRI) {
+    tri_coords(item, p.tri, mb, nb);
+    s0 = p.st_begin;
+    s1 = p.st_end;
+    q0 = 0;
+  } else if (split_p) {
     const int tile = item / split_p;
     q0 = item - tile * split_p;
     tile_coords(tile, p.mblocks, p.nblocks, mb, nb);
@@ -90,12 +106,23 @@ __device__ __forceinline__ void item_coords(const GemmArgs& p, int split_p, int 
     q0 = 0;
   }
 }
+// elements a SYRK stores (its triangle); everything for a GEMM
+template <bool TRI>
+__device__ __forceinline__ bool in_tri(const GemmArgs& p, int64_t row, int64_t col) {
+  return !TRI || (p.tri == 1 ? row >= col : row <= col);
+}
+// work items of a launch
+__host__ __device__ __forceinline__ int work_items(const GemmArgs& a) {
+  if (a.tri) return a.mblocks * (a.mblocks + 1) / 2;
+  return a.mblocks * a.nblocks * (a.split_p ? a.split_p : 1);
+}
 
 // DBG: debug export of one panel's bins instead of the combine (casc_debug_bins)
 // AB:  BLAS update C := alpha AB + beta C at each tile's last panel (NEXT-4)
 // SPLIT: split mode (small problems); a separate instantiation so the large-problem
 //        kernel carries none of its indexing (measured 1.3% at 16384^3)
-template <bool DBG, bool AB, bool SPLIT>
+// TRI:  SYRK, one triangle of tiles (p.tri)
+template <bool DBG, bool AB, bool SPLIT, bool TRI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -117,7 +144,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   __syncthreads();
 
   const int split_p = SPLIT ? p.split_p : 0;
-  const int ntiles = p.mblocks * p.nblocks * (split_p ? split_p : 1);  // work items
+  const int ntiles = TRI ? p.mblocks * (p.mblocks + 1) / 2
+                         : p.mblocks * p.nblocks * (split_p ? split_p : 1);  // work items
 
   if (warp < 4) {
     // ===================== TMA producer (warpgroup 0) =====================
@@ -146,7 +174,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
         }
         if (tile >= ntiles) continue;
         int mb, nb, s0, s1, q0;
-        item_coords(p, split_p, tile, mb, nb, s0, s1, q0);
+        item_coords<TRI>(p, split_p, tile, mb, nb, s0, s1, q0);
         const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)s0 * A_STAGE * 8;
         const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)s0 * B_STAGE * 8;
         for (int st = s0; st < s1; ++st, ++it) {
@@ -198,7 +226,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   uint32_t it = 0, pc = 0;  // stage counter (smem ring), panel counter (exponent ring)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int mb, nb, s0, s1, q0;
-    item_coords(p, split_p, tile, mb, nb, s0, s1, q0);
+    item_coords<TRI>(p, split_p, tile, mb, nb, s0, s1, q0);
     // destination: C, or the panel-sum buffer T_q in split mode
     double* dst_hi = split_p ? p.t_hi + (int64_t)q0 * p.m * p.n : p.C_hi;
     double* dst_lo = split_p ? p.t_lo + (int64_t)q0 * p.m * p.n : p.C_lo;
@@ -313,7 +341,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
               if (last) {
                 const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
                 const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
-                if (row < p.m && col < p.n) {
+                if (row < p.m && col < p.n && in_tri<TRI>(p, row, col)) {
                   if (AB && p.ab)
                     apply_alpha_beta(th, tl, p.alpha_hi, p.alpha_lo, p.beta_hi, p.beta_lo,
                                      p.ab == 2 ? p.C_hi[row * p.ldc + col] : 0.0,
@@ -343,7 +371,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
-            if (row < p.m && col < p.n)
+            if (row < p.m && col < p.n && in_tri<TRI>(p, row, col))
               dst_fl[row * p.n + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
           }
       }
@@ -359,11 +387,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   }
 }
 
-template <bool DBG, bool AB, bool SPLIT>
+template <bool DBG, bool AB, bool SPLIT, bool TRI = false>
 static cudaError_t launch_variant(GemmArgs& a, int grid, bool coop, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT>,
+    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT, TRI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)GEMM_SMEM);
     if (e != cudaSuccess) return e;
@@ -371,16 +399,16 @@ static cudaError_t launch_variant(GemmArgs& a, int grid, bool coop, cudaStream_t
   }
   if (coop) {  // co-residency of all CTAs is required by the wave barrier
     void* args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<DBG, AB, SPLIT>, dim3(grid),
+    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<DBG, AB, SPLIT, TRI>, dim3(grid),
                                        dim3(GEMM_THREADS), args, GEMM_SMEM, st);
   }
-  casc_gemm_kernel<DBG, AB, SPLIT><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+  casc_gemm_kernel<DBG, AB, SPLIT, TRI><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   GemmArgs a = a_in;
-  const int ntiles = a.mblocks * a.nblocks * (a.split_p ? a.split_p : 1);  // work items
+  const int ntiles = work_items(a);
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
   static int wave_sync = -1;
@@ -403,6 +431,7 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(a.wave_counter, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
   }
+  if (a.tri) return launch_variant<false, true, false, true>(a, grid, coop, st);
   if (a.split_p)
     return a.ab ? launch_variant<false, true, true>(a, grid, coop, st)
                 : launch_variant<false, false, true>(a, grid, coop, st);

@@ -91,6 +91,9 @@ struct GemmArgs {
   double* t_lo;
   uint8_t* fbuf;
   double un_b2;    // 2^(c1-c0): bin2' -> bin2 for the debug export
+  // SYRK (NEXT-4, casc_syrk_fp64x2): 0 all tiles; 1 lower triangle (tiles with
+  // nb <= mb, elements with row >= col stored); 2 upper (nb >= mb, row <= col)
+  int tri;
 };
 
 cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st);

@@ -497,3 +497,64 @@ def test_split_mode_bitwise(casc, m, n, k):
         finally:
             del os.environ["CASC_SPLIT_MODE"]
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+# ------------------------------------------------------------------ SYRK (NEXT-4)
+@pytest.mark.parametrize("uplo,trans,n,k", [("L", "N", 200, 300), ("U", "N", 129, 513),
+                                            ("L", "T", 100, 700), ("U", "T", 65, 256),
+                                            ("L", "N", 1100, 600)])
+def test_syrk_bitwise_gemm_triangle(casc, orc, uplo, trans, n, k):
+    """casc_syrk_fp64x2 runs only the triangle's tiles; every element it stores is
+    bitwise the casc_gemm_fp64x2_ex(trans, !trans, A, A) element (same kernel
+    arithmetic), the other triangle keeps its NaN sentinel, flags equal the
+    oracle's on the triangle, and the triangle is within the north-star bound
+    of the exact op(A) op(A)^T."""
+    import torch
+    d = I.make_config(2, m=n, n=k, k=k, seed=71)
+    A_hi, A_lo = d["A_hi"][:n, :k], d["A_lo"][:n, :k]
+    Ast = (A_hi.T.copy(), A_lo.T.copy()) if trans == "T" else (A_hi.copy(), A_lo.copy())
+    tb = "N" if trans == "T" else "T"
+    G_hi = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    G_lo = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    casc.casc_gemm_fp64x2_ex(trans, tb, 1.0, T(Ast[0]), T(Ast[1]), T(Ast[0]), T(Ast[1]), 0.0,
+                             G_hi, G_lo)
+    S_hi = torch.full((n, n), float("nan"), dtype=torch.float64, device="cuda")
+    S_lo = torch.full((n, n), float("nan"), dtype=torch.float64, device="cuda")
+    fl = torch.full((n, n), 9, dtype=torch.uint8, device="cuda")
+    casc.casc_syrk_fp64x2(uplo, trans, 1.0, T(Ast[0]), T(Ast[1]), 0.0, S_hi, S_lo, flags=fl)
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+    s_hi, s_lo, f = N(S_hi), N(S_lo), N(fl)
+    assert same_values(s_hi[tri], N(G_hi)[tri]) and same_values(s_lo[tri], N(G_lo)[tri])
+    assert np.all(np.isnan(s_hi[~tri])) and np.all(np.isnan(s_lo[~tri])) and np.all(f[~tri] == 9)
+    if n <= 200:
+        _, _, ofl = orc.casc_syrk(uplo, trans, (1.0, 0.0), *Ast, (0.0, 0.0), np.zeros((n, n)),
+                                  np.zeros((n, n)))
+        assert np.array_equal(f[tri], ofl[tri])
+        ii, jj = np.nonzero(tri)
+        r = orc.exact_entries(A_hi, A_lo, A_hi.T.copy(), A_lo.T.copy(), ii, jj, s_hi, s_lo)
+        assert np.all(np.abs(r["err"]) <= orc.north_star_bound(k, r["absab"]))
+
+
+def test_syrk_alpha_beta_and_degenerate(casc, orc):
+    """alpha / beta on the triangle (bitwise the GEMM update of the same
+    product), k = 0 and alpha = 0 scale only the triangle, bad uplo rejected."""
+    import torch
+    n, k = 150, 400
+    d = I.make_config(1, m=n, n=k, k=k, seed=73)
+    A_hi, A_lo = d["A_hi"][:n, :k].copy(), d["A_lo"][:n, :k].copy()
+    C0 = np.random.default_rng(2).uniform(-1, 1, (n, n))
+    al, be = (1.0 / 3.0, 2.0 ** -56), (-0.7, 2.0 ** -60)
+    G_hi, G_lo = T(C0), T(np.zeros((n, n)))
+    casc.casc_gemm_fp64x2_ex("N", "T", al, T(A_hi), T(A_lo), T(A_hi), T(A_lo), be, G_hi, G_lo)
+    S_hi, S_lo = T(C0), T(np.zeros((n, n)))
+    casc.casc_syrk_fp64x2("L", "N", al, T(A_hi), T(A_lo), be, S_hi, S_lo)
+    tri = np.tril(np.ones((n, n), bool))
+    assert same_values(N(S_hi)[tri], N(G_hi)[tri]) and same_values(N(S_lo)[tri], N(G_lo)[tri])
+    assert np.array_equal(N(S_hi)[~tri], C0[~tri])
+    # alpha == 0 (and k == 0): C := beta C on the triangle only
+    Z_hi, Z_lo = T(C0), T(np.zeros((n, n)))
+    casc.casc_syrk_fp64x2("U", "N", 0.0, None, None, (0.5, 0.0), Z_hi, Z_lo)
+    up = np.triu(np.ones((n, n), bool))
+    assert np.array_equal(N(Z_hi)[up], 0.5 * C0[up]) and np.array_equal(N(Z_hi)[~up], C0[~up])
+    with pytest.raises(ValueError):
+        casc.casc_syrk_fp64x2("X", "N", 1.0, T(A_hi), T(A_lo), 0.0, S_hi, S_lo)

@@ -439,6 +439,43 @@ def test_blas_ex_oracle(orc):
     assert Z[2].sum() == 0
 
 
+@pytest.mark.parametrize("uplo,trans", [("L", "N"), ("U", "N"), ("L", "T"), ("U", "T")])
+def test_syrk_oracle(orc, uplo, trans):
+    """NEXT-4 SYRK oracle: on its triangle, alpha = 1, beta = 0 is within
+    the north-star bound of the exact op(A) op(A)^T (exact rationals); the other
+    triangle and its flags are untouched; alpha = 2^p scales exactly; beta = 0
+    does not read C; alpha = 0 scales the triangle by beta."""
+    n, k = 11, 300
+    d = I.make_config(1, m=n, n=k, k=k, seed=19)
+    A_hi, A_lo = d["A_hi"][:n, :k], d["A_lo"][:n, :k]  # op(A): n x k
+    Ast = (A_hi.T.copy(), A_lo.T.copy()) if trans == "T" else (A_hi.copy(), A_lo.copy())
+    sent = np.full((n, n), 7.5)
+    fl0 = np.full((n, n), 9, np.uint8)
+    Ch, Cl, fl = orc.casc_syrk(uplo, trans, (1.0, 0.0), *Ast, (0.0, 0.0), sent, sent, fl0)
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+    assert np.all(Ch[~tri] == 7.5) and np.all(Cl[~tri] == 7.5) and np.all(fl[~tri] == 9)
+    assert np.all(fl[tri] <= 1)
+    for i in range(n):
+        for j in range(n):
+            if not tri[i, j]:
+                continue
+            ex = sum((fr(A_hi[i, p]) + fr(A_lo[i, p])) * (fr(A_hi[j, p]) + fr(A_lo[j, p]))
+                     for p in range(k))
+            absab = sum(abs(fr(A_hi[i, p]) + fr(A_lo[i, p])) * abs(fr(A_hi[j, p]) + fr(A_lo[j, p]))
+                        for p in range(k))
+            assert abs(fr(Ch[i, j]) + fr(Cl[i, j]) - ex) <= 4 * k * F(2) ** -104 * absab
+    S = orc.casc_syrk(uplo, trans, (8.0, 0.0), *Ast, (0.0, 0.0), sent, sent)
+    assert np.array_equal(S[0][tri], 8 * Ch[tri]) and np.array_equal(S[1][tri], 8 * Cl[tri])
+    nan = np.full((n, n), np.nan)
+    N_ = orc.casc_syrk(uplo, trans, (1.0, 0.0), *Ast, (0.0, 0.0), nan, nan)
+    assert np.array_equal(N_[0][tri], Ch[tri]) and np.all(np.isnan(N_[0][~tri]))
+    rng = np.random.default_rng(8)
+    C0 = rng.uniform(-1, 1, (n, n))
+    Z = orc.casc_syrk(uplo, trans, (0.0, 0.0), *Ast, (0.5, 0.0), C0, np.zeros((n, n)), fl0)
+    assert np.array_equal(Z[0][tri], 0.5 * C0[tri]) and np.array_equal(Z[0][~tri], C0[~tri])
+    assert np.all(Z[2][tri] == 0) and np.all(Z[2][~tri] == 9)
+
+
 def test_exact_accumulator_vs_fractions(orc):
     """ORACLE-EXACT superaccumulator equals Fraction sums, over
     wide exponent ranges and with exact cancellation."""
