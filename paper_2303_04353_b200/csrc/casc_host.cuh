@@ -76,20 +76,28 @@ int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
   bPBs = al(bPBs);
   bPA = al(bPA);
   const size_t total = nB * bB + J * bPBs + nA * bA + bPA + nC * bC;
+  cudaEvent_t ev_start, ev_done, ev_A[2], ev_packA[2], ev_B[2], ev_packB[2], ev_G[2], ev_D[2];
+  cudaEvent_t* evs[] = {&ev_start, &ev_done, &ev_A[0], &ev_A[1], &ev_packA[0], &ev_packA[1],
+                        &ev_B[0], &ev_B[1], &ev_packB[0], &ev_packB[1], &ev_G[0], &ev_G[1],
+                        &ev_D[0], &ev_D[1]};
+  int nev = 0;
+  for (cudaEvent_t* x : evs) {
+    if (cudaEventCreateWithFlags(x, cudaEventDisableTiming) != cudaSuccess) {
+      for (int i = 0; i < nev; ++i) cudaEventDestroy(*evs[i]);
+      return CASC_ERR_CUDA;
+    }
+    ++nev;
+  }
   uint8_t* base = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&base), total, st) != cudaSuccess)
+  if (cudaMallocAsync(reinterpret_cast<void**>(&base), total, st) != cudaSuccess) {
+    for (cudaEvent_t* x : evs) cudaEventDestroy(*x);
     return CASC_ERR_CUDA;
+  }
   uint8_t* dBbuf = base;
   uint8_t* pB = dBbuf + nB * bB;
   uint8_t* dAbuf = pB + J * bPBs;
   uint8_t* pA = dAbuf + nA * bA;
   uint8_t* dCbuf = pA + bPA;
-  cudaEvent_t ev_start, ev_done, ev_A[2], ev_packA[2], ev_B[2], ev_packB[2], ev_G[2], ev_D[2];
-  cudaEvent_t* evs[] = {&ev_start, &ev_done, &ev_A[0], &ev_A[1], &ev_packA[0], &ev_packA[1],
-                        &ev_B[0], &ev_B[1], &ev_packB[0], &ev_packB[1], &ev_G[0], &ev_G[1],
-                        &ev_D[0], &ev_D[1]};
-  for (cudaEvent_t* e : evs)
-    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return CASC_ERR_CUDA;
   cudaError_t e = cudaSuccess;
   int status = CASC_OK;
   auto ok = [&](cudaError_t x) {
