@@ -18,7 +18,10 @@ elif sys.argv[1] == "run":
     n = int(sys.argv[2])
     for v in names:
         env = dict(os.environ, CASC_LIB_PATH=os.path.abspath(f"paper_2303_04353_b200/libcasc_{v}.so"))
-        r = subprocess.run([sys.executable, __file__, "one", str(n)], env=env, capture_output=True, text=True)
+        try:
+            r = subprocess.run([sys.executable, __file__, "one", str(n)], env=env, capture_output=True, text=True, timeout=150)
+        except subprocess.TimeoutExpired:
+            print(v, "TIMEOUT", flush=True); continue
         print(v, r.stdout.strip(), r.stderr.strip()[-300:], flush=True)
 elif sys.argv[1] == "one":
     import torch
