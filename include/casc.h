@@ -325,8 +325,9 @@ int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
                         uint8_t* flags, int y, casc_stream_t stream);
 
 /* As casc_i8_gemm_fp64x2 with a caller-owned device workspace (256-byte
- * aligned, >= casc_i8_workspace_bytes(m, n, k, y)); no allocation, no host
- * synchronisation. */
+ * aligned, >= casc_i8_workspace_bytes(m, n, k, y)); no host synchronisation
+ * (small single-panel problems in split mode take a stream-ordered temporary,
+ * see casc_i8_gemm_ws_bytes). */
 int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                            const double* A_hi, const double* A_lo, int64_t lda,
                            const double* B_hi, const double* B_lo, int64_t ldb,
@@ -382,8 +383,11 @@ size_t casc_i8_packed_bytes(int64_t rows, int64_t k, int y);
 int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
                  int is_b, int y, void* packed, casc_stream_t stream);
 /* Bytes of the GEMM's own scratch: 6 x 128 x 128 x 8 bytes per CTA (the FP64x2
- * C accumulator and the exact group values of the tile in flight), then a
- * wave-synchronisation counter. */
+ * C accumulator and the exact group values of the tile in flight; all CTA
+ * pairs for problems small enough for split mode), then a wave-synchronisation
+ * counter.  Split mode (a single k panel and few tiles: one work item per
+ * (tile, k-block part), bitwise the same C) also takes a stream-ordered
+ * temporary for the parts' exact partial products. */
 size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
 /* Phases 2-3 (R24-R26) from packed operands of the same m, n, k, y: the fused
  * tcgen05 kernel on CTA pairs.  ws: >= casc_i8_gemm_ws_bytes(m, n) bytes of

@@ -485,6 +485,12 @@ struct GemmArgs {
   unsigned int* sync;   // wave-sync counter (zeroed before the launch) or null
   int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
   int64_t dbg_panel;
+  // split mode (small single-panel problems): ks > 1 k-block parts per tile, one
+  // work item per (tile, part); each item writes its exact partial panel product
+  // S (192-bit) to split_ws [item][rank][limb][128 x 128] and a reduce kernel
+  // sums the parts and rounds (bitwise the unsplit result: S is exact)
+  int ks;
+  unsigned long long* split_ws;
   int ab;               // NEXT-4 update at the final store: 0 none, 1 alpha, 2 alpha and beta
   double ah, al, bh, bl;
 };
@@ -802,11 +808,18 @@ __device__ __forceinline__ void tile_of(int tile, int64_t RP, int64_t RB, int64_
   cb = rr / gs;
 }
 
+// (row-pair block, column block) -> pair tile (inverse of tile_of)
+__device__ __forceinline__ int64_t tile_index(int64_t rp, int64_t cb, int64_t RP, int64_t RB) {
+  const int64_t grp = rp / GROUP_M, first = grp * GROUP_M;
+  const int64_t gs = min((int64_t)GROUP_M, RP - first);
+  return grp * GROUP_M * RB + cb * gs + (rp - first);
+}
+
 // The fused kernel on CTA pairs (cluster of 2, tcgen05 cta_group::2): the pair
 // computes a 256 x 128 C tile; CTA r holds A rows 128r..128r+127 of it and
 // rows 64r..64r+63 of every 128 x 128-byte B chunk; the leader (r = 0) issues
 // the M = 256 MMAs for both, each CTA's tensor memory holds its 128 rows.
-template <bool DBG>
+template <bool DBG, bool SPLITK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     i8_gemm_kernel(const GemmArgs p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB) {
@@ -862,6 +875,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int P = (int)p.ga.P;
   const int tiles = (int)(RP * RB);
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // work items: tiles, or (tile, k-block part) in split mode (P == 1)
+  const int ks = SPLITK ? p.ks : 1;
+  const int items = tiles * ks;
+  auto kb_range = [&](int item, int q, int64_t& kb0, int64_t& kb1) {
+    kb0 = (int64_t)q * KBP;
+    kb1 = min(kb0 + KBP, KBn);
+    if (SPLITK) {
+      const int64_t len = kb1 - kb0, part = item % ks;
+      kb1 = kb0 + (part + 1) * len / ks;
+      kb0 = kb0 + part * len / ks;
+    }
+  };
 
   if (warp == PRODUCER_WARP) {
     // ============================ TMA producer (both CTAs) ============================
@@ -886,13 +911,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     const int full_waves = tiles / npairs;  // waves in which every pair has a tile
     uint32_t sweep = 0;
-    for (int tile = CASC_I8_WAITS_ON ? pair : tiles; tile < tiles; tile += npairs) {
+    for (int item = CASC_I8_WAITS_ON ? pair : items; item < items; item += npairs) {
+      const int tile = item / ks;
       int64_t rp, cb;
       tile_of(tile, RP, RB, rp, cb);
       const int64_t rb = 2 * rp + rank;
       const bool synced = p.sync && (tile / npairs) < full_waves;
       for (int q = 0; q < P; ++q) {
-        const int64_t kb0 = (int64_t)q * KBP, kb1 = min(kb0 + KBP, KBn);
+        int64_t kb0, kb1;
+        kb_range(item, q, kb0, kb1);
         for (int go = 0; go < ngroups; ++go) {
           const int grp = ngroups - 1 - go;  // the MMA issuer's group order
           const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
@@ -940,9 +967,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (lane == 0)
         for (int x = 0; x < 64; ++x) g_i8prof[blockIdx.x][x] = 0;
 #endif
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      for (int item = pair; item < items; item += npairs) {
         for (int q = 0; q < P; ++q) {
-          const int kb0 = q * KBP, kb1 = (int)min((int64_t)kb0 + KBP, KBn);
+          int64_t kb0_, kb1_;
+          kb_range(item, q, kb0_, kb1_);
+          const int kb0 = (int)kb0_, kb1 = (int)kb1_;
           // groups in reverse order (bins y-4 .. y-1 first): the short group
           // 0 .. r-1 (most significant, fewest products) ends the panel, so the
           // epilogue's once-per-panel phase 2 overlaps the longest group's MMAs
@@ -983,7 +1012,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     double* Cl = Ch + TR * TR;
     long long* Vw = reinterpret_cast<long long*>(Cl + TR * TR);
     uint32_t gcount = 0;
-    for (int tile = pair; tile < tiles; tile += npairs) {
+    for (int item = pair; item < items; item += npairs) {
+      const int tile = item / ks;
       int64_t rp, cb;
       tile_of(tile, RP, RB, rp, cb);
       const int64_t gi = (2 * rp + rank) * TR + lr;
@@ -1081,6 +1111,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int g2 = 0; g2 < NGMAX; ++g2)
                 if (g2 < ngroups) S = u192_add(S, u192_from_shifted(xv[g2][i], ngroups - 1 - g2));
+              if (SPLITK) {  // the exact partial S of this k-block part
+                unsigned long long* sw =
+                    p.split_ws + ((int64_t)(item * 2 + (int)rank) * 3) * TR * TR + (c0 + i) * TR + lr;
+                sw[0] = S.l0;
+                sw[TR * TR] = S.l1;
+                sw[2 * TR * TR] = S.l2;
+                continue;
+              }
               const bool neg = (long long)S.l2 < 0;
               if (neg) S = u192_neg(S);
               const int w0 = ei + sF[c0 + i] - 12 - 8 * (y - 1);
@@ -1089,6 +1127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               th[i] = rn_u192(S, w0, neg, R, rneg);
               tl[i] = rn_u192(R, w0, neg != rneg, R2, r2neg);
             }
+            if (SPLITK) continue;  // rounding, detector and C in i8_split_reduce_kernel
 #pragma unroll
             for (int i = 0; i < EPI_SUB; ++i) {
               const int lc = c0 + i;
@@ -1165,6 +1204,12 @@ int grid_for(int64_t m, int64_t n, int sms) {  // CTAs: 2 per pair, one pair per
   const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
   return (int)(2 * pairs);
 }
+// CTAs the GEMM scratch is sized for: small problems may run in split mode on
+// every CTA pair (split_parts)
+int ws_grid(int64_t m, int64_t n, int sms) {
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  return tiles < 2 * (int64_t)(sms / 2) ? 2 * (sms / 2) : grid_for(m, n, sms);
+}
 // per-CTA T / C scratch, then the wave-sync counter
 size_t cta_ws_bytes(int grid) { return (size_t)grid * WS_PER_CTA * sizeof(double) + 256; }
 
@@ -1197,6 +1242,70 @@ cudaError_t slice_map(CUtensorMap* map, const void* packed, const Pack& g, uint3
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Split mode: C from the parts' exact partial products (P == 1): S = sum of the
+// parts (192-bit, exact), T = (RN(S 2^w0), RN(S 2^w0 - T.hi)) (R25 rev. 2), the
+// R26 detector, C = T, the R21 update -- the unsplit epilogue's steps on the
+// same exact S, hence bitwise the same C and flags.
+__global__ void __launch_bounds__(256) i8_split_reduce_kernel(const GemmArgs p) {
+  const int64_t RP = p.ga.R / 2, RB = p.gb.R;
+  const int y = p.ga.y;
+  const int64_t mn = p.m * p.n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    // consecutive threads: consecutive rows of one column (the workspace is
+    // column-major per tile)
+    const int64_t j = idx / p.m, i = idx - j * p.m;
+    const int64_t rp = i / (2 * TR), rank = (i / TR) & 1, lr = i % TR;
+    const int64_t cb = j / TR, col = j % TR;
+    const int64_t tile = tile_index(rp, cb, RP, RB);
+    U192 S{0ull, 0ull, 0ull};
+    for (int part = 0; part < p.ks; ++part) {
+      const unsigned long long* sw =
+          p.split_ws + ((tile * p.ks + part) * 2 + rank) * 3 * TR * TR + col * TR + lr;
+      S = u192_add(S, U192{sw[0], sw[TR * TR], sw[2 * TR * TR]});
+    }
+    const bool neg = (long long)S.l2 < 0;
+    if (neg) S = u192_neg(S);
+    const int ei = *reinterpret_cast<const int32_t*>(p.pa + exp_at(p.ga, i, 0));
+    const int fj = *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, j, 0));
+    const int w0 = ei + fj - 12 - 8 * (y - 1);
+    U192 R, R2;
+    bool rneg, r2neg;
+    double ch = rn_u192(S, w0, neg, R, rneg);
+    double cl = rn_u192(R, w0, neg != rneg, R2, r2neg);
+    const uint8_t flag = fabs(ch) <= mulp2((double)p.k, ei + fj - 50) ? 1 : 0;
+    double* oh = p.C_hi + i * p.ldc + j;
+    double* ol = p.C_lo + i * p.ldc + j;
+    if (p.ab)
+      apply_alpha_beta(ch, cl, p.ah, p.al, p.bh, p.bl, p.ab == 2 ? *oh : 0.0,
+                       p.ab == 2 ? *ol : 0.0, p.ab == 2);
+    *oh = ch;
+    *ol = cl;
+    if (p.flags) p.flags[i * p.n + j] = flag;
+  }
+}
+
+// Split plan: k-block parts per tile (1 = off) for single-panel problems whose
+// tiles fill the CTA pairs' last wave badly; the smallest part count within 2%
+// of the best wave efficiency.
+int split_parts(int64_t m, int64_t n, int64_t k, int sms) {
+  const char* env = getenv("CASC_I8_SPLIT");  // "0": never (tests compare both)
+  if (env && env[0] == '0') return 1;
+  if (k > KC8) return 1;
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  const int64_t np = sms / 2, kbn = (k + KB - 1) / KB;
+  if (tiles >= 2 * np) return 1;
+  auto eff = [&](int64_t ks) {
+    const int64_t it = tiles * ks;
+    return (double)it / (double)(((it + np - 1) / np) * np);
+  };
+  double best = eff(1);
+  for (int64_t ks = 2; ks <= 16 && ks <= kbn && tiles * ks <= 4 * np; ++ks) best = max(best, eff(ks));
+  for (int64_t ks = 1; ks <= 16 && ks <= kbn && tiles * ks <= 4 * np; ++ks)
+    if (eff(ks) >= best - 0.02) return (int)ks;
+  return 1;
+}
+
 cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
                  double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
                  int32_t* dbg, int64_t dbg_panel, cudaStream_t st, int ab = 0, double ah = 1.0,
@@ -1221,6 +1330,12 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   a.ws = ws;
   a.dbg = dbg;
   a.dbg_panel = dbg_panel;
+  // `grid`: the CTAs `ws` holds (ws_grid); the launch takes what the tiles need
+  int sms = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return cudaErrorInvalidDevice;
+  const int g0 = min(grid, grid_for(m, n, sms));
   const char* env = getenv("CASC_I8_WAVE_SYNC");  // "0": off (timing studies)
   if (!(env && env[0] == '0')) {
     a.sync = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(ws) +
@@ -1233,14 +1348,39 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TR / 2);
   if (e != cudaSuccess) return e;
   if (dbg) {
-    cudaFuncSetAttribute(i8_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(i8_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SMEM);
-    i8_gemm_kernel<true><<<grid, THREADS, SMEM, st>>>(a, mA, mB);
-  } else {
-    cudaFuncSetAttribute(i8_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SMEM);
-    i8_gemm_kernel<false><<<grid, THREADS, SMEM, st>>>(a, mA, mB);
+    i8_gemm_kernel<true, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
+    return cudaGetLastError();
   }
+  const int ks = split_parts(m, n, k, sms);
+  if (ks > 1) {
+    const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+    const int64_t items = tiles * ks;
+    const int g = (int)(2 * min(items, (int64_t)(sms / 2)));
+    if (g > grid) return cudaErrorInvalidValue;  // ws sized for `grid` CTAs
+    a.ks = ks;
+    a.sync = nullptr;  // no wave synchronisation for a few waves
+    if (cudaMallocAsync(reinterpret_cast<void**>(&a.split_ws),
+                        (size_t)items * 2 * 3 * TR * TR * sizeof(unsigned long long),
+                        st) != cudaSuccess)
+      return cudaErrorMemoryAllocation;
+    cudaFuncSetAttribute(i8_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
+    i8_gemm_kernel<false, true><<<g, THREADS, SMEM, st>>>(a, mA, mB);
+    cudaError_t e2 = cudaGetLastError();
+    if (e2 == cudaSuccess) {
+      int64_t blocks = (m * n + 255) / 256;
+      if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+      i8_split_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+      e2 = cudaGetLastError();
+    }
+    cudaFreeAsync(a.split_ws, st);
+    return e2;
+  }
+  cudaFuncSetAttribute(i8_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SMEM);
+  i8_gemm_kernel<false, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
   return cudaGetLastError();
 }
 
@@ -1291,7 +1431,7 @@ size_t casc_i8_packed_block_bytes(int64_t k, int y) {
 
 size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n) {
   if (m <= 0 || n <= 0) return 0;
-  return i8::cta_ws_bytes(i8::grid_for(m, n, host::current_sms()));
+  return i8::cta_ws_bytes(i8::ws_grid(m, n, host::current_sms()));
 }
 
 size_t casc_i8_workspace_bytes(int64_t m, int64_t n, int64_t k, int y) {
@@ -1332,7 +1472,7 @@ int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* pack
   if (!packed_a || !packed_b || !ws || ws_bytes < casc_i8_gemm_ws_bytes(m, n))
     return CASC_ERR_INVALID;
   const cudaError_t e = i8::gemm(packed_a, packed_b, m, n, k, y, C_hi, C_lo, ldc, flags,
-                                 static_cast<double*>(ws), i8::grid_for(m, n, sms), nullptr, 0,
+                                 static_cast<double*>(ws), i8::ws_grid(m, n, sms), nullptr, 0,
                                  S8(stream));
   if (e == cudaSuccess) host::set_launches(1);
   return st8(e);
@@ -1360,7 +1500,7 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,
   cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
   if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
   if (e == cudaSuccess)
-    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, ws, i8::grid_for(m, n, sms), nullptr,
+    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, ws, i8::ws_grid(m, n, sms), nullptr,
                  0, st);
   if (e == cudaSuccess) host::set_launches(7);
   return st8(e);
@@ -1390,7 +1530,7 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi
   };
   const int64_t sr = fit(slab_rows ? slab_rows : 4096, m);
   const int64_t sc = fit(slab_cols ? slab_cols : 4096, n);
-  const int gmax = i8::grid_for(sr, sc, sms);
+  const int gmax = 2 * (sms / 2);  // every block's ws_grid fits
   double* gws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&gws), i8::cta_ws_bytes(gmax), st) != cudaSuccess)
     return CASC_ERR_CUDA;
@@ -1408,7 +1548,7 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi
   auto gemm = [&](int64_t rows, int64_t cols, const void* pa, const void* pb, double* ch,
                   double* cl, uint8_t* fl) {
     const cudaError_t e = i8::gemm(pa, pb, rows, cols, k, y, ch, cl, cols, fl, gws,
-                                   i8::grid_for(rows, cols, sms), nullptr, 0, st);
+                                   gmax, nullptr, 0, st);
     launches += e == cudaSuccess;
     return st8(e);
   };
@@ -1472,7 +1612,7 @@ int casc_i8_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t
   const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
   const int ab = use_beta ? 2 : (unit_alpha ? 0 : 1);
   if (e == cudaSuccess)
-    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, gws, i8::grid_for(m, n, sms),
+    e = i8::gemm(pa, pb, m, n, k, y, C_hi, C_lo, ldc, flags, gws, i8::ws_grid(m, n, sms),
                  nullptr, 0, st, ab, alpha_hi, alpha_lo, beta_hi, beta_lo);
   if (owned) cudaFreeAsync(ws, st);
   if (e == cudaSuccess) host::set_launches(7);
@@ -1565,7 +1705,7 @@ int casc_i8_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, cons
   cudaError_t e = i8::pack(A_hi, A_lo, lda, m, k, y, false, pa, st);
   if (e == cudaSuccess) e = i8::pack(B_hi, B_lo, ldb, n, k, y, true, pb, st);
   if (e == cudaSuccess)
-    e = i8::gemm(pa, pb, m, n, k, y, nullptr, nullptr, n, nullptr, ws, i8::grid_for(m, n, sms),
+    e = i8::gemm(pa, pb, m, n, k, y, nullptr, nullptr, n, nullptr, ws, i8::ws_grid(m, n, sms),
                  bins, panel, st);
   cudaFreeAsync(buf, st);
   return st8(e);

@@ -366,3 +366,28 @@ def test_i8_host_operands_bitwise(casc, m, n, k, slab, scol, y):
                                                    slab_cols=scol)
     assert bitwise(C_hi.numpy(), ref[0]) and bitwise(C_lo.numpy(), ref[1])
     assert np.array_equal(fl.numpy(), ref[2])
+
+
+# ------------------------------------------------------------------ split mode
+@pytest.mark.parametrize("m,n,k", [(1024, 1024, 1024), (512, 300, 700), (256, 128, 8192),
+                                   (700, 520, 1000), (130, 257, 300)])
+def test_i8_split_mode_bitwise(casc, orc, m, n, k):
+    """Small single-panel problems run one work item per (tile, k-block part)
+    and sum the parts' exact partial products in a reduce kernel (R25 rev. 2
+    rounds the exact sum, so any partition is bitwise the same): split and
+    unsplit runs agree bitwise, and both match the oracle on sampled rows."""
+    import os
+    d = I.make_config(1, m=m, n=n, k=k, seed=81)
+    split = gpu_gemm(casc, d)
+    os.environ["CASC_I8_SPLIT"] = "0"
+    try:
+        whole = gpu_gemm(casc, d)
+    finally:
+        del os.environ["CASC_I8_SPLIT"]
+    for a, b in zip(split, whole):
+        assert np.array_equal(np.ascontiguousarray(a).view(np.uint8),
+                              np.ascontiguousarray(b).view(np.uint8))
+    rows = np.unique(np.linspace(0, m - 1, 6).astype(int))
+    o_hi, o_lo, o_fl = orc.i8_casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"], d["B_lo"])
+    assert bitwise(split[0][rows], o_hi) and bitwise(split[1][rows], o_lo)
+    assert np.array_equal(split[2][rows], o_fl)
