@@ -289,12 +289,15 @@ def test_i8_extreme_exponents(casc, orc, sa, sb, k):
 
 
 # ------------------------------------------------------------------ BLAS-style (NEXT-4)
-@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
-def test_i8_blas_ex_bit_exact(casc, orc, ta, tb):
+@pytest.mark.parametrize("ta,tb,k", [("N", "N", 8192 + 300), ("T", "N", 8192 + 300),
+                                     ("N", "T", 8192 + 300), ("T", "T", 8192 + 300),
+                                     ("N", "N", 700), ("T", "T", 700)])
+def test_i8_blas_ex_bit_exact(casc, orc, ta, tb, k):
     """casc_i8_gemm_fp64x2_ex: transposed operands, alpha / beta (reading R21)
-    bit-exact with oracle.i8_casc_gemm_ex, including a two-panel k and ragged tiles."""
+    bit-exact with oracle.i8_casc_gemm_ex, with a two-panel k and ragged tiles
+    and with a single panel (split mode: alpha / beta in the reduce kernel)."""
     import torch
-    m, n, k = 130, 257, 8192 + 300
+    m, n = 130, 257
     d = I.make_config(1, m=m, n=n, k=k, seed=41)
     A = (d["A_hi"].T.copy(), d["A_lo"].T.copy()) if ta == "T" else (d["A_hi"], d["A_lo"])
     B = (d["B_hi"].T.copy(), d["B_lo"].T.copy()) if tb == "T" else (d["B_hi"], d["B_lo"])
