@@ -151,17 +151,19 @@ __device__ __forceinline__ unsigned long long absbits(double x) {
 }
 
 // max |A_hi| per (row, panel): warp = one row x 1024 k, 8 rows per block.
+// kchunk (a multiple of 32 dividing 8192): k per warp; smaller for small
+// problems so that the grid covers the SMs.
 __global__ void __launch_bounds__(256) i8_rowmax_kernel(const double* __restrict__ hi, int64_t ld,
                                                         int64_t rows, int64_t k, Pack g,
-                                                        uint8_t* __restrict__ packed) {
+                                                        uint8_t* __restrict__ packed, int kchunk) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * 8 + warp;
-  const int64_t p0 = (int64_t)blockIdx.y * 1024;
+  const int64_t p0 = (int64_t)blockIdx.y * kchunk;
   if (r >= rows) return;
   unsigned long long m = 0;
   const double* row = hi + r * ld;
 #pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
+  for (int i = 0; i < kchunk / 32; ++i) {
     const int64_t p = p0 + i * 32 + lane;
     if (p < k) m = max(m, absbits(__ldg(row + p)));
   }
@@ -170,16 +172,17 @@ __global__ void __launch_bounds__(256) i8_rowmax_kernel(const double* __restrict
     atomicMax(reinterpret_cast<unsigned long long*>(packed + max_at(g, r, p0 / KC8)), m);
 }
 
-// max |B_hi| per (column, panel): thread = one column x 64 k.
+// max |B_hi| per (column, panel): thread = one column x kchunk k (a divisor of
+// 8192; smaller for small problems so that the grid covers the SMs).
 __global__ void __launch_bounds__(256) i8_colmax_kernel(const double* __restrict__ hi, int64_t ld,
                                                         int64_t cols, int64_t k, Pack g,
-                                                        uint8_t* __restrict__ packed) {
+                                                        uint8_t* __restrict__ packed, int kchunk) {
   const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  const int64_t p0 = (int64_t)blockIdx.y * 64;
+  const int64_t p0 = (int64_t)blockIdx.y * kchunk;
   if (j >= cols) return;
   unsigned long long m = 0;
 #pragma unroll 8
-  for (int i = 0; i < 64; ++i) {
+  for (int i = 0; i < kchunk; ++i) {
     const int64_t p = p0 + i;
     if (p < k) m = max(m, absbits(__ldg(hi + p * ld + j)));
   }
@@ -993,8 +996,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #ifdef CASC_I8_PROF
       if (lane == 0 && (blockIdx.x % 16) == 0) {
         const unsigned long long* g = g_i8prof[blockIdx.x];
-        printf("i8prof cta %d phase2 %llu x %llu | total %lld | tempty %llu %llu %llu %llu | fullB %llu %llu %llu %llu"
-               " | fullA %llu %llu %llu %llu\n", blockIdx.x, g[48], g[49], clock64() - tstart, g[0], g[2],
+        printf("i8prof cta %d loads %llu round %llu phase2 %llu x %llu | total %lld | tempty %llu %llu %llu %llu | fullB %llu %llu %llu %llu"
+               " | fullA %llu %llu %llu %llu\n", blockIdx.x, g[50], g[51], g[48], g[49], clock64() - tstart, g[0], g[2],
                g[6], g[10], g[16], g[18], g[22], g[26], g[32], g[34], g[38], g[42]);
       }
 #endif
@@ -1102,6 +1105,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 for (int i = 0; i < EPI_SUB; ++i)
                   xv[g2][i] = ld_na(&Vw[(int64_t)g2 * TR * TR + (c0 + i) * TR + lr]);
               }
+#ifdef CASC_I8_PROF
+            long long tpa = clock64();
+            if (xv[0][0] == 0x7fffffffffffffffll) tpa = 0;  // forces the loads to land
+            if (lane == 0 && ew == 1) g_i8prof[blockIdx.x][50] += clock64() - tpa;
+            tpa = clock64();
+#endif
 #pragma unroll
             for (int i = 0; i < EPI_SUB; ++i) {
               // R25 (rev. 2): S = sum_g V_g 2^(32 (ngroups-1-g)) exactly (the
@@ -1127,6 +1136,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               th[i] = rn_u192(S, w0, neg, R, rneg);
               tl[i] = rn_u192(R, w0, neg != rneg, R2, r2neg);
             }
+#ifdef CASC_I8_PROF
+            if (th[0] == 12345.0) tpa = 0;
+            if (lane == 0 && ew == 1) g_i8prof[blockIdx.x][51] += clock64() - tpa;
+#endif
             if (SPLITK) continue;  // rounding, detector and C in i8_split_reduce_kernel
 #pragma unroll
             for (int i = 0; i < EPI_SUB; ++i) {
@@ -1163,6 +1176,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     }
+#ifdef CASC_I8_PROF
+    if (lane == 0 && ew == 1 && (blockIdx.x % 16) == 0)
+      printf("i8epi cta %d loads %llu round %llu phase2 %llu x %llu\n", blockIdx.x,
+             g_i8prof[blockIdx.x][50], g_i8prof[blockIdx.x][51], g_i8prof[blockIdx.x][48],
+             g_i8prof[blockIdx.x][49]);
+#endif
   }
   tc_fence_before();
   cluster_sync_all();
@@ -1178,14 +1197,19 @@ cudaError_t pack(const double* hi, const double* lo, int64_t ld, int64_t rows, i
   const Pack g = pack_of(rows, k, y);
   uint8_t* pk = static_cast<uint8_t*>(packed);
   i8_zero_max_kernel<<<256, 256, 0, st>>>(g, pk);
+  // k per thread / warp of the max kernels: large enough to keep the atomics
+  // few, small enough that small problems still fill the machine
+  const int64_t elems = rows * k;
   if (cols) {
-    i8_colmax_kernel<<<dim3((unsigned)((rows + 255) / 256), (unsigned)((k + 63) / 64)), 256, 0,
-                       st>>>(hi, ld, rows, k, g, pk);
+    const int kc = elems >= ((int64_t)1 << 26) ? 64 : 16;
+    i8_colmax_kernel<<<dim3((unsigned)((rows + 255) / 256), (unsigned)((k + kc - 1) / kc)), 256,
+                       0, st>>>(hi, ld, rows, k, g, pk, kc);
     i8_digits_kernel<true><<<dim3((unsigned)g.R, (unsigned)g.KBn, 4), 256, 0, st>>>(
         hi, lo, ld, rows, k, g, pk);
   } else {
-    i8_rowmax_kernel<<<dim3((unsigned)((rows + 7) / 8), (unsigned)((k + 1023) / 1024)), 256, 0,
-                       st>>>(hi, ld, rows, k, g, pk);
+    const int kc = elems >= ((int64_t)1 << 26) ? 1024 : 256;
+    i8_rowmax_kernel<<<dim3((unsigned)((rows + 7) / 8), (unsigned)((k + kc - 1) / kc)), 256, 0,
+                       st>>>(hi, ld, rows, k, g, pk, kc);
     i8_digits_kernel<false><<<dim3((unsigned)(g.R * 4), (unsigned)g.KBn), 256, 0, st>>>(
         hi, lo, ld, rows, k, g, pk);
   }

@@ -6,6 +6,9 @@ VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
     "prof": ["CASC_I8_PROF"],
+    "sus0": ["CASC_I8_SUSPEND_NS=0"],
+    "sus2k": ["CASC_I8_SUSPEND_NS=2000"],
+    "sus20k": ["CASC_I8_SUSPEND_NS=20000"],
     "a10b8": ["CASC_I8_NSA=10"],
     "a9b10": ["CASC_I8_NSA=9", "CASC_I8_NSB=10"],
     "a8b12": ["CASC_I8_NSB=12"],
