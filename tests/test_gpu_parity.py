@@ -558,3 +558,48 @@ def test_syrk_alpha_beta_and_degenerate(casc, orc):
     assert np.array_equal(N(Z_hi)[up], 0.5 * C0[up]) and np.array_equal(N(Z_hi)[~up], C0[~up])
     with pytest.raises(ValueError):
         casc.casc_syrk_fp64x2("X", "N", 1.0, T(A_hi), T(A_lo), 0.0, S_hi, S_lo)
+
+
+def test_cuda_graph_capture_replay(casc):
+    """The C-ABI calls are stream-ordered with no host synchronisation inside
+    (caller workspaces; split modes allocate stream-ordered), so a step can be
+    captured into a CUDA graph (torch.cuda.graph) and replayed: bitwise the
+    eager results for both cascades, incl. the FP64 cooperative launch (> 148
+    tiles) and the INT8 split mode."""
+    import torch
+    outs = {}
+    for n, k in ((832, 300), (1024, 1024)):
+        d = I.make_config(1, m=n, n=n, k=k, seed=91)
+        A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+        C = [torch.empty(n, n, dtype=torch.float64, device="cuda") for _ in range(4)]
+        fl = [torch.empty(n, n, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        ws = torch.empty(casc.casc_workspace_bytes(n, n, k), dtype=torch.uint8, device="cuda")
+        ws8 = torch.empty(casc.casc_i8_workspace_bytes(n, n, k, 14), dtype=torch.uint8,
+                          device="cuda")
+
+        def step():
+            casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=C[0], C_lo=C[1], flags=fl[0],
+                                  workspace=ws)
+            casc.casc_i8_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=C[2], C_lo=C[3], flags=fl[1],
+                                     workspace=ws8)
+
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        ref = [N(t).copy() for t in C + fl]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for t in C:
+            t.fill_(float("nan"))
+        g.replay()
+        g.replay()
+        torch.cuda.synchronize()
+        got = [N(t) for t in C + fl]
+        outs[n] = all(np.array_equal(np.ascontiguousarray(a).view(np.uint8),
+                                     np.ascontiguousarray(b).view(np.uint8))
+                      for a, b in zip(got, ref))
+    assert all(outs.values()), outs
