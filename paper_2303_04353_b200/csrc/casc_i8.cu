@@ -301,6 +301,61 @@ __device__ __forceinline__ double rn_u192(const U192& M, int w, bool neg, U192& 
   return make_double(neg, q, w + c);
 }
 
+// T = (RN(x), RN(x - RN(x))) for x = S 2^w, S a signed 192-bit integer.  When
+// w >= -1022 every nonzero result is normal and the rounding position is
+// simply 53 bits below the leading bit: a 128-bit fast path (|S| < 2^145, so
+// the cut c = len - 53 <= 92); otherwise the general rn_u192 (subnormal grid).
+// Both give the same bits (tests/test_gpu_i8.py vs the big-integer oracle).
+__device__ __forceinline__ void rn_pair(U192 S, int w, double& hi, double& lo) {
+  const bool neg = (long long)S.l2 < 0;
+  if (neg) S = u192_neg(S);
+  if (w < -1022) {
+    U192 R, R2;
+    bool rneg, r2neg;
+    hi = rn_u192(S, w, neg, R, rneg);
+    lo = rn_u192(R, w, neg != rneg, R2, r2neg);
+    return;
+  }
+  typedef unsigned __int128 u128;
+  const int len = u192_bitlen(S);
+  if (len <= 53) {  // exact (S = 0 gives +0)
+    hi = make_double(neg, S.l0, w);
+    lo = 0.0;
+    return;
+  }
+  const int c = len - 53;
+  unsigned long long q;
+  u128 rem;
+  if (c < 64) {  // len < 117: S.l2 == 0
+    const u128 v = ((u128)S.l1 << 64) | S.l0;
+    q = (unsigned long long)(v >> c);
+    rem = v & (((u128)1 << c) - 1);
+  } else {
+    const u128 v = ((u128)S.l2 << 64) | S.l1;
+    q = (unsigned long long)(v >> (c - 64));
+    rem = ((u128)(S.l1 & ((1ull << (c - 64)) - 1)) << 64) | S.l0;
+  }
+  const u128 half = (u128)1 << (c - 1);
+  const bool up = rem > half || (rem == half && (q & 1ull));
+  const u128 R = up ? (((u128)1 << c) - rem) : rem;
+  hi = make_double(neg, q + (up ? 1ull : 0ull), w + c);
+  const bool lneg = neg != up;
+  const unsigned long long Rh = (unsigned long long)(R >> 64), Rl = (unsigned long long)R;
+  const int len2 = Rh ? 128 - __clzll((long long)Rh) : (Rl ? 64 - __clzll((long long)Rl) : 0);
+  if (len2 == 0) {
+    lo = 0.0;
+  } else if (len2 <= 53) {
+    lo = make_double(lneg, Rl, w);
+  } else {
+    const int c2 = len2 - 53;
+    const unsigned long long q2 = (unsigned long long)(R >> c2);
+    const u128 rem2 = R & (((u128)1 << c2) - 1);
+    const u128 half2 = (u128)1 << (c2 - 1);
+    const bool up2 = rem2 > half2 || (rem2 == half2 && (q2 & 1ull));
+    lo = make_double(lneg, q2 + (up2 ? 1ull : 0ull), w + c2);
+  }
+}
+
 // exact conversion of an integer-valued double (|w| < 2^126) to int128
 __device__ __forceinline__ __int128 to_i128(double w) {
   if (fabs(w) < 9.0e18) return (__int128)__double2ll_rz(w);
@@ -1128,13 +1183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 sw[2 * TR * TR] = S.l2;
                 continue;
               }
-              const bool neg = (long long)S.l2 < 0;
-              if (neg) S = u192_neg(S);
-              const int w0 = ei + sF[c0 + i] - 12 - 8 * (y - 1);
-              U192 R, R2;
-              bool rneg, r2neg;
-              th[i] = rn_u192(S, w0, neg, R, rneg);
-              tl[i] = rn_u192(R, w0, neg != rneg, R2, r2neg);
+              rn_pair(S, ei + sF[c0 + i] - 12 - 8 * (y - 1), th[i], tl[i]);
             }
 #ifdef CASC_I8_PROF
             if (th[0] == 12345.0) tpa = 0;
@@ -1288,15 +1337,10 @@ __global__ void __launch_bounds__(256) i8_split_reduce_kernel(const GemmArgs p) 
           p.split_ws + ((tile * p.ks + part) * 2 + rank) * 3 * TR * TR + col * TR + lr;
       S = u192_add(S, U192{sw[0], sw[TR * TR], sw[2 * TR * TR]});
     }
-    const bool neg = (long long)S.l2 < 0;
-    if (neg) S = u192_neg(S);
     const int ei = *reinterpret_cast<const int32_t*>(p.pa + exp_at(p.ga, i, 0));
     const int fj = *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, j, 0));
-    const int w0 = ei + fj - 12 - 8 * (y - 1);
-    U192 R, R2;
-    bool rneg, r2neg;
-    double ch = rn_u192(S, w0, neg, R, rneg);
-    double cl = rn_u192(R, w0, neg != rneg, R2, r2neg);
+    double ch, cl;
+    rn_pair(S, ei + fj - 12 - 8 * (y - 1), ch, cl);
     const uint8_t flag = fabs(ch) <= mulp2((double)p.k, ei + fj - 50) ? 1 : 0;
     double* oh = p.C_hi + i * p.ldc + j;
     double* ol = p.C_lo + i * p.ldc + j;

@@ -394,3 +394,38 @@ def test_i8_split_mode_bitwise(casc, orc, m, n, k):
     o_hi, o_lo, o_fl = orc.i8_casc_gemm(d["A_hi"][rows], d["A_lo"][rows], d["B_hi"], d["B_lo"])
     assert bitwise(split[0][rows], o_hi) and bitwise(split[1][rows], o_lo)
     assert np.array_equal(split[2][rows], o_fl)
+
+
+def test_i8_rounding_ties_and_near_ties(casc, orc):
+    """Panel values whose exact product sits exactly halfway between two
+    doubles (at T.hi's and at T.lo's rounding position) or one unit of the
+    fixed-point grid away from it: the kernel's integer rounding (R25 rev. 2,
+    the 128-bit fast path) must pick the same neighbour as the oracle's big
+    integer rounding, bit for bit."""
+    rng = np.random.default_rng(17)
+    m, n = 40, 36
+    A_hi = np.zeros((m, 1))
+    B_hi = np.zeros((1, n))
+    # (1 + a 2^-26)(1 + b 2^-27) = 1 + a 2^-26 + b 2^-27 + ab 2^-53: ties at the
+    # 2^-53 position for odd ab, different parities of the kept part
+    for i in range(m):
+        A_hi[i, 0] = (1.0 + float(rng.integers(1, 2**20)) * 2.0**-46) * (-1.0) ** i
+    for j in range(n):
+        B_hi[0, j] = 1.0 + float(rng.integers(1, 2**20)) * 2.0**-47
+    A_hi[::3, 0] = 1.0 + 2.0**-26
+    B_hi[0, ::4] = 1.0 + 2.0**-27
+    A_lo = np.zeros_like(A_hi)
+    B_lo = np.zeros_like(B_hi)
+    A_lo[1::5, 0] = 2.0**-60  # ties at the lo position too
+    B_lo[0, 2::5] = -(2.0**-61)
+    d = {"A_hi": A_hi, "A_lo": A_lo, "B_hi": B_hi, "B_lo": B_lo}
+    C_hi, C_lo, fl = gpu_gemm(casc, d)
+    o_hi, o_lo, o_fl = orc.i8_casc_gemm(A_hi, A_lo, B_hi, B_lo)
+    assert bitwise(C_hi, o_hi) and bitwise(C_lo, o_lo) and np.array_equal(fl, o_fl)
+    # the products really are DD-exact here: C_hi + C_lo == the exact product
+    from fractions import Fraction as F
+    for i in range(0, m, 7):
+        for j in range(0, n, 5):
+            ex = (F(A_hi[i, 0]) + F(A_lo[i, 0])) * (F(B_hi[0, j]) + F(B_lo[0, j]))
+            err = abs(F(C_hi[i, j]) + F(C_lo[i, j]) - ex)
+            assert err <= abs(ex) * F(2) ** -104
