@@ -106,7 +106,8 @@ size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k);
  * copies overlap the kernels, pageable memory works but serialises them.
  * Result: bitwise the casc_gemm_fp64x2 result of the same operands.
  * Pipeline over blocks of C = row slabs of A (slab_rows rows) x column slabs
- * of B (slab_cols columns; each 0 = 4096, rounded up to a multiple of 64), row slab
+ * of B (slab_cols columns; each 0 = 4096 for a dimension >= 8192, else half the
+ * dimension but at least 1024; rounded up to a multiple of 64), row slab
  * outer: an internal H2D stream copies A_0, then the column slabs of B, then
  * the next row slabs of A ahead of their use; the caller's stream splits each
  * slab once and multiplies block after block; an internal D2H stream returns
@@ -336,7 +337,8 @@ int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                            casc_stream_t stream);
 
 /* casc_gemm_fp64x2_host for the INT8 cascade: host-resident operands streamed
- * in blocks (slab_rows, slab_cols: 0 = 4096, rounded up to multiples of 256), bitwise
+ * in blocks (slab_rows, slab_cols: 0 = the casc_gemm_fp64x2_host default,
+ * rounded up to multiples of 256), bitwise
  * the casc_i8_gemm_fp64x2 result; memory, ordering and errors as
  * casc_gemm_fp64x2_host (CASC_ERR_INVALID also for y outside [3, 15]). */
 int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k,

@@ -404,8 +404,8 @@ int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi, c
     const int64_t l = (lim + blk - 1) / blk * blk;
     return v < l ? v : l;
   };
-  const int64_t sr = fit(slab_rows ? slab_rows : 4096, casc::TM, m);
-  const int64_t sc = fit(slab_cols ? slab_cols : 4096, casc::TN, n);
+  const int64_t sr = fit(slab_rows ? slab_rows : casc::hostpipe::default_slab(m), casc::TM, m);
+  const int64_t sc = fit(slab_cols ? slab_cols : casc::hostpipe::default_slab(n), casc::TN, n);
   const casc::Widths w = widths_for(k);
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
   int launches = 0;

@@ -40,6 +40,15 @@ inline int streams(Streams** out) {
   return CASC_OK;
 }
 
+// Default slab extent along a dimension of `dim`: 4096 for large matrices; half
+// the dimension (at least 1024) below 8192, so that the first blocks arrive
+// early while each block still fills several waves of the GPU.
+inline int64_t default_slab(int64_t dim) {
+  if (dim >= 8192) return 4096;
+  const int64_t h = (dim + 1) / 2;
+  return h > 1024 ? h : 1024;
+}
+
 // k == 0: C := 0 and flags := 0 on the host, after the stream's prior work
 inline int zero_host_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc,
                        uint8_t* flags, cudaStream_t st) {

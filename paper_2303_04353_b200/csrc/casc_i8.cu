@@ -1596,8 +1596,8 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi
     const int64_t l = (lim + blk - 1) / blk * blk;
     return v < l ? v : l;
   };
-  const int64_t sr = fit(slab_rows ? slab_rows : 4096, m);
-  const int64_t sc = fit(slab_cols ? slab_cols : 4096, n);
+  const int64_t sr = fit(slab_rows ? slab_rows : casc::hostpipe::default_slab(m), m);
+  const int64_t sc = fit(slab_cols ? slab_cols : casc::hostpipe::default_slab(n), n);
   const int gmax = 2 * (sms / 2);  // every block's ws_grid fits
   double* gws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&gws), i8::cta_ws_bytes(gmax), st) != cudaSuccess)
