@@ -82,6 +82,10 @@ def _setup(L):
                                    ctypes.c_int]
     L.orc_casc_syrk.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
                                 _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
+    L.orc_dd_div.argtypes = [_d, _d, _d, _d, _pd, _pd]
+    L.orc_trsm_diag_inv.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _pd, _pd, _i64, _pd, _pd]
+    L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
+                                _pd, _pd, _i64, ctypes.c_int]
     L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
                               _i64, ctypes.c_int]
     L.orc_exact_entries.argtypes = [_i64, _pd, _pd, _i64, _pd, _pd, _i64, _i64, _pi64, _pi64,
@@ -268,6 +272,41 @@ def casc_syrk(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, nthr
                         A_hi.shape[1] if A_hi.size else 1, beta[0], beta[1], _p(C_hi), _p(C_lo),
                         n, _p(flags, _pu8), nthreads)
     return C_hi, C_lo, flags
+
+
+TRSM_NB = 256
+
+
+def dd_div(xh, xl, yh, yl):
+    """FP64x2 long division (reading R27)."""
+    return _pair(lib().orc_dd_div, xh, xl, yh, yl)
+
+
+def trsm_diag_inv(uplo, diag, A_hi, A_lo):
+    """Inverses of the TRSM_NB diagonal blocks of the triangular A (R27):
+    (nblk, TRSM_NB, TRSM_NB) hi and lo arrays."""
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    m = A_hi.shape[0]
+    nblk = -(-m // TRSM_NB)
+    Ih = np.zeros((nblk, TRSM_NB, TRSM_NB))
+    Il = np.zeros((nblk, TRSM_NB, TRSM_NB))
+    lib().orc_trsm_diag_inv(lo_, dg, m, _p(A_hi), _p(A_lo), m, _p(Ih), _p(Il))
+    return Ih, Il
+
+
+def casc_trsm(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, nthreads: int = 0):
+    """NEXT-4 TRSM (reading R27): X with op(A) X = alpha B, left side, no
+    transpose; A m x m triangular; returns new (X_hi, X_lo)."""
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
+    m, n = X_hi.shape
+    lib().orc_casc_trsm(lo_, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo), max(m, 1),
+                        _p(X_hi), _p(X_lo), max(n, 1), nthreads)
+    return X_hi, X_lo
 
 
 def dd_gemm(A_hi, A_lo, B_hi, B_lo, nthreads: int = 0):

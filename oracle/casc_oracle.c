@@ -644,3 +644,118 @@ void orc_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, double 
   free(Tl);
   free(Tf);
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-4, level-3 BLAS on the cascaded GEMM ("All Level-3 BLAS */
+/* algorithms can be written in terms of GEMM ... integrating Phase 1 into    */
+/* specific calls of say TRSM"): TRSM, reading R27.            */
+/* ------------------------------------------------------------------------- */
+#define TRSM_NB 256
+
+/* DD / DD, long division: q1 = xh / yh; r = x - q1 y (DD); q2 = r.hi / yh;
+ * Fast2Sum(q1, q2). */
+void orc_dd_div(double xh, double xl, double yh, double yl, double* rh, double* rl) {
+  const double q1 = xh / yh;
+  double ph, pl, sh, sl;
+  orc_dd_mul(q1, 0.0, yh, yl, &ph, &pl);
+  orc_dd_add(xh, xl, -ph, -pl, &sh, &sl);
+  const double q2 = sh / yh;
+  orc_fast_two_sum(q1, q2, rh, rl);
+}
+
+/* Inverses of the diagonal blocks (TRSM_NB, the last one ragged) of the m x m
+ * triangular A (uplo 0 lower / 1 upper; diag 0 non-unit / 1 unit): block b is
+ * Inv[b][TRSM_NB][TRSM_NB] (row-major, zeros outside its triangle), column j by
+ * substitution in FP64x2: lower y_j = 1 / a_jj, then for i > j
+ * y_i = -(sum_{l=j}^{i-1} a_il y_l) / a_ii (l ascending); upper mirrored. */
+void orc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* Ahi, const double* Alo,
+                       int64_t lda, double* Ihi, double* Ilo) {
+  const int64_t nblk = (m + TRSM_NB - 1) / TRSM_NB;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t r0 = b * TRSM_NB;
+    const int nb = (int)((m - r0) < TRSM_NB ? (m - r0) : TRSM_NB);
+    double* yh = Ihi + b * TRSM_NB * TRSM_NB;
+    double* yl = Ilo + b * TRSM_NB * TRSM_NB;
+    for (int i = 0; i < TRSM_NB * TRSM_NB; ++i) yh[i] = yl[i] = 0.0;
+#define AH(i, l) Ahi[(r0 + (i)) * lda + r0 + (l)]
+#define AL(i, l) Alo[(r0 + (i)) * lda + r0 + (l)]
+    for (int j = 0; j < nb; ++j) {
+      if (diag) {
+        yh[j * TRSM_NB + j] = 1.0;
+      } else {
+        orc_dd_div(1.0, 0.0, AH(j, j), AL(j, j), &yh[j * TRSM_NB + j], &yl[j * TRSM_NB + j]);
+      }
+      const int step = uplo == 0 ? 1 : -1;
+      for (int i = j + step; i >= 0 && i < nb; i += step) {
+        double sh = 0.0, sl = 0.0;
+        const int lo = uplo == 0 ? j : i + 1, hi = uplo == 0 ? i - 1 : j;
+        for (int l = lo; l <= hi; ++l) {
+          double ph, pl;
+          orc_dd_mul(AH(i, l), AL(i, l), yh[l * TRSM_NB + j], yl[l * TRSM_NB + j], &ph, &pl);
+          orc_dd_add(sh, sl, ph, pl, &sh, &sl);
+        }
+        if (diag) {
+          yh[i * TRSM_NB + j] = -sh;
+          yl[i * TRSM_NB + j] = -sl;
+        } else {
+          orc_dd_div(-sh, -sl, AH(i, i), AL(i, i), &yh[i * TRSM_NB + j], &yl[i * TRSM_NB + j]);
+        }
+      }
+    }
+#undef AH
+#undef AL
+  }
+}
+
+/* TRSM, left side, no transpose: solve op(A) X = alpha B, X overwrites the
+ * m x n B (ldb).  B := alpha (x) B; the diagonal blocks are inverted
+ * (orc_trsm_diag_inv); then block by block (ascending for lower, descending
+ * for upper): X_b = Inv_b B_b and B_rest := B_rest - A_rest,b X_b, both with the
+ * cascaded GEMM (orc_casc_gemm_ex: alpha 1, beta 0, then alpha -1, beta 1). */
+void orc_casc_trsm(int uplo, int diag, int64_t m, int64_t n, double ah, double al,
+                   const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
+                   int64_t ldb, int nthreads) {
+  if (m == 0 || n == 0) return;
+  if (!(ah == 1.0 && al == 0.0))
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double rh = 0.0, rl = 0.0;
+        if (!(ah == 0.0 && al == 0.0))
+          orc_dd_mul(ah, al, Bhi[i * ldb + j], Blo[i * ldb + j], &rh, &rl);
+        Bhi[i * ldb + j] = rh;
+        Blo[i * ldb + j] = rl;
+      }
+  if (ah == 0.0 && al == 0.0) return;
+  const int64_t nblk = (m + TRSM_NB - 1) / TRSM_NB;
+  double* Ihi = (double*)malloc(sizeof(double) * (size_t)(nblk * TRSM_NB * TRSM_NB));
+  double* Ilo = (double*)malloc(sizeof(double) * (size_t)(nblk * TRSM_NB * TRSM_NB));
+  double* Th = (double*)malloc(sizeof(double) * (size_t)(TRSM_NB * n));
+  double* Tl = (double*)malloc(sizeof(double) * (size_t)(TRSM_NB * n));
+  orc_trsm_diag_inv(uplo, diag, m, Ahi, Alo, lda, Ihi, Ilo);
+  for (int64_t s = 0; s < nblk; ++s) {
+    const int64_t b = uplo == 0 ? s : nblk - 1 - s;
+    const int64_t r0 = b * TRSM_NB, nb = (m - r0) < TRSM_NB ? (m - r0) : TRSM_NB;
+    const int64_t r1 = r0 + nb;
+    /* X_b = Inv_b B_b (into T, then back into B_b) */
+    orc_casc_gemm_ex(0, 0, nb, n, nb, 1.0, 0.0, Ihi + b * TRSM_NB * TRSM_NB,
+                     Ilo + b * TRSM_NB * TRSM_NB, TRSM_NB, Bhi + r0 * ldb, Blo + r0 * ldb, ldb,
+                     0.0, 0.0, Th, Tl, n, NULL, nthreads);
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        Bhi[(r0 + i) * ldb + j] = Th[i * n + j];
+        Blo[(r0 + i) * ldb + j] = Tl[i * n + j];
+      }
+    /* B_rest := B_rest - A_rest,b X_b */
+    if (uplo == 0 && r1 < m)
+      orc_casc_gemm_ex(0, 0, m - r1, n, nb, -1.0, 0.0, Ahi + r1 * lda + r0, Alo + r1 * lda + r0,
+                       lda, Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
+                       Blo + r1 * ldb, ldb, NULL, nthreads);
+    if (uplo == 1 && r0 > 0)
+      orc_casc_gemm_ex(0, 0, r0, n, nb, -1.0, 0.0, Ahi + r0, Alo + r0, lda, Bhi + r0 * ldb,
+                       Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi, Blo, ldb, NULL, nthreads);
+  }
+  free(Ihi);
+  free(Ilo);
+  free(Th);
+  free(Tl);
+}

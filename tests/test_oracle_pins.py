@@ -476,6 +476,88 @@ def test_syrk_oracle(orc, uplo, trans):
     assert np.all(Z[2][tri] == 0) and np.all(Z[2][~tri] == 9)
 
 
+def _tri_dd(m, uplo, seed, unit=False):
+    """Diagonally dominant triangular FP64x2 matrix (well conditioned)."""
+    rng = np.random.default_rng(seed)
+    hi = rng.uniform(-1, 1, (m, m)) / m
+    hi = np.tril(hi) if uplo == "L" else np.triu(hi)
+    lo = hi * 2.0 ** -53 * rng.uniform(-1, 1, (m, m))
+    d = 1.0 + rng.uniform(0, 1, m)
+    hi[np.arange(m), np.arange(m)] = 1.0 if unit else d
+    lo[np.arange(m), np.arange(m)] = 0.0 if unit else d * 2.0 ** -54
+    return hi, lo
+
+
+def test_dd_div_oracle(orc):
+    """R27 FP64x2 division: within 2^-100 of the exact quotient (Fractions)."""
+    rng = random.Random(5)
+    for _ in range(3000):
+        xh = rng.uniform(-1, 1) * 2.0 ** rng.randint(-40, 40)
+        yh = rng.uniform(0.5, 1) * (-1) ** rng.randint(0, 1) * 2.0 ** rng.randint(-40, 40)
+        xl = xh * 2.0 ** -53 * rng.uniform(-1, 1)
+        yl = yh * 2.0 ** -53 * rng.uniform(-1, 1)
+        qh, ql = orc.dd_div(xh, xl, yh, yl)
+        ex = (fr(xh) + fr(xl)) / (fr(yh) + fr(yl))
+        assert abs(fr(qh) + fr(ql) - ex) <= abs(ex) * F(2) ** -100
+        assert abs(ql) <= abs(qh) * 2.0 ** -52  # normalised
+
+
+@pytest.mark.parametrize("uplo,unit", [("L", False), ("U", False), ("L", True)])
+def test_trsm_diag_inverse_oracle(orc, uplo, unit):
+    """R27 diagonal-block inverses: Inv_b A_bb = I within 2^-95 (exact rationals),
+    zeros outside the triangle, the ragged last block included."""
+    m = 300
+    A_hi, A_lo = _tri_dd(m, uplo, 3, unit)
+    Ih, Il = orc.trsm_diag_inv(uplo, "U" if unit else "N", A_hi, A_lo)
+    assert Ih.shape == (2, 256, 256)
+    for b, (r0, nb, cols) in enumerate([(0, 256, (0, 97, 255)), (256, 44, range(44))]):
+        inv = Ih[b][:nb, :nb]
+        tri = np.tril(np.ones((nb, nb), bool)) if uplo == "L" else np.triu(np.ones((nb, nb), bool))
+        assert np.all(inv[~tri] == 0) and np.all(Ih[b][nb:, :] == 0)
+        for j in cols:
+            for i in range(0, nb, 7 if nb > 64 else 1):
+                s = sum((fr(Ih[b][i, l]) + fr(Il[b][i, l]))
+                        * (fr(A_hi[r0 + l, r0 + j]) + fr(A_lo[r0 + l, r0 + j])) for l in range(nb))
+                assert abs(s - (1 if i == j else 0)) <= F(2) ** -95
+
+
+@pytest.mark.parametrize("uplo,unit,m,n", [("L", False, 40, 5), ("U", False, 300, 3),
+                                           ("L", True, 300, 2)])
+def test_trsm_oracle(orc, uplo, unit, m, n):
+    """R27 TRSM: the exact residual of op(A) X = B (dyadic rationals, no
+    rounding) within 2^-96 (|A||X|) row by row (diagonally dominant A, so X is
+    then accurate; two blocks with the cascaded-GEMM update for m = 300) and,
+    for m = 40, X within 2^-95 of the exact solution; alpha = 2 scales exactly;
+    alpha = 0 gives X = 0."""
+    A_hi, A_lo = _tri_dd(m, uplo, 7, unit)
+    rng = np.random.default_rng(9)
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -53 * rng.uniform(-1, 1, (m, n))
+    X_hi, X_lo = orc.casc_trsm(uplo, "U" if unit else "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    A = [[fr(A_hi[i, j]) + fr(A_lo[i, j]) for j in range(m)] for i in range(m)]
+    X = [[fr(X_hi[i, j]) + fr(X_lo[i, j]) for j in range(n)] for i in range(m)]
+    for i in range(0, m, 1 if m <= 40 else 9):
+        lo, hi = (0, i + 1) if uplo == "L" else (i, m)
+        for j in range(n):
+            r = sum(A[i][l] * X[l][j] for l in range(lo, hi)) - (fr(B_hi[i, j]) + fr(B_lo[i, j]))
+            mag = sum(abs(A[i][l] * X[l][j]) for l in range(lo, hi))
+            assert abs(r) <= F(2) ** -96 * mag
+    if m <= 40:  # exact solution by substitution
+        order = range(m) if uplo == "L" else range(m - 1, -1, -1)
+        for j in range(n):
+            x = [F(0)] * m
+            for i in order:
+                lo, hi = (0, i) if uplo == "L" else (i + 1, m)
+                x[i] = (fr(B_hi[i, j]) + fr(B_lo[i, j])
+                        - sum(A[i][l] * x[l] for l in range(lo, hi))) / A[i][i]
+            for i in range(m):
+                assert abs(X[i][j] - x[i]) <= F(2) ** -95 * (abs(x[i]) + 1)
+    Y = orc.casc_trsm(uplo, "U" if unit else "N", (2.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    assert np.array_equal(Y[0], 2 * X_hi) and np.array_equal(Y[1], 2 * X_lo)
+    Z = orc.casc_trsm(uplo, "N", (0.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    assert np.all(Z[0] == 0) and np.all(Z[1] == 0)
+
+
 def test_exact_accumulator_vs_fractions(orc):
     """ORACLE-EXACT superaccumulator equals Fraction sums, over
     wide exponent ranges and with exact cancellation."""
