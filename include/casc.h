@@ -258,6 +258,30 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
                      uint8_t* flags, void* workspace, size_t workspace_bytes,
                      casc_stream_t stream);
 
+/* NEXT-4, TRSM on the cascaded GEMM (reading R27):
+ * left side, no transpose: solve op(A) X = alpha (x) B for X, A m x m
+ * triangular (uplo CASC_LOWER / CASC_UPPER; diag CASC_NONUNIT / CASC_UNIT:
+ * the diagonal is taken as 1 and not read), X overwrites the m x n B (ldb >=
+ * max(1,n)); only A's triangle is read.  B := alpha (x) B; the 256 x 256
+ * diagonal blocks of A are inverted in FP64x2 (casc_trsm_diag_inv); then, block
+ * by block (ascending for lower, descending for upper), X_b = Inv_b B_b and
+ * B_rest := B_rest - A_rest,b X_b with casc_gemm_fp64x2_ex.  Device memory for
+ * the inverses and one block of X comes from the stream-ordered pool; no host
+ * synchronisation.  alpha == 0: X := 0, A not read.  Errors as
+ * casc_gemm_fp64x2_ex (CASC_ERR_INVALID also for bad uplo / diag and for B
+ * overlapping A). */
+typedef enum { CASC_NONUNIT = 0, CASC_UNIT = 1 } casc_diag;
+int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n,
+                     double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda,
+                     double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream);
+/* Test / inspection export of the TRSM's first step: the inverses of the
+ * 256 x 256 diagonal blocks of the triangular A, inv_hi / inv_lo =
+ * [ceil(m/256)][256][256] row-major FP64x2 (zeros outside the triangle and
+ * beyond a ragged last block), by column substitution in the oracle's order. */
+int casc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi, const double* A_lo,
+                       int64_t lda, double* inv_hi, double* inv_lo, casc_stream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* The paper's simple path (§4.2): phases as separate kernels.  */
 /* ------------------------------------------------------------------------ */

@@ -72,7 +72,8 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_packed_bytes", "casc_i8_finalize", "casc_i8_split", "casc_i8_debug_bins",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
-            "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2"]
+            "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
+            "casc_trsm_diag_inv"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -97,6 +98,48 @@ _sig("casc_gemm_fp64x2_ex", [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, ctype
                              ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _sz, _vp])
 CASC_OP_N, CASC_OP_T = 0, 1
 CASC_LOWER, CASC_UPPER = 0, 1
+CASC_NONUNIT, CASC_UNIT = 0, 1
+TRSM_NB = 256
+_sig("casc_trsm_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double, ctypes.c_double,
+                          _vp, _vp, _i64, _vp, _vp, _i64, _vp])
+_sig("casc_trsm_diag_inv", [ctypes.c_int, ctypes.c_int, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
+
+
+def _uplo_diag(uplo, diag):
+    if uplo not in ("L", "l", "U", "u", 0, 1):
+        raise ValueError("uplo must be 'L' or 'U'")
+    if diag not in ("N", "n", "U", "u", 0, 1):
+        raise ValueError("diag must be 'N' or 'U'")
+    return (CASC_LOWER if uplo in ("L", "l", 0) else CASC_UPPER,
+            CASC_UNIT if diag in ("U", "u", 1) else CASC_NONUNIT)
+
+
+def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, stream=None):
+    """TRSM on the cascaded GEMM (NEXT-4, reading R27): solve op(A) X = alpha B
+    (left side, no transpose), A m x m triangular; X overwrites B_hi / B_lo."""
+    lo, dg = _uplo_diag(uplo, diag)
+    ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, n = B_hi.shape
+    if tuple(A_hi.shape) != (m, m):
+        raise ValueError("A must be m x m")
+    _check(_lib.casc_trsm_fp64x2(lo, dg, m, n, float(ah), float(al), _ptr(A_hi), _ptr(A_lo), lda,
+                                 _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)), "casc_trsm_fp64x2")
+    return B_hi, B_lo
+
+
+def casc_trsm_diag_inv(uplo, diag, A_hi, A_lo, stream=None):
+    """The TRSM's inverted 256 x 256 diagonal blocks: (nblk, 256, 256) hi, lo."""
+    lo, dg = _uplo_diag(uplo, diag)
+    lda = _ld_pair(A_hi, A_lo, "A")
+    m = A_hi.shape[0]
+    nblk = -(-m // TRSM_NB)
+    inv_hi = torch.empty((nblk, TRSM_NB, TRSM_NB), dtype=torch.float64, device=A_hi.device)
+    inv_lo = torch.empty_like(inv_hi)
+    _check(_lib.casc_trsm_diag_inv(lo, dg, m, _ptr(A_hi), _ptr(A_lo), lda, _ptr(inv_hi),
+                                   _ptr(inv_lo), _stream(stream)), "casc_trsm_diag_inv")
+    return inv_hi, inv_lo
 _sig("casc_syrk_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double, ctypes.c_double,
                           _vp, _vp, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp, _i64, _vp,
                           _vp, _sz, _vp])

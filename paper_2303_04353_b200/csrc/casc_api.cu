@@ -18,6 +18,9 @@ cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
                                 const double* t_lo, const uint8_t* fbuf, double* C_hi,
                                 double* C_lo, int64_t ldc, uint8_t* flags, int ab, double ah,
                                 double al, double bh, double bl, int num_sms, cudaStream_t st);
+cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi,
+                                 const double* A_lo, int64_t lda, double* I_hi, double* I_lo,
+                                 cudaStream_t st);
 cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
                                 double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
                                 int num_sms, int uplo, cudaStream_t st);
@@ -668,6 +671,106 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------- TRSM (NEXT-4)
+// Left side, no transpose: op(A) X = alpha B, X overwrites B (reading R27).
+static constexpr int64_t kTrsmNb = 256;
+
+int casc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi, const double* A_lo,
+                       int64_t lda, double* inv_hi, double* inv_lo, casc_stream_t stream) {
+  g_launches = 0;
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (diag != CASC_NONUNIT && diag != CASC_UNIT))
+    return CASC_ERR_INVALID;
+  int r;
+  if ((r = check_mat(A_hi, m, m, lda)) || (r = check_mat(A_lo, m, m, lda))) return r;
+  if (m > 0 && (!inv_hi || !inv_lo)) return CASC_ERR_INVALID;
+  if ((r = device_check(nullptr))) return r;
+  if (m == 0) return CASC_OK;
+  const cudaError_t e =
+      casc::launch_trsm_diag_inv(uplo, diag, m, A_hi, A_lo, lda, inv_hi, inv_lo, S(stream));
+  if (e == cudaSuccess) g_launches = 1;
+  return cuda_status(e);
+}
+
+int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n, double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda, double* B_hi,
+                     double* B_lo, int64_t ldb, casc_stream_t stream) {
+  g_launches = 0;
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (diag != CASC_NONUNIT && diag != CASC_UNIT))
+    return CASC_ERR_INVALID;
+  if (m < 0 || n < 0) return CASC_ERR_INVALID;
+  int r;
+  if ((r = check_mat(A_hi, m, m, lda)) || (r = check_mat(A_lo, m, m, lda))) return r;
+  if ((r = check_mat(B_hi, m, n, ldb)) || (r = check_mat(B_lo, m, n, ldb))) return r;
+  const size_t ea = extent(m, m, lda), eb = extent(m, n, ldb);
+  if (ranges_overlap(B_hi, eb, A_hi, ea) || ranges_overlap(B_hi, eb, A_lo, ea) ||
+      ranges_overlap(B_lo, eb, A_hi, ea) || ranges_overlap(B_lo, eb, A_lo, ea) ||
+      ranges_overlap(B_hi, eb, B_lo, eb))
+    return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  const cudaStream_t st = S(stream);
+  int launches = 0;
+  const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
+  const bool zero_alpha = (alpha_hi == 0.0 && alpha_lo == 0.0);
+  if (!unit_alpha) {  // B := alpha (x) B
+    const cudaError_t e = casc::launch_scale_c(m, n, alpha_hi, alpha_lo, zero_alpha ? 0 : 1, B_hi,
+                                               B_lo, ldb, nullptr, sms, st);
+    if (e != cudaSuccess) return CASC_ERR_CUDA;
+    ++launches;
+  }
+  if (zero_alpha) {
+    g_launches = launches;
+    return CASC_OK;
+  }
+  const int64_t nblk = (m + kTrsmNb - 1) / kTrsmNb;
+  const size_t inv_elems = (size_t)nblk * kTrsmNb * kTrsmNb, t_elems = (size_t)kTrsmNb * n;
+  double* buf = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), (2 * inv_elems + 2 * t_elems) * 8, st) !=
+      cudaSuccess)
+    return CASC_ERR_CUDA;
+  double* inv_hi = buf;
+  double* inv_lo = buf + inv_elems;
+  double* t_hi = inv_lo + inv_elems;
+  double* t_lo = t_hi + t_elems;
+  cudaError_t e = casc::launch_trsm_diag_inv(uplo, diag, m, A_hi, A_lo, lda, inv_hi, inv_lo, st);
+  r = e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA;
+  ++launches;
+  for (int64_t s = 0; s < nblk && r == CASC_OK; ++s) {
+    const int64_t b = uplo == CASC_LOWER ? s : nblk - 1 - s;
+    const int64_t r0 = b * kTrsmNb, nb = std::min(kTrsmNb, m - r0), r1 = r0 + nb;
+    // X_b = Inv_b B_b, into T and back into B_b
+    r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, nb, n, nb, 1.0, 0.0,
+                            inv_hi + b * kTrsmNb * kTrsmNb, inv_lo + b * kTrsmNb * kTrsmNb,
+                            kTrsmNb, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 0.0, 0.0, t_hi, t_lo,
+                            n, nullptr, nullptr, 0, stream);
+    launches += g_launches;
+    if (r) break;
+    if (cudaMemcpy2DAsync(B_hi + r0 * ldb, ldb * 8, t_hi, n * 8, n * 8, nb,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpy2DAsync(B_lo + r0 * ldb, ldb * 8, t_lo, n * 8, n * 8, nb,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      r = CASC_ERR_CUDA;
+      break;
+    }
+    // B_rest := B_rest - A_rest,b X_b
+    g_launches = 0;
+    if (uplo == CASC_LOWER && r1 < m)
+      r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + r1 * lda + r0,
+                              A_lo + r1 * lda + r0, lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb,
+                              1.0, 0.0, B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, nullptr, 0,
+                              stream);
+    if (uplo == CASC_UPPER && r0 > 0)
+      r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + r0, A_lo + r0,
+                              lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo,
+                              ldb, nullptr, nullptr, 0, stream);
+    launches += g_launches;
+  }
+  cudaFreeAsync(buf, st);
+  g_launches = r == CASC_OK ? launches : 0;
   return r;
 }
 

@@ -95,4 +95,64 @@ cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_b
   return launch_scale_c_uplo(m, n, bh, bl, use_beta, C_hi, C_lo, ldc, flags, num_sms, -1, st);
 }
 
+// ---------------------------------------------------------------- TRSM (NEXT-4)
+// Inverses of the TRSM_NB diagonal blocks of the triangular A (reading R27):
+// CTA b inverts block b, thread j computes column j by FP64x2 substitution in
+// the oracle's order (orc_trsm_diag_inv): bitwise the same inverse.  The
+// inverse is written to Inv[b][TRSM_NB][TRSM_NB] (zeros outside the triangle);
+// each thread reads back only its own column.
+constexpr int TRSM_NB = 256;
+
+__global__ void __launch_bounds__(TRSM_NB) trsm_diag_inv_kernel(
+    int uplo, int diag, int64_t m, const double* __restrict__ A_hi,
+    const double* __restrict__ A_lo, int64_t lda, double* __restrict__ I_hi,
+    double* __restrict__ I_lo) {
+  const int64_t b = blockIdx.x, r0 = b * TRSM_NB;
+  const int nb = (int)min((int64_t)TRSM_NB, m - r0);
+  const int j = threadIdx.x;
+  double* yh = I_hi + b * TRSM_NB * TRSM_NB + j;  // column j: element l at yh[l * TRSM_NB]
+  double* yl = I_lo + b * TRSM_NB * TRSM_NB + j;
+  for (int i = 0; i < TRSM_NB; ++i) yh[i * TRSM_NB] = yl[i * TRSM_NB] = 0.0;
+  if (j >= nb) return;
+  const double* ah = A_hi + r0 * lda + r0;
+  const double* al = A_lo + r0 * lda + r0;
+  if (diag) {
+    yh[j * TRSM_NB] = 1.0;
+  } else {
+    double qh, ql;
+    dd_div(1.0, 0.0, ah[j * lda + j], al[j * lda + j], qh, ql);
+    yh[j * TRSM_NB] = qh;
+    yl[j * TRSM_NB] = ql;
+  }
+  const int step = uplo == 0 ? 1 : -1;
+  for (int i = j + step; i >= 0 && i < nb; i += step) {
+    double sh = 0.0, sl = 0.0;
+    const int lo = uplo == 0 ? j : i + 1, hi = uplo == 0 ? i - 1 : j;
+    for (int l = lo; l <= hi; ++l) {
+      double ph, pl;
+      dd_mul(ah[i * lda + l], al[i * lda + l], yh[l * TRSM_NB], yl[l * TRSM_NB], ph, pl);
+      dd_add(sh, sl, ph, pl, sh, sl);
+    }
+    if (diag) {
+      yh[i * TRSM_NB] = -sh;
+      yl[i * TRSM_NB] = -sl;
+    } else {
+      double qh, ql;
+      dd_div(-sh, -sl, ah[i * lda + i], al[i * lda + i], qh, ql);
+      yh[i * TRSM_NB] = qh;
+      yl[i * TRSM_NB] = ql;
+    }
+  }
+}
+
+cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi,
+                                 const double* A_lo, int64_t lda, double* I_hi, double* I_lo,
+                                 cudaStream_t st) {
+  const int64_t nblk = (m + TRSM_NB - 1) / TRSM_NB;
+  if (nblk == 0) return cudaSuccess;
+  trsm_diag_inv_kernel<<<(unsigned)nblk, TRSM_NB, 0, st>>>(uplo, diag, m, A_hi, A_lo, lda, I_hi,
+                                                           I_lo);
+  return cudaGetLastError();
+}
+
 }  // namespace casc

@@ -44,6 +44,18 @@ __device__ __forceinline__ void dd_mul(double xh, double xl, double yh, double y
   fast_two_sum(p, e, rh, rl);
 }
 
+// FP64x2 long division (reading R27): q1 = x.hi / y.hi; r = x - q1 y;
+// q2 = r.hi / y.hi; Fast2Sum(q1, q2).
+__device__ __forceinline__ void dd_div(double xh, double xl, double yh, double yl, double& rh,
+                                       double& rl) {
+  const double q1 = __ddiv_rn(xh, yh);
+  double ph, pl, sh, sl;
+  dd_mul(q1, 0.0, yh, yl, ph, pl);
+  dd_add(xh, xl, -ph, -pl, sh, sl);
+  const double q2 = __ddiv_rn(sh, yh);
+  fast_two_sum(q1, q2, rh, rl);
+}
+
 // BLAS-style update C := alpha (x) T (+) beta (x) C_old (NEXT-4, reading R21).
 __device__ __forceinline__ void apply_alpha_beta(double& th, double& tl, double ah, double al,
                                                  double bh, double bl, double ch, double cl,

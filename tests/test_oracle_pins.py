@@ -532,7 +532,7 @@ def test_trsm_oracle(orc, uplo, unit, m, n):
     A_hi, A_lo = _tri_dd(m, uplo, 7, unit)
     rng = np.random.default_rng(9)
     B_hi = rng.uniform(-1, 1, (m, n))
-    B_lo = B_hi * 2.0 ** -53 * rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))  # normalised pairs: exact scaling
     X_hi, X_lo = orc.casc_trsm(uplo, "U" if unit else "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo)
     A = [[fr(A_hi[i, j]) + fr(A_lo[i, j]) for j in range(m)] for i in range(m)]
     X = [[fr(X_hi[i, j]) + fr(X_lo[i, j]) for j in range(n)] for i in range(m)]
