@@ -372,6 +372,19 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k,
                              uint8_t* flags, int y, int64_t slab_rows, int64_t slab_cols,
                              casc_stream_t stream);
 
+/* SYRK on the INT8 cascade (NEXT-4): casc_syrk_fp64x2's semantics (uplo,
+ * trans, alpha, beta, untouched other triangle, flags n x n) through y int8
+ * slices; only the pair tiles holding triangle elements run, and every
+ * stored element is bitwise what casc_i8_gemm_fp64x2_ex(trans, !trans, ...,
+ * A, A, ...) stores there.  Stream-ordered temporary workspace.  Errors as
+ * casc_i8_gemm_fp64x2_ex. */
+int casc_i8_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
+                        double alpha_hi, double alpha_lo,
+                        const double* A_hi, const double* A_lo, int64_t lda,
+                        double beta_hi, double beta_lo,
+                        double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, int y, casc_stream_t stream);
+
 /* NEXT-4 on the INT8 cascade: C := alpha (x) op(A) op(B) (+) beta (x) C with the
  * semantics, argument layout and errors of casc_gemm_fp64x2_ex (reading R21),
  * the product computed through y int8 slices (bitwise the casc_i8_gemm_fp64x2

@@ -106,6 +106,8 @@ def _setup(L):
     L.orc_i8_casc_gemm_ex.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _i64, _d, _d,
                                       _pd, _pd, _i64, _pd, _pd, _i64, _d, _d, _pd, _pd, _i64,
                                       _pu8, ctypes.c_int, ctypes.c_int]
+    L.orc_i8_casc_syrk.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
+                                   _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int, ctypes.c_int]
 
 
 def _p(a, ptr=_pd):
@@ -428,6 +430,23 @@ def i8_panel_value(b, w0: int):
     nearest x = sum_s b[s] 2^(w0 + 8(y-1-s)), y = len(b)."""
     b = np.ascontiguousarray(b, dtype=np.int64)
     return _pair(lib().orc_i8_panel_value, _p(b, _pi64), b.size, int(w0))
+
+
+def i8_casc_syrk(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, y: int = 14,
+                 nthreads: int = 0):
+    """NEXT-4 SYRK on the INT8 cascade: the triangle of i8_casc_gemm_ex(trans,
+    not trans, alpha, A, A, beta, C); other triangle and its flags unchanged."""
+    lo = 0 if uplo in ("L", "l", 0) else 1
+    tr = int(trans in ("T", "t", 1, True))
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    C_hi, C_lo = _c64(C_hi).copy(), _c64(C_lo).copy()
+    n = C_hi.shape[0]
+    k = A_hi.shape[0] if tr else A_hi.shape[1]
+    flags = np.zeros((n, n), dtype=np.uint8) if flags is None else np.array(flags, np.uint8)
+    lib().orc_i8_casc_syrk(lo, tr, n, k, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                           A_hi.shape[1] if A_hi.size else 1, beta[0], beta[1], _p(C_hi),
+                           _p(C_lo), n, _p(flags, _pu8), int(y), nthreads)
+    return C_hi, C_lo, flags
 
 
 def i8_casc_gemm(A_hi, A_lo, B_hi, B_lo, y: int = 14, nthreads: int = 0):

@@ -347,3 +347,32 @@ void orc_i8_casc_gemm_ex(int transa, int transb, int64_t m, int64_t n, int64_t k
   free(p_h);
   free(p_l);
 }
+
+/* NEXT-4 SYRK on the INT8 cascade: by definition the lower
+ * (uplo 0) / upper (uplo 1) triangle of orc_i8_casc_gemm_ex(trans, !trans, A,
+ * A); the other triangle of C and flags (n x n, nullable) is left as it is. */
+void orc_i8_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, double al,
+                      const double* Ahi, const double* Alo, int64_t lda, double bh, double bl,
+                      double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int y,
+                      int nthreads) {
+  double* Th = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  double* Tl = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  uint8_t* Tf = (uint8_t*)calloc((size_t)(n * n + 1), 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Th[i * n + j] = Chi[i * ldc + j];
+      Tl[i * n + j] = Clo[i * ldc + j];
+    }
+  orc_i8_casc_gemm_ex(trans, !trans, n, n, k, ah, al, Ahi, Alo, lda, Ahi, Alo, lda, bh, bl, Th,
+                      Tl, n, Tf, y, nthreads);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      if (uplo == 0 ? j > i : j < i) continue;
+      Chi[i * ldc + j] = Th[i * n + j];
+      Clo[i * ldc + j] = Tl[i * n + j];
+      if (flags) flags[i * n + j] = Tf[i * n + j];
+    }
+  free(Th);
+  free(Tl);
+  free(Tf);
+}

@@ -73,7 +73,7 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
-            "casc_trsm_diag_inv"]
+            "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -112,6 +112,33 @@ def _uplo_diag(uplo, diag):
         raise ValueError("diag must be 'N' or 'U'")
     return (CASC_LOWER if uplo in ("L", "l", 0) else CASC_UPPER,
             CASC_UNIT if diag in ("U", "u", 1) else CASC_NONUNIT)
+
+
+_sig("casc_i8_syrk_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double,
+                             ctypes.c_double, _vp, _vp, _i64, ctypes.c_double, ctypes.c_double, _vp,
+                             _vp, _i64, _vp, ctypes.c_int, _vp])
+
+
+def casc_i8_syrk_fp64x2(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, y: int = 14,
+                        stream=None):
+    """casc_syrk_fp64x2 on the INT8 cascade (NEXT-3 + NEXT-4)."""
+    lo, _ = _uplo_diag(uplo, "N")
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
+    bh, bl = (beta, 0.0) if isinstance(beta, (int, float)) else beta
+    n = C_hi.shape[0]
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    if A_hi is None:
+        lda, k = 1, 0
+    else:
+        lda = _ld_pair(A_hi, A_lo, "A")
+        k = A_hi.shape[0] if tr else A_hi.shape[1]
+    if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (n, n)):
+        raise TypeError("flags must be a contiguous (n, n) uint8 CUDA tensor")
+    _check(_lib.casc_i8_syrk_fp64x2(lo, tr, n, k, float(ah), float(al), _ptr(A_hi), _ptr(A_lo),
+                                    lda, float(bh), float(bl), _ptr(C_hi), _ptr(C_lo), ldc,
+                                    _ptr(flags), int(y), _stream(stream)), "casc_i8_syrk_fp64x2")
+    return C_hi, C_lo, flags
 
 
 def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, stream=None):

@@ -549,6 +549,9 @@ struct GemmArgs {
   // sums the parts and rounds (bitwise the unsplit result: S is exact)
   int ks;
   unsigned long long* split_ws;
+  // SYRK (NEXT-4): 0 every tile; 1 lower (pair tiles touching row >= col, only
+  // those elements stored); 2 upper
+  int tri;
   int ab;               // NEXT-4 update at the final store: 0 none, 1 alpha, 2 alpha and beta
   double ah, al, bh, bl;
 };
@@ -873,11 +876,27 @@ __device__ __forceinline__ int64_t tile_index(int64_t rp, int64_t cb, int64_t RP
   return grp * GROUP_M * RB + cb * gs + (rp - first);
 }
 
+// SYRK work list: the pair tiles (256 rows x 128 columns) that hold elements of
+// the triangle, row pair by row pair: lower cb <= 2 rp + 1, upper cb >= 2 rp
+__device__ __forceinline__ int64_t tri_count(int tri, int64_t rp, int64_t RB) {
+  return tri == 1 ? min(2 * rp + 2, RB) : max(RB - 2 * rp, (int64_t)0);
+}
+__device__ __forceinline__ void tri_tile_of(int tile, int tri, int64_t RP, int64_t RB,
+                                            int64_t& rp, int64_t& cb) {
+  int64_t t = tile;
+  for (rp = 0; rp < RP; ++rp) {
+    const int64_t c = tri_count(tri, rp, RB);
+    if (t < c) break;
+    t -= c;
+  }
+  cb = tri == 1 ? t : 2 * rp + t;
+}
+
 // The fused kernel on CTA pairs (cluster of 2, tcgen05 cta_group::2): the pair
 // computes a 256 x 128 C tile; CTA r holds A rows 128r..128r+127 of it and
 // rows 64r..64r+63 of every 128 x 128-byte B chunk; the leader (r = 0) issues
 // the M = 256 MMAs for both, each CTA's tensor memory holds its 128 rows.
-template <bool DBG, bool SPLITK>
+template <bool DBG, bool SPLITK, bool TRI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     i8_gemm_kernel(const GemmArgs p, const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB) {
@@ -931,7 +950,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int64_t RA = p.ga.R, RB = p.gb.R, KBn = p.ga.KBn;
   const int64_t RP = RA / 2;
   const int P = (int)p.ga.P;
-  const int tiles = (int)(RP * RB);
+  int tiles = (int)(RP * RB);
+  if (TRI) {
+    tiles = 0;
+    for (int64_t r = 0; r < RP; ++r) tiles += (int)tri_count(p.tri, r, RB);
+  }
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   // work items: tiles, or (tile, k-block part) in split mode (P == 1)
   const int ks = SPLITK ? p.ks : 1;
@@ -972,7 +995,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int item = CASC_I8_WAITS_ON ? pair : items; item < items; item += npairs) {
       const int tile = item / ks;
       int64_t rp, cb;
-      tile_of(tile, RP, RB, rp, cb);
+      if (TRI)
+        tri_tile_of(tile, p.tri, RP, RB, rp, cb);
+      else
+        tile_of(tile, RP, RB, rp, cb);
       const int64_t rb = 2 * rp + rank;
       const bool synced = p.sync && (tile / npairs) < full_waves;
       for (int q = 0; q < P; ++q) {
@@ -1073,7 +1099,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int item = pair; item < items; item += npairs) {
       const int tile = item / ks;
       int64_t rp, cb;
-      tile_of(tile, RP, RB, rp, cb);
+      if (TRI)
+        tri_tile_of(tile, p.tri, RP, RB, rp, cb);
+      else
+        tile_of(tile, RP, RB, rp, cb);
       const int64_t gi = (2 * rp + rank) * TR + lr;
       uint64_t fl = 0;  // detector bits of this thread's 64 columns
       for (int q = 0; q < P; ++q) {
@@ -1204,7 +1233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 Cl[widx] = cl;
               } else {
                 const int64_t gj = cb * TR + lc;
-                if (gi < p.m && gj < p.n) {
+                if (gi < p.m && gj < p.n && (!TRI || (p.tri == 1 ? gi >= gj : gi <= gj))) {
                   double* oh = p.C_hi + gi * p.ldc + gj;
                   double* ol = p.C_lo + gi * p.ldc + gj;
                   // NEXT-4 (reading R21): C := alpha (x) P (+) beta (x) C
@@ -1377,8 +1406,9 @@ int split_parts(int64_t m, int64_t n, int64_t k, int sms) {
 cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
                  double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
                  int32_t* dbg, int64_t dbg_panel, cudaStream_t st, int ab = 0, double ah = 1.0,
-                 double al = 0.0, double bh = 0.0, double bl = 0.0) {
+                 double al = 0.0, double bh = 0.0, double bl = 0.0, int tri = 0) {
   GemmArgs a{};
+  a.tri = tri;
   a.ab = ab;
   a.ah = ah;
   a.al = al;
@@ -1416,12 +1446,12 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TR / 2);
   if (e != cudaSuccess) return e;
   if (dbg) {
-    cudaFuncSetAttribute(i8_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SMEM);
-    i8_gemm_kernel<true, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
+    cudaFuncSetAttribute(i8_gemm_kernel<true, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    i8_gemm_kernel<true, false, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
     return cudaGetLastError();
   }
-  const int ks = split_parts(m, n, k, sms);
+  const int ks = tri ? 1 : split_parts(m, n, k, sms);
   if (ks > 1) {
     const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
     const int64_t items = tiles * ks;
@@ -1433,9 +1463,9 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
                         (size_t)items * 2 * 3 * TR * TR * sizeof(unsigned long long),
                         st) != cudaSuccess)
       return cudaErrorMemoryAllocation;
-    cudaFuncSetAttribute(i8_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SMEM);
-    i8_gemm_kernel<false, true><<<g, THREADS, SMEM, st>>>(a, mA, mB);
+    cudaFuncSetAttribute(i8_gemm_kernel<false, true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    i8_gemm_kernel<false, true, false><<<g, THREADS, SMEM, st>>>(a, mA, mB);
     cudaError_t e2 = cudaGetLastError();
     if (e2 == cudaSuccess) {
       int64_t blocks = (m * n + 255) / 256;
@@ -1446,9 +1476,15 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
     cudaFreeAsync(a.split_ws, st);
     return e2;
   }
-  cudaFuncSetAttribute(i8_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)SMEM);
-  i8_gemm_kernel<false, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
+  if (tri) {
+    cudaFuncSetAttribute(i8_gemm_kernel<false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    i8_gemm_kernel<false, false, true><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
+    return cudaGetLastError();
+  }
+  cudaFuncSetAttribute(i8_gemm_kernel<false, false, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  i8_gemm_kernel<false, false, false><<<g0, THREADS, SMEM, st>>>(a, mA, mB);
   return cudaGetLastError();
 }
 
@@ -1457,6 +1493,9 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
 
 // ====================================================================== C ABI
 namespace casc {
+cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
+                                double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                                int num_sms, int uplo, cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -1626,6 +1665,55 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi
   cudaFreeAsync(gws, st);
   host::set_launches(r == CASC_OK ? launches : 0);
   return r;
+}
+
+// SYRK on the INT8 cascade (NEXT-4): the triangle's pair tiles only, every stored
+// element bitwise the casc_i8_gemm_fp64x2_ex(trans, !trans, A, A) element.
+int casc_i8_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
+                        double alpha_lo, const double* A_hi, const double* A_lo, int64_t lda,
+                        double beta_hi, double beta_lo, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, int y, casc_stream_t stream) {
+  host::set_launches(0);
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (trans != CASC_OP_N && trans != CASC_OP_T))
+    return CASC_ERR_INVALID;
+  if (n < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
+  const int64_t ar = trans ? k : n, ac = trans ? n : k;
+  const bool no_product = (k == 0) || (alpha_hi == 0.0 && alpha_lo == 0.0);
+  int r;
+  if (!no_product && ((r = host::check_mat(A_hi, ar, ac, lda)) ||
+                      (r = host::check_mat(A_lo, ar, ac, lda))))
+    return r;
+  if ((r = host::check_mat(C_hi, n, n, ldc)) || (r = host::check_mat(C_lo, n, n, ldc))) return r;
+  if (n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  const bool use_beta = !(beta_hi == 0.0 && beta_lo == 0.0);
+  if (no_product) {
+    const cudaError_t e = casc::launch_scale_c_uplo(n, n, beta_hi, beta_lo, use_beta, C_hi, C_lo,
+                                                    ldc, flags, sms, uplo == CASC_LOWER ? 0 : 1,
+                                                    st);
+    if (e == cudaSuccess) host::set_launches(1);
+    return st8(e);
+  }
+  const size_t need = casc_i8_workspace_bytes(n, n, k, y);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+  uint8_t* pa = static_cast<uint8_t*>(ws);
+  uint8_t* pb = pa + al256h(casc_i8_packed_bytes(n, k, y));
+  double* gws = reinterpret_cast<double*>(pb + al256h(casc_i8_packed_bytes(n, k, y)));
+  // op(A) as the A operand; op(A)^T as the B operand: its columns are op(A)'s
+  // rows, and A and B operands share the packed format, so one pack serves both
+  cudaError_t e = i8::pack(A_hi, A_lo, lda, n, k, y, trans == CASC_OP_T, pa, st);
+  (void)pb;
+  const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
+  const int ab = use_beta ? 2 : (unit_alpha ? 0 : 1);
+  if (e == cudaSuccess)
+    e = i8::gemm(pa, pa, n, n, k, y, C_hi, C_lo, ldc, flags, gws, i8::ws_grid(n, n, sms), nullptr,
+                 0, st, ab, alpha_hi, alpha_lo, beta_hi, beta_lo, uplo == CASC_LOWER ? 1 : 2);
+  cudaFreeAsync(ws, st);
+  if (e == cudaSuccess) host::set_launches(4);
+  return st8(e);
 }
 
 int casc_i8_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,

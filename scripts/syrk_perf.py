@@ -21,7 +21,10 @@ for name, call in [
         ("syrk", lambda: casc.casc_syrk_fp64x2("L", "N", 1.0, A_hi, A_lo, 0.0, C_hi, C_lo,
                                                workspace=ws)),
         ("gemm_ex", lambda: casc.casc_gemm_fp64x2_ex("N", "T", 1.0, A_hi, A_lo, A_hi, A_lo, 0.0,
-                                                     C_hi, C_lo, workspace=ws))]:
+                                                     C_hi, C_lo, workspace=ws)),
+        ("i8_syrk", lambda: casc.casc_i8_syrk_fp64x2("L", "N", 1.0, A_hi, A_lo, 0.0, C_hi, C_lo)),
+        ("i8_gemm_ex", lambda: casc.casc_i8_gemm_fp64x2_ex("N", "T", 1.0, A_hi, A_lo, A_hi, A_lo,
+                                                           0.0, C_hi, C_lo))]:
     call()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

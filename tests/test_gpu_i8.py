@@ -429,3 +429,25 @@ def test_i8_rounding_ties_and_near_ties(casc, orc):
             ex = (F(A_hi[i, 0]) + F(A_lo[i, 0])) * (F(B_hi[0, j]) + F(B_lo[0, j]))
             err = abs(F(C_hi[i, j]) + F(C_lo[i, j]) - ex)
             assert err <= abs(ex) * F(2) ** -104
+
+
+# ------------------------------------------------------------------ SYRK (NEXT-4)
+@pytest.mark.parametrize("uplo,trans,n,k,al,be", [
+    ("L", "N", 300, 700, (1.0, 0.0), (0.0, 0.0)), ("U", "N", 520, 8192 + 100, (1.0, 0.0), (0.0, 0.0)),
+    ("L", "T", 257, 300, (1.0 / 3.0, 2.0 ** -56), (-0.7, 2.0 ** -60)),
+    ("U", "T", 64, 64, (2.0, 0.0), (1.0, 0.0))])
+def test_i8_syrk_bit_exact(casc, orc, uplo, trans, n, k, al, be):
+    """casc_i8_syrk_fp64x2 (triangular pair-tile list): bit-exact with the
+    oracle's triangle, the other triangle and its flags untouched."""
+    import torch
+    d = I.make_config(2, m=n, n=k, k=k, seed=97)
+    A_hi, A_lo = d["A_hi"][:n, :k], d["A_lo"][:n, :k]
+    Ast = (A_hi.T.copy(), A_lo.T.copy()) if trans == "T" else (A_hi.copy(), A_lo.copy())
+    rng = np.random.default_rng(3)
+    C0 = rng.uniform(-1, 1, (n, n))
+    C_hi, C_lo = T(C0), T(np.zeros((n, n)))
+    fl = torch.full((n, n), 9, dtype=torch.uint8, device="cuda")
+    casc.casc_i8_syrk_fp64x2(uplo, trans, al, T(Ast[0]), T(Ast[1]), be, C_hi, C_lo, flags=fl)
+    o_hi, o_lo, o_fl = orc.i8_casc_syrk(uplo, trans, al, *Ast, be, C0, np.zeros((n, n)),
+                                        np.full((n, n), 9, np.uint8))
+    assert bitwise(N(C_hi), o_hi) and bitwise(N(C_lo), o_lo) and np.array_equal(N(fl), o_fl)

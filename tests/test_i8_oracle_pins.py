@@ -325,3 +325,31 @@ def test_i8_blas_ex_oracle(orc):
         B = d["B_hi"][:kk]
         r = orc.i8_casc_gemm_ex("N", "N", alpha, A, A, B, B, (2.0, 0.0), X_hi, X_lo)
         assert np.array_equal(r[0], 2 * X_hi) and np.all(r[2] == 0)
+
+
+@pytest.mark.parametrize("uplo,trans", [("L", "N"), ("U", "T")])
+def test_i8_syrk_oracle(orc, uplo, trans):
+    """NEXT-4 SYRK on the INT8 cascade: on its triangle within the north-star
+    bound of the exact op(A) op(A)^T (exact rationals), the other triangle and
+    its flags untouched, alpha = 2^p exact."""
+    from fractions import Fraction as F
+    n, k = 9, 200
+    d = I.make_config(1, m=n, n=k, k=k, seed=21)
+    A_hi, A_lo = d["A_hi"][:n, :k], d["A_lo"][:n, :k]
+    Ast = (A_hi.T.copy(), A_lo.T.copy()) if trans == "T" else (A_hi.copy(), A_lo.copy())
+    sent = np.full((n, n), 3.25)
+    fl0 = np.full((n, n), 7, np.uint8)
+    Ch, Cl, fl = orc.i8_casc_syrk(uplo, trans, (1.0, 0.0), *Ast, (0.0, 0.0), sent, sent, fl0)
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+    assert np.all(Ch[~tri] == 3.25) and np.all(fl[~tri] == 7) and np.all(fl[tri] <= 1)
+    for i in range(n):
+        for j in range(n):
+            if not tri[i, j]:
+                continue
+            a = [F(A_hi[i, p]) + F(A_lo[i, p]) for p in range(k)]
+            b = [F(A_hi[j, p]) + F(A_lo[j, p]) for p in range(k)]
+            ex = sum(x * z for x, z in zip(a, b))
+            absab = sum(abs(x * z) for x, z in zip(a, b))
+            assert abs(F(Ch[i, j]) + F(Cl[i, j]) - ex) <= 4 * k * F(2) ** -104 * absab
+    S = orc.i8_casc_syrk(uplo, trans, (0.5, 0.0), *Ast, (0.0, 0.0), sent, sent)
+    assert np.array_equal(S[0][tri], 0.5 * Ch[tri]) and np.array_equal(S[1][tri], 0.5 * Cl[tri])
