@@ -259,19 +259,20 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
                      casc_stream_t stream);
 
 /* NEXT-4, TRSM on the cascaded GEMM (reading R27):
- * left side, no transpose: solve op(A) X = alpha (x) B for X, A m x m
- * triangular (uplo CASC_LOWER / CASC_UPPER; diag CASC_NONUNIT / CASC_UNIT:
- * the diagonal is taken as 1 and not read), X overwrites the m x n B (ldb >=
- * max(1,n)); only A's triangle is read.  B := alpha (x) B; the 256 x 256
- * diagonal blocks of A are inverted in FP64x2 (casc_trsm_diag_inv); then, block
- * by block (ascending for lower, descending for upper), X_b = Inv_b B_b and
- * B_rest := B_rest - A_rest,b X_b with casc_gemm_fp64x2_ex.  Device memory for
- * the inverses and one block of X comes from the stream-ordered pool; no host
- * synchronisation.  alpha == 0: X := 0, A not read.  Errors as
- * casc_gemm_fp64x2_ex (CASC_ERR_INVALID also for bad uplo / diag and for B
- * overlapping A). */
+ * left side: solve op(A) X = alpha (x) B for X, op(A) = A (trans CASC_OP_N) or
+ * A^T (CASC_OP_T), A m x m triangular (uplo CASC_LOWER / CASC_UPPER; diag
+ * CASC_NONUNIT / CASC_UNIT: the diagonal is taken as 1 and not read), X
+ * overwrites the m x n B (ldb >= max(1,n)); only A's triangle is read.
+ * B := alpha (x) B; the 256 x 256 diagonal blocks of A are inverted in FP64x2
+ * (casc_trsm_diag_inv; op(A_bb)^-1 = op(Inv_b)); then, block by block in the
+ * order of op(A)'s triangle (ascending when op(A) is lower, descending when
+ * upper), X_b = op(Inv_b) B_b and B_rest := B_rest - op(A)_rest,b X_b with
+ * casc_gemm_fp64x2_ex.  Device memory for the inverses and one block of X comes
+ * from the stream-ordered pool; no host synchronisation.  alpha == 0: X := 0,
+ * A not read.  Errors as casc_gemm_fp64x2_ex (CASC_ERR_INVALID also for bad
+ * uplo / trans / diag and for B overlapping A). */
 typedef enum { CASC_NONUNIT = 0, CASC_UNIT = 1 } casc_diag;
-int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n,
+int casc_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n,
                      double alpha_hi, double alpha_lo,
                      const double* A_hi, const double* A_lo, int64_t lda,
                      double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream);

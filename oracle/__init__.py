@@ -84,8 +84,8 @@ def _setup(L):
                                 _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
     L.orc_dd_div.argtypes = [_d, _d, _d, _d, _pd, _pd]
     L.orc_trsm_diag_inv.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _pd, _pd, _i64, _pd, _pd]
-    L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
-                                _pd, _pd, _i64, ctypes.c_int]
+    L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd,
+                                _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
     L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
                               _i64, ctypes.c_int]
     L.orc_exact_entries.argtypes = [_i64, _pd, _pd, _i64, _pd, _pd, _i64, _i64, _pi64, _pi64,
@@ -298,15 +298,16 @@ def trsm_diag_inv(uplo, diag, A_hi, A_lo):
     return Ih, Il
 
 
-def casc_trsm(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, nthreads: int = 0):
-    """NEXT-4 TRSM (reading R27): X with op(A) X = alpha B, left side, no
-    transpose; A m x m triangular; returns new (X_hi, X_lo)."""
+def casc_trsm(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", nthreads: int = 0):
+    """NEXT-4 TRSM (reading R27): X with op(A) X = alpha B, left side, op(A) = A
+    or A^T; A m x m triangular; returns new (X_hi, X_lo)."""
     lo_ = 0 if uplo in ("L", "l", 0) else 1
+    tr = 1 if trans in ("T", "t", 1, True) else 0
     dg = 1 if diag in ("U", "u", 1, True) else 0
     A_hi, A_lo = map(_c64, (A_hi, A_lo))
     X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
     m, n = X_hi.shape
-    lib().orc_casc_trsm(lo_, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo), max(m, 1),
+    lib().orc_casc_trsm(lo_, tr, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo), max(m, 1),
                         _p(X_hi), _p(X_lo), max(n, 1), nthreads)
     return X_hi, X_lo
 

@@ -707,12 +707,14 @@ void orc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* Ahi, const d
   }
 }
 
-/* TRSM, left side, no transpose: solve op(A) X = alpha B, X overwrites the
- * m x n B (ldb).  B := alpha (x) B; the diagonal blocks are inverted
- * (orc_trsm_diag_inv); then block by block (ascending for lower, descending
- * for upper): X_b = Inv_b B_b and B_rest := B_rest - A_rest,b X_b, both with the
- * cascaded GEMM (orc_casc_gemm_ex: alpha 1, beta 0, then alpha -1, beta 1). */
-void orc_casc_trsm(int uplo, int diag, int64_t m, int64_t n, double ah, double al,
+/* TRSM, left side: solve op(A) X = alpha B, op(A) = A (trans 0) or A^T (trans
+ * 1); X overwrites the m x n B (ldb).  B := alpha (x) B; the diagonal blocks of
+ * A are inverted (orc_trsm_diag_inv, op(A_bb)^-1 = op(Inv_b)); then block by
+ * block in the order of op(A)'s triangle (ascending when op(A) is lower,
+ * descending when upper): X_b = op(Inv_b) B_b and B_rest := B_rest -
+ * op(A)_rest,b X_b, both with the cascaded GEMM (orc_casc_gemm_ex: alpha 1,
+ * beta 0, then alpha -1, beta 1; op(A)_rest,b read transposed when trans). */
+void orc_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double ah, double al,
                    const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
                    int64_t ldb, int nthreads) {
   if (m == 0 || n == 0) return;
@@ -726,6 +728,7 @@ void orc_casc_trsm(int uplo, int diag, int64_t m, int64_t n, double ah, double a
         Blo[i * ldb + j] = rl;
       }
   if (ah == 0.0 && al == 0.0) return;
+  const int eff_lower = (uplo == 0) != (trans == 1);
   const int64_t nblk = (m + TRSM_NB - 1) / TRSM_NB;
   double* Ihi = (double*)malloc(sizeof(double) * (size_t)(nblk * TRSM_NB * TRSM_NB));
   double* Ilo = (double*)malloc(sizeof(double) * (size_t)(nblk * TRSM_NB * TRSM_NB));
@@ -733,11 +736,11 @@ void orc_casc_trsm(int uplo, int diag, int64_t m, int64_t n, double ah, double a
   double* Tl = (double*)malloc(sizeof(double) * (size_t)(TRSM_NB * n));
   orc_trsm_diag_inv(uplo, diag, m, Ahi, Alo, lda, Ihi, Ilo);
   for (int64_t s = 0; s < nblk; ++s) {
-    const int64_t b = uplo == 0 ? s : nblk - 1 - s;
+    const int64_t b = eff_lower ? s : nblk - 1 - s;
     const int64_t r0 = b * TRSM_NB, nb = (m - r0) < TRSM_NB ? (m - r0) : TRSM_NB;
     const int64_t r1 = r0 + nb;
-    /* X_b = Inv_b B_b (into T, then back into B_b) */
-    orc_casc_gemm_ex(0, 0, nb, n, nb, 1.0, 0.0, Ihi + b * TRSM_NB * TRSM_NB,
+    /* X_b = op(Inv_b) B_b (into T, then back into B_b) */
+    orc_casc_gemm_ex(trans, 0, nb, n, nb, 1.0, 0.0, Ihi + b * TRSM_NB * TRSM_NB,
                      Ilo + b * TRSM_NB * TRSM_NB, TRSM_NB, Bhi + r0 * ldb, Blo + r0 * ldb, ldb,
                      0.0, 0.0, Th, Tl, n, NULL, nthreads);
     for (int64_t i = 0; i < nb; ++i)
@@ -745,14 +748,18 @@ void orc_casc_trsm(int uplo, int diag, int64_t m, int64_t n, double ah, double a
         Bhi[(r0 + i) * ldb + j] = Th[i * n + j];
         Blo[(r0 + i) * ldb + j] = Tl[i * n + j];
       }
-    /* B_rest := B_rest - A_rest,b X_b */
-    if (uplo == 0 && r1 < m)
-      orc_casc_gemm_ex(0, 0, m - r1, n, nb, -1.0, 0.0, Ahi + r1 * lda + r0, Alo + r1 * lda + r0,
-                       lda, Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
+    /* B_rest := B_rest - op(A)_rest,b X_b */
+    if (eff_lower && r1 < m) {
+      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
+      orc_casc_gemm_ex(trans, 0, m - r1, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
+                       Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
                        Blo + r1 * ldb, ldb, NULL, nthreads);
-    if (uplo == 1 && r0 > 0)
-      orc_casc_gemm_ex(0, 0, r0, n, nb, -1.0, 0.0, Ahi + r0, Alo + r0, lda, Bhi + r0 * ldb,
+    }
+    if (!eff_lower && r0 > 0) {
+      const int64_t off = trans ? r0 * lda : r0;
+      orc_casc_gemm_ex(trans, 0, r0, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda, Bhi + r0 * ldb,
                        Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi, Blo, ldb, NULL, nthreads);
+    }
   }
   free(Ihi);
   free(Ilo);

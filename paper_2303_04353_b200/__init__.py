@@ -100,8 +100,8 @@ CASC_OP_N, CASC_OP_T = 0, 1
 CASC_LOWER, CASC_UPPER = 0, 1
 CASC_NONUNIT, CASC_UNIT = 0, 1
 TRSM_NB = 256
-_sig("casc_trsm_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double, ctypes.c_double,
-                          _vp, _vp, _i64, _vp, _vp, _i64, _vp])
+_sig("casc_trsm_fp64x2", [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double,
+                          ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
 _sig("casc_trsm_diag_inv", [ctypes.c_int, ctypes.c_int, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 
 
@@ -141,18 +141,20 @@ def casc_i8_syrk_fp64x2(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=
     return C_hi, C_lo, flags
 
 
-def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, stream=None):
+def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", stream=None):
     """TRSM on the cascaded GEMM (NEXT-4, reading R27): solve op(A) X = alpha B
-    (left side, no transpose), A m x m triangular; X overwrites B_hi / B_lo."""
+    (left side, op(A) = A or A^T), A m x m triangular; X overwrites B_hi / B_lo."""
     lo, dg = _uplo_diag(uplo, diag)
+    tr = 1 if trans in ("T", "t", 1, True) else 0
     ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
     lda = _ld_pair(A_hi, A_lo, "A")
     ldb = _ld_pair(B_hi, B_lo, "B")
     m, n = B_hi.shape
     if tuple(A_hi.shape) != (m, m):
         raise ValueError("A must be m x m")
-    _check(_lib.casc_trsm_fp64x2(lo, dg, m, n, float(ah), float(al), _ptr(A_hi), _ptr(A_lo), lda,
-                                 _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)), "casc_trsm_fp64x2")
+    _check(_lib.casc_trsm_fp64x2(lo, tr, dg, m, n, float(ah), float(al), _ptr(A_hi), _ptr(A_lo),
+                                 lda, _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)),
+           "casc_trsm_fp64x2")
     return B_hi, B_lo
 
 

@@ -675,7 +675,7 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
 }
 
 // ---------------------------------------------------------------- TRSM (NEXT-4)
-// Left side, no transpose: op(A) X = alpha B, X overwrites B (reading R27).
+// Left side: op(A) X = alpha B, op(A) = A or A^T, X overwrites B (reading R27).
 static constexpr int64_t kTrsmNb = 256;
 
 int casc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi, const double* A_lo,
@@ -694,11 +694,12 @@ int casc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi, const 
   return cuda_status(e);
 }
 
-int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n, double alpha_hi, double alpha_lo,
-                     const double* A_hi, const double* A_lo, int64_t lda, double* B_hi,
-                     double* B_lo, int64_t ldb, casc_stream_t stream) {
+int casc_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, double alpha_hi,
+                     double alpha_lo, const double* A_hi, const double* A_lo, int64_t lda,
+                     double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream) {
   g_launches = 0;
-  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (diag != CASC_NONUNIT && diag != CASC_UNIT))
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (diag != CASC_NONUNIT && diag != CASC_UNIT) ||
+      (trans != CASC_OP_N && trans != CASC_OP_T))
     return CASC_ERR_INVALID;
   if (m < 0 || n < 0) return CASC_ERR_INVALID;
   int r;
@@ -739,11 +740,13 @@ int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n, double alpha_hi, 
   cudaError_t e = casc::launch_trsm_diag_inv(uplo, diag, m, A_hi, A_lo, lda, inv_hi, inv_lo, st);
   r = e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA;
   ++launches;
+  // op(A) is lower when (uplo lower) xor (transposed); op(A_bb)^-1 = op(Inv_b)
+  const bool eff_lower = (uplo == CASC_LOWER) != (trans == CASC_OP_T);
   for (int64_t s = 0; s < nblk && r == CASC_OK; ++s) {
-    const int64_t b = uplo == CASC_LOWER ? s : nblk - 1 - s;
+    const int64_t b = eff_lower ? s : nblk - 1 - s;
     const int64_t r0 = b * kTrsmNb, nb = std::min(kTrsmNb, m - r0), r1 = r0 + nb;
-    // X_b = Inv_b B_b, into T and back into B_b
-    r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, nb, n, nb, 1.0, 0.0,
+    // X_b = op(Inv_b) B_b, into T and back into B_b
+    r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, nb, n, nb, 1.0, 0.0,
                             inv_hi + b * kTrsmNb * kTrsmNb, inv_lo + b * kTrsmNb * kTrsmNb,
                             kTrsmNb, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 0.0, 0.0, t_hi, t_lo,
                             n, nullptr, nullptr, 0, stream);
@@ -756,17 +759,20 @@ int casc_trsm_fp64x2(int uplo, int diag, int64_t m, int64_t n, double alpha_hi, 
       r = CASC_ERR_CUDA;
       break;
     }
-    // B_rest := B_rest - A_rest,b X_b
+    // B_rest := B_rest - op(A)_rest,b X_b (op(A)_rest,b read transposed when trans)
     g_launches = 0;
-    if (uplo == CASC_LOWER && r1 < m)
-      r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + r1 * lda + r0,
-                              A_lo + r1 * lda + r0, lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb,
-                              1.0, 0.0, B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, nullptr, 0,
-                              stream);
-    if (uplo == CASC_UPPER && r0 > 0)
-      r = casc_gemm_fp64x2_ex(CASC_OP_N, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + r0, A_lo + r0,
-                              lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo,
-                              ldb, nullptr, nullptr, 0, stream);
+    if (eff_lower && r1 < m) {
+      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
+      r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + off, A_lo + off,
+                              lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0,
+                              B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, nullptr, 0, stream);
+    }
+    if (!eff_lower && r0 > 0) {
+      const int64_t off = trans ? r0 * lda : r0;
+      r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + off, A_lo + off, lda,
+                              B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo, ldb,
+                              nullptr, nullptr, 0, stream);
+    }
     launches += g_launches;
   }
   cudaFreeAsync(buf, st);

@@ -631,9 +631,10 @@ def test_trsm_diag_inverse_bitwise(casc, orc, uplo, diag, m):
     assert np.array_equal(g_lo.view(np.uint64), o_lo.view(np.uint64))
 
 
-@pytest.mark.parametrize("uplo,diag,m,n", [("L", "N", 300, 70), ("U", "N", 600, 130),
-                                           ("L", "U", 520, 33), ("U", "N", 200, 1)])
-def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n):
+@pytest.mark.parametrize("uplo,diag,m,n,trans", [("L", "N", 300, 70, "N"), ("U", "N", 600, 130, "N"),
+                                                 ("L", "U", 520, 33, "N"), ("U", "N", 200, 1, "N"),
+                                                 ("L", "N", 600, 40, "T"), ("U", "U", 300, 9, "T")])
+def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n, trans):
     """GPU TRSM vs the oracle's (same blocked algorithm; the GEMM updates agree to
     the cascade's bound, not bitwise): within 2^-96 relative on diagonally
     dominant systems, and the residual op(A) X - B small against |A||X|;
@@ -644,9 +645,9 @@ def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n):
     B_hi = rng.uniform(-1, 1, (m, n))
     B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))  # normalised pairs: exact scaling
     Xh, Xl = T(B_hi), T(B_lo)
-    casc.casc_trsm_fp64x2(uplo, diag, 1.0, T(A_hi), T(A_lo), Xh, Xl)
+    casc.casc_trsm_fp64x2(uplo, diag, 1.0, T(A_hi), T(A_lo), Xh, Xl, trans=trans)
     x_hi, x_lo = N(Xh), N(Xl)
-    o_hi, o_lo = orc.casc_trsm(uplo, diag, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    o_hi, o_lo = orc.casc_trsm(uplo, diag, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
     diff = np.abs((x_hi - o_hi) + (x_lo - o_lo))
     assert np.all(diff <= 2.0 ** -96 * (np.abs(o_hi) + 1e-300) + 2.0 ** -110)
     # residual through the exact evaluator (A X, rows sampled)
@@ -654,12 +655,14 @@ def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n):
     A_use = A_hi.copy()
     if diag == "U":
         A_use[np.arange(m), np.arange(m)] = 1.0
+    opA = (A_use.T.copy(), A_lo.T.copy()) if trans == "T" else (A_use, A_lo)
     ii, jj = np.meshgrid(rows, np.arange(n), indexing="ij")
-    r = orc.exact_entries(A_use, A_lo, x_hi, x_lo, ii.ravel(), jj.ravel(), B_hi, B_lo)
+    r = orc.exact_entries(opA[0], opA[1], x_hi, x_lo, ii.ravel(), jj.ravel(), B_hi, B_lo)
     assert np.all(np.abs(r["err"]) <= 2.0 ** -96 * r["absab"] + 2.0 ** -120)
     # alpha = 4: exact scaling; B as a column window of a wider buffer
     wide_h = T(np.pad(B_hi, ((0, 0), (0, 3)), constant_values=5.0))
     wide_l = T(np.pad(B_lo, ((0, 0), (0, 3)), constant_values=5.0))
-    casc.casc_trsm_fp64x2(uplo, diag, 4.0, T(A_hi), T(A_lo), wide_h[:, :n], wide_l[:, :n])
+    casc.casc_trsm_fp64x2(uplo, diag, 4.0, T(A_hi), T(A_lo), wide_h[:, :n], wide_l[:, :n],
+                          trans=trans)
     assert np.array_equal(N(wide_h)[:, :n], 4 * x_hi) and np.array_equal(N(wide_l)[:, :n], 4 * x_lo)
     assert np.all(N(wide_h)[:, n:] == 5.0)

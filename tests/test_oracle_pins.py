@@ -521,40 +521,45 @@ def test_trsm_diag_inverse_oracle(orc, uplo, unit):
                 assert abs(s - (1 if i == j else 0)) <= F(2) ** -95
 
 
-@pytest.mark.parametrize("uplo,unit,m,n", [("L", False, 40, 5), ("U", False, 300, 3),
-                                           ("L", True, 300, 2)])
-def test_trsm_oracle(orc, uplo, unit, m, n):
+@pytest.mark.parametrize("uplo,trans,unit,m,n", [("L", "N", False, 40, 5), ("U", "N", False, 300, 3),
+                                                 ("L", "N", True, 300, 2), ("L", "T", False, 300, 2),
+                                                 ("U", "T", False, 40, 3)])
+def test_trsm_oracle(orc, uplo, trans, unit, m, n):
     """R27 TRSM: the exact residual of op(A) X = B (dyadic rationals, no
-    rounding) within 2^-96 (|A||X|) row by row (diagonally dominant A, so X is
-    then accurate; two blocks with the cascaded-GEMM update for m = 300) and,
-    for m = 40, X within 2^-95 of the exact solution; alpha = 2 scales exactly;
-    alpha = 0 gives X = 0."""
+    rounding) within 2^-96 (|op(A)||X|) row by row (diagonally dominant A, so
+    X is then accurate; two blocks with the cascaded-GEMM update for m = 300)
+    and, for m = 40, X within 2^-95 of the exact solution; alpha = 2 scales
+    exactly; alpha = 0 gives X = 0."""
     A_hi, A_lo = _tri_dd(m, uplo, 7, unit)
     rng = np.random.default_rng(9)
     B_hi = rng.uniform(-1, 1, (m, n))
     B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))  # normalised pairs: exact scaling
-    X_hi, X_lo = orc.casc_trsm(uplo, "U" if unit else "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    X_hi, X_lo = orc.casc_trsm(uplo, "U" if unit else "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo,
+                               trans=trans)
     A = [[fr(A_hi[i, j]) + fr(A_lo[i, j]) for j in range(m)] for i in range(m)]
+    if trans == "T":
+        A = [list(r) for r in zip(*A)]  # op(A)
+    lower = (uplo == "L") != (trans == "T")
     X = [[fr(X_hi[i, j]) + fr(X_lo[i, j]) for j in range(n)] for i in range(m)]
     for i in range(0, m, 1 if m <= 40 else 9):
-        lo, hi = (0, i + 1) if uplo == "L" else (i, m)
+        lo, hi = (0, i + 1) if lower else (i, m)
         for j in range(n):
             r = sum(A[i][l] * X[l][j] for l in range(lo, hi)) - (fr(B_hi[i, j]) + fr(B_lo[i, j]))
             mag = sum(abs(A[i][l] * X[l][j]) for l in range(lo, hi))
             assert abs(r) <= F(2) ** -96 * mag
     if m <= 40:  # exact solution by substitution
-        order = range(m) if uplo == "L" else range(m - 1, -1, -1)
+        order = range(m) if lower else range(m - 1, -1, -1)
         for j in range(n):
             x = [F(0)] * m
             for i in order:
-                lo, hi = (0, i) if uplo == "L" else (i + 1, m)
+                lo, hi = (0, i) if lower else (i + 1, m)
                 x[i] = (fr(B_hi[i, j]) + fr(B_lo[i, j])
                         - sum(A[i][l] * x[l] for l in range(lo, hi))) / A[i][i]
             for i in range(m):
                 assert abs(X[i][j] - x[i]) <= F(2) ** -95 * (abs(x[i]) + 1)
-    Y = orc.casc_trsm(uplo, "U" if unit else "N", (2.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    Y = orc.casc_trsm(uplo, "U" if unit else "N", (2.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
     assert np.array_equal(Y[0], 2 * X_hi) and np.array_equal(Y[1], 2 * X_lo)
-    Z = orc.casc_trsm(uplo, "N", (0.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    Z = orc.casc_trsm(uplo, "N", (0.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
     assert np.all(Z[0] == 0) and np.all(Z[1] == 0)
 
 
