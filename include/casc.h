@@ -20,6 +20,16 @@
  *   6. cancellation flag = OR over panels of (bin0 == 0) (§3.7, §4.4
  *      P:L3380-3382).
  *
+ * Entry points (in this order below):
+ *   the north-star call casc_gemm_fp64x2 (+ _ws, workspace sizing, finalize);
+ *   host-resident operands casc_gemm_fp64x2_host; phases separately
+ *   (casc_pack_a / casc_pack_b / casc_gemm_packed, used by the multi-GPU layer);
+ *   inspection exports (casc_split_a/b, casc_debug_bins); the simple path
+ *   (casc_gemm_fp64x2_simple, casc_slice_product); BLAS-style generality
+ *   (casc_gemm_fp64x2_ex, casc_syrk_fp64x2, casc_trsm_fp64x2,
+ *   casc_trsm_diag_inv); the INT8 cascade (casc_i8_*: GEMM, _ws, _ex, _host,
+ *   SYRK, pack / packed GEMM, split and bins exports).
+ *
  * Conventions (all entry points):
  *   - Matrices are row-major with a leading dimension (elements).  An FP64x2
  *     value is the unevaluated sum hi + lo of two binary64 arrays (SoA).
