@@ -361,11 +361,18 @@ def main():
     import paper_2303_04353_b200 as casc
     from paper_2303_04353_b200.multigpu import ShardedCascGemm, col_slab, row_shard
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # CASC_BENCH_PLUMBING=1 (tests only, never a measurement): every rank on
+    # cuda:0 with the gloo backend, to exercise the N > 1 code path on one GPU
+    plumbing = os.environ.get("CASC_BENCH_PLUMBING") == "1"
+    dev_index = 0 if plumbing else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if plumbing:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     m, n, k = CONFIGS[args.config]
     r0, r1 = row_shard(m, world, rank)
     c0, c1, _ = col_slab(n, world, rank)
@@ -605,6 +612,8 @@ def main():
         "clocks": clocks,
         "next3_int8_cascade": int8,
     }
+    if plumbing:
+        out["plumbing_test"] = "all ranks on cuda:0 with gloo: NOT a measurement"
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
