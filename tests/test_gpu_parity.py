@@ -666,3 +666,28 @@ def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n, trans):
                           trans=trans)
     assert np.array_equal(N(wide_h)[:, :n], 4 * x_hi) and np.array_equal(N(wide_l)[:, :n], 4 * x_lo)
     assert np.all(N(wide_h)[:, n:] == 5.0)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (256, 1), (257, 3), (512, 2)])
+def test_trsm_edges(casc, orc, m, n):
+    """TRSM at block edges (1 x 1, exactly one block, one row past a block, two
+    full blocks), alpha = 0 (X = 0, A never read) and bad arguments."""
+    import torch
+    A_hi, A_lo = _tri_dd(m, "L", 19)
+    rng = np.random.default_rng(23)
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    Xh, Xl = T(B_hi), T(B_lo)
+    casc.casc_trsm_fp64x2("L", "N", 1.0, T(A_hi), T(A_lo), Xh, Xl)
+    o_hi, o_lo = orc.casc_trsm("L", "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo)
+    diff = np.abs((N(Xh) - o_hi) + (N(Xl) - o_lo))
+    assert np.all(diff <= 2.0 ** -96 * np.abs(o_hi) + 2.0 ** -110)
+    nanA = T(np.full((m, m), np.nan))
+    Zh, Zl = T(B_hi), T(B_lo)
+    casc.casc_trsm_fp64x2("U", "U", 0.0, nanA, nanA, Zh, Zl)
+    assert np.all(N(Zh) == 0) and np.all(N(Zl) == 0)
+    with pytest.raises(ValueError):
+        casc.casc_trsm_fp64x2("X", "N", 1.0, T(A_hi), T(A_lo), Xh, Xl)
+    with pytest.raises(casc.CascError):  # B overlapping A
+        buf_h = torch.zeros((m + 1, m), dtype=torch.float64, device="cuda")
+        casc.casc_trsm_fp64x2("L", "N", 1.0, buf_h[:m], buf_h[:m], buf_h[1:, :1], buf_h[1:, :1])
