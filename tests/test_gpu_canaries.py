@@ -70,3 +70,35 @@ def test_output_canaries(m, n, k):
             tri = np.tril(np.ones((s, s), bool)) if uplo == "L" else np.triu(np.ones((s, s), bool))
             _check(bh, vh, s, s, tri=tri)
             _check(bl, vl, s, s, tri=tri)
+
+
+def test_trsm_and_host_canaries():
+    """TRSM writes only its B (ragged m, strided ldb); the host-operand entry
+    writes only its host C block (sentinels in pinned host memory)."""
+    import torch
+
+    import paper_2303_04353_b200 as casc
+    m, n = 300, 37
+    rng = np.random.default_rng(5)
+    L = np.tril(rng.uniform(-1, 1, (m, m)) / m) + np.diag(1.0 + rng.uniform(0, 1, m))
+    bh, vh = _boxed(torch, m, n)
+    bl, vl = _boxed(torch, m, n)
+    vh.copy_(torch.from_numpy(rng.uniform(-1, 1, (m, n))).cuda())
+    vl.zero_()
+    Lh = torch.from_numpy(L).cuda()
+    casc.casc_trsm_fp64x2("L", "N", 1.0, Lh, Lh * 2.0 ** -54, vh, vl)
+    torch.cuda.synchronize()
+    _check(bh, vh, m, n)
+    _check(bl, vl, m, n)
+    # host-operand entry: C as a window of a sentinel-filled pinned host buffer
+    d = I.make_config(2, m=200, n=150, k=300, seed=7)
+    P = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hb = torch.full((400, 160), SENT, dtype=torch.float64).pin_memory()
+    lb = torch.full((400, 160), SENT, dtype=torch.float64).pin_memory()
+    casc.casc_gemm_fp64x2_host(P(d["A_hi"]), P(d["A_lo"]), P(d["B_hi"]), P(d["B_lo"]),
+                               C_hi=hb[100:300, 5:155], C_lo=lb[100:300, 5:155], want_flags=False,
+                               slab_rows=64, slab_cols=64)
+    for b in (hb.numpy(), lb.numpy()):
+        inside = np.zeros((400, 160), bool)
+        inside[100:300, 5:155] = True
+        assert np.all(b[~inside] == SENT) and np.all(np.isfinite(b[inside]))
