@@ -343,6 +343,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-int8", action="store_true",
                     help="skip the NEXT-3 INT8-cascade measurement on the same workload")
+    ap.add_argument("--no-next4", action="store_true",
+                    help="skip the NEXT-4 SYRK / TRSM measurements (N = 1)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -560,6 +562,48 @@ def main():
             dist.destroy_process_group()
         return
 
+    # ---- NEXT-4 level-3 ops on the cascaded GEMM, N = 1 (context lines, not the metric)
+    next4 = None
+    if world == 1 and not args.no_next4 and k >= m:
+        try:
+            def ev_time(f, reps=2):
+                f()
+                torch.cuda.synchronize()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                for _ in range(reps):
+                    f()
+                a1.record()
+                torch.cuda.synchronize()
+                return a0.elapsed_time(a1) / reps
+            S_hi = torch.zeros((m, m), dtype=torch.float64, device=dev)
+            S_lo = torch.zeros_like(S_hi)
+            t_syrk = ev_time(lambda: casc.casc_syrk_fp64x2("L", "N", 1.0, A_hi, A_lo, 0.0, S_hi,
+                                                           S_lo))
+            t_syrk8 = ev_time(lambda: casc.casc_i8_syrk_fp64x2("L", "N", 1.0, A_hi, A_lo, 0.0,
+                                                               S_hi, S_lo))
+            # TRSM: a well-conditioned lower-triangular m x m system, B = this rank's B
+            Lt = torch.tril(A_hi[:, :m] / m) + torch.diag(2.0 + A_hi.diagonal().abs())
+            Lt_lo = Lt * 2.0**-54
+            X_hi, X_lo = B_hi.clone(), B_lo.clone()
+
+            def trsm():
+                X_hi.copy_(B_hi)
+                X_lo.copy_(B_lo)
+                casc.casc_trsm_fp64x2("L", "N", 1.0, Lt, Lt_lo, X_hi, X_lo)
+            t_trsm = ev_time(trsm)
+            next4 = {
+                "syrk": {"op": "C := A A^T (lower triangle), m x k = %d x %d" % (m, k),
+                         "ms": t_syrk, "gflops_n2k": m * m * k / (t_syrk * 1e-3) / 1e9},
+                "i8_syrk": {"ms": t_syrk8, "gflops_n2k": m * m * k / (t_syrk8 * 1e-3) / 1e9},
+                "trsm": {"op": "L X = B, L %d x %d lower, B %d x %d" % (m, m, m, n),
+                         "ms": t_trsm, "gflops_m2n": m * m * n / (t_trsm * 1e-3) / 1e9}}
+            del S_hi, S_lo, Lt, Lt_lo, X_hi, X_lo
+            torch.cuda.empty_cache()
+        except Exception as ex:  # reported, never silently replaced
+            next4 = {"error": repr(ex)}
+
     # ---- context: cuBLAS DGEMM time for the paper's t / t_DGEMM (off the hot path)
     dgemm_ratio = None
     if world == 1:
@@ -611,6 +655,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "next3_int8_cascade": int8,
+        "next4_level3": next4,
     }
     if plumbing:
         out["plumbing_test"] = "all ranks on cuda:0 with gloo: NOT a measurement"
