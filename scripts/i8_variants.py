@@ -6,6 +6,9 @@ VARIANTS = {
     "base": [],
     "noepi": ["CASC_I8_NO_EPI"],
     "prof": ["CASC_I8_PROF"],
+    "gm4": ["CASC_I8_GROUP_M=4"],
+    "gm8": ["CASC_I8_GROUP_M=8"],
+    "gm3": ["CASC_I8_GROUP_M=3"],
     "sus0": ["CASC_I8_SUSPEND_NS=0"],
     "sus2k": ["CASC_I8_SUSPEND_NS=2000"],
     "sus20k": ["CASC_I8_SUSPEND_NS=20000"],
