@@ -396,6 +396,15 @@ int casc_i8_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
                         double* C_hi, double* C_lo, int64_t ldc,
                         uint8_t* flags, int y, casc_stream_t stream);
 
+/* TRSM on the INT8 cascade (NEXT-4): casc_trsm_fp64x2's semantics and blocked
+ * algorithm (reading R27) with casc_i8_gemm_fp64x2_ex (y slices) as the GEMM;
+ * bit-exact with its oracle.  Errors as casc_trsm_fp64x2 (CASC_ERR_INVALID also
+ * for y outside [3, 15]). */
+int casc_i8_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n,
+                        double alpha_hi, double alpha_lo,
+                        const double* A_hi, const double* A_lo, int64_t lda,
+                        double* B_hi, double* B_lo, int64_t ldb, int y, casc_stream_t stream);
+
 /* NEXT-4 on the INT8 cascade: C := alpha (x) op(A) op(B) (+) beta (x) C with the
  * semantics, argument layout and errors of casc_gemm_fp64x2_ex (reading R21),
  * the product computed through y int8 slices (bitwise the casc_i8_gemm_fp64x2

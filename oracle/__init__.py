@@ -108,6 +108,8 @@ def _setup(L):
                                       _pu8, ctypes.c_int, ctypes.c_int]
     L.orc_i8_casc_syrk.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
                                    _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int, ctypes.c_int]
+    L.orc_i8_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d,
+                                   _pd, _pd, _i64, _pd, _pd, _i64, ctypes.c_int, ctypes.c_int]
 
 
 def _p(a, ptr=_pd):
@@ -448,6 +450,20 @@ def i8_casc_syrk(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, y
                            A_hi.shape[1] if A_hi.size else 1, beta[0], beta[1], _p(C_hi),
                            _p(C_lo), n, _p(flags, _pu8), int(y), nthreads)
     return C_hi, C_lo, flags
+
+
+def i8_casc_trsm(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", y: int = 14,
+                 nthreads: int = 0):
+    """NEXT-4 TRSM on the INT8 cascade (reading R27): X with op(A) X = alpha B."""
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
+    m, n = X_hi.shape
+    lib().orc_i8_casc_trsm(lo_, tr, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo), max(m, 1),
+                           _p(X_hi), _p(X_lo), max(n, 1), int(y), nthreads)
+    return X_hi, X_lo
 
 
 def i8_casc_gemm(A_hi, A_lo, B_hi, B_lo, y: int = 14, nthreads: int = 0):

@@ -376,3 +376,61 @@ void orc_i8_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, doub
   free(Tl);
   free(Tf);
 }
+
+/* NEXT-4 TRSM on the INT8 cascade (reading R27 with the INT8 cascade as the
+ * GEMM): the blocked solve of orc_casc_trsm with orc_i8_casc_gemm_ex (y slices)
+ * for X_b = op(Inv_b) B_b and the updates; same diagonal-block inverses. */
+#define I8_TRSM_NB 256
+void orc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* Ahi, const double* Alo,
+                       int64_t lda, double* Ihi, double* Ilo);
+void orc_i8_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double ah, double al,
+                      const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
+                      int64_t ldb, int y, int nthreads) {
+  if (m == 0 || n == 0) return;
+  if (!(ah == 1.0 && al == 0.0))
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        double rh = 0.0, rl = 0.0;
+        if (!(ah == 0.0 && al == 0.0))
+          orc_dd_mul(ah, al, Bhi[i * ldb + j], Blo[i * ldb + j], &rh, &rl);
+        Bhi[i * ldb + j] = rh;
+        Blo[i * ldb + j] = rl;
+      }
+  if (ah == 0.0 && al == 0.0) return;
+  const int eff_lower = (uplo == 0) != (trans == 1);
+  const int64_t nblk = (m + I8_TRSM_NB - 1) / I8_TRSM_NB;
+  double* Ihi = (double*)malloc(sizeof(double) * (size_t)(nblk * I8_TRSM_NB * I8_TRSM_NB));
+  double* Ilo = (double*)malloc(sizeof(double) * (size_t)(nblk * I8_TRSM_NB * I8_TRSM_NB));
+  double* Th = (double*)malloc(sizeof(double) * (size_t)(I8_TRSM_NB * n));
+  double* Tl = (double*)malloc(sizeof(double) * (size_t)(I8_TRSM_NB * n));
+  orc_trsm_diag_inv(uplo, diag, m, Ahi, Alo, lda, Ihi, Ilo);
+  for (int64_t s = 0; s < nblk; ++s) {
+    const int64_t b = eff_lower ? s : nblk - 1 - s;
+    const int64_t r0 = b * I8_TRSM_NB, nb = (m - r0) < I8_TRSM_NB ? (m - r0) : I8_TRSM_NB;
+    const int64_t r1 = r0 + nb;
+    orc_i8_casc_gemm_ex(trans, 0, nb, n, nb, 1.0, 0.0, Ihi + b * I8_TRSM_NB * I8_TRSM_NB,
+                        Ilo + b * I8_TRSM_NB * I8_TRSM_NB, I8_TRSM_NB, Bhi + r0 * ldb,
+                        Blo + r0 * ldb, ldb, 0.0, 0.0, Th, Tl, n, NULL, y, nthreads);
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        Bhi[(r0 + i) * ldb + j] = Th[i * n + j];
+        Blo[(r0 + i) * ldb + j] = Tl[i * n + j];
+      }
+    if (eff_lower && r1 < m) {
+      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
+      orc_i8_casc_gemm_ex(trans, 0, m - r1, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
+                          Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
+                          Blo + r1 * ldb, ldb, NULL, y, nthreads);
+    }
+    if (!eff_lower && r0 > 0) {
+      const int64_t off = trans ? r0 * lda : r0;
+      orc_i8_casc_gemm_ex(trans, 0, r0, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
+                          Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi, Blo, ldb, NULL, y,
+                          nthreads);
+    }
+  }
+  free(Ihi);
+  free(Ilo);
+  free(Th);
+  free(Tl);
+}

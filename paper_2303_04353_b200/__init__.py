@@ -73,7 +73,7 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
-            "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2"]
+            "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -155,6 +155,28 @@ def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", strea
     _check(_lib.casc_trsm_fp64x2(lo, tr, dg, m, n, float(ah), float(al), _ptr(A_hi), _ptr(A_lo),
                                  lda, _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)),
            "casc_trsm_fp64x2")
+    return B_hi, B_lo
+
+
+_sig("casc_i8_trsm_fp64x2", [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64,
+                             ctypes.c_double, ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64,
+                             ctypes.c_int, _vp])
+
+
+def casc_i8_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", y: int = 14,
+                        stream=None):
+    """casc_trsm_fp64x2 with the INT8 cascade as the GEMM (bit-exact with its oracle)."""
+    lo, dg = _uplo_diag(uplo, diag)
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = (alpha, 0.0) if isinstance(alpha, (int, float)) else alpha
+    lda = _ld_pair(A_hi, A_lo, "A")
+    ldb = _ld_pair(B_hi, B_lo, "B")
+    m, n = B_hi.shape
+    if tuple(A_hi.shape) != (m, m):
+        raise ValueError("A must be m x m")
+    _check(_lib.casc_i8_trsm_fp64x2(lo, tr, dg, m, n, float(ah), float(al), _ptr(A_hi),
+                                    _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo), ldb, int(y),
+                                    _stream(stream)), "casc_i8_trsm_fp64x2")
     return B_hi, B_lo
 
 

@@ -1496,6 +1496,9 @@ namespace casc {
 cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
                                 double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
                                 int num_sms, int uplo, cudaStream_t st);
+cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi,
+                                 const double* A_lo, int64_t lda, double* I_hi, double* I_lo,
+                                 cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -1664,6 +1667,80 @@ int casc_i8_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi
                           pack_b, pack_a, gemm);
   cudaFreeAsync(gws, st);
   host::set_launches(r == CASC_OK ? launches : 0);
+  return r;
+}
+
+// TRSM on the INT8 cascade (NEXT-4, reading R27): casc_trsm_fp64x2's blocked solve
+// with casc_i8_gemm_fp64x2_ex as the GEMM; bit-exact with orc_i8_casc_trsm.
+int casc_i8_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, double alpha_hi,
+                        double alpha_lo, const double* A_hi, const double* A_lo, int64_t lda,
+                        double* B_hi, double* B_lo, int64_t ldb, int y, casc_stream_t stream) {
+  host::set_launches(0);
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (diag != CASC_NONUNIT && diag != CASC_UNIT) ||
+      (trans != CASC_OP_N && trans != CASC_OP_T) || y < i8::YMIN || y > i8::YMAX)
+    return CASC_ERR_INVALID;
+  if (m < 0 || n < 0) return CASC_ERR_INVALID;
+  int r;
+  if ((r = host::check_mat(A_hi, m, m, lda)) || (r = host::check_mat(A_lo, m, m, lda))) return r;
+  if ((r = host::check_mat(B_hi, m, n, ldb)) || (r = host::check_mat(B_lo, m, n, ldb))) return r;
+  if (B_hi == B_lo || B_hi == A_hi || B_hi == A_lo || B_lo == A_hi || B_lo == A_lo)
+    return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = host::device_check(&sms))) return r;
+  const cudaStream_t st = S8(stream);
+  const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
+  const bool zero_alpha = (alpha_hi == 0.0 && alpha_lo == 0.0);
+  if (!unit_alpha &&
+      casc::launch_scale_c(m, n, alpha_hi, alpha_lo, zero_alpha ? 0 : 1, B_hi, B_lo, ldb, nullptr,
+                           sms, st) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  if (zero_alpha) return CASC_OK;
+  const int64_t NB = 256, nblk = (m + NB - 1) / NB;
+  const size_t inv_elems = (size_t)nblk * NB * NB, t_elems = (size_t)NB * n;
+  double* buf = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), (2 * inv_elems + 2 * t_elems) * 8, st) !=
+      cudaSuccess)
+    return CASC_ERR_CUDA;
+  double* inv_hi = buf;
+  double* inv_lo = buf + inv_elems;
+  double* t_hi = inv_lo + inv_elems;
+  double* t_lo = t_hi + t_elems;
+  r = casc::launch_trsm_diag_inv(uplo, diag, m, A_hi, A_lo, lda, inv_hi, inv_lo, st) ==
+              cudaSuccess
+          ? CASC_OK
+          : CASC_ERR_CUDA;
+  const bool eff_lower = (uplo == CASC_LOWER) != (trans == CASC_OP_T);
+  for (int64_t s = 0; s < nblk && r == CASC_OK; ++s) {
+    const int64_t b = eff_lower ? s : nblk - 1 - s;
+    const int64_t r0 = b * NB, nb = std::min(NB, m - r0), r1 = r0 + nb;
+    r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, nb, n, nb, 1.0, 0.0, inv_hi + b * NB * NB,
+                               inv_lo + b * NB * NB, NB, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb,
+                               0.0, 0.0, t_hi, t_lo, n, nullptr, y, nullptr, 0, stream);
+    if (r) break;
+    if (cudaMemcpy2DAsync(B_hi + r0 * ldb, ldb * 8, t_hi, n * 8, n * 8, nb,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpy2DAsync(B_lo + r0 * ldb, ldb * 8, t_lo, n * 8, n * 8, nb,
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      r = CASC_ERR_CUDA;
+      break;
+    }
+    if (eff_lower && r1 < m) {
+      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
+      r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + off,
+                                 A_lo + off, lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0,
+                                 B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, y, nullptr, 0,
+                                 stream);
+    }
+    if (!eff_lower && r0 > 0) {
+      const int64_t off = trans ? r0 * lda : r0;
+      r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + off, A_lo + off,
+                                 lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo,
+                                 ldb, nullptr, y, nullptr, 0, stream);
+    }
+  }
+  cudaFreeAsync(buf, st);
+  host::set_launches(0);
   return r;
 }
 

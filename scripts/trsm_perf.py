@@ -8,15 +8,17 @@ import torch
 sys.path.insert(0, ".")
 import paper_2303_04353_b200 as casc  # noqa: E402
 
-m = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-n = int(sys.argv[2]) if len(sys.argv) > 2 else m
+args = [x for x in sys.argv[1:] if not x.startswith("--")]
+m = int(args[0]) if args else 8192
+n = int(args[1]) if len(args) > 1 else m
 g = torch.Generator(device="cuda").manual_seed(0)
 A_hi = torch.tril(torch.rand(m, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1) / m
 A_hi += torch.diag(1.0 + torch.rand(m, dtype=torch.float64, device="cuda", generator=g))
 A_lo = A_hi * 2.0**-54
 B0 = torch.rand(m, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
 B_hi, B_lo = B0.clone(), B0 * 2.0**-54
-call = lambda: casc.casc_trsm_fp64x2("L", "N", 1.0, A_hi, A_lo, B_hi, B_lo)
+fn = casc.casc_i8_trsm_fp64x2 if "--i8" in sys.argv else casc.casc_trsm_fp64x2
+call = lambda: fn("L", "N", 1.0, A_hi, A_lo, B_hi, B_lo)
 call()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -451,3 +451,26 @@ def test_i8_syrk_bit_exact(casc, orc, uplo, trans, n, k, al, be):
     o_hi, o_lo, o_fl = orc.i8_casc_syrk(uplo, trans, al, *Ast, be, C0, np.zeros((n, n)),
                                         np.full((n, n), 9, np.uint8))
     assert bitwise(N(C_hi), o_hi) and bitwise(N(C_lo), o_lo) and np.array_equal(N(fl), o_fl)
+
+
+# ------------------------------------------------------------------ TRSM (NEXT-4)
+@pytest.mark.parametrize("uplo,trans,diag,m,n", [("L", "N", "N", 300, 40), ("U", "N", "U", 520, 9),
+                                                 ("L", "T", "N", 600, 17), ("U", "T", "N", 256, 5)])
+def test_i8_trsm_bit_exact(casc, orc, uplo, trans, diag, m, n):
+    """casc_i8_trsm_fp64x2 (reading R27 with the INT8 cascade as the GEMM):
+    bit-exact with orc_i8_casc_trsm (diagonal inverses bitwise, INT8 GEMMs
+    bit-exact), alpha = 2^p included."""
+    rng = np.random.default_rng(29)
+    A_hi = rng.uniform(-1, 1, (m, m)) / m
+    A_hi = np.tril(A_hi) if uplo == "L" else np.triu(A_hi)
+    A_lo = A_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, m))
+    dgl = 1.0 + rng.uniform(0, 1, m)
+    A_hi[np.arange(m), np.arange(m)] = dgl
+    A_lo[np.arange(m), np.arange(m)] = dgl * 2.0 ** -55
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    for al in ((1.0, 0.0), (4.0, 0.0)):
+        Xh, Xl = T(B_hi), T(B_lo)
+        casc.casc_i8_trsm_fp64x2(uplo, diag, al, T(A_hi), T(A_lo), Xh, Xl, trans=trans)
+        o_hi, o_lo = orc.i8_casc_trsm(uplo, diag, al, A_hi, A_lo, B_hi, B_lo, trans=trans)
+        assert bitwise(N(Xh), o_hi) and bitwise(N(Xl), o_lo), al

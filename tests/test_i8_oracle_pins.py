@@ -353,3 +353,31 @@ def test_i8_syrk_oracle(orc, uplo, trans):
             assert abs(F(Ch[i, j]) + F(Cl[i, j]) - ex) <= 4 * k * F(2) ** -104 * absab
     S = orc.i8_casc_syrk(uplo, trans, (0.5, 0.0), *Ast, (0.0, 0.0), sent, sent)
     assert np.array_equal(S[0][tri], 0.5 * Ch[tri]) and np.array_equal(S[1][tri], 0.5 * Cl[tri])
+
+
+@pytest.mark.parametrize("uplo,trans,m,n", [("L", "N", 40, 3), ("U", "T", 300, 2)])
+def test_i8_trsm_oracle(orc, uplo, trans, m, n):
+    """NEXT-4 TRSM on the INT8 cascade: the exact residual of op(A) X = B within
+    2^-90 (|op(A)||X|) row by row for a diagonally dominant A."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(31)
+    A_hi = rng.uniform(-1, 1, (m, m)) / m
+    A_hi = np.tril(A_hi) if uplo == "L" else np.triu(A_hi)
+    A_lo = A_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, m))
+    dg = 1.0 + rng.uniform(0, 1, m)
+    A_hi[np.arange(m), np.arange(m)] = dg
+    A_lo[np.arange(m), np.arange(m)] = 0.0
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    X_hi, X_lo = orc.i8_casc_trsm(uplo, "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
+    A = [[F(A_hi[i, j]) + F(A_lo[i, j]) for j in range(m)] for i in range(m)]
+    if trans == "T":
+        A = [list(r) for r in zip(*A)]
+    lower = (uplo == "L") != (trans == "T")
+    for i in range(0, m, 1 if m <= 40 else 11):
+        lo, hi = (0, i + 1) if lower else (i, m)
+        for j in range(n):
+            x = [F(X_hi[l, j]) + F(X_lo[l, j]) for l in range(lo, hi)]
+            r = sum(a * b for a, b in zip(A[i][lo:hi], x)) - (F(B_hi[i, j]) + F(B_lo[i, j]))
+            mag = sum(abs(a * b) for a, b in zip(A[i][lo:hi], x))
+            assert abs(r) <= F(2) ** -90 * mag
