@@ -383,6 +383,9 @@ void orc_i8_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, doub
 #define I8_TRSM_NB 256
 void orc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* Ahi, const double* Alo,
                        int64_t lda, double* Ihi, double* Ilo);
+void orc_trsm_update(int trans, int64_t R0, int64_t R1, int64_t C0, int64_t C1, int64_t n,
+                     const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
+                     int64_t ldb, int nthreads, int i8);
 void orc_i8_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double ah, double al,
                       const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
                       int64_t ldb, int y, int nthreads) {
@@ -416,17 +419,14 @@ void orc_i8_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, doubl
         Bhi[(r0 + i) * ldb + j] = Th[i * n + j];
         Blo[(r0 + i) * ldb + j] = Tl[i * n + j];
       }
-    if (eff_lower && r1 < m) {
-      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
-      orc_i8_casc_gemm_ex(trans, 0, m - r1, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
-                          Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
-                          Blo + r1 * ldb, ldb, NULL, y, nthreads);
-    }
-    if (!eff_lower && r0 > 0) {
-      const int64_t off = trans ? r0 * lda : r0;
-      orc_i8_casc_gemm_ex(trans, 0, r0, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
-                          Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi, Blo, ldb, NULL, y,
-                          nthreads);
+    const int64_t S0 = (b / 4) * 4 * I8_TRSM_NB;
+    const int64_t S1 = S0 + 4 * I8_TRSM_NB < m ? S0 + 4 * I8_TRSM_NB : m;
+    if (eff_lower) {
+      orc_trsm_update(trans, r1, S1, r0, r1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, y);
+      if (r1 == S1) orc_trsm_update(trans, S1, m, S0, S1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, y);
+    } else {
+      orc_trsm_update(trans, S0, r0, r0, r1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, y);
+      if (r0 == S0) orc_trsm_update(trans, 0, S0, S0, S1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, y);
     }
   }
   free(Ihi);

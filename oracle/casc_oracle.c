@@ -707,13 +707,38 @@ void orc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* Ahi, const d
   }
 }
 
+#define TRSM_SB 4 /* diagonal blocks per super-block of the trailing updates */
+/* B[R0:R1) := B[R0:R1) - op(A)[R0:R1, C0:C1) X[C0:C1) (X = B's rows C0..C1-1),
+ * with the cascaded GEMM (i8 = 0) or, when i8 = y > 0, the INT8 cascade. */
+void orc_i8_casc_gemm_ex(int transa, int transb, int64_t m, int64_t n, int64_t k, double ah,
+                         double al, const double* Ahi, const double* Alo, int64_t lda,
+                         const double* Bhi, const double* Blo, int64_t ldb, double bh, double bl,
+                         double* Chi, double* Clo, int64_t ldc, uint8_t* flags, int y,
+                         int nthreads);
+void orc_trsm_update(int trans, int64_t R0, int64_t R1, int64_t C0, int64_t C1, int64_t n,
+                     const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
+                     int64_t ldb, int nthreads, int i8) {
+  if (R1 <= R0 || C1 <= C0) return;
+  const int64_t off = trans ? C0 * lda + R0 : R0 * lda + C0;
+  if (i8)
+    orc_i8_casc_gemm_ex(trans, 0, R1 - R0, n, C1 - C0, -1.0, 0.0, Ahi + off, Alo + off, lda,
+                        Bhi + C0 * ldb, Blo + C0 * ldb, ldb, 1.0, 0.0, Bhi + R0 * ldb,
+                        Blo + R0 * ldb, ldb, NULL, i8, nthreads);
+  else
+    orc_casc_gemm_ex(trans, 0, R1 - R0, n, C1 - C0, -1.0, 0.0, Ahi + off, Alo + off, lda,
+                     Bhi + C0 * ldb, Blo + C0 * ldb, ldb, 1.0, 0.0, Bhi + R0 * ldb,
+                     Blo + R0 * ldb, ldb, NULL, nthreads);
+}
+
 /* TRSM, left side: solve op(A) X = alpha B, op(A) = A (trans 0) or A^T (trans
  * 1); X overwrites the m x n B (ldb).  B := alpha (x) B; the diagonal blocks of
  * A are inverted (orc_trsm_diag_inv, op(A_bb)^-1 = op(Inv_b)); then block by
  * block in the order of op(A)'s triangle (ascending when op(A) is lower,
- * descending when upper): X_b = op(Inv_b) B_b and B_rest := B_rest -
- * op(A)_rest,b X_b, both with the cascaded GEMM (orc_casc_gemm_ex: alpha 1,
- * beta 0, then alpha -1, beta 1; op(A)_rest,b read transposed when trans). */
+ * descending when upper): X_b = op(Inv_b) B_b, then the remaining rows of its
+ * super-block of TRSM_SB blocks are updated with X_b and, after the super-
+ * block's last block, the trailing rows with the whole super-block's X (k up
+ * to 1024: fewer, deeper updates), all with the cascaded GEMM
+ * (orc_casc_gemm_ex: alpha 1, beta 0, then alpha -1, beta 1). */
 void orc_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double ah, double al,
                    const double* Ahi, const double* Alo, int64_t lda, double* Bhi, double* Blo,
                    int64_t ldb, int nthreads) {
@@ -748,17 +773,16 @@ void orc_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double a
         Bhi[(r0 + i) * ldb + j] = Th[i * n + j];
         Blo[(r0 + i) * ldb + j] = Tl[i * n + j];
       }
-    /* B_rest := B_rest - op(A)_rest,b X_b */
-    if (eff_lower && r1 < m) {
-      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
-      orc_casc_gemm_ex(trans, 0, m - r1, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda,
-                       Bhi + r0 * ldb, Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi + r1 * ldb,
-                       Blo + r1 * ldb, ldb, NULL, nthreads);
-    }
-    if (!eff_lower && r0 > 0) {
-      const int64_t off = trans ? r0 * lda : r0;
-      orc_casc_gemm_ex(trans, 0, r0, n, nb, -1.0, 0.0, Ahi + off, Alo + off, lda, Bhi + r0 * ldb,
-                       Blo + r0 * ldb, ldb, 1.0, 0.0, Bhi, Blo, ldb, NULL, nthreads);
+    /* updates: inside the super-block (TRSM_SB blocks) with this block's X,
+     * then, after its last block, the trailing rows with the whole super-block */
+    const int64_t S0 = (b / TRSM_SB) * TRSM_SB * TRSM_NB;
+    const int64_t S1 = S0 + TRSM_SB * TRSM_NB < m ? S0 + TRSM_SB * TRSM_NB : m;
+    if (eff_lower) {
+      orc_trsm_update(trans, r1, S1, r0, r1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, 0);
+      if (r1 == S1) orc_trsm_update(trans, S1, m, S0, S1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, 0);
+    } else {
+      orc_trsm_update(trans, S0, r0, r0, r1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, 0);
+      if (r0 == S0) orc_trsm_update(trans, 0, S0, S0, S1, n, Ahi, Alo, lda, Bhi, Blo, ldb, nthreads, 0);
     }
   }
   free(Ihi);

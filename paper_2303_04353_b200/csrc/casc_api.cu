@@ -677,6 +677,7 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
 // ---------------------------------------------------------------- TRSM (NEXT-4)
 // Left side: op(A) X = alpha B, op(A) = A or A^T, X overwrites B (reading R27).
 static constexpr int64_t kTrsmNb = 256;
+static constexpr int64_t kTrsmSb = 4;  // diagonal blocks per super-block of the trailing updates
 
 int casc_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi, const double* A_lo,
                        int64_t lda, double* inv_hi, double* inv_lo, casc_stream_t stream) {
@@ -759,20 +760,27 @@ int casc_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, double
       r = CASC_ERR_CUDA;
       break;
     }
-    // B_rest := B_rest - op(A)_rest,b X_b (op(A)_rest,b read transposed when trans)
+    // updates: the super-block's remaining rows with X_b, then, after its last
+    // block, the trailing rows with the whole super-block's X (reading R27)
+    auto update = [&](int64_t R0, int64_t R1, int64_t C0, int64_t C1) {
+      if (r != CASC_OK || R1 <= R0 || C1 <= C0) return;
+      const int64_t off = trans ? C0 * lda + R0 : R0 * lda + C0;
+      r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, R1 - R0, n, C1 - C0, -1.0, 0.0, A_hi + off,
+                              A_lo + off, lda, B_hi + C0 * ldb, B_lo + C0 * ldb, ldb, 1.0, 0.0,
+                              B_hi + R0 * ldb, B_lo + R0 * ldb, ldb, nullptr, nullptr, 0, stream);
+      launches += g_launches;
+    };
+    const int64_t S0 = (b / kTrsmSb) * kTrsmSb * kTrsmNb;
+    const int64_t S1 = std::min(S0 + kTrsmSb * kTrsmNb, m);
     g_launches = 0;
-    if (eff_lower && r1 < m) {
-      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
-      r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + off, A_lo + off,
-                              lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0,
-                              B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, nullptr, 0, stream);
+    if (eff_lower) {
+      update(r1, S1, r0, r1);
+      if (r1 == S1) update(S1, m, S0, S1);
+    } else {
+      update(S0, r0, r0, r1);
+      if (r0 == S0) update(0, S0, S0, S1);
     }
-    if (!eff_lower && r0 > 0) {
-      const int64_t off = trans ? r0 * lda : r0;
-      r = casc_gemm_fp64x2_ex(trans, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + off, A_lo + off, lda,
-                              B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo, ldb,
-                              nullptr, nullptr, 0, stream);
-    }
+    g_launches = 0;
     launches += g_launches;
   }
   cudaFreeAsync(buf, st);

@@ -1725,18 +1725,21 @@ int casc_i8_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, dou
       r = CASC_ERR_CUDA;
       break;
     }
-    if (eff_lower && r1 < m) {
-      const int64_t off = trans ? r0 * lda + r1 : r1 * lda + r0;
-      r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, m - r1, n, nb, -1.0, 0.0, A_hi + off,
-                                 A_lo + off, lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0,
-                                 B_hi + r1 * ldb, B_lo + r1 * ldb, ldb, nullptr, y, nullptr, 0,
+    auto update = [&](int64_t R0, int64_t R1, int64_t C0, int64_t C1) {
+      if (r != CASC_OK || R1 <= R0 || C1 <= C0) return;
+      const int64_t off = trans ? C0 * lda + R0 : R0 * lda + C0;
+      r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, R1 - R0, n, C1 - C0, -1.0, 0.0, A_hi + off,
+                                 A_lo + off, lda, B_hi + C0 * ldb, B_lo + C0 * ldb, ldb, 1.0, 0.0,
+                                 B_hi + R0 * ldb, B_lo + R0 * ldb, ldb, nullptr, y, nullptr, 0,
                                  stream);
-    }
-    if (!eff_lower && r0 > 0) {
-      const int64_t off = trans ? r0 * lda : r0;
-      r = casc_i8_gemm_fp64x2_ex(trans, CASC_OP_N, r0, n, nb, -1.0, 0.0, A_hi + off, A_lo + off,
-                                 lda, B_hi + r0 * ldb, B_lo + r0 * ldb, ldb, 1.0, 0.0, B_hi, B_lo,
-                                 ldb, nullptr, y, nullptr, 0, stream);
+    };
+    const int64_t S0 = (b / 4) * 4 * NB, S1 = std::min(S0 + 4 * NB, m);
+    if (eff_lower) {
+      update(r1, S1, r0, r1);
+      if (r1 == S1) update(S1, m, S0, S1);
+    } else {
+      update(S0, r0, r0, r1);
+      if (r0 == S0) update(0, S0, S0, S1);
     }
   }
   cudaFreeAsync(buf, st);

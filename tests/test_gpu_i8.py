@@ -455,7 +455,8 @@ def test_i8_syrk_bit_exact(casc, orc, uplo, trans, n, k, al, be):
 
 # ------------------------------------------------------------------ TRSM (NEXT-4)
 @pytest.mark.parametrize("uplo,trans,diag,m,n", [("L", "N", "N", 300, 40), ("U", "N", "U", 520, 9),
-                                                 ("L", "T", "N", 600, 17), ("U", "T", "N", 256, 5)])
+                                                 ("L", "T", "N", 600, 17), ("U", "T", "N", 256, 5),
+                                                 ("L", "N", "N", 1100, 6), ("U", "T", "N", 1300, 3)])
 def test_i8_trsm_bit_exact(casc, orc, uplo, trans, diag, m, n):
     """casc_i8_trsm_fp64x2 (reading R27 with the INT8 cascade as the GEMM):
     bit-exact with orc_i8_casc_trsm (diagonal inverses bitwise, INT8 GEMMs

@@ -633,7 +633,8 @@ def test_trsm_diag_inverse_bitwise(casc, orc, uplo, diag, m):
 
 @pytest.mark.parametrize("uplo,diag,m,n,trans", [("L", "N", 300, 70, "N"), ("U", "N", 600, 130, "N"),
                                                  ("L", "U", 520, 33, "N"), ("U", "N", 200, 1, "N"),
-                                                 ("L", "N", 600, 40, "T"), ("U", "U", 300, 9, "T")])
+                                                 ("L", "N", 600, 40, "T"), ("U", "U", 300, 9, "T"),
+                                                 ("L", "N", 1100, 20, "N"), ("U", "N", 1300, 7, "T")])
 def test_trsm_vs_oracle_and_residual(casc, orc, uplo, diag, m, n, trans):
     """GPU TRSM vs the oracle's (same blocked algorithm; the GEMM updates agree to
     the cascade's bound, not bitwise): within 2^-96 relative on diagonally

@@ -523,7 +523,8 @@ def test_trsm_diag_inverse_oracle(orc, uplo, unit):
 
 @pytest.mark.parametrize("uplo,trans,unit,m,n", [("L", "N", False, 40, 5), ("U", "N", False, 300, 3),
                                                  ("L", "N", True, 300, 2), ("L", "T", False, 300, 2),
-                                                 ("U", "T", False, 40, 3)])
+                                                 ("U", "T", False, 40, 3), ("L", "N", False, 1100, 1),
+                                                 ("U", "T", False, 1100, 1)])
 def test_trsm_oracle(orc, uplo, trans, unit, m, n):
     """R27 TRSM: the exact residual of op(A) X = B (dyadic rationals, no
     rounding) within 2^-96 (|op(A)||X|) row by row (diagonally dominant A, so
@@ -541,7 +542,7 @@ def test_trsm_oracle(orc, uplo, trans, unit, m, n):
         A = [list(r) for r in zip(*A)]  # op(A)
     lower = (uplo == "L") != (trans == "T")
     X = [[fr(X_hi[i, j]) + fr(X_lo[i, j]) for j in range(n)] for i in range(m)]
-    for i in range(0, m, 1 if m <= 40 else 9):
+    for i in range(0, m, 1 if m <= 40 else (9 if m <= 300 else 97)):
         lo, hi = (0, i + 1) if lower else (i, m)
         for j in range(n):
             r = sum(A[i][l] * X[l][j] for l in range(lo, hi)) - (fr(B_hi[i, j]) + fr(B_lo[i, j]))
