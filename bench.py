@@ -130,7 +130,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         oC_hi = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
         oC_lo = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
         oF = torch.empty((mloc, n), dtype=torch.uint8).pin_memory()
-        e2e_steps = max(1, min(steps, 2))
+        e2e_steps = 5
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -180,6 +180,51 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
                                      "plus the epilogue's group-value workspace"},
         "clocks": cs.summary(),
     }
+
+
+def measure_small(casc, dev, peak_sus, sizes=(512, 1024, 2048), reps=20):
+    """Small problems on one GPU (cfg1 = 1024^3 among them): casc_gemm_fp64x2
+    (split + fused GEMM, caller workspace) on device-resident cfg1-style
+    inputs, median of `reps` calls after 3 warm-ups, CUDA events, clocks
+    sampled while they run.  Context lines (the metric is cfg4's)."""
+    import numpy as np
+    import torch
+
+    import casc_inputs as I
+    out = {}
+    with ClockSampler(None) as cs:
+        for nn in sizes:
+            d = I.make_config(1, m=nn, n=nn, k=nn, seed=1)
+            A_hi, A_lo, B_hi, B_lo = (torch.from_numpy(np.ascontiguousarray(d[x])).to(dev)
+                                      for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+            C = [torch.empty((nn, nn), dtype=torch.float64, device=dev) for _ in range(2)]
+            fl = torch.empty((nn, nn), dtype=torch.uint8, device=dev)
+            ws = torch.empty(casc.casc_workspace_bytes(nn, nn, nn), dtype=torch.uint8, device=dev)
+
+            def call():
+                casc.casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=C[0], C_lo=C[1], flags=fl,
+                                      workspace=ws)
+            for _ in range(3):
+                call()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record()
+                call()
+                a1.record()
+                a1.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            t = statistics.median(ts)
+            v = 2.0 * nn ** 3 / (t * 1e-3) / 1e9
+            out[f"{nn}^3"] = {"ms_median": t, "ms_min": min(ts), "value": v, "unit": UNIT,
+                              "frac_of_fp64tc_roofline": v / 1e3 / (peak_sus / 10.0)}
+            del A_hi, A_lo, B_hi, B_lo, C, fl, ws
+    out["clocks"] = cs.summary()
+    out["note"] = ("casc_gemm_fp64x2_ws per call (split A, split B, fused GEMM; split mode and "
+                   "its reduction where the plan picks them), inputs resident, median of %d" % reps)
+    return out
 
 
 def load_ncu_traffic():
@@ -347,9 +392,24 @@ def main():
                     help="skip the NEXT-4 SYRK / TRSM measurements (N = 1)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not under torchrun: launch the N ranks ourselves (one process per GPU,
+        # NCCL), the same command line the driver uses; rank 0 prints the line
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: the two must "
+                         "agree (launch one rank per GPU)\n")
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference(args, rank)
@@ -433,16 +493,18 @@ def main():
             barrier()
         total_ms = t_start.elapsed_time(t_end)
         ph = {name: 0.0 for name in op.phase_names}
+        per_step = []
         for s in range(args.steps):
             e = ev[s]
             for i, name in enumerate(op.phase_names):
                 ph[name] += e[i].elapsed_time(e[i + 1])
+            per_step.append(e[0].elapsed_time(e[len(op.phase_names)]))
         ph = {key: v / args.steps for key, v in ph.items()}
-        return total_ms, ph, cs.summary(), launches
+        return total_ms, ph, cs.summary(), launches, per_step
 
-    total_ms, phases, clocks, launches = timed_region()
+    total_ms, phases, clocks, launches, per_step = timed_region()
     if any(r in clocks.get("reasons", []) for r in REJECT_REASONS):
-        total_ms, phases, clocks, launches = timed_region()  # re-measure once
+        total_ms, phases, clocks, launches, per_step = timed_region()  # re-measure once
         clocks["remeasured"] = True
 
     # ---- max over ranks
@@ -452,6 +514,13 @@ def main():
     total_ms = t.item()
     ms_per_step = total_ms / args.steps
     value = 2.0 * m * n * k / (ms_per_step * 1e-3) / 1e9
+    tm = torch.tensor([statistics.median(per_step), min(per_step), max(per_step)],
+                      dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    step_stats = {"median_ms": tm[0].item(), "min_ms": tm[1].item(), "max_ms": tm[2].item(),
+                  "median_value": 2.0 * m * n * k / (tm[0].item() * 1e-3) / 1e9,
+                  "note": "per-step CUDA-event times (max over ranks); value = mean of K steps"}
 
     # ---- e2e through the public API with host buffers (pinned), every step:
     # H2D of this rank's inputs, the call, D2H of the result (C_hi, C_lo, flags)
@@ -460,7 +529,7 @@ def main():
         oC_hi = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
         oC_lo = torch.empty((mloc, n), dtype=torch.float64).pin_memory()
         oF = torch.empty((mloc, n), dtype=torch.uint8).pin_memory()
-        e2e_steps = max(1, min(args.steps, 2))
+        e2e_steps = 5
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -604,6 +673,14 @@ def main():
         except Exception as ex:  # reported, never silently replaced
             next4 = {"error": repr(ex)}
 
+    # ---- small problems (cfg1 among them), N = 1, with their own clock record
+    small = None
+    if world == 1:
+        try:
+            small = measure_small(casc, dev, peak_sus)
+        except Exception as ex:  # reported, never silently replaced
+            small = {"error": repr(ex)}
+
     # ---- context: cuBLAS DGEMM time for the paper's t / t_DGEMM (off the hot path)
     dgemm_ratio = None
     if world == 1:
@@ -639,7 +716,8 @@ def main():
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "step_stats": step_stats,
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(args, world),
         "frac_of_fp64tc_roofline": value / 1e3 / (world * peak_sus / 10.0),
@@ -656,6 +734,7 @@ def main():
         "clocks": clocks,
         "next3_int8_cascade": int8,
         "next4_level3": next4,
+        "small_problems": small,
     }
     if plumbing:
         out["plumbing_test"] = "all ranks on cuda:0 with gloo: NOT a measurement"

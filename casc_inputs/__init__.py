@@ -186,6 +186,9 @@ def make_config(cfg: int, seed: int | None = None, m: int | None = None,
                 B_lo[p0 + span:p0 + span + w, :] = -B_lo[p0:p0 + w, :] + pert
         else:
             raise ValueError(f"unknown cfg3 variant {variant}")
+        # the 2^-60 perturbation went into the lo limb: renormalise the pairs
+        # (|lo| <= ulp(hi)/2 again for small |hi|; reading R15)
+        B_hi, B_lo = _renormalise(B_hi, B_lo)
         B_hi = np.ascontiguousarray(B_hi[:, cols])
         B_lo = np.ascontiguousarray(B_lo[:, cols])
     return dict(A_hi=A_hi, A_lo=A_lo, B_hi=B_hi, B_lo=B_lo, m=m, n=n, k=k, name=name)

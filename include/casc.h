@@ -36,12 +36,18 @@
  *   - Unless stated otherwise, pointers are DEVICE pointers owned by the
  *     caller; the library reads inputs and writes outputs only.
  *   - Work is enqueued on `stream` (NULL = legacy default stream).  The library
- *     never synchronises the host except where stated (allocation of its own
- *     workspace); kernel faults surface at the caller's next synchronisation.
+ *     never synchronises the host except where stated (the teardown calls
+ *     casc_finalize / casc_i8_finalize, and k == 0 of the host-operand
+ *     entries); kernel faults surface at the caller's next synchronisation.
+ *     Every call is re-entrant: concurrent calls on different streams or host
+ *     threads share no device memory (workspaces are the caller's or
+ *     stream-ordered allocations of the call).
  *   - Preconditions (not checked): inputs finite; pairs normalised
- *     (|lo| <= ulp(hi)/2); every row-panel / column-panel max |hi| in
- *     [2^-1000, 2^1000).  Outside them results are computed but the paper's
- *     error bound is not guaranteed.
+ *     (|lo| <= ulp(hi)/2).  Outside them results are computed but the
+ *     paper's error bound is not guaranteed.  Any finite exponent range is
+ *     handled exactly: the scalings by 2^-e (split) and 2^(e+f) (combine) are
+ *     ldexp-exact, subnormal results and overflow to +-inf included (reading
+ *     R16).
  *   - Return value: a casc_status.  No exception crosses the ABI.
  *   - Results are deterministic: the same inputs give the same bits on every
  *     call, every grid size and every number of GPUs.
@@ -95,18 +101,20 @@ int casc_select_widths(int64_t k, int* c);
  *               (catastrophic cancellation suspected, §3.7); the library
  *               performs no correction.
  *   stream:     CUDA stream.
- * Uses a library-owned device workspace of casc_workspace_bytes(m, n, k)
- * bytes, allocated (host-synchronising cudaMalloc) on first use or growth
- * and reused; release it with casc_finalize().  Not re-entrant across host
- * threads on the same device. */
+ * Takes a workspace of casc_workspace_bytes(m, n, k) bytes from the device's
+ * stream-ordered pool for the duration of the call (cudaMallocAsync /
+ * cudaFreeAsync on `stream`; the pool keeps it cached, casc_finalize returns
+ * it).  No host synchronisation; re-entrant. */
 int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
                      const double* A_hi, const double* A_lo, int64_t lda,
                      const double* B_hi, const double* B_lo, int64_t ldb,
                      double* C_hi, double* C_lo, int64_t ldc,
                      uint8_t* flags, casc_stream_t stream);
 
-/* Bytes of device workspace needed by casc_gemm_fp64x2 for (m, n, k):
- * casc_packed_a_bytes(m, k) + casc_packed_b_bytes(k, n). */
+/* Bytes of device workspace needed by casc_gemm_fp64x2 for (m, n, k): the
+ * packed A and B (each rounded up to 256 bytes), the small-problem split-mode
+ * panel sums when that mode applies, and a 256-byte slot for the fused
+ * kernel's per-launch tile-wave counter. */
 size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k);
 
 /* casc_gemm_fp64x2 with HOST-resident operands (BASELINE north star's call,
@@ -146,7 +154,9 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k,
                         uint8_t* flags, void* workspace, size_t workspace_bytes,
                         casc_stream_t stream);
 
-/* Free the library-owned workspace of the current device (host-synchronising). */
+/* Teardown: wait for the current device and return the cached memory of its
+ * default stream-ordered pool (the per-call workspaces of both cascades) to
+ * the system (cudaMemPoolTrimTo).  Host-synchronising. */
 int casc_finalize(void);
 
 /* ------------------------------------------------------------------------ */
@@ -216,6 +226,14 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k,
                     const double* A_hi, const double* A_lo, int64_t lda,
                     const double* B_hi, const double* B_lo, int64_t ldb,
                     int64_t panel, double* bins, casc_stream_t stream);
+
+/* Test export of the device power-of-two scaling the split (2^-e) and the
+ * combine (2^(e_i+f_j)) use: out[i] = x[i] 2^n[i] rounded once
+ * to nearest-even for any int n[i] (bitwise C99 ldexp: subnormal results,
+ * overflow to +-inf, signed zeros; reading R16).  x, n, out: device arrays of
+ * `count` elements (out may equal x). */
+int casc_debug_ldexp(int64_t count, const double* x, const int32_t* n, double* out,
+                     casc_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* BLAS-style generality ("other level-3 BLAS").  */
@@ -348,12 +366,10 @@ int casc_slice_product(int64_t m, int64_t n, int64_t k,
 
 /* C := A B through y int8 slices, 3 <= y <= 15 (CASC_ERR_INVALID otherwise).
  * Arguments, aliasing rules, k == 0 / m == 0 / n == 0 behaviour and errors as
- * casc_gemm_fp64x2 (flags semantics: R26 above).  Uses a library-owned device
- * workspace of casc_i8_workspace_bytes(m, n, k, y) bytes (allocated with a
- * host-synchronising cudaMalloc on first use or growth; casc_i8_finalize frees it).
- * Not re-entrant across host threads or concurrent streams on the same device
- * (the workspace also holds the kernel's wave-synchronisation counter): use
- * casc_i8_gemm_fp64x2_ws with one workspace per concurrent call. */
+ * casc_gemm_fp64x2 (flags semantics: R26 above).  Takes a workspace of
+ * casc_i8_workspace_bytes(m, n, k, y) bytes from the device's stream-ordered
+ * pool for the duration of the call (as casc_gemm_fp64x2); no host
+ * synchronisation, re-entrant. */
 int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k,
                         const double* A_hi, const double* A_lo, int64_t lda,
                         const double* B_hi, const double* B_lo, int64_t ldb,
@@ -454,7 +470,7 @@ size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
 int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
                         const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
                         uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream);
-/* Free the library-owned INT8-cascade workspace of the current device. */
+/* Same as casc_finalize (kept for the INT8 cascade's API symmetry). */
 int casc_i8_finalize(void);
 
 /* Test export of the split (R22, R23) as computed by the GEMM's split kernels:

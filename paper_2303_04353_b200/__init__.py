@@ -57,6 +57,7 @@ _sig("casc_split_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_split_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp])
 _sig("casc_last_launch_count", [])
+_sig("casc_debug_ldexp", [_i64, _vp, _vp, _vp, _vp])
 _sig("casc_gemm_fp64x2_simple", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
                                  _i64, _vp, _vp])
 _sig("casc_slice_product", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_int,
@@ -73,7 +74,8 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_packed_block_bytes", "casc_i8_pack", "casc_i8_gemm_ws_bytes",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
-            "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2"]
+            "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2",
+            "casc_debug_ldexp"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -420,7 +422,7 @@ def casc_gemm_fp64x2(A_hi, A_lo, B_hi, B_lo, C_hi=None, C_lo=None, flags=None,
                      want_flags=True, stream=None, workspace=None):
     """C := A B (cascaded FP64x2).  Returns (C_hi, C_lo, flags).  With
     `workspace` (uint8 CUDA tensor of casc_workspace_bytes(m, n, k)) this calls
-    casc_gemm_fp64x2_ws, otherwise the library-owned workspace is used."""
+    casc_gemm_fp64x2_ws, otherwise a stream-ordered per-call workspace is used."""
     lda = _ld_pair(A_hi, A_lo, "A")
     ldb = _ld_pair(B_hi, B_lo, "B")
     m, k = A_hi.shape
@@ -529,6 +531,19 @@ def casc_debug_bins(A_hi, A_lo, B_hi, B_lo, panel: int, stream=None):
     _check(_lib.casc_debug_bins(m, n, k, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi), _ptr(B_lo),
                                 ldb, panel, _ptr(bins), _stream(stream)), "casc_debug_bins")
     return bins
+
+
+def casc_debug_ldexp(x, n, stream=None):
+    """x * 2^n per element as the kernels scale (bitwise ldexp), x float64 and n
+    int32 CUDA tensors of the same shape."""
+    x = x.contiguous()
+    n = n.to(torch.int32).contiguous()
+    if x.shape != n.shape:
+        raise ValueError("x and n differ in shape")
+    out = torch.empty_like(x)
+    _check(_lib.casc_debug_ldexp(x.numel(), _ptr(x), _ptr(n), _ptr(out), _stream(stream)),
+           "casc_debug_ldexp")
+    return out
 
 
 def casc_gemm_fp64x2_simple(A_hi, A_lo, B_hi, B_lo, C_hi=None, C_lo=None, flags=None,

@@ -24,6 +24,8 @@ cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_
 cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,
                                 double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
                                 int num_sms, int uplo, cudaStream_t st);
+cudaError_t launch_ldexp(int64_t count, const double* x, const int32_t* n, double* out,
+                         cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -107,6 +109,15 @@ int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
   return CASC_OK;
 }
 
+// X (= B, overwritten) must not overlap the triangle A or itself (both TRSMs)
+bool trsm_overlap(int64_t m, int64_t n, const double* A_hi, const double* A_lo, int64_t lda,
+                  const double* B_hi, const double* B_lo, int64_t ldb) {
+  const size_t ea = extent(m, m, lda), eb = extent(m, n, ldb);
+  return ranges_overlap(B_hi, eb, A_hi, ea) || ranges_overlap(B_hi, eb, A_lo, ea) ||
+         ranges_overlap(B_lo, eb, A_hi, ea) || ranges_overlap(B_lo, eb, A_lo, ea) ||
+         ranges_overlap(B_hi, eb, B_lo, eb);
+}
+
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
 
 struct AlphaBeta {
@@ -132,7 +143,15 @@ int split_plan(int64_t m, int64_t n, int64_t k, int sms) {
   if ((double)P * m * n * 17.0 > (double)(1ull << 31)) return 0;
   return (int)P;
 }
-size_t split_bytes(int64_t m, int64_t n, int P) { return P ? (size_t)P * m * n * 17 : 0; }
+size_t split_bytes(int64_t m, int64_t n, int P) {
+  return P ? ((size_t)P * m * n * 17 + 255) / 256 * 256 : 0;
+}
+// the fused kernel's per-launch scratch (wave counter, WIDE list) at the end of a
+// workspace: sized for the most work items a call with (m, n, k) can have
+size_t scratch_bytes_for(int64_t m, int64_t n, int P) {
+  const int64_t tiles = ((m + casc::TM - 1) / casc::TM) * ((n + casc::TN - 1) / casc::TN);
+  return casc::gemm_scratch_bytes(tiles * (P > 1 ? P : 1));
+}
 
 int current_sms() {
   int dev = 0, sms = 0;
@@ -147,7 +166,8 @@ int current_sms() {
 int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void* pb,
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
-                     const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0) {
+                     const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0,
+                     void* scratch = nullptr) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -178,14 +198,30 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.tri = tri;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
   const int P = (!dbg && !tri && st_begin == 0 && st_end == nst) ? split_plan(m, n, k, sms) : 0;
+  // per-launch scratch of the fused kernel (wave counter, WIDE list): the caller's
+  // workspace slot, else a stream-ordered allocation of this call (never shared
+  // between launches or streams)
+  const int64_t items = P ? (int64_t)a.mblocks * a.nblocks * P
+                          : (tri ? (int64_t)a.mblocks * (a.mblocks + 1) / 2
+                                 : (int64_t)a.mblocks * a.nblocks);
+  bool own_scratch = false;
+  if (!dbg && !scratch) {
+    if (cudaMallocAsync(&scratch, casc::gemm_scratch_bytes(items), st) != cudaSuccess)
+      return CASC_ERR_CUDA;
+    own_scratch = true;
+  }
+  a.scratch = scratch;
   if (!P) {
     cudaError_t e = casc::launch_gemm(a, sms, st);
-    if (e == cudaSuccess) ++g_launches;
+    if (own_scratch) cudaFreeAsync(scratch, st);
+    if (e == cudaSuccess) g_launches += dbg ? 1 : 2;
     return cuda_status(e);
   }
   void* buf = split_ws;
-  if (!buf && cudaMallocAsync(&buf, split_bytes(m, n, P), st) != cudaSuccess)
+  if (!buf && cudaMallocAsync(&buf, split_bytes(m, n, P), st) != cudaSuccess) {
+    if (own_scratch) cudaFreeAsync(scratch, st);
     return CASC_ERR_CUDA;
+  }
   const int64_t mn = m * n;
   a.split_p = P;
   a.t_hi = static_cast<double*>(buf);
@@ -197,16 +233,11 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
     e = casc::launch_split_reduce(P, m, n, a.t_hi, a.t_lo, a.fbuf, C_hi, C_lo, ldc, flags, abv.ab,
                                   abv.ah, abv.al, abv.bh, abv.bl, sms, st);
   if (!split_ws) cudaFreeAsync(buf, st);
-  if (e == cudaSuccess) g_launches += 2;
+  if (own_scratch) cudaFreeAsync(scratch, st);
+  if (e == cudaSuccess) g_launches += 3;
   return cuda_status(e);
 }
 
-struct Workspace {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-Workspace g_ws[64];
-std::mutex g_ws_mu;
 
 }  // namespace
 
@@ -245,7 +276,12 @@ size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k) {
   const size_t a = (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
   const size_t b = (casc_packed_b_bytes(k, n) + 255) / 256 * 256;
   const int P = (m > 0 && n > 0 && k > 0) ? split_plan(m, n, k, current_sms()) : 0;
-  return a + b + split_bytes(m, n, P);
+  return a + b + split_bytes(m, n, P) + scratch_bytes_for(m, n, P);
+}
+// the fused kernel's scratch inside a workspace of casc_workspace_bytes(m, n, k) bytes
+static void* ws_counter(void* ws, int64_t m, int64_t n, int64_t k) {
+  const int P = (m > 0 && n > 0 && k > 0) ? split_plan(m, n, k, current_sms()) : 0;
+  return static_cast<uint8_t*>(ws) + casc_workspace_bytes(m, n, k) - scratch_bytes_for(m, n, P);
 }
 
 int casc_last_launch_count(void) { return g_launches; }
@@ -347,7 +383,7 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
   g_launches = 0;
   r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr,
-                       AlphaBeta(), ps);
+                       AlphaBeta(), ps, 0, ws_counter(workspace, m, n, k));
   g_launches = (r == CASC_OK) ? g_launches + 2 : 0;  // + the two split kernels
   return r;
 }
@@ -362,30 +398,19 @@ int casc_gemm_fp64x2(int64_t m, int64_t n, int64_t k, const double* A_hi, const 
     return casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
                                nullptr, 0, stream);
   if ((r = device_check(nullptr))) return r;
+  // Stream-ordered workspace of this call (the device's default pool keeps the
+  // memory cached: release threshold set in device_check): no host
+  // synchronisation, and concurrent calls on different streams never share it.
   const size_t need = casc_workspace_bytes(m, n, k);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
+  const cudaStream_t st = S(stream);
   void* ws = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_ws_mu);
-    Workspace& W = g_ws[dev];
-    if (W.bytes < need) {
-      if (W.ptr) {
-        cudaDeviceSynchronize();
-        cudaFree(W.ptr);
-        W.ptr = nullptr;
-        W.bytes = 0;
-      }
-      if (cudaMalloc(&W.ptr, need) != cudaSuccess) {
-        W.ptr = nullptr;
-        return CASC_ERR_CUDA;
-      }
-      W.bytes = need;
-    }
-    ws = W.ptr;
-  }
-  return casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
-                             ws, need, stream);
+  if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+  r = casc_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags, ws,
+                          need, stream);
+  const int launches = g_launches;
+  cudaFreeAsync(ws, st);
+  g_launches = launches;
+  return r;
 }
 
 // Host-resident operands (casc.h), the row-slab pipeline of casc_host.cuh.
@@ -438,17 +463,15 @@ int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi, c
 }
 
 int casc_finalize(void) {
+  // Return the cached stream-ordered memory of this device's default pool (the
+  // workspaces of casc_gemm_fp64x2 / casc_i8_gemm_fp64x2) to the system.  A
+  // teardown call: it waits for the device's work first.
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  Workspace& W = g_ws[dev];
-  if (W.ptr) {
-    cudaDeviceSynchronize();
-    cudaFree(W.ptr);
-  }
-  W.ptr = nullptr;
-  W.bytes = 0;
-  return CASC_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return CASC_ERR_CUDA;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return CASC_ERR_CUDA;
+  return cuda_status(cudaMemPoolTrimTo(pool, 0));
 }
 
 int casc_split_a(int64_t m, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
@@ -526,6 +549,17 @@ int casc_debug_bins(int64_t m, int64_t n, int64_t k, const double* A_hi, const d
   return r;
 }
 
+int casc_debug_ldexp(int64_t count, const double* x, const int32_t* n, double* out,
+                     casc_stream_t stream) {
+  g_launches = 0;
+  if (count < 0 || (count > 0 && (!x || !n || !out))) return CASC_ERR_INVALID;
+  int r;
+  if ((r = device_check(nullptr))) return r;
+  const cudaError_t e = casc::launch_ldexp(count, x, n, out, S(stream));
+  if (e == cudaSuccess && count > 0) g_launches = 1;
+  return cuda_status(e);
+}
+
 // ---------------------------------------------------------------- BLAS-style (NEXT-4)
 int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
                         double alpha_hi, double alpha_lo, const double* A_hi, const double* A_lo,
@@ -594,7 +628,7 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
   uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
   g_launches = 0;
   r = (e == cudaSuccess) ? gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
-                                            nst, nullptr, abv, ps)
+                                            nst, nullptr, abv, ps, 0, ws_counter(ws, m, n, k))
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
@@ -667,7 +701,7 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
   g_launches = 0;
   r = (e == cudaSuccess) ? gemm_packed_impl(n, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
                                             nst, nullptr, abv, nullptr,
-                                            uplo == CASC_LOWER ? 1 : 2)
+                                            uplo == CASC_LOWER ? 1 : 2, ws_counter(ws, n, n, k))
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
@@ -706,11 +740,7 @@ int casc_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, double
   int r;
   if ((r = check_mat(A_hi, m, m, lda)) || (r = check_mat(A_lo, m, m, lda))) return r;
   if ((r = check_mat(B_hi, m, n, ldb)) || (r = check_mat(B_lo, m, n, ldb))) return r;
-  const size_t ea = extent(m, m, lda), eb = extent(m, n, ldb);
-  if (ranges_overlap(B_hi, eb, A_hi, ea) || ranges_overlap(B_hi, eb, A_lo, ea) ||
-      ranges_overlap(B_lo, eb, A_hi, ea) || ranges_overlap(B_lo, eb, A_lo, ea) ||
-      ranges_overlap(B_hi, eb, B_lo, eb))
-    return CASC_ERR_INVALID;
+  if (trsm_overlap(m, n, A_hi, A_lo, lda, B_hi, B_lo, ldb)) return CASC_ERR_INVALID;
   if (m == 0 || n == 0) return CASC_OK;
   int sms = 0;
   if ((r = device_check(&sms))) return r;
@@ -927,6 +957,10 @@ int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
   return ::check_mat(p, rows, cols, ld);
 }
 int current_sms() { return ::current_sms(); }
+bool trsm_overlap(int64_t m, int64_t n, const double* A_hi, const double* A_lo, int64_t lda,
+                  const double* B_hi, const double* B_lo, int64_t ldb) {
+  return ::trsm_overlap(m, n, A_hi, A_lo, lda, B_hi, B_lo, ldb);
+}
 void set_launches(int n) { g_launches = n; }
 }  // namespace host
 }  // namespace casc

@@ -5,6 +5,8 @@
 // last panel, casc_gemm.cu) after transposed splits (casc_split.cu).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "casc_dd.cuh"
 #include "casc_layout.cuh"
 
@@ -35,8 +37,8 @@ __global__ void __launch_bounds__(256) scale_c_kernel(int64_t m, int64_t n, doub
   }
 }
 
-// Split mode reduction (small problems, casc_gemm.cu item_coords): C := T_0 (+)
-// T_1 (+) ... (+) T_{P-1} in panel order -- the same FP64x2 additions, in the
+// Split mode reduction (small problems, casc_gemm.cu item_coords): C := (0, 0)
+// (+) T_0 (+) T_1 (+) ... (+) T_{P-1} in panel order -- the same FP64x2 additions, in the
 // same order, as the fused kernel's per-panel accumulation -- flags := OR, then
 // the optional BLAS update.
 __global__ void __launch_bounds__(256) split_reduce_kernel(
@@ -47,9 +49,9 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(
   const int64_t mn = m * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    double th = t_hi[idx], tl = t_lo[idx];
-    uint8_t fl = fbuf[idx];
-    for (int q = 1; q < P; ++q) {
+    double th = 0.0, tl = 0.0;  // C starts at (0, 0) (reading R10), as the fused kernel
+    uint8_t fl = 0;
+    for (int q = 0; q < P; ++q) {
       dd_add(th, tl, t_hi[q * mn + idx], t_lo[q * mn + idx], th, tl);
       fl |= fbuf[q * mn + idx];
     }
@@ -152,6 +154,23 @@ cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_
   if (nblk == 0) return cudaSuccess;
   trsm_diag_inv_kernel<<<(unsigned)nblk, TRSM_NB, 0, st>>>(uplo, diag, m, A_hi, A_lo, lda, I_hi,
                                                            I_lo);
+  return cudaGetLastError();
+}
+
+// Test export of the exact power-of-two scaling (casc_debug_ldexp)
+__global__ void __launch_bounds__(256) ldexp_kernel(int64_t count, const double* __restrict__ x,
+                                                    const int32_t* __restrict__ n,
+                                                    double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ldexp_rn(x[i], n[i]);
+}
+
+cudaError_t launch_ldexp(int64_t count, const double* x, const int32_t* n, double* out,
+                         cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 8);
+  ldexp_kernel<<<(unsigned)blocks, 256, 0, st>>>(count, x, n, out);
   return cudaGetLastError();
 }
 

@@ -70,16 +70,42 @@ __device__ __forceinline__ void apply_alpha_beta(double& th, double& tl, double 
 
 // fl_casc of one element (reading R9), bins in the
 // kernel's pre-aligned scales: T = TwoSum(2^-2c0 bin2', 2^-D2 bin36);
-// T = T (+) 2^-c0 bin1; T = T (+) bin0; T *= 2^escale.
+// T = T (+) 2^-c0 bin1; T = T (+) bin0; T = (ldexp(T.hi, escale), ldexp(T.lo, escale)).
+// WIDE: e_i + f_j may lie outside [-1022, 1023] (then each limb is scaled
+// ldexp-exactly, reading R16); otherwise 2^escale is one normal double.
+template <bool WIDE = true>
 __device__ __forceinline__ void combine_bins(double b0, double b1, double b2p, double b36,
                                              int c0, int D2, int escale, double& th,
                                              double& tl) {
   two_sum(__dmul_rn(b2p, pow2i(-2 * c0)), __dmul_rn(b36, pow2i(-D2)), th, tl);
   dd_add_d(th, tl, __dmul_rn(b1, pow2i(-c0)));
   dd_add_d(th, tl, b0);
-  const double sc = pow2i(escale);
-  th = __dmul_rn(th, sc);
-  tl = __dmul_rn(tl, sc);
+#ifdef CASC_EXPERIMENT_POW2I  // timing experiment only: round-1 scaling (wrong outside the range)
+  if (true) {
+#else
+  if (!WIDE) {
+#endif
+    const double sc = pow2i(escale);
+    th = __dmul_rn(th, sc);
+    tl = __dmul_rn(tl, sc);
+  } else {
+#if defined(CASC_WIDE_CALL)
+    th = ldexp_rn_wide(th, escale);
+    tl = ldexp_rn_wide(tl, escale);
+#elif defined(CASC_WIDE_2STEP)
+    const bool up = escale > 1023, down = escale < -1074;
+    const int n0 = up ? 1023 : (down ? escale + 1074 : escale);
+    const int n1 = up ? escale - 1023 : (down ? -1074 : 0);
+    const double s0 = pow2_any(n0), s1 = pow2_any(n1);
+    th = __dmul_rn(__dmul_rn(th, s0), s1);
+    tl = __dmul_rn(__dmul_rn(tl, s0), s1);
+#else
+    double sc[3];
+    pow2_steps(escale, sc);
+    th = __dmul_rn(__dmul_rn(__dmul_rn(th, sc[0]), sc[1]), sc[2]);
+    tl = __dmul_rn(__dmul_rn(__dmul_rn(tl, sc[0]), sc[1]), sc[2]);
+#endif
+  }
 }
 
 }  // namespace casc

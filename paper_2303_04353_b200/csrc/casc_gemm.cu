@@ -11,7 +11,8 @@
 //       bin36 += A0 B3 + A1 B4' + A2' B5'' + A3 B6        (FP64-rounded)
 //   phase 3 (fl_casc; order bin 3-6 -> 2 -> 1 -> 0):
 //       T = TwoSum(2^-2c0 bin2', 2^-D2 bin36); T = T (+) 2^-c0 bin1;
-//       T = T (+) bin0; T *= 2^(e_i + f_j);  C (+)= T (FP64x2);
+//       T = T (+) bin0; T *= 2^(e_i + f_j) (ldexp per limb);
+//       C (+)= T (FP64x2; C = (0, 0) before the first panel);
 //       flag |= (bin0 == 0)  (§3.7, §4.4).
 //
 // Structure (Blackwell): persistent CTAs (one per SM), 384 threads,
@@ -55,6 +56,14 @@ constexpr int GROUP_M = 16;                  // tile raster grouping (L2 reuse)
 constexpr int EXP_RING = 8;  // > NSTAGE: a panel's exponents outlive the stages that carried them
 constexpr size_t EXP_OFFSET =
     (size_t)NSTAGE * (A_STAGE + B_STAGE) * sizeof(double) + 2 * NSTAGE * sizeof(uint64_t) + 16;
+// Longest wait of a producer at a tile-wave barrier (a cfg4 wave takes ~5.6 ms;
+// the CTAs of a co-resident grid meet within microseconds).
+constexpr uint64_t WAVE_WAIT_NS = 200000;
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr size_t GEMM_SMEM = EXP_OFFSET + (size_t)EXP_RING * (TM + TN) * sizeof(int32_t);
 
 
@@ -122,7 +131,9 @@ __host__ __device__ __forceinline__ int work_items(const GemmArgs& a) {
 // SPLIT: split mode (small problems); a separate instantiation so the large-problem
 //        kernel carries none of its indexing (measured 1.3% at 16384^3)
 // TRI:  SYRK, one triangle of tiles (p.tri)
-template <bool DBG, bool AB, bool SPLIT, bool TRI>
+// WIDE: the re-run of the work items whose scales 2^(e_i + f_j) leave the
+//       normal powers of two (reading R16), listed by the first launch
+template <bool DBG, bool AB, bool SPLIT, bool TRI, bool WIDE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmArgs p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   double* As = reinterpret_cast<double*>(smem);
@@ -133,6 +144,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   // ring of per-panel scale exponents [EXP_RING][A 64 | B 64] int32, filled by TMA
   int32_t* sexp = reinterpret_cast<int32_t*>(smem + EXP_OFFSET);
 
+  if (WIDE && *p.wide_count == 0) return;  // the common case: nothing to re-run
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
@@ -144,8 +156,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   __syncthreads();
 
   const int split_p = SPLIT ? p.split_p : 0;
-  const int ntiles = TRI ? p.mblocks * (p.mblocks + 1) / 2
-                         : p.mblocks * p.nblocks * (split_p ? split_p : 1);  // work items
+  // work items (WIDE: the entries item * 8 + warp listed by the first launch)
+  const int ntiles = WIDE ? (int)*p.wide_count
+                          : (TRI ? p.mblocks * (p.mblocks + 1) / 2
+                                 : p.mblocks * p.nblocks * (split_p ? split_p : 1));
 
   if (warp < 4) {
     // ===================== TMA producer (warpgroup 0) =====================
@@ -155,26 +169,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       const int nwaves = (ntiles + gridDim.x - 1) / gridDim.x;
       for (int wave = 0; wave < nwaves; ++wave) {
         const int tile = blockIdx.x + wave * gridDim.x;
-        if (p.wave_counter && wave > 0) {
+        if (!WIDE && p.wave_counter && wave > 0) {
           // Re-align all producers at every tile wave so that the tiles in flight
           // (a GROUP_M x ~9 block of C sharing A and B blocks) sweep k in step and
           // hit each other's slices in L2 instead of re-reading HBM.  A CTA without
           // a tile in this wave still arrives, so the count always completes.
+          // The wait is bounded (WAVE_WAIT_NS): co-residency of the whole grid is
+          // an optimisation here, never a correctness requirement, so the kernel
+          // needs no cooperative launch and cannot hang when other work (another
+          // stream, another process) holds some of the SMs.
           atomicAdd(p.wave_counter, 1u);
           if (tile < ntiles) {
             const unsigned int target = (unsigned int)wave * gridDim.x;
+            const uint64_t t0 = globaltimer_ns();
             unsigned int v;
-            do {
+            for (;;) {
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
                            : "=r"(v)
                            : "l"(p.wave_counter)
                            : "memory");
-            } while (v < target);
+              if (v >= target || globaltimer_ns() - t0 > WAVE_WAIT_NS) break;
+            }
           }
         }
         if (tile >= ntiles) continue;
         int mb, nb, s0, s1, q0;
-        item_coords<TRI>(p, split_p, tile, mb, nb, s0, s1, q0);
+        item_coords<TRI>(p, split_p, WIDE ? (int)(p.wide_list[tile] >> 3) : tile, mb, nb, s0, s1,
+                         q0);
         const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)s0 * A_STAGE * 8;
         const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)s0 * B_STAGE * 8;
         for (int st = s0; st < s1; ++st, ++it) {
@@ -226,7 +247,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   uint32_t it = 0, pc = 0;  // stage counter (smem ring), panel counter (exponent ring)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int mb, nb, s0, s1, q0;
-    item_coords<TRI>(p, split_p, tile, mb, nb, s0, s1, q0);
+    const unsigned int entry = WIDE ? p.wide_list[tile] : 0u;
+    const int item = WIDE ? (int)(entry >> 3) : tile;
+    item_coords<TRI>(p, split_p, item, mb, nb, s0, s1, q0);
+    // Scales 2^(e_i + f_j) outside the normal powers of two (reading R16) are
+    // rare; the combine of this kernel assumes one exact power of two per
+    // element, and a warp that meets another scale in any panel of the item
+    // stores no C (so C and beta C stay intact) and lists (item, warp) for the
+    // WIDE re-run, whose combine scales ldexp-exactly.  Keeping that scaling out
+    // of this kernel keeps its registers spill-free (measured: a warp-uniform
+    // branch between the two scalings made ptxas spill in the k loop, -3%).
+    bool wide_seen = false;
     // destination: C, or the panel-sum buffer T_q in split mode
     double* dst_hi = split_p ? p.t_hi + (int64_t)q0 * p.m * p.n : p.C_hi;
     double* dst_lo = split_p ? p.t_lo + (int64_t)q0 * p.m * p.n : p.C_lo;
@@ -314,6 +345,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
             }
         continue;
       }
+      if constexpr (!WIDE) {  // this panel's scales: all normal powers of two for the warp?
+        int emin = 1 << 30, emax = -(1 << 30), fmin = 1 << 30, fmax = -(1 << 30);
+#pragma unroll
+        for (int ms = 0; ms < 4; ++ms) {
+          const int e = pex[wm * 32 + ms * 8 + g];
+          emin = min(emin, e);
+          emax = max(emax, e);
+        }
+#pragma unroll
+        for (int ns = 0; ns < 2; ++ns)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int f = pex[TM + wn * 16 + ns * 8 + 2 * c + i];
+            fmin = min(fmin, f);
+            fmax = max(fmax, f);
+          }
+        wide_seen |= !__all_sync(0xffffffffu, emin + fmin >= -1022 && emax + fmax <= 1023);
+      }
+      const bool store_c = WIDE ? (cw == (int)(entry & 7u)) : !wide_seen;
       // two halves (m-subtiles 0-1, 2-3): 8 elements = 32 TMEM columns each
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -332,16 +382,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
             for (int i = 0; i < 2; ++i) {
               const int x = (m2 * 4 + ns * 2 + i) * 4;
               double th, tl;
-              combine_bins(acc[0][ms][ns][i], acc[1][ms][ns][i], acc[2][ms][ns][i],
-                           acc[3][ms][ns][i], p.c0, p.D2,
-                           e + pex[TM + wn * 16 + ns * 8 + 2 * c + i], th, tl);
-              if (!first)
-                dd_add(__hiloint2double(cv[x + 1], cv[x]), __hiloint2double(cv[x + 3], cv[x + 2]),
-                       th, tl, th, tl);
+              combine_bins<WIDE>(
+                  acc[0][ms][ns][i], acc[1][ms][ns][i], acc[2][ms][ns][i], acc[3][ms][ns][i],
+                  p.c0, p.D2, e + pex[TM + wn * 16 + ns * 8 + 2 * c + i], th, tl);
+              // C (+)= T with C = (0, 0) before the first panel (reading R10: the
+              // FP64x2 addition also renormalises a T whose limbs were rounded
+              // separately onto the subnormal grid, and turns -0 into +0, as the
+              // oracle).  Split mode stores the raw panel value T_q; the reduction
+              // adds (0, 0) (+) T_0 (+) T_1 ... in the same order.
+              if constexpr (!SPLIT)
+                dd_add(first ? 0.0 : __hiloint2double(cv[x + 1], cv[x]),
+                       first ? 0.0 : __hiloint2double(cv[x + 3], cv[x + 2]), th, tl, th, tl);
               if (last) {
                 const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
                 const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
-                if (row < p.m && col < p.n && in_tri<TRI>(p, row, col)) {
+                if (store_c && row < p.m && col < p.n && in_tri<TRI>(p, row, col)) {
                   if (AB && p.ab)
                     apply_alpha_beta(th, tl, p.alpha_hi, p.alpha_lo, p.beta_hi, p.beta_lo,
                                      p.ab == 2 ? p.C_hi[row * p.ldc + col] : 0.0,
@@ -361,8 +416,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       }
       if (!last) tmem_wait_st();
     }
+    if (!WIDE && wide_seen && lane == 0)  // C of this warp's elements: the WIDE re-run
+      p.wide_list[atomicAdd(p.wide_count, 1u)] = ((unsigned int)item << 3) | (unsigned int)cw;
     // ------------------------------ cancellation flags of this tile
-    if (!DBG && dst_fl) {
+    // (independent of the scales: the first launch stores them for every warp)
+    if (!DBG && !WIDE && dst_fl) {
 #pragma unroll
       for (int ms = 0; ms < 4; ++ms) {
         const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
@@ -387,56 +445,58 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   }
 }
 
-template <bool DBG, bool AB, bool SPLIT, bool TRI = false>
-static cudaError_t launch_variant(GemmArgs& a, int grid, bool coop, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT, TRI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)GEMM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  if (coop) {  // co-residency of all CTAs is required by the wave barrier
-    void* args[] = {&a};
-    return cudaLaunchCooperativeKernel((const void*)casc_gemm_kernel<DBG, AB, SPLIT, TRI>, dim3(grid),
-                                       dim3(GEMM_THREADS), args, GEMM_SMEM, st);
-  }
-  casc_gemm_kernel<DBG, AB, SPLIT, TRI><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+template <bool DBG, bool AB, bool SPLIT, bool TRI = false, bool WIDE = false>
+static cudaError_t launch_variant(GemmArgs& a, int grid, cudaStream_t st) {
+  // per launch (the attribute is per device; the call is cheap and thread-safe)
+  cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+  if (e != cudaSuccess) return e;
+  casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
+// the product launch, then the WIDE re-run of what it listed (exits at once
+// when the list is empty)
+template <bool AB, bool SPLIT, bool TRI = false>
+static cudaError_t launch_pair(GemmArgs& a, int grid, cudaStream_t st) {
+  cudaError_t e = launch_variant<false, AB, SPLIT, TRI, false>(a, grid, st);
+  if (e == cudaSuccess) e = launch_variant<false, AB, SPLIT, TRI, true>(a, grid, st);
+  return e;
+}
+
+static bool wave_sync_on() {
+  // default on: 10x less HBM traffic for the fused kernel at ~0.2% time cost
+  // (profiles/r01c); CASC_WAVE_SYNC=0 turns it off
+  const char* s = getenv("CASC_WAVE_SYNC");
+  return !(s && s[0] == '0');
+}
+
+size_t gemm_scratch_bytes(int64_t items) {
+  return ((size_t)GEMM_SCRATCH_HEAD + (size_t)items * NCW * sizeof(unsigned int) + 255) / 256 * 256;
+}
+
+// a.scratch: gemm_scratch_bytes(work items) bytes of the caller's device memory,
+// stream-ordered with this launch (wave counter, WIDE list count and entries).
 cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   GemmArgs a = a_in;
   const int ntiles = work_items(a);
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
-  static int wave_sync = -1;
-  if (wave_sync < 0) {
-    // default on: 10x less HBM traffic for the fused kernel at ~0.2% time cost
-    // (profiles/r01c); CASC_WAVE_SYNC=0 turns it off
-    const char* s = getenv("CASC_WAVE_SYNC");
-    wave_sync = (s && s[0] == '0') ? 0 : 1;
+  if (a.dbg) {
+    a.wave_counter = nullptr;
+    return launch_variant<true, false, false>(a, grid, st);
   }
-  a.wave_counter = nullptr;
-  if (a.dbg) return launch_variant<true, false, false>(a, grid, false, st);
-  const bool coop = wave_sync && ntiles > grid && !a.split_p;  // small problems: no barrier
-  if (coop) {
-    static unsigned int* counters[64] = {nullptr};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!counters[dev] && cudaMalloc(&counters[dev], sizeof(unsigned int)) != cudaSuccess)
-      return cudaErrorMemoryAllocation;
-    a.wave_counter = counters[dev];
-    cudaError_t e = cudaMemsetAsync(a.wave_counter, 0, sizeof(unsigned int), st);
-    if (e != cudaSuccess) return e;
-  }
-  if (a.tri) return launch_variant<false, true, false, true>(a, grid, coop, st);
+  if (!a.scratch) return cudaErrorInvalidValue;
+  a.wave_counter = reinterpret_cast<unsigned int*>(a.scratch);
+  a.wide_count = a.wave_counter + 1;
+  a.wide_list = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(a.scratch) + GEMM_SCRATCH_HEAD);
+  cudaError_t e = cudaMemsetAsync(a.scratch, 0, 2 * sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  if (a.split_p || ntiles <= num_sms || !wave_sync_on()) a.wave_counter = nullptr;
+  if (a.tri) return launch_pair<true, false, true>(a, grid, st);
   if (a.split_p)
-    return a.ab ? launch_variant<false, true, true>(a, grid, coop, st)
-                : launch_variant<false, false, true>(a, grid, coop, st);
-  return a.ab ? launch_variant<false, true, false>(a, grid, coop, st)
-              : launch_variant<false, false, false>(a, grid, coop, st);
+    return a.ab ? launch_pair<true, true>(a, grid, st) : launch_pair<false, true>(a, grid, st);
+  return a.ab ? launch_pair<true, false>(a, grid, st) : launch_pair<false, false>(a, grid, st);
 }
 
 }  // namespace casc

@@ -11,10 +11,12 @@
 //   R23  X = rint(hi 2^(F-e)) + rint(lo 2^(F-e)), F = 6 + 8(y-1); slices = the
 //        balanced base-256 digits of X (d_0 in [-64, 64], others [-128, 127]).
 //   R24  bin_s = sum_p sum_(i+j=s) dA_i dB_j, s < y.
-//   R25  groups of four bins aligned at the least significant bin (bins
-//        0 .. r-1, r = (y-1) % 4 + 1, first) -> exact FP64x2 group value G, scaled by
-//        2^(e+f-12-8(s+nb-1)); panel value T = FP64x2 sum of the groups, most
-//        significant first; C = C (+) T over panels.
+//   R25  (rev. 2) groups of four bins aligned at the least significant bin
+//        (bins 0 .. r-1, r = (y-1) % 4 + 1, first) -> exact int64 group values
+//        V_g; the panel's exact product S = sum_g V_g 2^(32(ng-1-g)) (192-bit)
+//        is rounded to the nearest FP64x2 number T = (RN(x), RN(x - T.hi)),
+//        x = S 2^(e+f-12-8(y-1)), with integer instructions only (subnormals
+//        included); C = T over the first panel, C = C (+) T over the others.
 //   R26  flag |= |T.hi| <= kp 2^(e+f-50).
 //
 // Phase 1 (HBM-bound):
@@ -31,7 +33,7 @@
 //   warp 8     TMA producer (both CTAs): 2-SM tensor copies
 //              (cp.async.bulk.tensor.2d.cta_group::2) of the CTA's half of each
 //              operand chunk (A: its 128 rows, 16 KB; B: its 64 of the chunk's
-//              128 columns, 8 KB) into rings of 8 + 8 slots, completing on the
+//              128 columns, 8 KB) into rings of 9 (A) + 10 (B) slots, completing on the
 //              leader CTA's mbarriers; a soft wave synchronisation aligns the
 //              producers of all CTAs at every (panel, group) sweep (L2 reuse);
 //   warp 9     MMA issuer (leader CTA; also allocates TMEM): tcgen05.mma
@@ -43,9 +45,10 @@
 //              resident; commits are multicast to both CTAs;
 //   warps 0-7  epilogue (both CTAs): tcgen05.ld of the int32 bins of the CTA's
 //              128 rows (warp w reads TMEM lane quarter w%4, column half w/4)
-//              into exact int64 group values (then TMEM is released), then the
-//              FP64x2 panel sum T and C in a per-CTA workspace, the detector, and
-//              the final store of C and the flags.
+//              into exact int64 group values (then TMEM is released), then once
+//              per panel the exact panel product rounded to T (R25 rev. 2), C in a
+//              per-CTA workspace, the detector, and the final store of C and the
+//              flags.
 // Producer and MMA warps have the highest warp ids: the sub-partition scheduler
 // favours them over the epilogue warps they share an issue slot with.
 #include <cuda.h>
@@ -1512,6 +1515,8 @@ int zero_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc, uint8_
 int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld);
 int current_sms();
 void set_launches(int n);
+bool trsm_overlap(int64_t m, int64_t n, const double* A_hi, const double* A_lo, int64_t lda,
+                  const double* B_hi, const double* B_lo, int64_t ldb);
 }  // namespace host
 }  // namespace casc
 
@@ -1520,11 +1525,6 @@ using namespace casc;
 inline cudaStream_t S8(casc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int st8(cudaError_t e) { return e == cudaSuccess ? CASC_OK : CASC_ERR_CUDA; }
 inline size_t al256h(size_t b) { return (b + 255) / 256 * 256; }
-struct I8Ws {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-I8Ws g_i8ws[64];
 }  // namespace
 
 extern "C" {
@@ -1683,8 +1683,7 @@ int casc_i8_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n, dou
   int r;
   if ((r = host::check_mat(A_hi, m, m, lda)) || (r = host::check_mat(A_lo, m, m, lda))) return r;
   if ((r = host::check_mat(B_hi, m, n, ldb)) || (r = host::check_mat(B_lo, m, n, ldb))) return r;
-  if (B_hi == B_lo || B_hi == A_hi || B_hi == A_lo || B_lo == A_hi || B_lo == A_lo)
-    return CASC_ERR_INVALID;
+  if (host::trsm_overlap(m, n, A_hi, A_lo, lda, B_hi, B_lo, ldb)) return CASC_ERR_INVALID;
   if (m == 0 || n == 0) return CASC_OK;
   int sms = 0;
   if ((r = host::device_check(&sms))) return r;
@@ -1866,35 +1865,16 @@ int casc_i8_gemm_fp64x2(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   if ((r = host::device_check(nullptr))) return r;
   if (k == 0) return host::zero_c(m, n, C_hi, C_lo, ldc, flags, S8(stream));
   const size_t need = casc_i8_workspace_bytes(m, n, k, y);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
-  I8Ws& w = g_i8ws[dev];
-  if (w.bytes < need) {
-    if (w.ptr) {
-      cudaDeviceSynchronize();
-      cudaFree(w.ptr);
-      w.ptr = nullptr;
-      w.bytes = 0;
-    }
-    if (cudaMalloc(&w.ptr, need) != cudaSuccess) return CASC_ERR_CUDA;
-    w.bytes = need;
-  }
-  return casc_i8_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags,
-                                y, w.ptr, w.bytes, stream);
+  const cudaStream_t st = S8(stream);
+  void* ws = nullptr;  // stream-ordered, per call (see casc_gemm_fp64x2)
+  if (cudaMallocAsync(&ws, need, st) != cudaSuccess) return CASC_ERR_CUDA;
+  r = casc_i8_gemm_fp64x2_ws(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags, y,
+                             ws, need, stream);
+  cudaFreeAsync(ws, st);
+  return r;
 }
 
-int casc_i8_finalize(void) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return CASC_ERR_CUDA;
-  I8Ws& w = g_i8ws[dev];
-  if (w.ptr) {
-    cudaDeviceSynchronize();
-    if (cudaFree(w.ptr) != cudaSuccess) return CASC_ERR_CUDA;
-  }
-  w.ptr = nullptr;
-  w.bytes = 0;
-  return CASC_OK;
-}
+int casc_i8_finalize(void) { return casc_finalize(); }
 
 int casc_i8_split(int64_t rows, int64_t k, const double* hi, const double* lo, int64_t ld,
                   int is_b, int y, int8_t* digits, int32_t* e, casc_stream_t stream) {

@@ -65,6 +65,61 @@ __device__ __forceinline__ double pow2i(int n) {  // 2^n for n in [-1022, 1023],
   return __longlong_as_double((long long)(n + 1023) << 52);
 }
 
+// 2^n exactly for n in [-1074, 1023] (a subnormal double below -1022).
+__device__ __forceinline__ double pow2_any(int n) {
+  return n >= -1022 ? pow2i(n) : __longlong_as_double(1LL << (n + 1074));
+}
+
+// x 2^n rounded once to nearest-even for ANY int n, i.e. bitwise C99 ldexp(x, n)
+// (the oracle scales with ldexp, reading R16): subnormal results on the
+// 2^-1074 grid, overflow to +-inf, signed zeros kept.
+//   n in [-1074, 1023]: one multiply by the exact power 2^n (IEEE multiplication
+//               rounds the exact product once, also for a subnormal factor);
+//   n > 1023:   factors 2^1023 (at most twice), then the rest; every factor is
+//               >= 1, so a step is exact or overflows, and an intermediate
+//               overflow means the result overflows too;
+//   n < -1074:  y = x 2^(n+1074), then y 2^-1074.  y is exact whenever it is
+//               normal; if not, |x 2^n| < 2^-2096 and both sides give +-0.
+#ifdef CASC_LDEXP_NOINLINE  // timing experiment: the rare path as a call
+static __device__ __noinline__
+#else
+static __device__ __forceinline__
+#endif
+double ldexp_rn_wide(double x, int n) {
+  if (n >= -1074 && n <= 1023) return __dmul_rn(x, pow2_any(n));
+  if (n > 1023) {
+    x = __dmul_rn(x, pow2i(1023));
+    n -= 1023;
+    if (n > 1023) {
+      x = __dmul_rn(x, pow2i(1023));
+      n -= 1023;
+    }
+    return __dmul_rn(x, pow2i(n > 1023 ? 1023 : n));
+  }
+  const int s = n + 1074 < -1074 ? -1074 : n + 1074;  // clamped: the result is +-0 anyway
+  return __dmul_rn(__dmul_rn(x, pow2_any(s)), __longlong_as_double(1LL));
+}
+// The same scaling as three exact powers of two applied in order,
+// x 2^n = ((x s[0]) s[1]) s[2], for n in [-2148, 3069] (every e_i + f_j of
+// binary64 operands, e, f in [-1073, 1024]) -- branch-free, for unrolled code:
+//   n in [-1074, 1023]: (2^n, 1, 1)                      one rounding;
+//   n > 1023:  (2^1023, 2^min(n-1023, 1023), 2^rest)     factors >= 1;
+//   n < -1074: (2^(n+1074), 2^-1074, 1)                  as ldexp_rn_wide.
+__device__ __forceinline__ void pow2_steps(int n, double s[3]) {
+  const bool up = n > 1023, down = n < -1074;
+  const int r = n - 1023, r2 = r < 1023 ? r : 1023;
+  const int n0 = up ? 1023 : (down ? n + 1074 : n);
+  const int n1 = up ? r2 : (down ? -1074 : 0);
+  const int n2 = up ? r - r2 : 0;
+  s[0] = pow2_any(n0 < -1074 ? -1074 : n0);
+  s[1] = pow2_any(n1);
+  s[2] = pow2i(n2);
+}
+__device__ __forceinline__ double ldexp_rn(double x, int n) {
+  if ((unsigned)(n + 1022) <= 2045u) return __dmul_rn(x, pow2i(n));  // the common case
+  return ldexp_rn_wide(x, n);
+}
+
 // Arguments of the fused cascaded-GEMM kernel (casc_gemm.cu).
 struct GemmArgs {
   const uint8_t* pa;
@@ -80,7 +135,11 @@ struct GemmArgs {
   int64_t ldc;
   uint8_t* flags;  // m x n (ld n) or null
   double* dbg;     // debug: bins of the single panel, 4 x m x n (canonical scales)
-  unsigned int* wave_counter;  // zeroed per launch; producers meet here at each tile wave
+  void* scratch;               // per launch (caller memory, gemm_scratch_bytes): the
+                               // three below, set and zeroed by launch_gemm
+  unsigned int* wave_counter;  // producers meet here at each tile wave (or null)
+  unsigned int* wide_count;    // work items * 8 + warp listed for the WIDE re-run
+  unsigned int* wide_list;
   // NEXT-4 BLAS update at the tile's last panel: C := alpha (x) AB (+) beta (x) C
   int ab;        // 0: plain C := AB; 1: apply alpha; 2: apply alpha and beta (reads C)
   double alpha_hi, alpha_lo, beta_hi, beta_lo;
@@ -96,7 +155,9 @@ struct GemmArgs {
   int tri;
 };
 
+constexpr int GEMM_SCRATCH_HEAD = 256;  // wave counter, WIDE count; then the WIDE list
 cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st);
+size_t gemm_scratch_bytes(int64_t work_items);
 
 // Arguments of the single slice-GEMM kernel of the simple path (casc_simple.cu).
 struct SliceArgs {

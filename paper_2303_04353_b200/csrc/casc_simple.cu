@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) casc_epilogue_kernel(
     combine_bins(b0, b1, b2, b36, c0, D2, e + f, th, tl);
     double* ch = C_hi + i * ldc + j;
     double* cl = C_lo + i * ldc + j;
-    if (!first) dd_add(*ch, *cl, th, tl, th, tl);
+    dd_add(first ? 0.0 : *ch, first ? 0.0 : *cl, th, tl, th, tl);  // C from (0, 0), reading R10
     *ch = th;
     *cl = tl;
     if (flags) {
@@ -153,14 +153,10 @@ __global__ void __launch_bounds__(256) casc_epilogue_kernel(
 }
 
 cudaError_t launch_slice_gemm(const SliceArgs& a, int num_sms, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(slice_gemm_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)S_SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // per launch: the attribute is per device, and the call is cheap
+  cudaError_t e = cudaFuncSetAttribute(slice_gemm_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S_SMEM);
+  if (e != cudaSuccess) return e;
   const int ntiles = a.mblocks * a.nblocks;
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;

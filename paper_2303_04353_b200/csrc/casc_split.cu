@@ -50,9 +50,11 @@ __host__ inline SplitConsts make_consts(Widths w) {
 }
 
 // Appendix A, one limb.
-__device__ __forceinline__ void split_limb(double x, double scale, const SplitConsts& K,
+// v = x 2^-e: one multiply by scale = 2^-e when that power is a normal double,
+// else the exact ldexp (panel maxima >= 2^1023 or < 2^-1024; reading R16).
+__device__ __forceinline__ void split_limb(double x, double scale, int ne, const SplitConsts& K,
                                            double s[4]) {
-  double v = __dmul_rn(x, scale);
+  double v = scale != 0.0 ? __dmul_rn(x, scale) : ldexp_rn_wide(x, ne);
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
     const double r = __dsub_rn(__dadd_rn(v, K.M[t]), K.M[t]);
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(256) split_a_kernel(
     mx = fmax(mx, fabs(h[it]));
   }
   const int e = group_exponent(mx, g, c, kq);
-  const double scale = pow2i(-e);
+  const double scale = (unsigned)(-e + 1022) <= 2045u ? pow2i(-e) : 0.0;  // 0: wide
 
   uint8_t* blk = packed + mb * blk_bytes;
   double* sl = reinterpret_cast<double*>(blk);
@@ -117,8 +119,8 @@ __global__ void __launch_bounds__(256) split_a_kernel(
     const int64_t ks = (int64_t)q * (KC / 4) + kq + 8 * it;
     if (ks >= nks) break;
     double sh[4], slo[4];
-    split_limb(h[it], scale, K, sh);
-    split_limb(l[it], scale, K, slo);
+    split_limb(h[it], scale, -e, K, sh);
+    split_limb(l[it], scale, -e, K, slo);
     double chi[4];
 #pragma unroll
     for (int s = 0; s < 4; ++s) chi[s] = __dadd_rn(sh[s], slo[s]);
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(256) split_b_kernel(
     mx = fmax(mx, fabs(h[it]));
   }
   const int f = group_exponent(mx, g, c, kq);
-  const double scale = pow2i(-f);
+  const double scale = (unsigned)(-f + 1022) <= 2045u ? pow2i(-f) : 0.0;  // 0: wide
 
   uint8_t* blk = packed + nb * blk_bytes;
   double* sl = reinterpret_cast<double*>(blk);
@@ -168,8 +170,8 @@ __global__ void __launch_bounds__(256) split_b_kernel(
     const int64_t ks = (int64_t)q * (KC / 4) + kq + 8 * it;
     if (ks >= nks) break;
     double sh[4], slo[4];
-    split_limb(h[it], scale, K, sh);
-    split_limb(l[it], scale, K, slo);
+    split_limb(h[it], scale, -f, K, sh);
+    split_limb(l[it], scale, -f, K, slo);
     double y[7];
 #pragma unroll
     for (int s = 0; s < 4; ++s) y[s] = __dadd_rn(sh[s], slo[s]);

@@ -7,6 +7,9 @@ VARIANTS = {
     "bk16ns2": ["CASC_BK=16", "CASC_NSTAGE=2"],
     "bk8ns5": ["CASC_NSTAGE=5"],
     "bk4ns8": ["CASC_BK=4", "CASC_NSTAGE=8"],
+    "pow2i": ["CASC_EXPERIMENT_POW2I"],
+    "noinl": ["CASC_LDEXP_NOINLINE"],
+    "always3": ["CASC_SCALE_ALWAYS3"],
 }
 if sys.argv[1] == "build":
     from paper_2303_04353_b200 import _build

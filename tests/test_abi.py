@@ -59,7 +59,7 @@ def test_library_is_sm100a_only(lib):
     # the product kernel (no debug export, no alpha/beta) and the split kernels
     # are spill-free
     funcs = re.split(r"\n\s*Function : ", sass)
-    main = [f for f in funcs if f.startswith("_ZN4casc16casc_gemm_kernelILb0ELb0ELb0E")]
+    main = [f for f in funcs if f.startswith("_ZN4casc16casc_gemm_kernelILb0ELb0ELb0ELb0ELb0E")]
     splits = [f for f in funcs if "split_a_kernel" in f[:60] or "split_b_kernel" in f[:60]]
     assert len(main) == 1 and len(splits) == 4
     for f in main + splits:
@@ -78,7 +78,8 @@ def test_widths_and_sizes(lib):
     # k = 300 -> kpad 304 -> 76 k4-steps; 2 panels of exponents
     assert casc.casc_packed_a_block_bytes(300) == 76 * 1024 * 8 + 2 * 64 * 4
     assert casc.casc_packed_b_block_bytes(300) == 76 * 1792 * 8 + 2 * 64 * 4
-    assert casc.casc_workspace_bytes(0, 5, 5) == casc.casc_packed_b_bytes(5, 5)
+    # + the fused kernel's 256-byte scratch head (wave counter, WIDE list count)
+    assert casc.casc_workspace_bytes(0, 5, 5) == casc.casc_packed_b_bytes(5, 5) + 256
     assert casc.casc_status_string(0) == "CASC_OK"
     assert "invalid" in casc.casc_status_string(1)
 

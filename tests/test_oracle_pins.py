@@ -607,6 +607,10 @@ def test_inputs_normalised_and_blockwise():
     assert np.array_equal(blk["A_hi"], d["A_hi"][16:40])
     assert np.array_equal(blk["A_lo"], d["A_lo"][16:40])
     assert np.abs(d["A_hi"]).max() <= 1.0
+    for v in ("a", "b", "c"):  # cfg3's perturbed pairs are renormalised too (R15)
+        c3 = I.make_config(3, m=8, n=64, k=1024, variant=v)
+        assert np.all(c3["B_hi"] + c3["B_lo"] == c3["B_hi"])
+        assert np.all(c3["A_hi"] + c3["A_lo"] == c3["A_hi"])
     for cfg in (1, 2, 3, 4):  # column slabs of B (the multi-GPU slab generation)
         kw = dict(m=12, n=200, k=300)
         f = I.make_config(cfg, **kw)
