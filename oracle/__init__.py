@@ -60,6 +60,20 @@ _pu8 = ctypes.POINTER(ctypes.c_uint8)
 _pint = ctypes.POINTER(ctypes.c_int)
 
 
+def dd_trsm_plain(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N"):
+    """Plain (unblocked) FP64x2 substitution for op(A) X = alpha B: the
+    reference for the blocked casc_trsm (no shared block sizes)."""
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
+    m, n = X_hi.shape
+    lib().orc_dd_trsm_plain(lo_, tr, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo), max(m, 1),
+                            _p(X_hi), _p(X_lo), max(n, 1))
+    return X_hi, X_lo
+
+
 def _setup(L):
     L.orc_two_sum.argtypes = [_d, _d, _pd, _pd]
     L.orc_fast_two_sum.argtypes = [_d, _d, _pd, _pd]
@@ -86,6 +100,8 @@ def _setup(L):
     L.orc_trsm_diag_inv.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _pd, _pd, _i64, _pd, _pd]
     L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd,
                                 _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
+    L.orc_dd_trsm_plain.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d,
+                                    _d, _pd, _pd, _i64, _pd, _pd, _i64]
     L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,
                               _i64, ctypes.c_int]
     L.orc_exact_entries.argtypes = [_i64, _pd, _pd, _i64, _pd, _pd, _i64, _i64, _pi64, _pi64,

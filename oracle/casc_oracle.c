@@ -790,3 +790,35 @@ void orc_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double a
   free(Th);
   free(Tl);
 }
+
+/* ------------------------------------------------------------------------- */
+/* Plain FP64x2 triangular solve, the textbook column-by-column substitution  */
+/* with no blocking (the reference the blocked orc_casc_trsm is checked        */
+/* against, independently of its block sizes): op(A) X = alpha B, left side;  */
+/* for each column j, rows in the order of op(A)'s triangle:                  */
+/*   x_i = (alpha b_i - sum_l op(A)_il x_l) / op(A)_ii   (l ascending),        */
+/* every operation an FP64x2 one (orc_dd_mul, orc_dd_add, orc_dd_div).          */
+/* ------------------------------------------------------------------------- */
+void orc_dd_trsm_plain(int uplo, int trans, int diag, int64_t m, int64_t n, double ah, double al,
+                       const double* Ahi, const double* Alo, int64_t lda, double* Bhi,
+                       double* Blo, int64_t ldb) {
+  const int lower = (uplo == 0) != (trans != 0); /* op(A) lower triangular */
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t t = 0; t < m; ++t) {
+      const int64_t i = lower ? t : m - 1 - t;
+      double sh, sl;
+      orc_dd_mul(ah, al, Bhi[i * ldb + j], Blo[i * ldb + j], &sh, &sl);
+      const int64_t l0 = lower ? 0 : i + 1, l1 = lower ? i : m;
+      for (int64_t l = l0; l < l1; ++l) {
+        const int64_t o = trans ? l * lda + i : i * lda + l; /* op(A)_il */
+        double ph, pl;
+        orc_dd_mul(Ahi[o], Alo[o], Bhi[l * ldb + j], Blo[l * ldb + j], &ph, &pl);
+        orc_dd_add(sh, sl, -ph, -pl, &sh, &sl);
+      }
+      if (diag == 0)
+        orc_dd_div(sh, sl, Ahi[i * lda + i], Alo[i * lda + i], &sh, &sl);
+      Bhi[i * ldb + j] = sh;
+      Blo[i * ldb + j] = sl;
+    }
+}
+

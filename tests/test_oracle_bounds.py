@@ -1,0 +1,286 @@
+"""More pins of the CPU oracle (-m "not gpu"), round 2:
+
+* eq:cascerr and eq:fp642err: `cascerr_bound`
+  is pinned to the paper's own specialisation of it, the oracle's error on
+  cfg0-2-style data sits under it, the 61-bit guarantee holds wherever bin 0
+  is not zero, and the §3.6 worst case breaks that guarantee and is flagged;
+* the cross-bin FP64x2 combine (reading R9) bit for bit against its exact
+  rational semantics (every TwoSum error term exact, Fast2Sum only where its
+  precondition holds, bins in the order 6 -> 0), on hand-built bins where a
+  Fast2Sum in place of the first TwoSum, or the order 0 -> 6, gives other
+  bits;
+* the blocked TRSM (reading R27) against a plain unblocked FP64x2
+  substitution that shares none of its block sizes, itself pinned to exact
+  rational solutions.
+Ground truth is fractions.Fraction and the paper's printed formulas.
+"""
+
+import math
+import random
+from fractions import Fraction as F
+
+import numpy as np
+import pytest
+
+import casc_inputs as I
+
+W256 = (22, 21, 21)
+
+
+def fr(x):
+    return F(float(x))
+
+
+def rn(q):
+    """nearest double, ties to even (Python's correctly rounded float(Fraction))"""
+    return float(q)
+
+
+# ----------------------------------------------------------------- eq:cascerr / eq:fp642err
+def test_cascerr_bound_matches_papers_specialisation(orc):
+    """P:L2899-2916 specialises eq:cascerr to k = 256, D2 + 53 = 117 and bin 0 != 0
+    (so |x|^T|y| >= 2^-42 ||x|| ||y||): the bound is <= |x|^T|y| (2^-106 + k 2^-61).
+    The oracle's cascerr_bound must reproduce that (it fails with a wrong
+    constant 40, a k instead of k^2, or a wrong epsilon)."""
+    rng = np.random.default_rng(1)
+    nx = rng.uniform(0.5, 1.0, 200)
+    ny = rng.uniform(0.5, 1.0, 200)
+    absab = nx * ny * 2.0 ** -42 * rng.uniform(1.0, 4.0, 200)  # at the paper's lower limit
+    b = orc.cascerr_bound(256, absab, nx, ny, W256)
+    assert np.all(b <= absab * (2.0 ** -106 + 256 * 2.0 ** -61))
+    # and not loose by more than the paper's rounding of 40 * 2^-67 up to 2^-61
+    at_limit = orc.cascerr_bound(256, nx * ny * 2.0 ** -42, nx, ny, W256)
+    ratio = at_limit / (nx * ny * 2.0 ** -42 * (2.0 ** -106 + 256 * 2.0 ** -61))
+    assert np.all((ratio > 0.6) & (ratio <= 1.0))
+    # eps_tilde = 2^-(D2 + 53): 2^-117 at (22, 21, 21)
+    one = orc.cascerr_bound(1, 0.0, 1.0, 1.0, W256)
+    assert one == 40 * 2.0 ** -117
+
+
+def _panel_terms(d, p0, p1):
+    a, b = np.abs(d["A_hi"][:, p0:p1]), np.abs(d["B_hi"][p0:p1])
+    return a @ b * (1 + 2.0 ** -40), a.max(1)[:, None], b.max(0)[None, :]
+
+
+@pytest.mark.parametrize("cfg,m,n,k", [(0, 64, 64, 64), (1, 30, 26, 700), (2, 28, 33, 513),
+                                       (3, 16, 12, 1024)])
+def test_oracle_error_within_cascerr(orc, cfg, m, n, k):
+    """Every entry: |C - C*| <= sum over panels of eq:cascerr (x2 for the terms the
+    paper's "approximately" drops) + the FP64x2 rounding of each panel value and
+    accumulation step ((2P + 2) 2^-104 |A||B|)."""
+    d = I.make_config(cfg, m=m, n=n, k=k, variant="b") if cfg == 3 else \
+        I.make_config(cfg, m=m, n=n, k=k)
+    C_hi, C_lo, _ = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    c = orc.select_widths(k)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel(),
+                          C_hi, C_lo)
+    P = -(-k // 256)
+    bound = 0.0
+    for p0 in range(0, k, 256):
+        p1 = min(k, p0 + 256)
+        absab, nx, ny = _panel_terms(d, p0, p1)
+        bound = bound + 2 * orc.cascerr_bound(p1 - p0, absab, nx, ny, c) \
+            + (2 * P + 2) * 2.0 ** -104 * absab
+    bound = bound.ravel()
+    assert np.all(np.abs(r["err"]) <= bound)
+    # the bound is not vacuous: on this data it is within 2^20 of the error seen
+    nz = np.abs(r["err"]) > 0
+    if nz.any():
+        assert np.min(bound[nz] / np.abs(r["err"][nz])) < 2.0 ** 20
+
+
+@pytest.mark.parametrize("gen", ["uniform", "wide"])
+def test_fp642err_where_bin0_nonzero(orc, gen):
+    """eq:fp642err: k <= 256 and bin 0 != 0 (flag clear) ->
+    |C - C*| <= |x|^T|y| (2^-106 + k 2^-61): at least 61 correct bits."""
+    k = 256
+    if gen == "uniform":
+        d = I.make_config(1, m=40, n=36, k=k, seed=5)
+    else:  # rows / columns scaled over 2^+-30 and entries spanning 20 binades
+        d = I.make_config(2, m=40, n=36, k=k, seed=6)
+        rng = np.random.default_rng(2)
+        s = np.ldexp(1.0, rng.integers(-20, 1, (40, k)))
+        d["A_hi"], d["A_lo"] = d["A_hi"] * s, d["A_lo"] * s
+    C_hi, C_lo, fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    ii, jj = np.nonzero(fl == 0)
+    assert ii.size > 0
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii, jj, C_hi, C_lo)
+    assert np.all(np.abs(r["err"]) <= r["absab"] * (2.0 ** -106 + k * 2.0 ** -61))
+
+
+def test_worst_case_breaks_61_bits_and_is_flagged(orc):
+    """§3.6 worst case x = (1, eps), y = (0, 1): bin 0 vanishes, the
+    cascade returns only fl64(eps) -- an error beyond eq:fp642err's 61-bit
+    guarantee, which therefore needs bin 0 != 0 -- and the detector flags it."""
+    eps_hi = 3e-25  # an FP64x2 eps: 106 bits, of which slice 3 keeps RN(eps)
+    eps_lo = math.ldexp(eps_hi, -54) * 0.71875
+    A_hi = np.array([[1.0, eps_hi]])
+    A_lo = np.array([[0.0, eps_lo]])
+    B_hi = np.array([[0.0], [1.0]])
+    C_hi, C_lo, fl = orc.casc_gemm(A_hi, A_lo, B_hi, np.zeros((2, 1)))
+    eps = fr(eps_hi) + fr(eps_lo)
+    err = abs(fr(C_hi[0, 0]) + fr(C_lo[0, 0]) - eps)
+    absab = eps  # |x|^T |y|
+    assert err > absab * (F(2) ** -106 + 2 * F(2) ** -61)
+    assert fl[0, 0] == 1
+
+
+# ----------------------------------------------------------------- R9 combine, bit for bit
+def _two_sum(a, b):
+    s = rn(fr(a) + fr(b))
+    return s, rn(fr(a) + fr(b) - fr(s))  # the error term is exact (representable)
+
+
+def _fast_two_sum(a, b):  # Dekker, as the floating-point sequence (valid iff |a| >= |b|)
+    s = a + b
+    return s, b - (s - a)
+
+
+def _dd_add_d(h, l, x):
+    s, e = _two_sum(h, x)
+    e = rn(fr(e) + fr(l))
+    return _fast_two_sum(s, e)  # |s| >= |e| here
+
+
+def r9_model(b0, b1, b2, b36, escale, widths, first="two_sum", order="6to0"):
+    """fl_casc with reading R9 in exact rational semantics:
+    T = TwoSum(s2 bin2, s3 bin36); T (+)= s1 bin1; T (+)= bin0; T *= 2^escale.
+    `first` / `order` build the mutants the pins must reject."""
+    D0, D1, D2 = widths[0], widths[0] + widths[1], sum(widths)
+    x = [b0, math.ldexp(b1, -D0), math.ldexp(b2, -D1), math.ldexp(b36, -D2)]
+    if order == "0to6":
+        x = x[::-1]
+    pair = _two_sum if first == "two_sum" else _fast_two_sum
+    h, l = pair(x[2], x[3])
+    h, l = _dd_add_d(h, l, x[1])
+    h, l = _dd_add_d(h, l, x[0])
+    return math.ldexp(h, escale), math.ldexp(l, escale)
+
+
+def _hand_built():
+    """Bins where the mutants differ from R9 (found by a seeded search over
+    integer bins 0-2 and a large bin 3-6, kept verbatim; test below)."""
+    return [
+        # |s3 bin36| > |s2 bin2| != 0: Fast2Sum(s2 bin2, s3 bin36) loses its error term
+        (80.0, 733566.0, -507.0, -2.330459858142828e+22, 0),
+        (-270418.0, -22623082379.0, -873.0, -5.637044100322801e+22, 0),
+        (-224.0, -9448879903.0, -575697.0, 2.9822777494948886e+22, 0),
+        (0.0, 1.0, 1.0000000000000004, -1.3835058055282168e+19, -3),
+        # combining bin 0 first (order 0 -> 6) rounds differently
+        (-46009623603976.0, 9130610.0, 738119913.0, -2.5482292947405016e+16, 0),
+        (-4901247767.0, -8462.0, 4.0, -1956345731594.116, 0),
+        (9357439136729.0, 5923932.0, -479498940924.0, 1.0452897947103362e+16, 0),
+        # plain cases: bin 0 dominant, all bins comparable, a scale
+        (4503599627370497.0, 1048577.0, -2199023255553.0, 9.223372036854774e+18, 1),
+        (3.0, 1.0, 1.0, 1.0, 7),
+    ]
+
+
+def test_combine_r9_bitwise(orc):
+    """The oracle's combine equals the exact-semantics model of reading R9 bit for
+    bit on hand-built and 20000 random bins (bins 0-2 integers below 2^53 as the
+    split makes them, bin 3-6 any double, scales across the range)."""
+    cases = list(_hand_built())
+    rng = random.Random(11)
+    for _ in range(20000):
+        b0 = float(rng.randint(-2 ** 53 + 1, 2 ** 53 - 1) >> rng.randint(0, 52))
+        b1 = float(rng.randint(-2 ** 53 + 1, 2 ** 53 - 1) >> rng.randint(0, 52))
+        b2 = float(rng.randint(-2 ** 53 + 1, 2 ** 53 - 1) >> rng.randint(0, 52))
+        b36 = rng.choice([-1, 1]) * math.ldexp(rng.random() + 0.5, rng.randint(-10, 70))
+        cases.append((b0, b1, b2, b36, rng.randint(-60, 60)))
+    for b0, b1, b2, b36, es in cases:
+        got = orc.combine(b0, b1, b2, b36, es, W256)
+        want = r9_model(b0, b1, b2, b36, es, W256)
+        assert np.array_equal(np.array(got).view(np.uint64), np.array(want).view(np.uint64)), \
+            (b0, b1, b2, b36, es, got, want)
+
+
+def test_combine_r9_rejects_mutants():
+    """The pins discriminate: on the hand-built bins a Fast2Sum first step, or
+    combining bin 0 first (order 0 -> 6), gives other bits than R9 (so the
+    bitwise pin above would catch either mistake)."""
+    diff_fast = diff_order = 0
+    for b in _hand_built():
+        ref = r9_model(*b, W256)
+        diff_fast += r9_model(*b, W256, first="fast") != ref
+        diff_order += r9_model(*b, W256, order="0to6") != ref
+    assert diff_fast >= 3 and diff_order >= 3
+
+
+def test_combine_error_terms_exact(orc):
+    """Each T the oracle returns is an exact FP64x2 representation of the
+    rounded sum of its inputs: T.hi = RN(T.hi + T.lo) (normalised), and
+    |T - exact weighted bin sum| <= 2^-104 |exact| on the hand-built bins where
+    Fast2Sum would lose a whole error term."""
+    D0, D1, D2 = 22, 43, 64
+    for b0, b1, b2, b36, es in _hand_built():
+        th, tl = orc.combine(b0, b1, b2, b36, es, W256)
+        assert rn(fr(th) + fr(tl)) == th
+        ex = (fr(b0) + fr(b1) * F(2) ** -D0 + fr(b2) * F(2) ** -D1 + fr(b36) * F(2) ** -D2) \
+            * F(2) ** es
+        assert abs(fr(th) + fr(tl) - ex) <= F(2) ** -104 * abs(ex)
+
+
+# ----------------------------------------------------------------- TRSM vs plain substitution
+def _tri_dd(m, uplo, seed, unit=False):
+    rng = np.random.default_rng(seed)
+    hi = rng.uniform(-1, 1, (m, m)) / m
+    hi = np.tril(hi) if uplo == "L" else np.triu(hi)
+    lo = hi * 2.0 ** -53 * rng.uniform(-1, 1, (m, m))
+    dg = 1.0 + rng.uniform(0, 1, m)
+    hi[np.arange(m), np.arange(m)] = 1.0 if unit else dg
+    lo[np.arange(m), np.arange(m)] = 0.0 if unit else dg * 2.0 ** -54
+    s = hi + lo
+    return s, lo - (s - hi)
+
+
+@pytest.mark.parametrize("uplo,trans,unit", [("L", "N", False), ("U", "T", True)])
+def test_plain_trsm_exact_rationals(orc, uplo, trans, unit):
+    """The plain FP64x2 substitution itself: within 2^-100 (|x| + 1) of the exact
+    rational solution (12 x 12, three right-hand sides)."""
+    m, n = 12, 3
+    A_hi, A_lo = _tri_dd(m, uplo, 31, unit)
+    rng = np.random.default_rng(4)
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    X_hi, X_lo = orc.dd_trsm_plain(uplo, "U" if unit else "N", (1.0, 0.0), A_hi, A_lo, B_hi, B_lo,
+                                   trans=trans)
+    A = [[fr(A_hi[i, j]) + fr(A_lo[i, j]) for j in range(m)] for i in range(m)]
+    if unit:
+        for i in range(m):
+            A[i][i] = F(1)
+    if trans == "T":
+        A = [list(r) for r in zip(*A)]
+    lower = (uplo == "L") != (trans == "T")
+    order = range(m) if lower else range(m - 1, -1, -1)
+    for j in range(n):
+        x = [F(0)] * m
+        for i in order:
+            lo, hi = (0, i) if lower else (i + 1, m)
+            x[i] = (fr(B_hi[i, j]) + fr(B_lo[i, j]) - sum(A[i][l] * x[l] for l in range(lo, hi))) \
+                / A[i][i]
+        for i in range(m):
+            assert abs(fr(X_hi[i, j]) + fr(X_lo[i, j]) - x[i]) <= F(2) ** -100 * (abs(x[i]) + 1)
+
+
+@pytest.mark.parametrize("uplo,trans,unit,m,n", [("L", "N", False, 1100, 3), ("U", "N", False, 700, 2),
+                                                 ("L", "T", True, 1300, 2), ("U", "T", False, 257, 4)])
+def test_blocked_trsm_vs_plain_substitution(orc, uplo, trans, unit, m, n):
+    """R27's blocked TRSM (256-row diagonal inverses, 1024-row super-blocks,
+    cascaded-GEMM updates) agrees with the plain unblocked substitution to
+    2^-92 (|X| + 2^-20) on diagonally dominant systems that span several
+    blocks and super-blocks -- a pin that does not depend on the block sizes."""
+    A_hi, A_lo = _tri_dd(m, uplo, 13, unit)
+    rng = np.random.default_rng(15)
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    dg = "U" if unit else "N"
+    Xb = orc.casc_trsm(uplo, dg, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
+    Xp = orc.dd_trsm_plain(uplo, dg, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
+    diff = np.abs((Xb[0] - Xp[0]) + (Xb[1] - Xp[1]))
+    assert np.all(diff <= 2.0 ** -92 * (np.abs(Xp[0]) + 2.0 ** -20))
+    # and the comparison is sharp enough to see a 2^-80 error in one row
+    bad_lo = Xb[1].copy()
+    bad_lo[m // 2] += 2.0 ** -80
+    assert np.any(np.abs((Xb[0] - Xp[0]) + (bad_lo - Xp[1])) > 2.0 ** -92 * (np.abs(Xp[0]) + 2.0 ** -20))
