@@ -199,6 +199,16 @@ int casc_pack_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, in
 int casc_gemm_packed(int64_t m, int64_t n, int64_t k, const void* packed_a,
                      const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
                      uint8_t* flags, casc_stream_t stream);
+/* casc_gemm_packed with the flags' leading dimension ldf >= n (CASC_ERR_INVALID
+ * otherwise), so that a column block of C and of the flags can be computed on
+ * its own: with packed_b pointing at the packed blocks of columns [c0, c1)
+ * (c0 a multiple of 64: a byte range of the packed B, casc_pack_b) and C /
+ * flags pointing at column c0, the result is bitwise the same block of the
+ * full product (per-column scales are column-local).  The multi-GPU layer
+ * multiplies its local column slab this way while the other slabs arrive. */
+int casc_gemm_packed_ld(int64_t m, int64_t n, int64_t k, const void* packed_a,
+                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, int64_t ldf, casc_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Test / inspection entry points (same kernels as the product path).        */
@@ -470,6 +480,12 @@ size_t casc_i8_gemm_ws_bytes(int64_t m, int64_t n);
 int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
                         const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
                         uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream);
+/* casc_i8_gemm_packed with the flags' leading dimension ldf >= n (column
+ * blocks as casc_gemm_packed_ld; c0 a multiple of 256, the INT8 slab unit). */
+int casc_i8_gemm_packed_ld(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
+                           const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                           uint8_t* flags, int64_t ldf, void* ws, size_t ws_bytes,
+                           casc_stream_t stream);
 /* Same as casc_finalize (kept for the INT8 cascade's API symmetry). */
 int casc_i8_finalize(void);
 

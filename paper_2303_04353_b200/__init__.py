@@ -53,6 +53,7 @@ _sig("casc_packed_b_block_bytes", [_i64], _sz)
 _sig("casc_pack_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp])
 _sig("casc_pack_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp])
 _sig("casc_gemm_packed", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp])
+_sig("casc_gemm_packed_ld", [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp])
 _sig("casc_split_a", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_split_b", [_i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp])
 _sig("casc_debug_bins", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp])
@@ -75,7 +76,7 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
             "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2",
-            "casc_debug_ldexp"]
+            "casc_debug_ldexp", "casc_gemm_packed_ld", "casc_i8_gemm_packed_ld"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -92,6 +93,8 @@ _sig("casc_i8_pack", [_i64, _i64, _vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _v
 _sig("casc_i8_gemm_ws_bytes", [_i64, _i64], _sz)
 _sig("casc_i8_gemm_packed", [_i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _i64, _vp, _vp,
                              _sz, _vp])
+_sig("casc_i8_gemm_packed_ld", [_i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _i64, _vp,
+                                  _i64, _vp, _sz, _vp])
 I8_KC = 8192
 I8_DEFAULT_SLICES = 14
 
@@ -344,17 +347,27 @@ def casc_finalize():
     _check(_lib.casc_finalize(), "casc_finalize")
 
 
-def _outputs(m, n, device, C_hi, C_lo, flags, want_flags):
+def _outputs(m, n, device, C_hi, C_lo, flags, want_flags, strided_flags=False):
     if C_hi is None:
         C_hi = torch.empty((m, n), dtype=torch.float64, device=device)
     if C_lo is None:
         C_lo = torch.empty((m, n), dtype=torch.float64, device=device)
     if flags is None and want_flags:
         flags = torch.empty((m, n), dtype=torch.uint8, device=device)
-    if flags is not None and (flags.dtype != torch.uint8 or not flags.is_contiguous()
-                              or tuple(flags.shape) != (m, n)):
-        raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
+    if flags is not None:
+        ok = flags.dtype == torch.uint8 and tuple(flags.shape) == (m, n)
+        if strided_flags:
+            ok = ok and (m * n == 0 or flags.stride(1) == 1)
+        else:
+            ok = ok and flags.is_contiguous()
+        if not ok:
+            raise TypeError("flags must be a (m, n) uint8 CUDA tensor (row-contiguous)")
     return C_hi, C_lo, flags
+
+
+def _ldf(flags, n):
+    return max(n, 1) if flags is None or flags.dim() != 2 or flags.shape[0] <= 1 \
+        else flags.stride(0)
 
 
 _sig("casc_gemm_fp64x2_host", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
@@ -487,13 +500,14 @@ def casc_pack_b(B_hi, B_lo, packed=None, stream=None):
 
 def casc_gemm_packed(m, n, k, packed_a, packed_b, C_hi=None, C_lo=None, flags=None,
                      want_flags=True, stream=None):
-    """Phases 2-3 from packed operands.  Returns (C_hi, C_lo, flags)."""
+    """Phases 2-3 from packed operands.  Returns (C_hi, C_lo, flags).  C and
+    flags may be column blocks of larger row-major arrays (casc_gemm_packed_ld)."""
     dev = packed_a.device if packed_a is not None else torch.device("cuda")
-    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags)
+    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags, strided_flags=True)
     ldc = _ld_pair(C_hi, C_lo, "C") if m and n else max(n, 1)
-    _check(_lib.casc_gemm_packed(m, n, k, _ptr(packed_a), _ptr(packed_b), _ptr(C_hi),
-                                 _ptr(C_lo), ldc, _ptr(flags), _stream(stream)),
-           "casc_gemm_packed")
+    _check(_lib.casc_gemm_packed_ld(m, n, k, _ptr(packed_a), _ptr(packed_b), _ptr(C_hi),
+                                    _ptr(C_lo), ldc, _ptr(flags), _ldf(flags, n),
+                                    _stream(stream)), "casc_gemm_packed_ld")
     return C_hi, C_lo, flags
 
 
@@ -676,13 +690,15 @@ def casc_i8_pack(hi, lo, is_b: bool, y: int = I8_DEFAULT_SLICES, packed=None, st
 
 def casc_i8_gemm_packed(m, n, k, packed_a, packed_b, y: int = I8_DEFAULT_SLICES, C_hi=None,
                         C_lo=None, flags=None, want_flags=True, ws=None, stream=None):
-    """Phases 2-3 of the INT8 cascade from packed operands.  Returns (C_hi, C_lo, flags)."""
+    """Phases 2-3 of the INT8 cascade from packed operands.  Returns (C_hi, C_lo, flags).
+    C and flags may be column blocks of larger arrays (casc_i8_gemm_packed_ld)."""
     dev = packed_a.device if packed_a is not None else torch.device("cuda")
-    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags)
+    C_hi, C_lo, flags = _outputs(m, n, dev, C_hi, C_lo, flags, want_flags, strided_flags=True)
     ldc = _ld_pair(C_hi, C_lo, "C") if m and n else max(n, 1)
     if ws is None:
         ws = torch.empty(max(casc_i8_gemm_ws_bytes(m, n), 1), dtype=torch.uint8, device=dev)
-    _check(_lib.casc_i8_gemm_packed(m, n, k, int(y), _ptr(packed_a), _ptr(packed_b), _ptr(C_hi),
-                                    _ptr(C_lo), ldc, _ptr(flags), _ptr(ws), ws.numel(),
-                                    _stream(stream)), "casc_i8_gemm_packed")
+    _check(_lib.casc_i8_gemm_packed_ld(m, n, k, int(y), _ptr(packed_a), _ptr(packed_b),
+                                       _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags), _ldf(flags, n),
+                                       _ptr(ws), ws.numel(), _stream(stream)),
+           "casc_i8_gemm_packed_ld")
     return C_hi, C_lo, flags

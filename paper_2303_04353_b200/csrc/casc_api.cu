@@ -16,8 +16,9 @@
 namespace casc {
 cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
                                 const double* t_lo, const uint8_t* fbuf, double* C_hi,
-                                double* C_lo, int64_t ldc, uint8_t* flags, int ab, double ah,
-                                double al, double bh, double bl, int num_sms, cudaStream_t st);
+                                double* C_lo, int64_t ldc, uint8_t* flags, int64_t ldf, int ab,
+                                double ah, double al, double bh, double bl, int num_sms,
+                                cudaStream_t st);
 cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_hi,
                                  const double* A_lo, int64_t lda, double* I_hi, double* I_lo,
                                  cudaStream_t st);
@@ -167,7 +168,7 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
                      const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0,
-                     void* scratch = nullptr) {
+                     void* scratch = nullptr, int64_t ldf = -1) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -193,6 +194,7 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.C_lo = C_lo;
   a.ldc = ldc;
   a.flags = flags;
+  a.ldf = ldf < 0 ? n : ldf;
   a.dbg = dbg;
   a.un_b2 = std::ldexp(1.0, w.c1 - w.c0);
   a.tri = tri;
@@ -230,8 +232,8 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.ab = 0;  // alpha / beta go to the reduction
   cudaError_t e = casc::launch_gemm(a, sms, st);
   if (e == cudaSuccess)
-    e = casc::launch_split_reduce(P, m, n, a.t_hi, a.t_lo, a.fbuf, C_hi, C_lo, ldc, flags, abv.ab,
-                                  abv.ah, abv.al, abv.bh, abv.bl, sms, st);
+    e = casc::launch_split_reduce(P, m, n, a.t_hi, a.t_lo, a.fbuf, C_hi, C_lo, ldc, flags, a.ldf,
+                                  abv.ab, abv.ah, abv.al, abv.bh, abv.bl, sms, st);
   if (!split_ws) cudaFreeAsync(buf, st);
   if (own_scratch) cudaFreeAsync(scratch, st);
   if (e == cudaSuccess) g_launches += 3;
@@ -313,29 +315,37 @@ int casc_pack_b(int64_t k, int64_t n, const double* B_hi, const double* B_lo, in
 }
 
 static int zero_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
-                  cudaStream_t st) {
+                  cudaStream_t st, int64_t ldf = -1) {
   cudaError_t e = cudaMemset2DAsync(C_hi, ldc * sizeof(double), 0, n * sizeof(double), m, st);
   if (e == cudaSuccess)
     e = cudaMemset2DAsync(C_lo, ldc * sizeof(double), 0, n * sizeof(double), m, st);
-  if (e == cudaSuccess && flags) e = cudaMemsetAsync(flags, 0, (size_t)(m * n), st);
+  if (e == cudaSuccess && flags)
+    e = cudaMemset2DAsync(flags, (size_t)(ldf < 0 ? n : ldf), 0, (size_t)n, (size_t)m, st);
   return cuda_status(e);
+}
+
+int casc_gemm_packed_ld(int64_t m, int64_t n, int64_t k, const void* packed_a,
+                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, int64_t ldf, casc_stream_t stream) {
+  g_launches = 0;
+  int r;
+  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
+  if ((r = check_mat(C_hi, m, n, ldc)) || (r = check_mat(C_lo, m, n, ldc))) return r;
+  if (flags && ldf < (n > 1 ? n : 1)) return CASC_ERR_INVALID;
+  if (m == 0 || n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  if (k == 0) return zero_c(m, n, C_hi, C_lo, ldc, flags, S(stream), ldf);
+  if (!packed_a || !packed_b) return CASC_ERR_INVALID;
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  return gemm_packed_impl(m, n, k, packed_a, packed_b, C_hi, C_lo, ldc, flags, sms, S(stream), 0,
+                          nst, nullptr, AlphaBeta(), nullptr, 0, nullptr, ldf);
 }
 
 int casc_gemm_packed(int64_t m, int64_t n, int64_t k, const void* packed_a, const void* packed_b,
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
                      casc_stream_t stream) {
-  g_launches = 0;
-  int r;
-  if (m < 0 || n < 0 || k < 0) return CASC_ERR_INVALID;
-  if ((r = check_mat(C_hi, m, n, ldc)) || (r = check_mat(C_lo, m, n, ldc))) return r;
-  if (m == 0 || n == 0) return CASC_OK;
-  int sms = 0;
-  if ((r = device_check(&sms))) return r;
-  if (k == 0) return zero_c(m, n, C_hi, C_lo, ldc, flags, S(stream));
-  if (!packed_a || !packed_b) return CASC_ERR_INVALID;
-  const int nst = (int)(casc::kpad_of(k) / casc::BK);
-  return gemm_packed_impl(m, n, k, packed_a, packed_b, C_hi, C_lo, ldc, flags, sms, S(stream), 0,
-                          nst, nullptr);
+  return casc_gemm_packed_ld(m, n, k, packed_a, packed_b, C_hi, C_lo, ldc, flags, n, stream);
 }
 
 static int validate_gemm(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,

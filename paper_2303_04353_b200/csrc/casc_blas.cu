@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(
     int P, int64_t m, int64_t n, const double* __restrict__ t_hi,
     const double* __restrict__ t_lo, const uint8_t* __restrict__ fbuf,
     double* __restrict__ C_hi, double* __restrict__ C_lo, int64_t ldc,
-    uint8_t* __restrict__ flags, int ab, double ah, double al, double bh, double bl) {
+    uint8_t* __restrict__ flags, int64_t ldf, int ab, double ah, double al, double bh, double bl) {
   const int64_t mn = m * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -62,20 +62,21 @@ __global__ void __launch_bounds__(256) split_reduce_kernel(
                              ab == 2);
     *ch = th;
     *cl = tl;
-    if (flags) flags[idx] = fl;
+    if (flags) flags[i * ldf + j] = fl;
   }
 }
 
 cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
                                 const double* t_lo, const uint8_t* fbuf, double* C_hi,
-                                double* C_lo, int64_t ldc, uint8_t* flags, int ab, double ah,
-                                double al, double bh, double bl, int num_sms, cudaStream_t st) {
+                                double* C_lo, int64_t ldc, uint8_t* flags, int64_t ldf, int ab,
+                                double ah, double al, double bh, double bl, int num_sms,
+                                cudaStream_t st) {
   const int64_t mn = m * n;
   if (mn == 0) return cudaSuccess;
   int64_t blocks = (mn + 255) / 256;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   split_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(P, m, n, t_hi, t_lo, fbuf, C_hi, C_lo, ldc,
-                                                        flags, ab, ah, al, bh, bl);
+                                                        flags, ldf, ab, ah, al, bh, bl);
   return cudaGetLastError();
 }
 

@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     double* dst_lo = split_p ? p.t_lo + (int64_t)q0 * p.m * p.n : p.C_lo;
     const int64_t ldd = split_p ? p.n : p.ldc;
     uint8_t* dst_fl = split_p ? p.fbuf + (int64_t)q0 * p.m * p.n : p.flags;
+    const int64_t ldfl = split_p ? p.n : p.ldf;
     uint32_t flagbits = 0;
     for (int st = s0; st < s1; ++st, ++it) {
       if (st == s0 || (st % STAGES_PER_PANEL) == 0) {
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           for (int i = 0; i < 2; ++i) {
             const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
             if (row < p.m && col < p.n && in_tri<TRI>(p, row, col))
-              dst_fl[row * p.n + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
+              dst_fl[row * ldfl + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
           }
       }
     }

@@ -542,6 +542,7 @@ struct GemmArgs {
   double* C_lo;
   int64_t ldc;
   uint8_t* flags;
+  int64_t ldf;          // leading dimension of flags
   double* ws;           // per CTA: C hi, C lo, V[NGMAX] (WS_PER_CTA doubles)
   unsigned int* sync;   // wave-sync counter (zeroed before the launch) or null
   int32_t* dbg;         // debug: bins of panel dbg_panel (y x m x n int32) instead of C
@@ -1245,7 +1246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                      p.ab == 2 ? *ol : 0.0, p.ab == 2);
                   *oh = ch;
                   *ol = cl;
-                  if (p.flags) p.flags[gi * p.n + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
+                  if (p.flags) p.flags[gi * p.ldf + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
                 }
               }
             }
@@ -1381,7 +1382,7 @@ __global__ void __launch_bounds__(256) i8_split_reduce_kernel(const GemmArgs p) 
                        p.ab == 2 ? *ol : 0.0, p.ab == 2);
     *oh = ch;
     *ol = cl;
-    if (p.flags) p.flags[i * p.n + j] = flag;
+    if (p.flags) p.flags[i * p.ldf + j] = flag;
   }
 }
 
@@ -1409,8 +1410,10 @@ int split_parts(int64_t m, int64_t n, int64_t k, int sms) {
 cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k, int y,
                  double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, double* ws, int grid,
                  int32_t* dbg, int64_t dbg_panel, cudaStream_t st, int ab = 0, double ah = 1.0,
-                 double al = 0.0, double bh = 0.0, double bl = 0.0, int tri = 0) {
+                 double al = 0.0, double bh = 0.0, double bl = 0.0, int tri = 0,
+                 int64_t ldf = -1) {
   GemmArgs a{};
+  a.ldf = ldf < 0 ? n : ldf;
   a.tri = tri;
   a.ab = ab;
   a.ah = ah;
@@ -1568,24 +1571,39 @@ int casc_i8_pack(int64_t rows, int64_t k, const double* hi, const double* lo, in
   return st8(e);
 }
 
-int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
-                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
-                        uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream) {
+int casc_i8_gemm_packed_ld(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
+                           const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                           uint8_t* flags, int64_t ldf, void* ws, size_t ws_bytes,
+                           casc_stream_t stream) {
   host::set_launches(0);
   int r;
   if (m < 0 || n < 0 || k < 0 || y < i8::YMIN || y > i8::YMAX) return CASC_ERR_INVALID;
   if ((r = host::check_mat(C_hi, m, n, ldc)) || (r = host::check_mat(C_lo, m, n, ldc))) return r;
+  if (flags && ldf < (n > 1 ? n : 1)) return CASC_ERR_INVALID;
   if (m == 0 || n == 0) return CASC_OK;
   int sms = 0;
   if ((r = host::device_check(&sms))) return r;
-  if (k == 0) return host::zero_c(m, n, C_hi, C_lo, ldc, flags, S8(stream));
+  if (k == 0) {
+    if (flags && ldf != n) {  // zero C, then the flags rows one by one (ld != n)
+      if ((r = host::zero_c(m, n, C_hi, C_lo, ldc, nullptr, S8(stream)))) return r;
+      return st8(cudaMemset2DAsync(flags, (size_t)ldf, 0, (size_t)n, (size_t)m, S8(stream)));
+    }
+    return host::zero_c(m, n, C_hi, C_lo, ldc, flags, S8(stream));
+  }
   if (!packed_a || !packed_b || !ws || ws_bytes < casc_i8_gemm_ws_bytes(m, n))
     return CASC_ERR_INVALID;
   const cudaError_t e = i8::gemm(packed_a, packed_b, m, n, k, y, C_hi, C_lo, ldc, flags,
                                  static_cast<double*>(ws), i8::ws_grid(m, n, sms), nullptr, 0,
-                                 S8(stream));
+                                 S8(stream), 0, 1.0, 0.0, 0.0, 0.0, 0, ldf);
   if (e == cudaSuccess) host::set_launches(1);
   return st8(e);
+}
+
+int casc_i8_gemm_packed(int64_t m, int64_t n, int64_t k, int y, const void* packed_a,
+                        const void* packed_b, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* ws, size_t ws_bytes, casc_stream_t stream) {
+  return casc_i8_gemm_packed_ld(m, n, k, y, packed_a, packed_b, C_hi, C_lo, ldc, flags, n, ws,
+                                ws_bytes, stream);
 }
 
 int casc_i8_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi,

@@ -133,7 +133,8 @@ struct GemmArgs {
   double* C_hi;
   double* C_lo;
   int64_t ldc;
-  uint8_t* flags;  // m x n (ld n) or null
+  uint8_t* flags;  // m x n (ld ldf) or null
+  int64_t ldf;
   double* dbg;     // debug: bins of the single panel, 4 x m x n (canonical scales)
   void* scratch;               // per launch (caller memory, gemm_scratch_bytes): the
                                // three below, set and zeroed by launch_gemm

@@ -8,10 +8,13 @@ One process per GPU (torch.distributed, NCCL).  Rank r of W:
   2. packs its column slab of B (casc_pack_b; per-column scales are
      column-local, so the slab's packed bytes are bit-identical to the same
      blocks of a single-GPU pack);
-  3. all-gathers the packed B slabs (one ncclAllGather of equal-size chunks;
-     the packed layout is 64-column-block major, so the gathered buffer IS
-     the packed B of the whole matrix);
-  4. runs the fused cascaded GEMM on its rows (casc_gemm_packed).
+  3. all-gathers the packed B slabs (one in-place ncclAllGather of equal-size
+     chunks; the packed layout is 64-column-block major, so the gathered
+     buffer IS the packed B of the whole matrix) -- while
+  4. the fused cascaded GEMM multiplies its rows by its OWN column slab
+     (casc_gemm_packed_ld on that column block of C); once the exchange has
+     landed (stream-ordered wait, no kernel spins on another), a second
+     launch multiplies the other columns.
 k is never split, so there is no reduction and every element is computed by
 exactly the same arithmetic as on one GPU: C is bitwise independent of W
 (P-invariance).
@@ -90,7 +93,8 @@ class ShardedCascGemm:
     allocated once and reused across calls (bench steps)."""
 
     def __init__(self, m: int, n: int, k: int, group=None, ops: Ops | None = None,
-                 device=None, block: int = BLOCK, gather: str = "packed"):
+                 device=None, block: int = BLOCK, gather: str = "packed",
+                 overlap: bool = True):
         """block: slab granularity (columns) of the packed B: 64 for the FP64
         cascade, I8_BLOCK with i8_cuda_ops().
         gather: what the ranks exchange (N > 1).  "packed": each rank splits its
@@ -98,7 +102,12 @@ class ShardedCascGemm:
         56 B per element of B; INT8 cascade: ~14 B).  "raw": the FP64x2 slabs
         themselves are all-gathered (16 B per element) and every rank splits all
         of B locally, slab by slab into the packed layout (the byte-cheaper
-        choice for the FP64 cascade).  Bitwise the same result."""
+        choice for the FP64 cascade).  Bitwise the same result.
+        overlap (N > 1): the exchange runs while the GEMM multiplies the rank's
+        own column slab (casc_gemm_packed_ld on a column block of C), then the
+        other columns are multiplied once it has landed -- two stream-ordered
+        launches, no kernel waits on another (B200_PROFILING.md); bitwise the
+        same C, since every element depends only on its row and column."""
         if gather not in ("packed", "raw"):
             raise ValueError("gather must be 'packed' or 'raw'")
         self.m, self.n, self.k = m, n, k
@@ -112,79 +121,127 @@ class ShardedCascGemm:
         self.r0, self.r1 = row_shard(m, self.world, self.rank)
         self.c0, self.c1, self.blocks_per_rank = col_slab(n, self.world, self.rank, block)
         blk = self.ops.packed_b_block_bytes(k)
+        self.blk = blk
         self.chunk = self.blocks_per_rank * blk
-        self.packed_b_local = torch.zeros(self.chunk, dtype=torch.uint8, device=self.device)
-        self.packed_b_full = (torch.empty(self.chunk * self.world, dtype=torch.uint8,
-                                          device=self.device) if self.world > 1 else None)
+        self.overlap = overlap and self.world > 1
+        # packed B of all ranks: chunk r = rank r's column slab (column-block major,
+        # so the gathered buffer IS the packed B of the whole matrix); with one
+        # rank it is just the local pack
+        self.packed_b_full = torch.zeros(self.chunk * self.world, dtype=torch.uint8,
+                                         device=self.device)
+        self.own = self.packed_b_full[self.rank * self.chunk:(self.rank + 1) * self.chunk]
         self.packed_a = None
         self.raw = self.gather == "raw" and self.world > 1
         if self.raw:  # [rank][hi | lo][k][slab width padded to whole blocks]
             self.wpad = self.blocks_per_rank * block
-            self.raw_local = torch.zeros((2, k, self.wpad), dtype=torch.float64,
-                                         device=self.device)
-            self.raw_full = torch.empty((self.world, 2, k, self.wpad), dtype=torch.float64,
+            self.raw_full = torch.zeros((self.world, 2, k, self.wpad), dtype=torch.float64,
                                         device=self.device)
-            self.slabs = [col_slab(n, self.world, r, block)[:2] for r in range(self.world)]
-        # names of the intervals between the 4 events of __call__ (bench phases)
-        self.phase_names = (["split_a", "allgather_raw", "split_b", "gemm"] if self.raw else
-                            ["split_a", "split_b", "allgather", "gemm"])
+        self.slabs = [col_slab(n, self.world, r, block)[:2] for r in range(self.world)]
+        # names of the intervals between the 5 events of __call__ (bench phases)
+        if self.overlap:
+            self.phase_names = ["split_a", "split_b_own", "gemm_own_cols", "gemm_other_cols"]
+        elif self.raw:
+            self.phase_names = ["split_a", "allgather_raw", "split_b", "gemm"]
+        else:
+            self.phase_names = ["split_a", "split_b", "allgather", "gemm"]
+        self.launches = 0
+
+    def _all_gather(self, full, mine, async_op=False):
+        """In-place all-gather of equal chunks (rank r's chunk at offset r): one
+        all_gather_into_tensor for every backend (NCCL over NVLink / NVSwitch on
+        the GPUs, gloo in the CPU tests)."""
+        return dist.all_gather_into_tensor(full, mine, group=self.group, async_op=async_op)
+
+    def _used(self, a0, a1):
+        return -(-(a1 - a0) // self.block) * self.blk
+
+    def _pack_slab(self, r, B_hi, B_lo, count):
+        a0, a1 = self.slabs[r]
+        if a1 > a0:
+            base = r * self.chunk
+            self.ops.pack_b(B_hi, B_lo, packed=self.packed_b_full[base:base + self._used(a0, a1)])
+            self.launches += count()
+
+    def _gemm_cols(self, pa, col0, col1, C_hi, C_lo, flags, count):
+        """C[:, col0:col1] from the packed blocks of those columns (col0 a slab
+        boundary: a byte range of the packed B)."""
+        if col1 <= col0:
+            return
+        mloc = self.r1 - self.r0
+        b0 = (col0 // self.block) * self.blk
+        self.ops.gemm_packed(mloc, col1 - col0, self.k, pa, self.packed_b_full[b0:],
+                             C_hi=C_hi[:, col0:col1], C_lo=C_lo[:, col0:col1],
+                             flags=None if flags is None else flags[:, col0:col1])
+        self.launches += count()
 
     def __call__(self, A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi=None, C_lo=None,
                  flags=None, events=None):
         """A_*_rows: this rank's rows (r1-r0) x k.  B_*_slab: k x (c1-c0).
         Returns this rank's (C_hi, C_lo, flags) rows.  `events`, if given, is a
-        list of 4 CUDA events recorded after pack_a, pack_b, all-gather, gemm."""
+        list of 4 CUDA events recorded at the ends of the phases `phase_names`."""
         mloc = self.r1 - self.r0
         count = getattr(self.ops, "launch_count", None) or (lambda: 0)
         self.launches = 0
+        if C_hi is None:
+            C_hi = torch.empty((mloc, self.n), dtype=torch.float64, device=self.device)
+        if C_lo is None:
+            C_lo = torch.empty((mloc, self.n), dtype=torch.float64, device=self.device)
+        if flags is None:
+            flags = torch.empty((mloc, self.n), dtype=torch.uint8, device=self.device)
         self.packed_a = self.ops.pack_a(A_hi_rows, A_lo_rows, packed=self.packed_a)
         self.launches += count()
         rec = (lambda i: events[i].record()) if events else (lambda i: None)
         rec(0)
-        if self.raw:
-            w = self.c1 - self.c0
-            if w > 0:
-                self.raw_local[0, :, :w].copy_(B_hi_slab)
-                self.raw_local[1, :, :w].copy_(B_lo_slab)
-            if dist.get_backend(self.group) == "gloo":  # CPU plumbing tests
-                dist.all_gather(list(self.raw_full.unbind(0)), self.raw_local, group=self.group)
-            else:  # NCCL over NVLink / NVSwitch
-                dist.all_gather_into_tensor(self.raw_full.view(-1), self.raw_local.view(-1),
-                                            group=self.group)
+        w = self.c1 - self.c0
+        if self.world == 1:
+            self._pack_slab(0, B_hi_slab, B_lo_slab, count)
             rec(1)
-            blk = self.ops.packed_b_block_bytes(self.k)
-            for r, (a0, a1) in enumerate(self.slabs):
-                if a1 > a0:
-                    used = -(-(a1 - a0) // self.block) * blk
-                    base = r * self.chunk
-                    self.ops.pack_b(self.raw_full[r, 0, :, :a1 - a0],
-                                    self.raw_full[r, 1, :, :a1 - a0],
-                                    packed=self.packed_b_full[base:base + used])
-                    self.launches += count()
             rec(2)
-            out = self.ops.gemm_packed(mloc, self.n, self.k, self.packed_a, self.packed_b_full,
-                                       C_hi=C_hi, C_lo=C_lo, flags=flags)
-            self.launches += count()
+            self._gemm_cols(self.packed_a, 0, self.n, C_hi, C_lo, flags, count)
             rec(3)
-            return out
-        if self.c1 > self.c0:
-            used = -(-(self.c1 - self.c0) // self.block) * self.ops.packed_b_block_bytes(self.k)
-            self.ops.pack_b(B_hi_slab, B_lo_slab, packed=self.packed_b_local[:used])
-            self.launches += count()
-        rec(1)
-        if self.world > 1:
-            if dist.get_backend(self.group) == "gloo":  # CPU plumbing tests
-                dist.all_gather(list(self.packed_b_full.chunk(self.world)), self.packed_b_local,
-                                group=self.group)
-            else:  # NCCL over NVLink / NVSwitch
-                dist.all_gather_into_tensor(self.packed_b_full, self.packed_b_local,
-                                            group=self.group)
-            pb = self.packed_b_full
+            return C_hi, C_lo, flags
+        if self.raw:
+            mine = self.raw_full[self.rank]
+            if w > 0:
+                mine[0, :, :w].copy_(B_hi_slab)
+                mine[1, :, :w].copy_(B_lo_slab)
+        if self.overlap:
+            # own slab first: packed locally, multiplied while the exchange runs
+            self._pack_slab(self.rank, B_hi_slab, B_lo_slab, count)
+            rec(1)
+            if self.raw:
+                work = self._all_gather(self.raw_full.view(-1), self.raw_full[self.rank].view(-1),
+                                        async_op=True)
+            else:
+                work = self._all_gather(self.packed_b_full, self.own, async_op=True)
+            self._gemm_cols(self.packed_a, self.c0, self.c1, C_hi, C_lo, flags, count)
+            rec(2)
+            work.wait()  # the current stream waits for the exchange
+            if self.raw:
+                for r in range(self.world):
+                    a0, a1 = self.slabs[r]
+                    if r != self.rank and a1 > a0:
+                        self._pack_slab(r, self.raw_full[r, 0, :, :a1 - a0],
+                                        self.raw_full[r, 1, :, :a1 - a0], count)
+            self._gemm_cols(self.packed_a, self.c1, self.n, C_hi, C_lo, flags, count)
+            self._gemm_cols(self.packed_a, 0, self.c0, C_hi, C_lo, flags, count)
+            rec(3)
+            return C_hi, C_lo, flags
+        # serial exchange: all of B gathered first, then one GEMM over all columns
+        if self.raw:
+            self._all_gather(self.raw_full.view(-1), self.raw_full[self.rank].view(-1))
+            rec(1)
+            for r in range(self.world):
+                a0, a1 = self.slabs[r]
+                if a1 > a0:
+                    self._pack_slab(r, self.raw_full[r, 0, :, :a1 - a0],
+                                    self.raw_full[r, 1, :, :a1 - a0], count)
+            rec(2)
         else:
-            pb = self.packed_b_local
-        rec(2)
-        out = self.ops.gemm_packed(mloc, self.n, self.k, self.packed_a, pb, C_hi=C_hi,
-                                   C_lo=C_lo, flags=flags)
-        self.launches += count()
+            self._pack_slab(self.rank, B_hi_slab, B_lo_slab, count)
+            rec(1)
+            self._all_gather(self.packed_b_full, self.own)
+            rec(2)
+        self._gemm_cols(self.packed_a, 0, self.n, C_hi, C_lo, flags, count)
         rec(3)
-        return out
+        return C_hi, C_lo, flags

@@ -692,3 +692,39 @@ def test_trsm_edges(casc, orc, m, n):
     with pytest.raises(casc.CascError):  # B overlapping A
         buf_h = torch.zeros((m + 1, m), dtype=torch.float64, device="cuda")
         casc.casc_trsm_fp64x2("L", "N", 1.0, buf_h[:m], buf_h[:m], buf_h[1:, :1], buf_h[1:, :1])
+
+
+# ------------------------------------------------------------------ column blocks (multi-GPU overlap)
+@pytest.mark.parametrize("kind,m,n,k,c0,c1", [("f64", 130, 700, 600, 128, 448),
+                                              ("f64", 64, 300, 256, 256, 300),
+                                              ("i8", 300, 900, 700, 256, 768),
+                                              ("i8", 256, 600, 300, 512, 600)])
+def test_packed_column_block_bitwise(casc, kind, m, n, k, c0, c1):
+    """casc_gemm_packed_ld / casc_i8_gemm_packed_ld on a column block [c0, c1)
+    (packed B offset by whole blocks, C and flags strided views of the full
+    arrays): bitwise the same block of the full product, nothing else written
+    (the multi-GPU layer multiplies its own slab first, multigpu.py)."""
+    import torch
+    d = I.make_config(2, m=m, n=n, k=k, seed=97)
+    A_hi, A_lo, B_hi, B_lo = (T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo"))
+    if kind == "f64":
+        pa, pb = casc.casc_pack_a(A_hi, A_lo), casc.casc_pack_b(B_hi, B_lo)
+        blk, W = casc.casc_packed_b_block_bytes(k), 64
+        gemm = casc.casc_gemm_packed
+    else:
+        y = 14
+        pa, pb = casc.casc_i8_pack(A_hi, A_lo, False, y), casc.casc_i8_pack(B_hi, B_lo, True, y)
+        blk, W = 2 * casc.casc_i8_packed_block_bytes(k, y), 256
+        gemm = lambda *a, **kw: casc.casc_i8_gemm_packed(*a, y=y, **kw)
+    full = [N(x) for x in gemm(m, n, k, pa, pb)]
+    C_hi = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    C_lo = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    fl = torch.full((m, n), 7, dtype=torch.uint8, device="cuda")
+    gemm(m, c1 - c0, k, pa, pb[(c0 // W) * blk:], C_hi=C_hi[:, c0:c1], C_lo=C_lo[:, c0:c1],
+         flags=fl[:, c0:c1])
+    g = [N(C_hi), N(C_lo), N(fl)]
+    for a, b in zip(g, full):
+        assert np.array_equal(np.ascontiguousarray(a[:, c0:c1]).view(np.uint8),
+                              np.ascontiguousarray(b[:, c0:c1]).view(np.uint8))
+    assert np.all(np.isnan(g[0][:, :c0])) and np.all(np.isnan(g[0][:, c1:]))
+    assert np.all(g[2][:, :c0] == 7) and np.all(g[2][:, c1:] == 7)

@@ -79,16 +79,23 @@ class _CpuOps:
         B_lo = torch.cat([blocks[j, 1] for j in range(nb)], dim=1)[:, :n].numpy()
         fn = oracle.i8_casc_gemm if self.i8 else oracle.casc_gemm
         h, l, f = fn(pa[0].numpy(), pa[1].numpy(), B_hi, B_lo)
-        return torch.from_numpy(h), torch.from_numpy(l), torch.from_numpy(f)
+        out = []
+        for dst, src in ((C_hi, h), (C_lo, l), (flags, f)):  # C may be a column block
+            if dst is None:
+                dst = torch.from_numpy(src)
+            else:
+                dst.copy_(torch.from_numpy(src))
+            out.append(dst)
+        return tuple(out)
 
 
-def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed"):
+def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed", overlap=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2303_04353_b200.multigpu import I8_BLOCK, ShardedCascGemm
     W = I8_BLOCK if i8 else 64
     op = ShardedCascGemm(m, n, k, ops=_CpuOps(k, W, i8), device=torch.device("cpu"), block=W,
-                         gather=gather)
+                         gather=gather, overlap=overlap)
     d = I.make_config(1, m=m, n=n, k=k, seed=21, rows=slice(op.r0, op.r1))
     A_hi, A_lo = torch.from_numpy(d["A_hi"]), torch.from_numpy(d["A_lo"])
     B_hi = torch.from_numpy(d["B_hi"][:, op.c0:op.c1].copy())
@@ -100,13 +107,19 @@ def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,n,k,gather", [(10, 150, 300, "packed"), (7, 64, 40, "packed"),
-                                          (10, 150, 300, "raw"), (5, 200, 70, "raw")])
-def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k, gather):
-    """gather="raw" exchanges the FP64x2 slabs and packs all of B on every rank
-    (SURVEY §8(e) byte-cheaper alternative): the same bits."""
-    world = 2
-    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), False, gather),
+@pytest.mark.parametrize("world,m,n,k,gather,overlap", [
+    (2, 10, 150, 300, "packed", True), (2, 7, 64, 40, "packed", True),
+    (2, 10, 150, 300, "raw", True), (2, 5, 200, 70, "raw", True),
+    (2, 10, 150, 300, "packed", False), (2, 5, 200, 70, "raw", False),
+    (4, 9, 300, 80, "packed", True), (4, 6, 200, 70, "raw", True), (4, 9, 130, 40, "packed", False)])
+def test_gloo_world_p_invariance(tmp_path, orc, world, m, n, k, gather, overlap):
+    """The production exchange (in-place all_gather_into_tensor, the call NCCL
+    runs on the GPUs) on gloo: world 2 and 4, packed and raw exchanges, with
+    the overlapped schedule (own column slab multiplied while the exchange
+    runs, then the other columns) and the serial one: the same bits as one
+    process.  gather="raw" exchanges the FP64x2 slabs and packs all of B on
+    every rank (SURVEY §8(e) byte-cheaper alternative)."""
+    mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), False, gather, overlap),
              nprocs=world, join=True)
     d = I.make_config(1, m=m, n=n, k=k, seed=21)
     ref_hi, ref_lo, ref_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
@@ -121,11 +134,10 @@ def test_gloo_world2_p_invariance(tmp_path, orc, m, n, k, gather):
     assert rows == m
 
 
-@pytest.mark.parametrize("m,n,k", [(9, 600, 70), (4, 256, 33)])
-def test_gloo_world2_i8_p_invariance(tmp_path, orc, m, n, k):
-    """The INT8 cascade's sharding (256-column slabs, NEXT-3): the gathered
-    result equals the single-process oracle bit for bit."""
-    world = 2
+@pytest.mark.parametrize("world,m,n,k", [(2, 9, 600, 70), (2, 4, 256, 33), (4, 8, 900, 40)])
+def test_gloo_world_i8_p_invariance(tmp_path, orc, world, m, n, k):
+    """The INT8 cascade's sharding (256-column slabs, NEXT-3), overlapped
+    exchange: the gathered result equals the single-process oracle bit for bit."""
     mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), True), nprocs=world,
              join=True)
     d = I.make_config(1, m=m, n=n, k=k, seed=21)
