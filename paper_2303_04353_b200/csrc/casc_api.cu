@@ -34,6 +34,10 @@ cudaError_t launch_split_a(const double*, const double*, int64_t, int64_t, int64
                            cudaStream_t, bool trans = false);
 cudaError_t launch_split_b(const double*, const double*, int64_t, int64_t, int64_t, Widths, void*,
                            cudaStream_t, bool trans = false);
+cudaError_t launch_split_ab(const double* Ahi, const double* Alo, int64_t lda, int64_t m,
+                            const double* Bhi, const double* Blo, int64_t ldb, int64_t n,
+                            int64_t k, Widths w, void* pa, void* pb, cudaStream_t st, bool ta,
+                            bool tb);
 cudaError_t launch_unpack_a(const void*, int64_t, int64_t, Widths, double*, int32_t*,
                             cudaStream_t);
 cudaError_t launch_unpack_b(const void*, int64_t, int64_t, Widths, double*, int32_t*,
@@ -141,11 +145,13 @@ int split_plan(int64_t m, int64_t n, int64_t k, int sms) {
   const double eff_t = (double)tiles / (double)(((tiles + sms - 1) / sms) * sms);
   const double eff_s = (double)units / (double)(((units + sms - 1) / sms) * sms);
   if (eff_s < eff_t + 0.04) return 0;
-  if ((double)P * m * n * 17.0 > (double)(1ull << 31)) return 0;
+  if ((double)P * (m + 63) * (n + 63) * 17.0 > (double)(1ull << 31)) return 0;
   return (int)P;
 }
-size_t split_bytes(int64_t m, int64_t n, int P) {
-  return P ? ((size_t)P * m * n * 17 + 255) / 256 * 256 : 0;
+size_t split_bytes(int64_t m, int64_t n, int P) {  // tile-major panel sums + flags, padded tiles
+  const int64_t padded = (m + casc::TM - 1) / casc::TM * ((n + casc::TN - 1) / casc::TN) *
+                         (casc::TM * casc::TN);
+  return P ? ((size_t)P * padded * 17 + 255) / 256 * 256 : 0;
 }
 // the fused kernel's per-launch scratch (wave counter, WIDE list) at the end of a
 // workspace: sized for the most work items a call with (m, n, k) can have
@@ -224,7 +230,7 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
     if (own_scratch) cudaFreeAsync(scratch, st);
     return CASC_ERR_CUDA;
   }
-  const int64_t mn = m * n;
+  const int64_t mn = (int64_t)a.mblocks * a.nblocks * (casc::TM * casc::TN);  // padded
   a.split_p = P;
   a.t_hi = static_cast<double*>(buf);
   a.t_lo = a.t_hi + (int64_t)P * mn;
@@ -385,16 +391,16 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   uint8_t* pa = static_cast<uint8_t*>(workspace);
   uint8_t* pb = pa + (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
   const casc::Widths w = widths_for(k);
-  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, S(stream));
-  if (e != cudaSuccess) return CASC_ERR_CUDA;
-  e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, S(stream));
+  // phase 1: both splits in one launch
+  cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, m, B_hi, B_lo, ldb, n, k, w, pa, pb,
+                                        S(stream), false, false);
   if (e != cudaSuccess) return CASC_ERR_CUDA;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
   uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
   g_launches = 0;
   r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr,
                        AlphaBeta(), ps, 0, ws_counter(workspace, m, n, k));
-  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;  // + the two split kernels
+  g_launches = (r == CASC_OK) ? g_launches + 1 : 0;  // + the split launch
   return r;
 }
 
@@ -624,9 +630,8 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
   uint8_t* pa = static_cast<uint8_t*>(ws);
   uint8_t* pb = pa + (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
   const casc::Widths w = widths_for(k);
-  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, m, k, w, pa, st, transa == CASC_OP_T);
-  if (e == cudaSuccess)
-    e = casc::launch_split_b(B_hi, B_lo, ldb, k, n, w, pb, st, transb == CASC_OP_T);
+  cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, m, B_hi, B_lo, ldb, n, k, w, pa, pb, st,
+                                        transa == CASC_OP_T, transb == CASC_OP_T);
   AlphaBeta abv;
   const bool unit_alpha = (alpha_hi == 1.0 && alpha_lo == 0.0);
   abv.ab = use_beta ? 2 : (unit_alpha ? 0 : 1);
@@ -641,7 +646,7 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
                                             nst, nullptr, abv, ps, 0, ws_counter(ws, m, n, k))
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
-  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
+  g_launches = (r == CASC_OK) ? g_launches + 1 : 0;
   return r;
 }
 
@@ -698,9 +703,8 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
   const casc::Widths w = widths_for(k);
   // op(A) (n x k) as the A operand; op(A)^T (k x n) as the B operand: stored as A
   // itself, read transposed when trans == N
-  cudaError_t e = casc::launch_split_a(A_hi, A_lo, lda, n, k, w, pa, st, trans == CASC_OP_T);
-  if (e == cudaSuccess)
-    e = casc::launch_split_b(A_hi, A_lo, lda, k, n, w, pb, st, trans == CASC_OP_N);
+  cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, n, A_hi, A_lo, lda, n, k, w, pa, pb, st,
+                                        trans == CASC_OP_T, trans == CASC_OP_N);
   AlphaBeta abv;
   abv.ab = use_beta ? 2 : ((alpha_hi == 1.0 && alpha_lo == 0.0) ? 0 : 1);  // as casc_gemm_fp64x2_ex
   abv.ah = alpha_hi;
@@ -714,7 +718,7 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
                                             uplo == CASC_LOWER ? 1 : 2, ws_counter(ws, n, n, k))
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
-  g_launches = (r == CASC_OK) ? g_launches + 2 : 0;
+  g_launches = (r == CASC_OK) ? g_launches + 1 : 0;
   return r;
 }
 

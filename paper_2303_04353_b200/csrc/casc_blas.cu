@@ -9,6 +9,7 @@
 
 #include "casc_dd.cuh"
 #include "casc_layout.cuh"
+#include "casc_ptx.cuh"
 
 namespace casc {
 
@@ -38,24 +39,35 @@ __global__ void __launch_bounds__(256) scale_c_kernel(int64_t m, int64_t n, doub
 }
 
 // Split mode reduction (small problems, casc_gemm.cu item_coords): C := (0, 0)
-// (+) T_0 (+) T_1 (+) ... (+) T_{P-1} in panel order -- the same FP64x2 additions, in the
-// same order, as the fused kernel's per-panel accumulation -- flags := OR, then
-// the optional BLAS update.
+// (+) T_0 (+) T_1 ... (+) T_{P-1} in panel order -- the same FP64x2 additions,
+// in the same order, as the fused kernel's per-panel accumulation -- flags :=
+// OR, then the optional BLAS update.  The panel sums are tile-major (the fused
+// kernel's split-mode store): [q][tile mb*nblocks+nb][warp 0..7][element
+// 0..15][lane 0..31], so consecutive threads read consecutive doubles.
 __global__ void __launch_bounds__(256) split_reduce_kernel(
     int P, int64_t m, int64_t n, const double* __restrict__ t_hi,
     const double* __restrict__ t_lo, const uint8_t* __restrict__ fbuf,
     double* __restrict__ C_hi, double* __restrict__ C_lo, int64_t ldc,
     uint8_t* __restrict__ flags, int64_t ldf, int ab, double ah, double al, double bh, double bl) {
-  const int64_t mn = m * n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the GEMM's panel sums are complete
+  const int64_t nblocks = (n + TN - 1) / TN;
+  const int64_t tot = (m + TM - 1) / TM * nblocks * (TM * TN);  // padded elements per panel
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
        idx += (int64_t)gridDim.x * blockDim.x) {
+    // the fused kernel's fragment coordinates of this slot
+    const int64_t t = idx / (TM * TN);
+    const int r = (int)(idx - t * (TM * TN));
+    const int cw = r >> 9, e = (r >> 5) & 15, lane = r & 31;
+    const int ms = e >> 2, ns = (e >> 1) & 1, ii = e & 1, g = lane >> 2, c = lane & 3;
+    const int64_t i = (t / nblocks) * TM + (cw >> 2) * 32 + ms * 8 + g;
+    const int64_t j = (t % nblocks) * TN + (cw & 3) * 16 + ns * 8 + 2 * c + ii;
+    if (i >= m || j >= n) continue;
     double th = 0.0, tl = 0.0;  // C starts at (0, 0) (reading R10), as the fused kernel
     uint8_t fl = 0;
     for (int q = 0; q < P; ++q) {
-      dd_add(th, tl, t_hi[q * mn + idx], t_lo[q * mn + idx], th, tl);
-      fl |= fbuf[q * mn + idx];
+      dd_add(th, tl, t_hi[q * tot + idx], t_lo[q * tot + idx], th, tl);
+      fl |= fbuf[q * tot + idx];
     }
-    const int64_t i = idx / n, j = idx - (idx / n) * n;
     double* ch = C_hi + i * ldc + j;
     double* cl = C_lo + i * ldc + j;
     if (ab) apply_alpha_beta(th, tl, ah, al, bh, bl, ab == 2 ? *ch : 0.0, ab == 2 ? *cl : 0.0,
@@ -71,13 +83,12 @@ cudaError_t launch_split_reduce(int P, int64_t m, int64_t n, const double* t_hi,
                                 double* C_lo, int64_t ldc, uint8_t* flags, int64_t ldf, int ab,
                                 double ah, double al, double bh, double bl, int num_sms,
                                 cudaStream_t st) {
-  const int64_t mn = m * n;
-  if (mn == 0) return cudaSuccess;
-  int64_t blocks = (mn + 255) / 256;
+  const int64_t tot = (m + TM - 1) / TM * ((n + TN - 1) / TN) * (TM * TN);
+  if (m * n == 0) return cudaSuccess;
+  int64_t blocks = (tot + 255) / 256;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-  split_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(P, m, n, t_hi, t_lo, fbuf, C_hi, C_lo, ldc,
-                                                        flags, ldf, ab, ah, al, bh, bl);
-  return cudaGetLastError();
+  return launch_pdl(split_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0, st, P, m, n, t_hi,
+                    t_lo, fbuf, C_hi, C_lo, ldc, flags, ldf, ab, ah, al, bh, bl);
 }
 
 cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int use_beta,

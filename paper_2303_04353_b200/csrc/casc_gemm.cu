@@ -144,6 +144,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   // ring of per-panel scale exponents [EXP_RING][A 64 | B 64] int32, filled by TMA
   int32_t* sexp = reinterpret_cast<int32_t*>(smem + EXP_OFFSET);
 
+  // Programmatic dependent launch (PDL): the product launch lets its dependent
+  // (the WIDE re-run) be scheduled at once, so that re-run's launch latency
+  // hides in this grid's tail; the WIDE grid waits for this grid's completion
+  // and memory (griddepcontrol.wait) before reading the list.
+  if constexpr (WIDE) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (WIDE && *p.wide_count == 0) return;  // the common case: nothing to re-run
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -259,11 +265,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     // branch between the two scalings made ptxas spill in the k loop, -3%).
     bool wide_seen = false;
     // destination: C, or the panel-sum buffer T_q in split mode
-    double* dst_hi = split_p ? p.t_hi + (int64_t)q0 * p.m * p.n : p.C_hi;
-    double* dst_lo = split_p ? p.t_lo + (int64_t)q0 * p.m * p.n : p.C_lo;
-    const int64_t ldd = split_p ? p.n : p.ldc;
-    uint8_t* dst_fl = split_p ? p.fbuf + (int64_t)q0 * p.m * p.n : p.flags;
-    const int64_t ldfl = split_p ? p.n : p.ldf;
+    // Split mode writes the panel sums tile-major, [q][tile mb*nblocks+nb][warp][element
+    // 0..15][lane]: every warp store is 256 contiguous bytes (split_reduce_kernel
+    // reads the same layout)
+    const int64_t toff = SPLIT ? (((int64_t)q0 * p.mblocks + mb) * p.nblocks + nb) * (TM * TN) +
+                                     cw * 512 + lane
+                               : 0;
+    double* dst_hi = SPLIT ? p.t_hi + toff : p.C_hi;
+    double* dst_lo = SPLIT ? p.t_lo + toff : p.C_lo;
+    uint8_t* dst_fl = SPLIT ? p.fbuf + toff : p.flags;
     uint32_t flagbits = 0;
     for (int st = s0; st < s1; ++st, ++it) {
       if (st == s0 || (st % STAGES_PER_PANEL) == 0) {
@@ -397,13 +407,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
               if (last) {
                 const int64_t row = (int64_t)mb * TM + wm * 32 + ms * 8 + g;
                 const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
-                if (store_c && row < p.m && col < p.n && in_tri<TRI>(p, row, col)) {
+                if constexpr (SPLIT) {  // padded tile-major panel sums (reduced later)
+                  if (store_c) {
+                    dst_hi[(m2 * 4 + ns * 2 + i + h * 8) * 32] = th;
+                    dst_lo[(m2 * 4 + ns * 2 + i + h * 8) * 32] = tl;
+                  }
+                } else if (store_c && row < p.m && col < p.n && in_tri<TRI>(p, row, col)) {
                   if (AB && p.ab)
                     apply_alpha_beta(th, tl, p.alpha_hi, p.alpha_lo, p.beta_hi, p.beta_lo,
                                      p.ab == 2 ? p.C_hi[row * p.ldc + col] : 0.0,
                                      p.ab == 2 ? p.C_lo[row * p.ldc + col] : 0.0, p.ab == 2);
-                  dst_hi[row * ldd + col] = th;
-                  dst_lo[row * ldd + col] = tl;
+                  dst_hi[row * p.ldc + col] = th;
+                  dst_lo[row * p.ldc + col] = tl;
                 }
               } else {
                 cv[x] = __double2loint(th);
@@ -431,7 +446,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           for (int i = 0; i < 2; ++i) {
             const int64_t col = (int64_t)nb * TN + wn * 16 + ns * 8 + 2 * c + i;
             if (row < p.m && col < p.n && in_tri<TRI>(p, row, col))
-              dst_fl[row * ldfl + col] = (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
+              dst_fl[SPLIT ? (int64_t)(ms * 4 + ns * 2 + i) * 32 : row * p.ldf + col] =
+                  (flagbits >> (ms * 4 + ns * 2 + i)) & 1u;
           }
       }
     }
@@ -452,8 +468,12 @@ static cudaError_t launch_variant(GemmArgs& a, int grid, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
   if (e != cudaSuccess) return e;
-  casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
-  return cudaGetLastError();
+  if (!WIDE) {
+    casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
+    return cudaGetLastError();
+  }
+  return launch_pdl(casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE>, dim3(grid), dim3(GEMM_THREADS),
+                    GEMM_SMEM, st, a);
 }
 
 // the product launch, then the WIDE re-run of what it listed (exits at once

@@ -86,13 +86,13 @@ __device__ __forceinline__ int group_exponent(double mx, int g, int c, int kq) {
 
 // TRANS: A is given transposed (stored k x m, element (i, p) at A[p * lda + i]; BLAS op 'T')
 template <bool TRANS>
-__global__ void __launch_bounds__(256) split_a_kernel(
+__device__ __forceinline__ void split_a_body(
     const double* __restrict__ Ahi, const double* __restrict__ Alo, int64_t lda, int64_t m,
-    int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
-    int64_t nks) {
+    int64_t k, const SplitConsts& K, uint8_t* __restrict__ packed, int64_t blk_bytes,
+    int64_t exp_off, int64_t nks, int64_t rg) {
   const int t = threadIdx.x, lane = t & 31, kq = t >> 5;
   const int g = lane >> 2, c = lane & 3;
-  const int64_t rg = blockIdx.x;  // 8-row group
+  // rg: 8-row group
   const int64_t mb = rg >> 3;
   const int within = (int)(rg & 7), mw = within >> 2, ms = within & 3;
   const int64_t row = rg * 8 + g;
@@ -137,13 +137,13 @@ __global__ void __launch_bounds__(256) split_a_kernel(
 
 // TRANS: B is given transposed (stored n x k, element (p, j) at B[j * ldb + p])
 template <bool TRANS>
-__global__ void __launch_bounds__(256) split_b_kernel(
+__device__ __forceinline__ void split_b_body(
     const double* __restrict__ Bhi, const double* __restrict__ Blo, int64_t ldb, int64_t n,
-    int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
-    int64_t nks) {
+    int64_t k, const SplitConsts& K, uint8_t* __restrict__ packed, int64_t blk_bytes,
+    int64_t exp_off, int64_t nks, int64_t cg) {
   const int t = threadIdx.x, lane = t & 31, kq = t >> 5;
   const int g = lane >> 2, c = lane & 3;
-  const int64_t cg = blockIdx.x;  // 8-column group
+  // cg: 8-column group
   const int64_t nb = cg >> 3;
   const int within = (int)(cg & 7), nw = within >> 1, ns = within & 1;
   const int64_t col = cg * 8 + g;
@@ -189,6 +189,49 @@ __global__ void __launch_bounds__(256) split_b_kernel(
     int32_t* ex = reinterpret_cast<int32_t*>(blk + exp_off);
     ex[q * TN + nw * 16 + ns * 8 + g] = f;
   }
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256) split_a_kernel(
+    const double* __restrict__ Ahi, const double* __restrict__ Alo, int64_t lda, int64_t m,
+    int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
+    int64_t nks) {
+  split_a_body<TRANS>(Ahi, Alo, lda, m, k, K, packed, blk_bytes, exp_off, nks, blockIdx.x);
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256) split_b_kernel(
+    const double* __restrict__ Bhi, const double* __restrict__ Blo, int64_t ldb, int64_t n,
+    int64_t k, SplitConsts K, uint8_t* __restrict__ packed, int64_t blk_bytes, int64_t exp_off,
+    int64_t nks) {
+  split_b_body<TRANS>(Bhi, Blo, ldb, n, k, K, packed, blk_bytes, exp_off, nks, blockIdx.x);
+}
+
+// Both splits of one GEMM in ONE launch (the first ga row groups split A, the
+// rest B's column groups): one launch and one tail instead of two, which
+// matters for small problems.  Bitwise the two kernels above.
+struct SplitABArgs {
+  const double* Ahi;
+  const double* Alo;
+  int64_t lda, m;
+  uint8_t* pa;
+  int64_t a_blk, a_exp;
+  const double* Bhi;
+  const double* Blo;
+  int64_t ldb, n;
+  uint8_t* pb;
+  int64_t b_blk, b_exp;
+  int64_t k, nks, ga;
+  SplitConsts K;
+};
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) split_ab_kernel(const SplitABArgs a) {
+  if ((int64_t)blockIdx.x < a.ga)
+    split_a_body<TA>(a.Ahi, a.Alo, a.lda, a.m, a.k, a.K, a.pa, a.a_blk, a.a_exp, a.nks,
+                     blockIdx.x);
+  else
+    split_b_body<TB>(a.Bhi, a.Blo, a.ldb, a.n, a.k, a.K, a.pb, a.b_blk, a.b_exp, a.nks,
+                     blockIdx.x - a.ga);
 }
 
 // ------------------------------------------------------------ debug export
@@ -271,6 +314,23 @@ cudaError_t launch_split_b(const double* Bhi, const double* Blo, int64_t ldb, in
   kern<<<grid, 256, 0, st>>>(Bhi, Blo, ldb, n, k, make_consts(w),
                                        static_cast<uint8_t*>(packed), b_block_bytes(k),
                                        b_exp_offset(k), kpad_of(k) / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_ab(const double* Ahi, const double* Alo, int64_t lda, int64_t m,
+                            const double* Bhi, const double* Blo, int64_t ldb, int64_t n,
+                            int64_t k, Widths w, void* pa, void* pb, cudaStream_t st, bool ta,
+                            bool tb) {
+  const int64_t mpad = (m + TM - 1) / TM * TM, npad = (n + TN - 1) / TN * TN;
+  const int64_t P = panels_of(k);
+  if ((mpad == 0 && npad == 0) || P == 0) return cudaSuccess;
+  SplitABArgs a{Ahi, Alo, lda, m, static_cast<uint8_t*>(pa), a_block_bytes(k), a_exp_offset(k),
+                Bhi, Blo, ldb, n, static_cast<uint8_t*>(pb), b_block_bytes(k), b_exp_offset(k),
+                k, kpad_of(k) / 4, mpad / 8, make_consts(w)};
+  dim3 grid((unsigned)(mpad / 8 + npad / 8), (unsigned)P);
+  auto kern = ta ? (tb ? split_ab_kernel<true, true> : split_ab_kernel<true, false>)
+                 : (tb ? split_ab_kernel<false, true> : split_ab_kernel<false, false>);
+  kern<<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
