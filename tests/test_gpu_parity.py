@@ -728,3 +728,53 @@ def test_packed_column_block_bitwise(casc, kind, m, n, k, c0, c1):
                               np.ascontiguousarray(b[:, c0:c1]).view(np.uint8))
     assert np.all(np.isnan(g[0][:, :c0])) and np.all(np.isnan(g[0][:, c1:]))
     assert np.all(g[2][:, :c0] == 7) and np.all(g[2][:, c1:] == 7)
+
+
+# ------------------------------------------------------------------ full sizes, every entry / cfg3b
+def test_cfg1_all_entries_exact(casc, orc):
+    """cfg1 (1024^3) at full size through casc_gemm_fp64x2 (small-problem split
+    mode, the launch configuration bench.py's small-problem line times): EVERY
+    one of the 10^6 entries against the exact product (oracle/exact_fixed.py,
+    pinned to the superaccumulator) within the north-star bound, and every flag
+    equal to ORACLE-CASCADE's ("all 1M entries checked exactly")."""
+    from oracle import exact_fixed as EF
+    d = I.make_config(1)
+    C_hi, C_lo, flags = run(casc, d)
+    err, _ = EF.errors(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], C_hi, C_lo)
+    absab = (np.abs(d["A_hi"]) + np.abs(d["A_lo"])) @ (np.abs(d["B_hi"]) + np.abs(d["B_lo"]))
+    bound = orc.north_star_bound(1024, absab * (1 - 2.0 ** -40))  # |A||B| to ~1e-13
+    assert np.all(np.abs(err) <= bound)
+    _, _, o_fl = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    assert np.array_equal(flags, o_fl) and flags.sum() == 0
+
+
+def test_cfg3b_full_size(casc, orc):
+    """cfg3 variant b (in-panel pairing, reading R13) at FULL size 4096 x 4096 x
+    32768 on the FP64 path: every entry flagged (bin 0 cancels in every panel),
+    flags equal the oracle's on sampled rows, and sampled entries stay within
+    eq:cascerr of the exact product (the north-star bound is not the bound for
+    adversarial cancellation, reading R14; the flag is)."""
+    import torch
+    d = I.make_config(3, variant="b")
+    m, n, k = d["m"], d["n"], d["k"]
+    C_hi, C_lo, flags = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                              T(d["B_lo"]))
+    torch.cuda.synchronize()
+    C_hi, C_lo, flags = N(C_hi), N(C_lo), N(flags)
+    assert flags.all()
+    rows = [0, 2049]
+    o_hi, o_lo, o_fl = _sub_oracle(orc, d, rows, n - 64, n)
+    assert np.array_equal(flags[rows, n - 64:], o_fl)
+    rng = np.random.default_rng(33)
+    ii = np.concatenate([rng.integers(0, m, 40), [m - 1]])
+    jj = np.concatenate([rng.integers(0, n, 40), [n - 1]])
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii, jj, C_hi, C_lo)
+    c = orc.select_widths(k)
+    bound = np.zeros(ii.size)
+    for p0 in range(0, k, 256):
+        a = np.abs(d["A_hi"][ii, p0:p0 + 256])
+        b = np.abs(d["B_hi"][p0:p0 + 256, jj])
+        absab = np.einsum("tk,kt->t", a, b) * (1 + 2.0 ** -40)
+        bound += 2 * orc.cascerr_bound(256, absab, a.max(1), b.max(0), c) \
+            + (2 * 128 + 2) * 2.0 ** -104 * absab
+    assert np.all(np.abs(r["err"]) <= bound)

@@ -284,3 +284,27 @@ def test_blocked_trsm_vs_plain_substitution(orc, uplo, trans, unit, m, n):
     bad_lo = Xb[1].copy()
     bad_lo[m // 2] += 2.0 ** -80
     assert np.any(np.abs((Xb[0] - Xp[0]) + (bad_lo - Xp[1])) > 2.0 ** -92 * (np.abs(Xp[0]) + 2.0 ** -20))
+
+
+# ----------------------------------------------------------------- ORACLE-EXACT, fixed-point form
+@pytest.mark.parametrize("cfg,m,n,k", [(1, 40, 30, 300), (2, 50, 40, 513), (1, 64, 64, 1024),
+                                       (3, 16, 20, 1024), (0, 64, 64, 64)])
+def test_exact_fixed_equals_superaccumulator(orc, cfg, m, n, k):
+    """oracle/exact_fixed.py (exact digit GEMMs + integer assembly, used for the
+    all-entries cfg1 check) gives the same exact error (C - C*), rounded once,
+    as the superaccumulator (orc_exact_entries, itself pinned to Fractions) on
+    every entry, for the oracle's own C and for a perturbed C."""
+    from oracle import exact_fixed as EF
+    d = I.make_config(cfg, m=m, n=n, k=k, variant="b") if cfg == 3 else \
+        I.make_config(cfg, m=m, n=n, k=k)
+    C_hi, C_lo, _ = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    for Cl in (C_lo, C_lo + 2.0 ** -90 * C_hi):
+        err, absx = EF.errors(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], C_hi, Cl)
+        r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel(),
+                              C_hi, Cl)
+        assert np.array_equal(err.ravel(), r["err"])
+        assert np.array_equal(absx.ravel(), np.abs(r["ex_hi"]))  # |RN(C*)|
+    with pytest.raises(ValueError):
+        EF.exact_product(np.ones((2, 1025)), np.zeros((2, 1025)), np.ones((1025, 2)),
+                         np.zeros((1025, 2)))
