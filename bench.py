@@ -165,6 +165,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         "e2e": e2e,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
                      "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
+                     "frac_vs_measured_peaks_bf16x2": achieved / _bf16x2_peak(),
                      "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
                      if (mloc, n, k) == (16384, 16384, 16384) else None,
                      "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
@@ -248,6 +249,16 @@ def _gemm_ms(ph):
     if "gemm" in ph:
         return ph["gemm"]
     return ph.get("gemm_own_cols", 0.0) + ph.get("gemm_other_cols", 0.0)
+
+
+def _bf16x2_peak():
+    """MEASURED_PEAKS.json sustained bf16 x 2 (the guide's nominal int8:bf16
+    ratio), the driver-measured alternative denominator for the INT8 GEMM."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return 2.0 * json.load(f)["bf16_tflops_sustained"]
+    except Exception:
+        return float("nan")
 
 
 def load_ncu_traffic():
@@ -413,6 +424,8 @@ def main():
                     help="skip the NEXT-3 INT8-cascade measurement on the same workload")
     ap.add_argument("--no-next4", action="store_true",
                     help="skip the NEXT-4 SYRK / TRSM measurements (N = 1)")
+    ap.add_argument("--no-small", action="store_true",
+                    help="skip the small-problem lines (N = 1)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -701,7 +714,7 @@ def main():
 
     # ---- small problems (cfg1 among them), N = 1, with their own clock record
     small = None
-    if world == 1:
+    if world == 1 and not args.no_small:
         try:
             small = measure_small(casc, dev, peak_sus)
         except Exception as ex:  # reported, never silently replaced

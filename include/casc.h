@@ -314,6 +314,45 @@ int casc_trsm_fp64x2(int uplo, int trans, int diag, int64_t m, int64_t n,
                      double alpha_hi, double alpha_lo,
                      const double* A_hi, const double* A_lo, int64_t lda,
                      double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream);
+/* NEXT-4, more level-3 BLAS on the cascaded GEMM (DESIGN.md
+ * readings R28, R29).  side: CASC_LEFT / CASC_RIGHT. */
+typedef enum { CASC_LEFT = 0, CASC_RIGHT = 1 } casc_side;
+/* SYMM: C := alpha (x) A B (+) beta (x) C (side LEFT, A m x m) or
+ * C := alpha (x) B A (+) beta (x) C (side RIGHT, A n x n), A symmetric and only
+ * its `uplo` triangle read (lda >= max(1, dim A)); B, C m x n (ldb, ldc >=
+ * max(1, n)); flags m x n (ld n) or NULL.  The symmetric A is expanded from its
+ * triangle into a stream-ordered temporary, then casc_gemm_fp64x2_ex computes
+ * the product: bitwise casc_gemm_fp64x2_ex of the full symmetric matrix.
+ * alpha == 0: C := beta C, A and B not read.  Errors as casc_gemm_fp64x2_ex
+ * (also bad side / uplo). */
+int casc_symm_fp64x2(int side, int uplo, int64_t m, int64_t n,
+                     double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda,
+                     const double* B_hi, const double* B_lo, int64_t ldb,
+                     double beta_hi, double beta_lo,
+                     double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                     casc_stream_t stream);
+/* TRMM: B := alpha (x) op(A) B (side LEFT, A m x m) or B := alpha (x) B op(A)
+ * (side RIGHT, A n x n), A triangular (uplo; diag CASC_UNIT: diagonal taken as
+ * 1, not read), op(A) = A or A^T; B m x n overwritten.  The triangular A (other
+ * triangle zero) is expanded into a stream-ordered temporary and the product is
+ * casc_gemm_fp64x2_ex of it, written back into B: bitwise that GEMM's result.
+ * alpha == 0: B := 0, A not read.  CASC_ERR_INVALID for bad enums, B
+ * overlapping A. */
+int casc_trmm_fp64x2(int side, int uplo, int trans, int diag, int64_t m, int64_t n,
+                     double alpha_hi, double alpha_lo,
+                     const double* A_hi, const double* A_lo, int64_t lda,
+                     double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream);
+/* Right-side TRSM: solve X op(A) = alpha (x) B, A n x n triangular, B m x n
+ * (X overwrites B).  The blocked algorithm of casc_trsm_fp64x2 on column
+ * blocks: X_b = B_b op(Inv_b), then B_c := B_c - X_b op(A)_(b,c) for the
+ * blocks still to solve (super-blocks of 4 x 256 as the left side), every
+ * product a casc_gemm_fp64x2_ex (op(A) read transposed by its split kernels,
+ * no transposed copy of B).  Arguments and errors as casc_trsm_fp64x2. */
+int casc_trsm_fp64x2_right(int uplo, int trans, int diag, int64_t m, int64_t n,
+                           double alpha_hi, double alpha_lo,
+                           const double* A_hi, const double* A_lo, int64_t lda,
+                           double* B_hi, double* B_lo, int64_t ldb, casc_stream_t stream);
 /* Test / inspection export of the TRSM's first step: the inverses of the
  * 256 x 256 diagonal blocks of the triangular A, inv_hi / inv_lo =
  * [ceil(m/256)][256][256] row-major FP64x2 (zeros outside the triangle and

@@ -60,6 +60,53 @@ _pu8 = ctypes.POINTER(ctypes.c_uint8)
 _pint = ctypes.POINTER(ctypes.c_int)
 
 
+def _side(side):
+    return 0 if side in ("L", "l", 0) else 1
+
+
+def casc_symm(side, uplo, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, nthreads: int = 0):
+    """NEXT-4 SYMM (reading R28): C := alpha A B + beta C (side 'L') or alpha B A
+    + beta C ('R'), A symmetric from its `uplo` triangle.  Returns new
+    (C_hi, C_lo, flags)."""
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    C_hi, C_lo = _c64(C_hi).copy(), _c64(C_lo).copy()
+    m, n = C_hi.shape
+    flags = np.zeros((m, n), dtype=np.uint8)
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    lib().orc_casc_symm(_side(side), lo_, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                        max(A_hi.shape[1], 1), _p(B_hi), _p(B_lo), max(n, 1), beta[0], beta[1],
+                        _p(C_hi), _p(C_lo), max(n, 1), _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags
+
+
+def casc_trmm(side, uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", nthreads: int = 0):
+    """NEXT-4 TRMM (reading R28): B := alpha op(A) B ('L') or alpha B op(A)
+    ('R'), A triangular.  Returns new (B_hi, B_lo)."""
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
+    m, n = X_hi.shape
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    lib().orc_casc_trmm(_side(side), lo_, tr, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                        max(A_hi.shape[1], 1), _p(X_hi), _p(X_lo), max(n, 1), nthreads)
+    return X_hi, X_lo
+
+
+def casc_trsm_right(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", nthreads: int = 0):
+    """NEXT-4 right-side TRSM (reading R29): X op(A) = alpha B, A n x n
+    triangular, via the left TRSM on the transposes.  Returns new (X_hi, X_lo)."""
+    A_hi, A_lo = map(_c64, (A_hi, A_lo))
+    X_hi, X_lo = _c64(B_hi).copy(), _c64(B_lo).copy()
+    m, n = X_hi.shape
+    lo_ = 0 if uplo in ("L", "l", 0) else 1
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    dg = 1 if diag in ("U", "u", 1, True) else 0
+    lib().orc_casc_trsm_right(lo_, tr, dg, m, n, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                              max(n, 1), _p(X_hi), _p(X_lo), max(n, 1), nthreads)
+    return X_hi, X_lo
+
+
 def dd_trsm_plain(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N"):
     """Plain (unblocked) FP64x2 substitution for op(A) X = alpha B: the
     reference for the blocked casc_trsm (no shared block sizes)."""
@@ -100,6 +147,12 @@ def _setup(L):
     L.orc_trsm_diag_inv.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _pd, _pd, _i64, _pd, _pd]
     L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd,
                                 _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
+    L.orc_casc_symm.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
+                                _pd, _pd, _i64, _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
+    L.orc_casc_trmm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64,
+                                _i64, _d, _d, _pd, _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
+    L.orc_casc_trsm_right.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d,
+                                      _d, _pd, _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
     L.orc_dd_trsm_plain.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d,
                                     _d, _pd, _pd, _i64, _pd, _pd, _i64]
     L.orc_dd_gemm.argtypes = [_i64, _i64, _i64, _pd, _pd, _i64, _pd, _pd, _i64, _pd, _pd,

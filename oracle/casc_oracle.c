@@ -792,6 +792,98 @@ void orc_casc_trsm(int uplo, int trans, int diag, int64_t m, int64_t n, double a
 }
 
 /* ------------------------------------------------------------------------- */
+/* NEXT-4, more level-3 BLAS as GEMMs ("All Level-3 BLAS         */
+/* algorithms can be written in terms of GEMM"; R28, R29).          */
+/* orc_expand: the dense n x n matrix of a stored triangle (uplo 0 lower / 1  */
+/* upper): mode 0 symmetric (mirror), mode 1 triangular (other triangle 0;    */
+/* unit: diagonal (1, 0), not read).                                          */
+/* ------------------------------------------------------------------------- */
+static void orc_expand(int64_t n, int uplo, int mode, int unit, const double* Ahi,
+                       const double* Alo, int64_t lda, double* Fhi, double* Flo) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const int stored = uplo == 0 ? j <= i : j >= i;
+      double h = 0.0, l = 0.0;
+      if (mode == 1 && i == j && unit) {
+        h = 1.0;
+      } else if (stored) {
+        h = Ahi[i * lda + j];
+        l = Alo[i * lda + j];
+      } else if (mode == 0) {
+        h = Ahi[j * lda + i];
+        l = Alo[j * lda + i];
+      }
+      Fhi[i * n + j] = h;
+      Flo[i * n + j] = l;
+    }
+}
+
+/* SYMM: C := alpha A B + beta C (side 0) or alpha B A + beta C (side 1), A     */
+/* symmetric from its uplo triangle: the GEMM of the symmetric matrix.         */
+void orc_casc_symm(int side, int uplo, int64_t m, int64_t n, double ah, double al,
+                   const double* Ahi, const double* Alo, int64_t lda, const double* Bhi,
+                   const double* Blo, int64_t ldb, double bh, double bl, double* Chi, double* Clo,
+                   int64_t ldc, uint8_t* flags, int nthreads) {
+  const int64_t ka = side == 0 ? m : n;
+  double* F = (double*)malloc(sizeof(double) * 2 * (size_t)(ka * ka > 0 ? ka * ka : 1));
+  orc_expand(ka, uplo, 0, 0, Ahi, Alo, lda, F, F + ka * ka);
+  if (side == 0)
+    orc_casc_gemm_ex(0, 0, m, n, m, ah, al, F, F + ka * ka, ka, Bhi, Blo, ldb, bh, bl, Chi, Clo,
+                     ldc, flags, nthreads);
+  else
+    orc_casc_gemm_ex(0, 0, m, n, n, ah, al, Bhi, Blo, ldb, F, F + ka * ka, ka, bh, bl, Chi, Clo,
+                     ldc, flags, nthreads);
+  free(F);
+}
+
+/* TRMM: B := alpha op(A) B (side 0) or alpha B op(A) (side 1), A triangular:  */
+/* the GEMM of the triangular matrix (other triangle zero), into B.            */
+void orc_casc_trmm(int side, int uplo, int trans, int diag, int64_t m, int64_t n, double ah,
+                   double al, const double* Ahi, const double* Alo, int64_t lda, double* Bhi,
+                   double* Blo, int64_t ldb, int nthreads) {
+  const int64_t ka = side == 0 ? m : n;
+  double* F = (double*)malloc(sizeof(double) * 2 * (size_t)(ka * ka > 0 ? ka * ka : 1));
+  double* T = (double*)malloc(sizeof(double) * 2 * (size_t)(m * n > 0 ? m * n : 1));
+  orc_expand(ka, uplo, 1, diag, Ahi, Alo, lda, F, F + ka * ka);
+  if (side == 0)
+    orc_casc_gemm_ex(trans, 0, m, n, m, ah, al, F, F + ka * ka, ka, Bhi, Blo, ldb, 0.0, 0.0, T,
+                     T + m * n, n, NULL, nthreads);
+  else
+    orc_casc_gemm_ex(0, trans, m, n, n, ah, al, Bhi, Blo, ldb, F, F + ka * ka, ka, 0.0, 0.0, T,
+                     T + m * n, n, NULL, nthreads);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Bhi[i * ldb + j] = T[i * n + j];
+      Blo[i * ldb + j] = T[m * n + i * n + j];
+    }
+  free(F);
+  free(T);
+}
+
+/* Right-side TRSM: X op(A) = alpha B  <=>  op(A)^T X^T = alpha B^T: the left   */
+/* TRSM (orc_casc_trsm, reading R27) with the opposite transposition, on the   */
+/* transposed right-hand sides (a mathematical identity, not the GPU's         */
+/* column-block algorithm).                                                    */
+void orc_casc_trsm_right(int uplo, int trans, int diag, int64_t m, int64_t n, double ah,
+                         double al, const double* Ahi, const double* Alo, int64_t lda,
+                         double* Bhi, double* Blo, int64_t ldb, int nthreads) {
+  if (m == 0 || n == 0) return;
+  double* T = (double*)malloc(sizeof(double) * 2 * (size_t)(m * n));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      T[j * m + i] = Bhi[i * ldb + j];
+      T[m * n + j * m + i] = Blo[i * ldb + j];
+    }
+  orc_casc_trsm(uplo, !trans, diag, n, m, ah, al, Ahi, Alo, lda, T, T + m * n, m, nthreads);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Bhi[i * ldb + j] = T[j * m + i];
+      Blo[i * ldb + j] = T[m * n + j * m + i];
+    }
+  free(T);
+}
+
+/* ------------------------------------------------------------------------- */
 /* Plain FP64x2 triangular solve, the textbook column-by-column substitution  */
 /* with no blocking (the reference the blocked orc_casc_trsm is checked        */
 /* against, independently of its block sizes): op(A) X = alpha B, left side;  */

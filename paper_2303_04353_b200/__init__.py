@@ -76,7 +76,8 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_gemm_packed", "casc_i8_gemm_fp64x2_ex", "casc_gemm_fp64x2_host",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
             "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2",
-            "casc_debug_ldexp", "casc_gemm_packed_ld", "casc_i8_gemm_packed_ld"]
+            "casc_debug_ldexp", "casc_gemm_packed_ld", "casc_i8_gemm_packed_ld",
+            "casc_symm_fp64x2", "casc_trmm_fp64x2", "casc_trsm_fp64x2_right"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -160,6 +161,81 @@ def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", strea
     _check(_lib.casc_trsm_fp64x2(lo, tr, dg, m, n, float(ah), float(al), _ptr(A_hi), _ptr(A_lo),
                                  lda, _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)),
            "casc_trsm_fp64x2")
+    return B_hi, B_lo
+
+
+_sig("casc_symm_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double,
+                          ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
+                          ctypes.c_double, _vp, _vp, _i64, _vp, _vp])
+_sig("casc_trmm_fp64x2", [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64,
+                          ctypes.c_double, ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, _vp])
+_sig("casc_trsm_fp64x2_right", [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64,
+                                ctypes.c_double, ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64,
+                                _vp])
+CASC_LEFT, CASC_RIGHT = 0, 1
+
+
+def _side(side):
+    if side not in ("L", "l", "R", "r", 0, 1):
+        raise ValueError("side must be 'L' or 'R'")
+    return CASC_LEFT if side in ("L", "l", 0) else CASC_RIGHT
+
+
+def _dd(x):
+    return (float(x), 0.0) if isinstance(x, (int, float)) else (float(x[0]), float(x[1]))
+
+
+def casc_symm_fp64x2(side, uplo, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, flags=None,
+                     stream=None):
+    """SYMM on the cascaded GEMM (casc.h): C := alpha A B + beta C (side 'L') or
+    alpha B A + beta C ('R'), A symmetric, only its `uplo` triangle read; C
+    (m x n) updated in place.  A_hi None means alpha = 0 (A, B not read)."""
+    sd = _side(side)
+    lo, _ = _uplo_diag(uplo, "N")
+    ah, al = _dd(alpha)
+    bh, bl = _dd(beta)
+    m, n = C_hi.shape
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    lda = _ld_pair(A_hi, A_lo, "A") if A_hi is not None else 1
+    ldb = _ld_pair(B_hi, B_lo, "B") if B_hi is not None else max(n, 1)
+    if A_hi is None:
+        ah = al = 0.0
+    if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (m, n)
+                              or not flags.is_contiguous()):
+        raise TypeError("flags must be a contiguous (m, n) uint8 CUDA tensor")
+    _check(_lib.casc_symm_fp64x2(sd, lo, m, n, ah, al, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                 _ptr(B_lo), ldb, bh, bl, _ptr(C_hi), _ptr(C_lo), ldc, _ptr(flags),
+                                 _stream(stream)), "casc_symm_fp64x2")
+    return C_hi, C_lo, flags
+
+
+def casc_trmm_fp64x2(side, uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", stream=None):
+    """TRMM on the cascaded GEMM: B := alpha op(A) B ('L') or alpha B op(A) ('R'),
+    A triangular; B overwritten."""
+    sd = _side(side)
+    lo, dg = _uplo_diag(uplo, diag)
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = _dd(alpha)
+    m, n = B_hi.shape
+    _check(_lib.casc_trmm_fp64x2(sd, lo, tr, dg, m, n, ah, al, _ptr(A_hi), _ptr(A_lo),
+                                 _ld_pair(A_hi, A_lo, "A"), _ptr(B_hi), _ptr(B_lo),
+                                 _ld_pair(B_hi, B_lo, "B"), _stream(stream)), "casc_trmm_fp64x2")
+    return B_hi, B_lo
+
+
+def casc_trsm_fp64x2_right(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", stream=None):
+    """Right-side TRSM: solve X op(A) = alpha B (A n x n triangular, B m x n);
+    X overwrites B."""
+    lo, dg = _uplo_diag(uplo, diag)
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = _dd(alpha)
+    m, n = B_hi.shape
+    if tuple(A_hi.shape) != (n, n):
+        raise ValueError("A must be n x n")
+    _check(_lib.casc_trsm_fp64x2_right(lo, tr, dg, m, n, ah, al, _ptr(A_hi), _ptr(A_lo),
+                                       _ld_pair(A_hi, A_lo, "A"), _ptr(B_hi), _ptr(B_lo),
+                                       _ld_pair(B_hi, B_lo, "B"), _stream(stream)),
+           "casc_trsm_fp64x2_right")
     return B_hi, B_lo
 
 

@@ -40,6 +40,25 @@ def rel_errors(d, C_hi, C_lo):
     return rel.reshape(m, n), r
 
 
+def cascerr_total(d):
+    """eq:cascerr summed over the k panels, x2 for the dropped
+    higher-order terms, plus the FP64x2 rounding of each panel value and
+    accumulation step ((2P + 2) 2^-104 |A||B|): the paper's own forward-error
+    bound for the cascade, as a diagnostic next to the north-star bound."""
+    k = d["k"]
+    c = oracle.select_widths(k)
+    P = -(-k // 256)
+    tot = 0.0
+    with np.errstate(over="ignore", under="ignore"):
+        for p0 in range(0, k, 256):
+            a, b = np.abs(d["A_hi"][:, p0:p0 + 256]), np.abs(d["B_hi"][p0:p0 + 256])
+            absab = (a @ b) * (1 + 2.0 ** -40)
+            tot = tot + 2 * oracle.cascerr_bound(a.shape[1], absab, a.max(1)[:, None],
+                                                 b.max(0)[None, :], c) \
+                + (2 * P + 2) * 2.0 ** -104 * absab
+    return tot
+
+
 def run_case(d, casc, torch):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     g_hi, g_lo, fl = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]))
@@ -53,10 +72,14 @@ def run_case(d, casc, torch):
     rd, _ = rel_errors(d, o_hi, o_lo)
     bound = oracle.north_star_bound(d["k"], r["absab"]).reshape(rc.shape)
     abs_c = np.abs(r["err"]).reshape(rc.shape)
+    casc_b = cascerr_total(d)  # eq:cascerr diagnostic (SURVEY §8(c) amb. 14)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        cr = np.where(casc_b > 0, abs_c / casc_b, 0.0)
     return dict(max_rel_cascade=float(rc.max()), max_rel_dd=float(rd.max()),
                 median_rel_cascade=float(np.median(rc)), median_rel_dd=float(np.median(rd)),
                 ratio_max_dd_over_cascade=float(rd.max() / rc.max()) if rc.max() > 0 else None,
                 flags=int(fl.sum()), within_north_star_bound=bool(np.all(abs_c <= bound)),
+                max_err_over_cascerr=float(cr.max()), within_cascerr=bool(np.all(cr <= 1.0)),
                 frac_elements_cascade_better=float(np.mean(rc < rd)),
                 frac_elements_cascade_not_worse=float(np.mean(rc <= rd)),
                 max_rel_int8=float(ri.max()), median_rel_int8=float(np.median(ri)),
@@ -69,7 +92,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="32,64,128,240,256,384")
     ap.add_argument("--seeds", type=int, default=1)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "accuracy_r01.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "accuracy_r02.json"))
     args = ap.parse_args()
     import torch
 

@@ -20,7 +20,7 @@ CMD4="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD4 > gpurun_out/plain4_$TAG.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:casc_gemm -s 3 -c 1 -o gpurun_out/prof_gemm_$TAG $CMD4 > gpurun_out/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
 $CMD4 > gpurun_out/plain5_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:split -s 6 -c 2 -o gpurun_out/prof_split_$TAG $CMD4 > gpurun_out/ncu_split_$TAG.log 2>&1; echo "ncu split rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:split -s 3 -c 1 -o gpurun_out/prof_split_$TAG $CMD4 > gpurun_out/ncu_split_$TAG.log 2>&1; echo "ncu split rc=$?"
 $CMD4 > gpurun_out/plain6_$TAG.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:i8_gemm -s 3 -c 1 -o gpurun_out/prof_i8gemm_$TAG $CMD4 > gpurun_out/ncu_i8gemm_$TAG.log 2>&1; echo "ncu i8 gemm rc=$?"
 $CMD4 > gpurun_out/plain7_$TAG.log 2>&1 && \

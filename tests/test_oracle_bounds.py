@@ -308,3 +308,101 @@ def test_exact_fixed_equals_superaccumulator(orc, cfg, m, n, k):
     with pytest.raises(ValueError):
         EF.exact_product(np.ones((2, 1025)), np.zeros((2, 1025)), np.ones((1025, 2)),
                          np.zeros((1025, 2)))
+
+
+# ----------------------------------------------------------------- SYMM / TRMM / right TRSM (R28, R29)
+def _sym_expand(hi, lo, uplo):
+    tri = np.tril(np.ones(hi.shape, bool)) if uplo == "L" else np.triu(np.ones(hi.shape, bool))
+    return np.where(tri, hi, hi.T), np.where(tri, lo, lo.T)
+
+
+@pytest.mark.parametrize("side,uplo,m,n", [("L", "L", 40, 30), ("R", "U", 25, 300), ("L", "U", 260, 5)])
+def test_symm_oracle_exact(orc, side, uplo, m, n):
+    """SYMM (R28): the other triangle of A is never read (NaN there), and C is
+    within the north-star bound of the exact alpha A_sym B (alpha = 1, beta = 0);
+    alpha = 2^p, beta = 0 scales exactly; alpha = 0 gives beta C bitwise."""
+    ka = m if side == "L" else n
+    rng = np.random.default_rng(3)
+    d = I.make_config(1, m=ka, n=ka, k=ka, seed=41)
+    S_hi, S_lo = _sym_expand(d["A_hi"], d["A_lo"], uplo)
+    other = np.triu(np.ones((ka, ka), bool), 1) if uplo == "L" else np.tril(np.ones((ka, ka), bool), -1)
+    A_hi = np.where(other, np.nan, d["A_hi"])
+    A_lo = np.where(other, np.nan, d["A_lo"])
+    B = I.make_config(1, m=m, n=n, k=ka, seed=43)
+    B_hi, B_lo = (B["A_hi"], B["A_lo"]) if side == "L" else (B["A_hi"][:, :n], B["A_lo"][:, :n])
+    B_hi, B_lo = np.ascontiguousarray(B_hi[:m, :n]), np.ascontiguousarray(B_lo[:m, :n])
+    Z = np.zeros((m, n))
+    C_hi, C_lo, fl = orc.casc_symm(side, uplo, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, (0.0, 0.0), Z, Z)
+    assert np.all(np.isfinite(C_hi))
+    L = (S_hi, S_lo, B_hi, B_lo) if side == "L" else (B_hi, B_lo, S_hi, S_lo)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    r = orc.exact_entries(*L, ii.ravel(), jj.ravel(), C_hi, C_lo)
+    assert np.all(np.abs(r["err"]) <= orc.north_star_bound(ka, r["absab"]))
+    C2 = orc.casc_symm(side, uplo, (4.0, 0.0), A_hi, A_lo, B_hi, B_lo, (0.0, 0.0), Z, Z)
+    assert np.array_equal(C2[0], 4 * C_hi) and np.array_equal(C2[1], 4 * C_lo)
+    C0 = rng.uniform(-1, 1, (m, n))
+    C3 = orc.casc_symm(side, uplo, (0.0, 0.0), A_hi, A_lo, B_hi, B_lo, (0.5, 0.0), C0, Z)
+    assert np.array_equal(C3[0], 0.5 * C0)
+
+
+@pytest.mark.parametrize("side,uplo,trans,diag,m,n", [("L", "L", "N", "N", 40, 7),
+                                                      ("L", "U", "T", "U", 300, 3),
+                                                      ("R", "L", "T", "N", 6, 280),
+                                                      ("R", "U", "N", "U", 9, 50)])
+def test_trmm_oracle_exact(orc, side, uplo, trans, diag, m, n):
+    """TRMM (R28): only A's triangle is read (NaN elsewhere, and on the diagonal
+    when unit), and B := alpha op(A) B is within the north-star bound of the
+    exact product with the triangular matrix."""
+    ka = m if side == "L" else n
+    d = I.make_config(1, m=ka, n=ka, k=ka, seed=47)
+    tri = np.tril(np.ones((ka, ka), bool)) if uplo == "L" else np.triu(np.ones((ka, ka), bool))
+    T_hi = np.where(tri, d["A_hi"], 0.0)
+    T_lo = np.where(tri, d["A_lo"], 0.0)
+    A_hi = np.where(tri, d["A_hi"], np.nan)
+    A_lo = np.where(tri, d["A_lo"], np.nan)
+    if diag == "U":
+        np.fill_diagonal(T_hi, 1.0)
+        np.fill_diagonal(T_lo, 0.0)
+        np.fill_diagonal(A_hi, np.nan)
+        np.fill_diagonal(A_lo, np.nan)
+    if trans == "T":
+        T_hi, T_lo = T_hi.T.copy(), T_lo.T.copy()
+    B = I.make_config(1, m=m, n=n, k=n, seed=49)
+    B_hi, B_lo = B["A_hi"], B["A_lo"]
+    X_hi, X_lo = orc.casc_trmm(side, uplo, diag, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
+    assert np.all(np.isfinite(X_hi))
+    L = (T_hi, T_lo, B_hi, B_lo) if side == "L" else (B_hi, B_lo, T_hi, T_lo)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    r = orc.exact_entries(*L, ii.ravel(), jj.ravel(), X_hi, X_lo)
+    assert np.all(np.abs(r["err"]) <= orc.north_star_bound(ka, r["absab"]))
+
+
+@pytest.mark.parametrize("uplo,trans,unit,m,n", [("L", "N", False, 5, 40), ("U", "N", False, 3, 300),
+                                                 ("L", "T", True, 4, 600), ("U", "T", False, 2, 1100)])
+def test_trsm_right_oracle(orc, uplo, trans, unit, m, n):
+    """Right-side TRSM (R29): the exact residual X op(A) - B within 2^-96 |X||op(A)|
+    row by row (dyadic rationals), and agreement with the plain unblocked
+    substitution on the transposed system to 2^-92."""
+    A_hi, A_lo = _tri_dd(n, uplo, 17, unit)
+    rng = np.random.default_rng(19)
+    B_hi = rng.uniform(-1, 1, (m, n))
+    B_lo = B_hi * 2.0 ** -54 * rng.uniform(-1, 1, (m, n))
+    dg = "U" if unit else "N"
+    X_hi, X_lo = orc.casc_trsm_right(uplo, dg, (1.0, 0.0), A_hi, A_lo, B_hi, B_lo, trans=trans)
+    ftr = "N" if trans == "T" else "T"
+    P = orc.dd_trsm_plain(uplo, dg, (1.0, 0.0), A_hi, A_lo, B_hi.T.copy(), B_lo.T.copy(), trans=ftr)
+    diff = np.abs((X_hi - P[0].T) + (X_lo - P[1].T))
+    assert np.all(diff <= 2.0 ** -92 * (np.abs(X_hi) + 2.0 ** -20))
+    A = np.array([[fr(A_hi[i, j]) + fr(A_lo[i, j]) for j in range(n)] for i in range(n)], dtype=object) \
+        if n <= 300 else None
+    if A is not None:
+        if unit:
+            for i in range(n):
+                A[i, i] = F(1)
+        opA = A.T if trans == "T" else A
+        for i in range(m):
+            for j in range(0, n, max(1, n // 25)):
+                col = opA[:, j]
+                terms = [(fr(X_hi[i, l]) + fr(X_lo[i, l])) * col[l] for l in range(n) if col[l] != 0]
+                r = sum(terms) - (fr(B_hi[i, j]) + fr(B_lo[i, j]))
+                assert abs(r) <= F(2) ** -96 * sum(abs(t) for t in terms)
