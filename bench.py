@@ -262,7 +262,7 @@ def _bf16x2_peak():
 
 
 def load_ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    p = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
     try:
         with open(p) as f:
             return json.load(f)
@@ -701,12 +701,41 @@ def main():
                 X_lo.copy_(B_lo)
                 casc.casc_trsm_fp64x2("L", "N", 1.0, Lt, Lt_lo, X_hi, X_lo)
             t_trsm = ev_time(trsm)
+            # round 2: SYMM (A's lower triangle as the symmetric matrix), TRMM and
+            # the right-side TRSM with the same operands
+            G_hi = torch.zeros((m, n), dtype=torch.float64, device=dev)
+            G_lo = torch.zeros_like(G_hi)
+            t_symm = ev_time(lambda: casc.casc_symm_fp64x2("L", "L", 1.0, A_hi[:, :m], A_lo[:, :m],
+                                                           B_hi, B_lo, 0.0, G_hi, G_lo), reps=1)
+
+            def trmm():
+                X_hi.copy_(B_hi)
+                X_lo.copy_(B_lo)
+                casc.casc_trmm_fp64x2("L", "L", "N", 1.0, Lt, Lt_lo, X_hi, X_lo)
+            t_trmm = ev_time(trmm, reps=1)
+
+            def trsm_r():
+                X_hi.copy_(B_hi)
+                X_lo.copy_(B_lo)
+                casc.casc_trsm_fp64x2_right("L", "N", 1.0, Lt, Lt_lo, X_hi, X_lo, trans="T")
+            t_trsm_r = ev_time(trsm_r, reps=1)
+            del G_hi, G_lo
             next4 = {
                 "syrk": {"op": "C := A A^T (lower triangle), m x k = %d x %d" % (m, k),
                          "ms": t_syrk, "gflops_n2k": m * m * k / (t_syrk * 1e-3) / 1e9},
                 "i8_syrk": {"ms": t_syrk8, "gflops_n2k": m * m * k / (t_syrk8 * 1e-3) / 1e9},
                 "trsm": {"op": "L X = B, L %d x %d lower, B %d x %d" % (m, m, m, n),
-                         "ms": t_trsm, "gflops_m2n": m * m * n / (t_trsm * 1e-3) / 1e9}}
+                         "ms": t_trsm, "gflops_m2n": m * m * n / (t_trsm * 1e-3) / 1e9},
+                "symm": {"op": "C := A B, A %d x %d symmetric (lower stored), B %d x %d"
+                               % (m, m, m, n),
+                         "ms": t_symm, "gflops_2m2n": 2 * m * m * n / (t_symm * 1e-3) / 1e9},
+                "trmm": {"op": "B := L B, L %d x %d lower" % (m, m),
+                         "ms": t_trmm, "gflops_m2n": m * m * n / (t_trmm * 1e-3) / 1e9,
+                         "note": "the GEMM of the expanded triangle: 2m^2n flops of work for "
+                                 "the m^2n of the convention"},
+                "trsm_right": {"op": "X L^T = B, L %d x %d lower, B %d x %d" % (m, m, m, n),
+                               "ms": t_trsm_r,
+                               "gflops_mn2": m * n * n / (t_trsm_r * 1e-3) / 1e9}}
             del S_hi, S_lo, Lt, Lt_lo, X_hi, X_lo
             torch.cuda.empty_cache()
         except Exception as ex:  # reported, never silently replaced

@@ -253,7 +253,10 @@ int casc_trsm_fp64x2_right(int uplo, int trans, int diag, int64_t m, int64_t n, 
     return CASC_OK;
   }
   const int64_t nblk = (n + NB - 1) / NB;
-  const size_t inv_elems = (size_t)nblk * NB * NB, t_elems = (size_t)m * NB;
+  // T: the current super-block's X (m x SB*NB, ld SB*NB), the A operand of the
+  // updates (a column block of B itself would overlap the updated columns' rows)
+  const int64_t ldt = SB * NB;
+  const size_t inv_elems = (size_t)nblk * NB * NB, t_elems = (size_t)m * ldt;
   double* buf = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&buf), (2 * inv_elems + 2 * t_elems) * 8, st) !=
       cudaSuccess)
@@ -265,39 +268,42 @@ int casc_trsm_fp64x2_right(int uplo, int trans, int diag, int64_t m, int64_t n, 
   r = st3(casc::launch_trsm_diag_inv(uplo, diag, n, A_hi, A_lo, lda, inv_hi, inv_lo, st));
   ++launches;
   const bool eff_upper = (uplo == CASC_UPPER) != (trans == CASC_OP_T);  // op(A) upper
-  // B_c -= X_b op(A)_(rows R, cols Cc): X block = columns [K0, K1) of B
-  auto update = [&](int64_t K0, int64_t K1, int64_t C0, int64_t C1) {
+  // B_c -= X_K op(A)_(K, C): X_K = columns [K0, K1) of the solved super-block
+  // starting at column S (held in T)
+  auto update = [&](int64_t S, int64_t K0, int64_t K1, int64_t C0, int64_t C1) {
     if (r != CASC_OK || K1 <= K0 || C1 <= C0) return;
     // op(A)_(K, C) = A[K rows, C cols] (N) or A[C rows, K cols]^T (T)
     const int64_t off = trans == CASC_OP_N ? K0 * lda + C0 : C0 * lda + K0;
-    r = casc_gemm_fp64x2_ex(CASC_OP_N, trans, m, C1 - C0, K1 - K0, -1.0, 0.0, B_hi + K0,
-                            B_lo + K0, ldb, A_hi + off, A_lo + off, lda, 1.0, 0.0, B_hi + C0,
-                            B_lo + C0, ldb, nullptr, nullptr, 0, stream);
+    r = casc_gemm_fp64x2_ex(CASC_OP_N, trans, m, C1 - C0, K1 - K0, -1.0, 0.0, t_hi + (K0 - S),
+                            t_lo + (K0 - S), ldt, A_hi + off, A_lo + off, lda, 1.0, 0.0,
+                            B_hi + C0, B_lo + C0, ldb, nullptr, nullptr, 0, stream);
     launches += casc_last_launch_count();
   };
   for (int64_t s = 0; s < nblk && r == CASC_OK; ++s) {
     const int64_t b = eff_upper ? s : nblk - 1 - s;
     const int64_t c0 = b * NB, nb = std::min(NB, n - c0), c1 = c0 + nb;
-    // X_b = B_b op(Inv_b), into T (m x nb) and back into B's columns
+    const int64_t S0 = (b / SB) * SB * NB, S1 = std::min(S0 + SB * NB, n);
+    // X_b = B_b op(Inv_b), into T's columns of block b and back into B's
+    double* xh = t_hi + (c0 - S0);
+    double* xl = t_lo + (c0 - S0);
     r = casc_gemm_fp64x2_ex(CASC_OP_N, trans, m, nb, nb, 1.0, 0.0, B_hi + c0, B_lo + c0, ldb,
-                            inv_hi + b * NB * NB, inv_lo + b * NB * NB, NB, 0.0, 0.0, t_hi, t_lo,
-                            nb, nullptr, nullptr, 0, stream);
+                            inv_hi + b * NB * NB, inv_lo + b * NB * NB, NB, 0.0, 0.0, xh, xl,
+                            ldt, nullptr, nullptr, 0, stream);
     launches += casc_last_launch_count();
     if (r) break;
-    if (cudaMemcpy2DAsync(B_hi + c0, ldb * 8, t_hi, nb * 8, nb * 8, m, cudaMemcpyDeviceToDevice,
+    if (cudaMemcpy2DAsync(B_hi + c0, ldb * 8, xh, ldt * 8, nb * 8, m, cudaMemcpyDeviceToDevice,
                           st) != cudaSuccess ||
-        cudaMemcpy2DAsync(B_lo + c0, ldb * 8, t_lo, nb * 8, nb * 8, m, cudaMemcpyDeviceToDevice,
+        cudaMemcpy2DAsync(B_lo + c0, ldb * 8, xl, ldt * 8, nb * 8, m, cudaMemcpyDeviceToDevice,
                           st) != cudaSuccess) {
       r = CASC_ERR_CUDA;
       break;
     }
-    const int64_t S0 = (b / SB) * SB * NB, S1 = std::min(S0 + SB * NB, n);
     if (eff_upper) {
-      update(c0, c1, c1, S1);                 // the super-block's remaining columns
-      if (c1 == S1) update(S0, S1, S1, n);    // then the trailing columns, k = the super-block
+      update(S0, c0, c1, c1, S1);              // the super-block's remaining columns
+      if (c1 == S1) update(S0, S0, S1, S1, n); // then the trailing columns, k = the super-block
     } else {
-      update(c0, c1, S0, c0);
-      if (c0 == S0) update(S0, S1, 0, S0);
+      update(S0, c0, c1, S0, c0);
+      if (c0 == S0) update(S0, S0, S1, 0, S0);
     }
   }
   cudaFreeAsync(buf, st);

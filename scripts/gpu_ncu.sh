@@ -9,6 +9,6 @@ $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
 CMD4="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-next4 --no-small"
 $CMD4 > gpurun_out/plain4_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:casc_gemm_kernel<0, 0, 0, 0, 0>" -s 3 -c 1 -o gpurun_out/prof_gemm_$TAG $CMD4 > gpurun_out/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:split_ab -s 3 -c 1 -o gpurun_out/prof_split_$TAG $CMD4 > gpurun_out/ncu_split_$TAG.log 2>&1; echo "ncu split rc=$?"
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:i8_gemm_kernel<0, 0, 0>" -s 3 -c 1 -o gpurun_out/prof_i8gemm_$TAG $CMD4 > gpurun_out/ncu_i8gemm_$TAG.log 2>&1; echo "ncu i8 gemm rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:casc_gemm_kernel -s 6 -c 1 -o gpurun_out/prof_gemm_$TAG $CMD4 > gpurun_out/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:split -s 6 -c 2 -o gpurun_out/prof_split_$TAG $CMD4 > gpurun_out/ncu_split_$TAG.log 2>&1; echo "ncu split rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:i8_gemm -s 3 -c 1 -o gpurun_out/prof_i8gemm_$TAG $CMD4 > gpurun_out/ncu_i8gemm_$TAG.log 2>&1; echo "ncu i8 gemm rc=$?"
