@@ -296,6 +296,22 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k,
                      uint8_t* flags, void* workspace, size_t workspace_bytes,
                      casc_stream_t stream);
 
+/* NEXT-4, SYR2K on the cascaded GEMM (reading R30): on the uplo
+ * triangle, C := alpha (x) op(A) op(B)^T (+) beta (x) C, then
+ * C := alpha (x) op(B) op(A)^T (+) C (two triangular launches of the fused
+ * kernel, each half the tiles of a GEMM; the R21 update sequence, the second
+ * with beta = 1); flags (n x n, ld n, nullable) = OR of the two products'
+ * flags.  A and B are stored n x k (trans CASC_OP_N, lda / ldb >= max(1,k))
+ * or k x n (CASC_OP_T).  k == 0 / alpha == 0: C := beta C on the triangle.
+ * Stream-ordered temporary workspace; errors as casc_syrk_fp64x2. */
+int casc_syr2k_fp64x2(int uplo, int trans, int64_t n, int64_t k,
+                      double alpha_hi, double alpha_lo,
+                      const double* A_hi, const double* A_lo, int64_t lda,
+                      const double* B_hi, const double* B_lo, int64_t ldb,
+                      double beta_hi, double beta_lo,
+                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                      casc_stream_t stream);
+
 /* NEXT-4, TRSM on the cascaded GEMM (reading R27):
  * left side: solve op(A) X = alpha (x) B for X, op(A) = A (trans CASC_OP_N) or
  * A^T (CASC_OP_T), A m x m triangular (uplo CASC_LOWER / CASC_UPPER; diag

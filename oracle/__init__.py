@@ -147,6 +147,8 @@ def _setup(L):
     L.orc_trsm_diag_inv.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _pd, _pd, _i64, _pd, _pd]
     L.orc_casc_trsm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd,
                                 _pd, _i64, _pd, _pd, _i64, ctypes.c_int]
+    L.orc_casc_syr2k.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
+                                 _pd, _pd, _i64, _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
     L.orc_casc_symm.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _i64, _d, _d, _pd, _pd, _i64,
                                 _pd, _pd, _i64, _d, _d, _pd, _pd, _i64, _pu8, ctypes.c_int]
     L.orc_casc_trmm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64,
@@ -344,6 +346,25 @@ def casc_syrk(uplo, trans, alpha, A_hi, A_lo, beta, C_hi, C_lo, flags=None, nthr
     lib().orc_casc_syrk(lo, tr, n, k, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
                         A_hi.shape[1] if A_hi.size else 1, beta[0], beta[1], _p(C_hi), _p(C_lo),
                         n, _p(flags, _pu8), nthreads)
+    return C_hi, C_lo, flags
+
+
+def casc_syr2k(uplo, trans, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, flags=None,
+               nthreads: int = 0):
+    """NEXT-4 SYR2K (reading R30): on the `uplo` triangle C := alpha op(A)
+    op(B)^T + beta C, then C := alpha op(B) op(A)^T + C (cascaded GEMMs, R21);
+    flags = OR of both.  A, B stored n x k ('N') or k x n ('T')."""
+    lo = 0 if uplo in ("L", "l", 0) else 1
+    tr = int(trans in ("T", "t", 1, True))
+    A_hi, A_lo, B_hi, B_lo = map(_c64, (A_hi, A_lo, B_hi, B_lo))
+    C_hi, C_lo = _c64(C_hi).copy(), _c64(C_lo).copy()
+    n = C_hi.shape[0]
+    k = A_hi.shape[0] if tr else A_hi.shape[1]
+    flags = np.zeros((n, n), dtype=np.uint8) if flags is None else np.array(flags, np.uint8)
+    lib().orc_casc_syr2k(lo, tr, n, k, alpha[0], alpha[1], _p(A_hi), _p(A_lo),
+                         A_hi.shape[1] if A_hi.size else 1, _p(B_hi), _p(B_lo),
+                         B_hi.shape[1] if B_hi.size else 1, beta[0], beta[1], _p(C_hi), _p(C_lo),
+                         n, _p(flags, _pu8), nthreads)
     return C_hi, C_lo, flags
 
 

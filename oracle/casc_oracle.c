@@ -645,6 +645,40 @@ void orc_casc_syrk(int uplo, int trans, int64_t n, int64_t k, double ah, double 
   free(Tf);
 }
 
+/* SYR2K (NEXT-4, reading R30): on one triangle,                              */
+/*   C := alpha op(A) op(B)^T (+) beta C,  then  C := alpha op(B) op(A)^T (+) C, */
+/* each the cascaded GEMM with the R21 update (the second with beta = 1);     */
+/* flags = OR of the two products' flags.                                     */
+void orc_casc_syr2k(int uplo, int trans, int64_t n, int64_t k, double ah, double al,
+                    const double* Ahi, const double* Alo, int64_t lda, const double* Bhi,
+                    const double* Blo, int64_t ldb, double bh, double bl, double* Chi,
+                    double* Clo, int64_t ldc, uint8_t* flags, int nthreads) {
+  double* Th = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  double* Tl = (double*)malloc(sizeof(double) * (size_t)(n * n + 1));
+  uint8_t* F1 = (uint8_t*)calloc((size_t)(n * n + 1), 1);
+  uint8_t* F2 = (uint8_t*)calloc((size_t)(n * n + 1), 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      Th[i * n + j] = Chi[i * ldc + j];
+      Tl[i * n + j] = Clo[i * ldc + j];
+    }
+  orc_casc_gemm_ex(trans, !trans, n, n, k, ah, al, Ahi, Alo, lda, Bhi, Blo, ldb, bh, bl, Th, Tl, n,
+                   F1, nthreads);
+  orc_casc_gemm_ex(trans, !trans, n, n, k, ah, al, Bhi, Blo, ldb, Ahi, Alo, lda, 1.0, 0.0, Th, Tl,
+                   n, F2, nthreads);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      if (uplo == 0 ? j > i : j < i) continue;
+      Chi[i * ldc + j] = Th[i * n + j];
+      Clo[i * ldc + j] = Tl[i * n + j];
+      if (flags) flags[i * n + j] = F1[i * n + j] | F2[i * n + j];
+    }
+  free(Th);
+  free(Tl);
+  free(F1);
+  free(F2);
+}
+
 /* ------------------------------------------------------------------------- */
 /* NEXT-4, level-3 BLAS on the cascaded GEMM ("All Level-3 BLAS */
 /* algorithms can be written in terms of GEMM ... integrating Phase 1 into    */

@@ -77,7 +77,8 @@ EXPORTED = ["casc_status_string", "casc_select_widths", "casc_gemm_fp64x2",
             "casc_i8_gemm_fp64x2_host", "casc_syrk_fp64x2", "casc_trsm_fp64x2",
             "casc_trsm_diag_inv", "casc_i8_syrk_fp64x2", "casc_i8_trsm_fp64x2",
             "casc_debug_ldexp", "casc_gemm_packed_ld", "casc_i8_gemm_packed_ld",
-            "casc_symm_fp64x2", "casc_trmm_fp64x2", "casc_trsm_fp64x2_right"]
+            "casc_symm_fp64x2", "casc_trmm_fp64x2", "casc_trsm_fp64x2_right",
+            "casc_syr2k_fp64x2"]
 
 _sig("casc_i8_gemm_fp64x2", [_i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                              _vp, ctypes.c_int, _vp])
@@ -162,6 +163,40 @@ def casc_trsm_fp64x2(uplo, diag, alpha, A_hi, A_lo, B_hi, B_lo, trans="N", strea
                                  lda, _ptr(B_hi), _ptr(B_lo), ldb, _stream(stream)),
            "casc_trsm_fp64x2")
     return B_hi, B_lo
+
+
+_sig("casc_syr2k_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double,
+                           ctypes.c_double, _vp, _vp, _i64, _vp, _vp, _i64, ctypes.c_double,
+                           ctypes.c_double, _vp, _vp, _i64, _vp, _vp])
+
+
+def casc_syr2k_fp64x2(uplo, trans, alpha, A_hi, A_lo, B_hi, B_lo, beta, C_hi, C_lo, flags=None,
+                      stream=None):
+    """SYR2K on the cascaded GEMM (casc.h, reading R30): on the 'L' / 'U'
+    triangle of the n x n C, C := alpha op(A) op(B)^T + alpha op(B) op(A)^T +
+    beta C.  A, B stored n x k ('N') or k x n ('T'); A_hi None means k = 0."""
+    lo = CASC_LOWER if uplo in ("L", "l", 0) else CASC_UPPER
+    if uplo not in ("L", "l", "U", "u", 0, 1):
+        raise ValueError("uplo must be 'L' or 'U'")
+    tr = 1 if trans in ("T", "t", 1, True) else 0
+    ah, al = _dd(alpha)
+    bh, bl = _dd(beta)
+    n = C_hi.shape[0]
+    ldc = _ld_pair(C_hi, C_lo, "C")
+    if A_hi is None:
+        lda = ldb = 1
+        k = 0
+    else:
+        lda = _ld_pair(A_hi, A_lo, "A")
+        ldb = _ld_pair(B_hi, B_lo, "B")
+        k = A_hi.shape[0] if tr else A_hi.shape[1]
+    if flags is not None and (flags.dtype != torch.uint8 or tuple(flags.shape) != (n, n)
+                              or not flags.is_contiguous()):
+        raise TypeError("flags must be a contiguous (n, n) uint8 CUDA tensor")
+    _check(_lib.casc_syr2k_fp64x2(lo, tr, n, k, ah, al, _ptr(A_hi), _ptr(A_lo), lda, _ptr(B_hi),
+                                  _ptr(B_lo), ldb, bh, bl, _ptr(C_hi), _ptr(C_lo), ldc,
+                                  _ptr(flags), _stream(stream)), "casc_syr2k_fp64x2")
+    return C_hi, C_lo, flags
 
 
 _sig("casc_symm_fp64x2", [ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_double,

@@ -27,6 +27,8 @@ cudaError_t launch_scale_c_uplo(int64_t m, int64_t n, double bh, double bl, int 
                                 int num_sms, int uplo, cudaStream_t st);
 cudaError_t launch_ldexp(int64_t count, const double* x, const int32_t* n, double* out,
                          cudaStream_t st);
+cudaError_t launch_or_flags(int64_t n, int uplo, uint8_t* flags, const uint8_t* f2, int num_sms,
+                            cudaStream_t st);
 cudaError_t launch_scale_c(int64_t m, int64_t n, double bh, double bl, int use_beta, double* C_hi,
                            double* C_lo, int64_t ldc, uint8_t* flags, int num_sms,
                            cudaStream_t st);
@@ -719,6 +721,98 @@ int casc_syrk_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi,
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 1 : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------- SYR2K (NEXT-4)
+// C := alpha op(A) op(B)^T + alpha op(B) op(A)^T + beta C on one triangle
+// (reading R30): two triangular launches of the fused kernel (half the tiles
+// each), the second with beta = 1 on the first's result; flags ORed.
+int casc_syr2k_fp64x2(int uplo, int trans, int64_t n, int64_t k, double alpha_hi, double alpha_lo,
+                      const double* A_hi, const double* A_lo, int64_t lda, const double* B_hi,
+                      const double* B_lo, int64_t ldb, double beta_hi, double beta_lo,
+                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags,
+                      casc_stream_t stream) {
+  g_launches = 0;
+  if ((uplo != CASC_LOWER && uplo != CASC_UPPER) || (trans != CASC_OP_N && trans != CASC_OP_T))
+    return CASC_ERR_INVALID;
+  if (n < 0 || k < 0) return CASC_ERR_INVALID;
+  const int64_t ar = trans ? k : n, ac = trans ? n : k;  // A, B as stored
+  const bool no_product = (k == 0) || (alpha_hi == 0.0 && alpha_lo == 0.0);
+  int r;
+  if (!no_product &&
+      ((r = check_mat(A_hi, ar, ac, lda)) || (r = check_mat(A_lo, ar, ac, lda)) ||
+       (r = check_mat(B_hi, ar, ac, ldb)) || (r = check_mat(B_lo, ar, ac, ldb))))
+    return r;
+  if ((r = check_mat(C_hi, n, n, ldc)) || (r = check_mat(C_lo, n, n, ldc))) return r;
+  if (!no_product) {
+    const void* ins[4] = {A_hi, A_lo, B_hi, B_lo};
+    const size_t ine[4] = {extent(ar, ac, lda), extent(ar, ac, lda), extent(ar, ac, ldb),
+                           extent(ar, ac, ldb)};
+    void* outs[3] = {C_hi, C_lo, flags};
+    const size_t oute[3] = {extent(n, n, ldc), extent(n, n, ldc), flags ? (size_t)(n * n) : 0};
+    for (int o = 0; o < 3; ++o)
+      for (int i = 0; i < 4; ++i)
+        if (ranges_overlap(outs[o], oute[o], ins[i], ine[i])) return CASC_ERR_INVALID;
+  }
+  if (n == 0) return CASC_OK;
+  int sms = 0;
+  if ((r = device_check(&sms))) return r;
+  const cudaStream_t st = S(stream);
+  const bool use_beta = !(beta_hi == 0.0 && beta_lo == 0.0);
+  if (no_product) {
+    cudaError_t e = casc::launch_scale_c_uplo(n, n, beta_hi, beta_lo, use_beta, C_hi, C_lo, ldc,
+                                              flags, sms, uplo == CASC_LOWER ? 0 : 1, st);
+    if (e == cudaSuccess) g_launches = 1;
+    return cuda_status(e);
+  }
+  const size_t need = casc_workspace_bytes(n, n, k);
+  const size_t fbytes = flags ? (size_t)(n * n + 255) / 256 * 256 : 0;
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, need + fbytes, st) != cudaSuccess) return CASC_ERR_CUDA;
+  uint8_t* pa = static_cast<uint8_t*>(ws);
+  uint8_t* pb = pa + (casc_packed_a_bytes(n, k) + 255) / 256 * 256;
+  uint8_t* f2 = flags ? static_cast<uint8_t*>(ws) + need : nullptr;
+  const casc::Widths w = widths_for(k);
+  const int nst = (int)(casc::kpad_of(k) / casc::BK);
+  const int tri = uplo == CASC_LOWER ? 1 : 2;
+  int launches = 0;
+  // 1) C := alpha op(A) op(B)^T (+) beta C on the triangle
+  cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, n, B_hi, B_lo, ldb, n, k, w, pa, pb, st,
+                                        trans == CASC_OP_T, trans == CASC_OP_N);
+  AlphaBeta abv;
+  abv.ab = use_beta ? 2 : ((alpha_hi == 1.0 && alpha_lo == 0.0) ? 0 : 1);
+  abv.ah = alpha_hi;
+  abv.al = alpha_lo;
+  abv.bh = beta_hi;
+  abv.bl = beta_lo;
+  g_launches = 0;
+  r = (e == cudaSuccess) ? gemm_packed_impl(n, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
+                                            nst, nullptr, abv, nullptr, tri,
+                                            ws_counter(ws, n, n, k))
+                         : CASC_ERR_CUDA;
+  launches += 1 + g_launches;
+  // 2) C := alpha op(B) op(A)^T (+) C, flags of this product into f2
+  if (r == CASC_OK) {
+    e = casc::launch_split_ab(B_hi, B_lo, ldb, n, A_hi, A_lo, lda, n, k, w, pa, pb, st,
+                              trans == CASC_OP_T, trans == CASC_OP_N);
+    AlphaBeta ab2 = abv;
+    ab2.ab = 2;
+    ab2.bh = 1.0;
+    ab2.bl = 0.0;
+    g_launches = 0;
+    r = (e == cudaSuccess) ? gemm_packed_impl(n, n, k, pa, pb, C_hi, C_lo, ldc, f2, sms, st, 0,
+                                              nst, nullptr, ab2, nullptr, tri,
+                                              ws_counter(ws, n, n, k))
+                           : CASC_ERR_CUDA;
+    launches += 1 + g_launches;
+  }
+  if (r == CASC_OK && flags) {
+    r = cuda_status(casc::launch_or_flags(n, uplo == CASC_LOWER ? 0 : 1, flags, f2, sms, st));
+    ++launches;
+  }
+  cudaFreeAsync(ws, st);
+  g_launches = r == CASC_OK ? launches : 0;
   return r;
 }
 

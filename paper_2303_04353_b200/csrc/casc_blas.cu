@@ -169,6 +169,25 @@ cudaError_t launch_trsm_diag_inv(int uplo, int diag, int64_t m, const double* A_
   return cudaGetLastError();
 }
 
+// flags |= f2 on one triangle of an n x n flag matrix (SYR2K, reading R30)
+__global__ void __launch_bounds__(256) or_flags_kernel(int64_t n, int uplo,
+                                                       uint8_t* __restrict__ flags,
+                                                       const uint8_t* __restrict__ f2) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / n, j = idx - (idx / n) * n;
+    if (uplo == 0 ? j <= i : j >= i) flags[idx] |= f2[idx];
+  }
+}
+
+cudaError_t launch_or_flags(int64_t n, int uplo, uint8_t* flags, const uint8_t* f2, int num_sms,
+                            cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n * n + 255) / 256, (int64_t)num_sms * 8);
+  or_flags_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, uplo, flags, f2);
+  return cudaGetLastError();
+}
+
 // Test export of the exact power-of-two scaling (casc_debug_ldexp)
 __global__ void __launch_bounds__(256) ldexp_kernel(int64_t count, const double* __restrict__ x,
                                                     const int32_t* __restrict__ n,

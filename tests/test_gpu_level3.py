@@ -181,3 +181,54 @@ def test_level3_bad_arguments(casc):
     with pytest.raises(casc.CascError):  # B overlapping A
         buf = torch.zeros((5, 4), dtype=torch.float64, device="cuda")
         casc.casc_trsm_fp64x2_right("L", "N", 1.0, buf[:4], buf[:4], buf[1:], buf[1:])
+
+
+@pytest.mark.parametrize("uplo,trans,n,k", [("L", "N", 200, 300), ("U", "T", 130, 513),
+                                            ("L", "T", 1100, 256)])
+def test_syr2k_bitwise_gemms_and_oracle(casc, orc, uplo, trans, n, k):
+    """SYR2K (R30): every stored element bitwise the two cascaded GEMM updates
+    C := alpha op(A) op(B)^T + beta C; C := alpha op(B) op(A)^T + C of
+    casc_gemm_fp64x2_ex (the triangular kernel computes the same tiles), the
+    other triangle keeps its sentinel, flags = OR of the two GEMMs' flags and
+    equal the oracle's; within twice the bound of the oracle."""
+    import torch
+    a = I.make_config(1, m=k, n=k, k=k, seed=91)
+    b = I.make_config(2, m=k, n=k, k=k, seed=93)
+    rows = min(n, k)
+    A_hi = np.concatenate([a["A_hi"]] * (-(-n // k)))[:n]
+    A_lo = np.concatenate([a["A_lo"]] * (-(-n // k)))[:n]
+    B_hi = np.concatenate([b["A_hi"]] * (-(-n // k)))[:n]
+    B_lo = np.concatenate([b["A_lo"]] * (-(-n // k)))[:n]
+    A_hi[5], A_lo[5] = 0.0, 0.0
+    B_hi[5], B_lo[5] = 0.0, 0.0
+    st = (lambda x: x.T.copy()) if trans == "T" else (lambda x: x.copy())
+    Ah, Al, Bh, Bl = (T(st(x)) for x in (A_hi, A_lo, B_hi, B_lo))
+    C0 = np.random.default_rng(7).uniform(-1, 1, (n, n))
+    al, be = (0.75, 2.0 ** -60), (-0.5, 0.0)
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+    C_hi = T(np.where(tri, C0, np.nan))
+    C_lo = T(np.zeros((n, n)))
+    fl = torch.full((n, n), 9, dtype=torch.uint8, device="cuda")
+    casc.casc_syr2k_fp64x2(uplo, trans, al, Ah, Al, Bh, Bl, be, C_hi, C_lo, flags=fl)
+    tb = "N" if trans == "T" else "T"
+    G_hi, G_lo = T(C0), T(np.zeros((n, n)))
+    f1 = torch.empty((n, n), dtype=torch.uint8, device="cuda")
+    f2 = torch.empty((n, n), dtype=torch.uint8, device="cuda")
+    casc.casc_gemm_fp64x2_ex(trans, tb, al, Ah, Al, Bh, Bl, be, G_hi, G_lo, flags=f1)
+    casc.casc_gemm_fp64x2_ex(trans, tb, al, Bh, Bl, Ah, Al, 1.0, G_hi, G_lo, flags=f2)
+    s_hi, s_lo, g_hi, g_lo = N(C_hi), N(C_lo), N(G_hi), N(G_lo)
+    assert np.array_equal(bits(s_hi[tri]), bits(g_hi[tri])) and np.array_equal(bits(s_lo[tri]), bits(g_lo[tri]))
+    assert np.all(np.isnan(s_hi[~tri]))
+    f = N(fl)
+    assert np.array_equal(f[tri], (N(f1) | N(f2))[tri]) and np.all(f[~tri] == 9)
+    assert f[5][tri[5]].all()
+    if n <= 200:
+        o_hi, o_lo, o_fl = orc.casc_syr2k(uplo, trans, al, st(A_hi), st(A_lo), st(B_hi), st(B_lo),
+                                          be, C0, np.zeros((n, n)))
+        assert np.array_equal(f[tri], o_fl[tri])
+        ii, jj = np.nonzero(tri)
+        r1 = orc.exact_entries(A_hi, A_lo, B_hi.T.copy(), B_lo.T.copy(), ii, jj)
+        r2 = orc.exact_entries(B_hi, B_lo, A_hi.T.copy(), A_lo.T.copy(), ii, jj)
+        bound = 2 * abs(al[0]) * 2 * orc.north_star_bound(k, r1["absab"] + r2["absab"]) \
+            + 2.0 ** -100 * np.abs(o_hi[tri])
+        assert np.all(np.abs((s_hi[tri] - o_hi[tri]) + (s_lo[tri] - o_lo[tri])) <= bound)

@@ -406,3 +406,34 @@ def test_trsm_right_oracle(orc, uplo, trans, unit, m, n):
                 terms = [(fr(X_hi[i, l]) + fr(X_lo[i, l])) * col[l] for l in range(n) if col[l] != 0]
                 r = sum(terms) - (fr(B_hi[i, j]) + fr(B_lo[i, j]))
                 assert abs(r) <= F(2) ** -96 * sum(abs(t) for t in terms)
+
+
+@pytest.mark.parametrize("uplo,trans,n,k", [("L", "N", 30, 300), ("U", "T", 25, 513)])
+def test_syr2k_oracle_exact(orc, uplo, trans, n, k):
+    """SYR2K (R30): the triangle of C within twice the north-star bound of the
+    exact op(A) op(B)^T + op(B) op(A)^T (alpha = 1, beta = 0); the other
+    triangle untouched; flags = OR of the two products' flags (here: zero rows
+    of A flag their row); alpha = 2^p scales exactly."""
+    a = I.make_config(1, m=k, n=k, k=k, seed=81)
+    b = I.make_config(2, m=k, n=k, k=k, seed=83)
+    A_hi, A_lo = a["A_hi"][:n].copy(), a["A_lo"][:n].copy()   # op(A): n x k
+    B_hi, B_lo = b["A_hi"][:n].copy(), b["A_lo"][:n].copy()
+    A_hi[3] = A_lo[3] = 0.0
+    B_hi[3] = B_lo[3] = 0.0
+    st = (lambda x: x.T.copy()) if trans == "T" else (lambda x: x)
+    C0 = np.full((n, n), 7.0)
+    C_hi, C_lo, fl = orc.casc_syr2k(uplo, trans, (1.0, 0.0), st(A_hi), st(A_lo), st(B_hi),
+                                    st(B_lo), (0.0, 0.0), C0, np.zeros((n, n)))
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "L" else np.triu(np.ones((n, n), bool))
+    assert np.all(C_hi[~tri] == 7.0)
+    ii, jj = np.nonzero(tri)
+    r1 = orc.exact_entries(A_hi, A_lo, B_hi.T.copy(), B_lo.T.copy(), ii, jj)
+    r2 = orc.exact_entries(B_hi, B_lo, A_hi.T.copy(), A_lo.T.copy(), ii, jj)
+    for t, (i, j) in enumerate(zip(ii, jj)):
+        exact = fr(r1["ex_hi"][t]) + fr(r1["ex_lo"][t]) + fr(r2["ex_hi"][t]) + fr(r2["ex_lo"][t])
+        bound = 2 * orc.north_star_bound(k, r1["absab"][t] + r2["absab"][t])
+        assert abs(fr(C_hi[i, j]) + fr(C_lo[i, j]) - exact) <= F(bound)
+    assert np.all(fl[3][tri[3]] == 1) and np.all(fl[:, 3][tri[:, 3]] == 1)
+    C2 = orc.casc_syr2k(uplo, trans, (0.25, 0.0), st(A_hi), st(A_lo), st(B_hi), st(B_lo),
+                        (0.0, 0.0), C0, np.zeros((n, n)))
+    assert np.array_equal(C2[0][tri], 0.25 * C_hi[tri])
