@@ -176,7 +176,7 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
                      const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0,
-                     void* scratch = nullptr, int64_t ldf = -1) {
+                     void* scratch = nullptr, int64_t ldf = -1, bool pdl = false) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -221,6 +221,7 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
     own_scratch = true;
   }
   a.scratch = scratch;
+  a.pdl = (pdl && !own_scratch && !dbg) ? 1 : 0;
   if (!P) {
     cudaError_t e = casc::launch_gemm(a, sms, st);
     if (own_scratch) cudaFreeAsync(scratch, st);
@@ -393,6 +394,11 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   uint8_t* pa = static_cast<uint8_t*>(workspace);
   uint8_t* pb = pa + (casc_packed_a_bytes(m, k) + 255) / 256 * 256;
   const casc::Widths w = widths_for(k);
+  // the fused kernel's scratch head is zeroed first, so that the split launch
+  // and the product launch are adjacent (programmatic dependent launch)
+  void* scr = ws_counter(workspace, m, n, k);
+  if (cudaMemsetAsync(scr, 0, 2 * sizeof(unsigned int), S(stream)) != cudaSuccess)
+    return CASC_ERR_CUDA;
   // phase 1: both splits in one launch
   cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, m, B_hi, B_lo, ldb, n, k, w, pa, pb,
                                         S(stream), false, false);
@@ -401,7 +407,7 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
   g_launches = 0;
   r = gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, S(stream), 0, nst, nullptr,
-                       AlphaBeta(), ps, 0, ws_counter(workspace, m, n, k));
+                       AlphaBeta(), ps, 0, scr, -1, true);
   g_launches = (r == CASC_OK) ? g_launches + 1 : 0;  // + the split launch
   return r;
 }

@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // PDL: this launch may start in the split kernel's tail; nothing below reads
+  // memory that kernel (or anything before it on the stream) writes before this
+  // wait returns (a no-op without the launch attribute)
+  if constexpr (!WIDE) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int split_p = SPLIT ? p.split_p : 0;
   // work items (WIDE: the entries item * 8 + warp listed by the first launch)
@@ -468,7 +472,7 @@ static cudaError_t launch_variant(GemmArgs& a, int grid, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
   if (e != cudaSuccess) return e;
-  if (!WIDE) {
+  if (!WIDE && !a.pdl) {
     casc_gemm_kernel<DBG, AB, SPLIT, TRI, WIDE><<<grid, GEMM_THREADS, GEMM_SMEM, st>>>(a);
     return cudaGetLastError();
   }
@@ -505,14 +509,17 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   if (grid == 0 || a.st_end <= a.st_begin) return cudaSuccess;
   if (a.dbg) {
     a.wave_counter = nullptr;
+    a.pdl = 0;
     return launch_variant<true, false, false>(a, grid, st);
   }
   if (!a.scratch) return cudaErrorInvalidValue;
   a.wave_counter = reinterpret_cast<unsigned int*>(a.scratch);
   a.wide_count = a.wave_counter + 1;
   a.wide_list = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(a.scratch) + GEMM_SCRATCH_HEAD);
-  cudaError_t e = cudaMemsetAsync(a.scratch, 0, 2 * sizeof(unsigned int), st);
-  if (e != cudaSuccess) return e;
+  if (!a.pdl) {  // else zeroed by the caller before the split launch (PDL edge kept)
+    cudaError_t e = cudaMemsetAsync(a.scratch, 0, 2 * sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+  }
   if (a.split_p || ntiles <= num_sms || !wave_sync_on()) a.wave_counter = nullptr;
   if (a.tri) return launch_pair<true, false, true>(a, grid, st);
   if (a.split_p)

@@ -154,6 +154,9 @@ struct GemmArgs {
   // SYRK (NEXT-4, casc_syrk_fp64x2): 0 all tiles; 1 lower triangle (tiles with
   // nb <= mb, elements with row >= col stored); 2 upper (nb >= mb, row <= col)
   int tri;
+  // 1: the caller zeroed the scratch head before the split launch that precedes
+  // this one, and the product kernel is a programmatic dependent launch of it
+  int pdl;
 };
 
 constexpr int GEMM_SCRATCH_HEAD = 256;  // wave counter, WIDE count; then the WIDE list

@@ -226,6 +226,9 @@ struct SplitABArgs {
 };
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) split_ab_kernel(const SplitABArgs a) {
+  // the fused GEMM that follows may be scheduled now (PDL); it waits for this
+  // grid's completion before it reads the packed slices
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if ((int64_t)blockIdx.x < a.ga)
     split_a_body<TA>(a.Ahi, a.Alo, a.lda, a.m, a.k, a.K, a.pa, a.a_blk, a.a_exp, a.nks,
                      blockIdx.x);
