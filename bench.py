@@ -731,8 +731,8 @@ def main():
                          "ms": t_symm, "gflops_2m2n": 2 * m * m * n / (t_symm * 1e-3) / 1e9},
                 "trmm": {"op": "B := L B, L %d x %d lower" % (m, m),
                          "ms": t_trmm, "gflops_m2n": m * m * n / (t_trmm * 1e-3) / 1e9,
-                         "note": "the GEMM of the expanded triangle: 2m^2n flops of work for "
-                                 "the m^2n of the convention"},
+                         "note": "the GEMM of the expanded triangle with each tile's k range "
+                                 "stopped at the zero triangle (~m^2n of work)"},
                 "trsm_right": {"op": "X L^T = B, L %d x %d lower, B %d x %d" % (m, m, m, n),
                                "ms": t_trsm_r,
                                "gflops_mn2": m * n * n / (t_trsm_r * 1e-3) / 1e9}}

@@ -352,7 +352,9 @@ int casc_symm_fp64x2(int side, int uplo, int64_t m, int64_t n,
  * (side RIGHT, A n x n), A triangular (uplo; diag CASC_UNIT: diagonal taken as
  * 1, not read), op(A) = A or A^T; B m x n overwritten.  The triangular A (other
  * triangle zero) is expanded into a stream-ordered temporary and the product is
- * casc_gemm_fp64x2_ex of it, written back into B: bitwise that GEMM's result.
+ * the cascaded GEMM of it (each tile's k range stopped at the zero triangle:
+ * about half the work), written back into B: the values of
+ * casc_gemm_fp64x2_ex of the expanded matrix (the skipped terms are zeros).
  * alpha == 0: B := 0, A not read.  CASC_ERR_INVALID for bad enums, B
  * overlapping A. */
 int casc_trmm_fp64x2(int side, int uplo, int trans, int diag, int64_t m, int64_t n,

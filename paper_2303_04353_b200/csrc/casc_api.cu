@@ -176,7 +176,8 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
                      double* C_hi, double* C_lo, int64_t ldc, uint8_t* flags, int sms,
                      cudaStream_t st, int st_begin, int st_end, double* dbg,
                      const AlphaBeta& abv = AlphaBeta(), void* split_ws = nullptr, int tri = 0,
-                     void* scratch = nullptr, int64_t ldf = -1, bool pdl = false) {
+                     void* scratch = nullptr, int64_t ldf = -1, bool pdl = false,
+                     int band = 0) {
   const casc::Widths w = widths_for(k);
   casc::GemmArgs a{};
   a.ab = abv.ab;
@@ -206,8 +207,10 @@ int gemm_packed_impl(int64_t m, int64_t n, int64_t k, const void* pa, const void
   a.dbg = dbg;
   a.un_b2 = std::ldexp(1.0, w.c1 - w.c0);
   a.tri = tri;
+  a.band = band;
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
-  const int P = (!dbg && !tri && st_begin == 0 && st_end == nst) ? split_plan(m, n, k, sms) : 0;
+  const int P = (!dbg && !tri && !band && st_begin == 0 && st_end == nst)
+                    ? split_plan(m, n, k, sms) : 0;
   // per-launch scratch of the fused kernel (wave counter, WIDE list): the caller's
   // workspace slot, else a stream-ordered allocation of this call (never shared
   // between launches or streams)
@@ -585,12 +588,32 @@ int casc_debug_ldexp(int64_t count, const double* x, const int32_t* n, double* o
 }
 
 // ---------------------------------------------------------------- BLAS-style (NEXT-4)
+static int gemm_ex_impl(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                        double alpha_hi, double alpha_lo, const double* A_hi, const double* A_lo,
+                        int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                        double beta_hi, double beta_lo, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* workspace, size_t workspace_bytes,
+                        casc_stream_t stream, int band);
+
 int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
                         double alpha_hi, double alpha_lo, const double* A_hi, const double* A_lo,
                         int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
                         double beta_hi, double beta_lo, double* C_hi, double* C_lo, int64_t ldc,
                         uint8_t* flags, void* workspace, size_t workspace_bytes,
                         casc_stream_t stream) {
+  return gemm_ex_impl(transa, transb, m, n, k, alpha_hi, alpha_lo, A_hi, A_lo, lda, B_hi, B_lo,
+                      ldb, beta_hi, beta_lo, C_hi, C_lo, ldc, flags, workspace, workspace_bytes,
+                      stream, 0);
+}
+
+}  // extern "C"
+
+static int gemm_ex_impl(int transa, int transb, int64_t m, int64_t n, int64_t k,
+                        double alpha_hi, double alpha_lo, const double* A_hi, const double* A_lo,
+                        int64_t lda, const double* B_hi, const double* B_lo, int64_t ldb,
+                        double beta_hi, double beta_lo, double* C_hi, double* C_lo, int64_t ldc,
+                        uint8_t* flags, void* workspace, size_t workspace_bytes,
+                        casc_stream_t stream, int band) {
   g_launches = 0;
   if ((transa != CASC_OP_N && transa != CASC_OP_T) || (transb != CASC_OP_N && transb != CASC_OP_T))
     return CASC_ERR_INVALID;
@@ -651,12 +674,15 @@ int casc_gemm_fp64x2_ex(int transa, int transb, int64_t m, int64_t n, int64_t k,
   uint8_t* ps = pb + (casc_packed_b_bytes(k, n) + 255) / 256 * 256;  // split-mode buffer
   g_launches = 0;
   r = (e == cudaSuccess) ? gemm_packed_impl(m, n, k, pa, pb, C_hi, C_lo, ldc, flags, sms, st, 0,
-                                            nst, nullptr, abv, ps, 0, ws_counter(ws, m, n, k))
+                                            nst, nullptr, abv, ps, 0, ws_counter(ws, m, n, k), -1,
+                                            false, band)
                          : CASC_ERR_CUDA;
   if (owned) cudaFreeAsync(ws, st);
   g_launches = (r == CASC_OK) ? g_launches + 1 : 0;
   return r;
 }
+
+extern "C" {
 
 // ---------------------------------------------------------------- SYRK (NEXT-4)
 // C := alpha op(A) op(A)^T + beta C on one triangle (level-3 BLAS
@@ -1074,6 +1100,14 @@ int current_sms() { return ::current_sms(); }
 bool trsm_overlap(int64_t m, int64_t n, const double* A_hi, const double* A_lo, int64_t lda,
                   const double* B_hi, const double* B_lo, int64_t ldb) {
   return ::trsm_overlap(m, n, A_hi, A_lo, lda, B_hi, B_lo, ldb);
+}
+// casc_gemm_fp64x2_ex with a banded (triangular) operand, GemmArgs::band (TRMM)
+int gemm_ex_band(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha_hi,
+                 double alpha_lo, const double* A_hi, const double* A_lo, int64_t lda,
+                 const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                 int64_t ldc, casc_stream_t stream, int band) {
+  return ::gemm_ex_impl(transa, transb, m, n, k, alpha_hi, alpha_lo, A_hi, A_lo, lda, B_hi, B_lo,
+                        ldb, 0.0, 0.0, C_hi, C_lo, ldc, nullptr, nullptr, 0, stream, band);
 }
 void set_launches(int n) { g_launches = n; }
 }  // namespace host

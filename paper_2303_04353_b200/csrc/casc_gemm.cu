@@ -94,7 +94,7 @@ __device__ __forceinline__ void tri_coords(int t, int tri, int& mb, int& nb) {
   mb = tri == 2 ? c : r;
   nb = tri == 2 ? r : c;
 }
-template <bool TRI>
+template <bool TRI, bool BAND = false>
 __device__ __forceinline__ void item_coords(const GemmArgs& p, int split_p, int item, int& mb,
                                             int& nb, int& s0, int& s1, int& q0) {
   if (TRI) {
@@ -113,6 +113,12 @@ __device__ __forceinline__ void item_coords(const GemmArgs& p, int split_p, int 
     s0 = p.st_begin;
     s1 = p.st_end;
     q0 = 0;
+    if (BAND && p.band) {  // the triangular operand's zero rows / columns: skip (TRMM)
+      if (p.band == 1) s1 = min(s1, (mb + 1) * (TM / BK));
+      if (p.band == 2) s0 = max(s0, mb * (TM / BK));
+      if (p.band == 3) s0 = max(s0, nb * (TN / BK));
+      if (p.band == 4) s1 = min(s1, (nb + 1) * (TN / BK));
+    }
   }
 }
 // elements a SYRK stores (its triangle); everything for a GEMM
@@ -204,7 +210,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
         }
         if (tile >= ntiles) continue;
         int mb, nb, s0, s1, q0;
-        item_coords<TRI>(p, split_p, WIDE ? (int)(p.wide_list[tile] >> 3) : tile, mb, nb, s0, s1,
+        item_coords<TRI, AB && !SPLIT>(p, split_p, WIDE ? (int)(p.wide_list[tile] >> 3) : tile, mb,
+                                       nb, s0, s1,
                          q0);
         const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)s0 * A_STAGE * 8;
         const uint8_t* srcB = p.pb + nb * p.b_blk + (int64_t)s0 * B_STAGE * 8;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
     int mb, nb, s0, s1, q0;
     const unsigned int entry = WIDE ? p.wide_list[tile] : 0u;
     const int item = WIDE ? (int)(entry >> 3) : tile;
-    item_coords<TRI>(p, split_p, item, mb, nb, s0, s1, q0);
+    item_coords<TRI, AB && !SPLIT>(p, split_p, item, mb, nb, s0, s1, q0);
     // Scales 2^(e_i + f_j) outside the normal powers of two (reading R16) are
     // rare; the combine of this kernel assumes one exact power of two per
     // element, and a warp that meets another scale in any panel of the item
@@ -520,11 +527,13 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(a.scratch, 0, 2 * sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
   }
-  if (a.split_p || ntiles <= num_sms || !wave_sync_on()) a.wave_counter = nullptr;
+  // no wave barrier for few waves, split mode, or banded tiles of unequal length
+  if (a.split_p || a.band || ntiles <= num_sms || !wave_sync_on()) a.wave_counter = nullptr;
   if (a.tri) return launch_pair<true, false, true>(a, grid, st);
   if (a.split_p)
     return a.ab ? launch_pair<true, true>(a, grid, st) : launch_pair<false, true>(a, grid, st);
-  return a.ab ? launch_pair<true, false>(a, grid, st) : launch_pair<false, false>(a, grid, st);
+  return (a.ab || a.band) ? launch_pair<true, false>(a, grid, st)
+                          : launch_pair<false, false>(a, grid, st);
 }
 
 }  // namespace casc

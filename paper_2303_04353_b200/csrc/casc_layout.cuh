@@ -157,6 +157,11 @@ struct GemmArgs {
   // 1: the caller zeroed the scratch head before the split launch that precedes
   // this one, and the product kernel is a programmatic dependent launch of it
   int pdl;
+  // TRMM (NEXT-4, reading R28): one operand triangular, so a tile's k range
+  // stops where that operand's rows / columns are zero.  0 none; 1 A lower
+  // (row block mb: k < 64 (mb+1)); 2 A upper (k >= 64 mb); 3 B lower (column
+  // block nb: k >= 64 nb); 4 B upper (k < 64 (nb+1)).  AB instantiations only.
+  int band;
 };
 
 constexpr int GEMM_SCRATCH_HEAD = 256;  // wave counter, WIDE count; then the WIDE list

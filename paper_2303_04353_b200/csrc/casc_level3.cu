@@ -7,7 +7,9 @@
 // stream-ordered temporary by one HBM-bound kernel (16 B read + 16 B written per
 // element, < 0.1% of the GEMM at 16384), after which the work is the cascaded
 // GEMM of casc_gemm_fp64x2_ex (transposes read directly by its split kernels).
-// Readings R28 (SYMM / TRMM) and R29 (right-side TRSM) in DESIGN.md.
+// TRMM's GEMM is banded: each tile's k range stops at op(A)'s zero triangle
+// (GemmArgs::band), about half the GEMM's work.
+// Readings R28 (SYMM / TRMM), R29 (right-side TRSM) and R30 (SYR2K) in DESIGN.md.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +31,10 @@ int check_mat(const void* p, int64_t rows, int64_t cols, int64_t ld);
 void set_launches(int n);
 bool trsm_overlap(int64_t m, int64_t n, const double* A_hi, const double* A_lo, int64_t lda,
                   const double* B_hi, const double* B_lo, int64_t ldb);
+int gemm_ex_band(int transa, int transb, int64_t m, int64_t n, int64_t k, double alpha_hi,
+                 double alpha_lo, const double* A_hi, const double* A_lo, int64_t lda,
+                 const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
+                 int64_t ldc, casc_stream_t stream, int band);
 }  // namespace host
 
 // Expand the stored triangle of an n x n FP64x2 matrix into a dense one (ld n):
@@ -189,13 +195,13 @@ int casc_trmm_fp64x2(int side, int uplo, int trans, int diag, int64_t m, int64_t
   r = st3(casc::expand(ka, uplo, 1, diag == CASC_UNIT, A_hi, A_lo, lda, F, F + fa, sms, st));
   int launches = 1;
   if (r == CASC_OK) {
+    // each tile's k range stops at op(A)'s zero triangle (half the GEMM's work)
+    const bool lower = (uplo == CASC_LOWER) != (trans == CASC_OP_T);  // op(A) lower
     r = side == CASC_LEFT
-            ? casc_gemm_fp64x2_ex(trans, CASC_OP_N, m, n, m, alpha_hi, alpha_lo, F, F + fa, ka,
-                                  B_hi, B_lo, ldb, 0.0, 0.0, T, T + tb, n, nullptr, nullptr, 0,
-                                  stream)
-            : casc_gemm_fp64x2_ex(CASC_OP_N, trans, m, n, n, alpha_hi, alpha_lo, B_hi, B_lo, ldb,
-                                  F, F + fa, ka, 0.0, 0.0, T, T + tb, n, nullptr, nullptr, 0,
-                                  stream);
+            ? casc::host::gemm_ex_band(trans, CASC_OP_N, m, n, m, alpha_hi, alpha_lo, F, F + fa,
+                                       ka, B_hi, B_lo, ldb, T, T + tb, n, stream, lower ? 1 : 2)
+            : casc::host::gemm_ex_band(CASC_OP_N, trans, m, n, n, alpha_hi, alpha_lo, B_hi, B_lo,
+                                       ldb, F, F + fa, ka, T, T + tb, n, stream, lower ? 3 : 4);
     launches += casc_last_launch_count();
   }
   if (r == CASC_OK &&
