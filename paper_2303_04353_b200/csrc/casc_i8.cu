@@ -76,16 +76,30 @@ constexpr int KBP = KC8 / KB;      // k blocks per panel (64)
 constexpr int TR = 128;            // rows (A) / columns (B) per chunk = tile edge
 constexpr int CHUNK = TR * KB;     // 16384 bytes
 constexpr int YMIN = 3, YMAX = 15;
+// C columns of a pair tile = the MMA's N (CASC_I8_TC, 128 or 64).  Tensor
+// memory holds 512 / TC int32 accumulators of the tile, so with TC = 64 one
+// sweep over k covers eight bins (two R25 value groups) instead of four, and
+// every operand chunk is streamed that much less often (the data movement is
+// what keeps the power-capped clock low: no operand loads at all runs at
+// 1.70 GHz instead of 1.46 GHz).
+#ifndef CASC_I8_TC
+#define CASC_I8_TC 128
+#endif
+constexpr int TC = CASC_I8_TC;
+static_assert(TC == 128 || TC == 64, "pair-tile columns: 128 or 64");
+constexpr int CPB = TR / TC;       // pair-tile column blocks per 128-column packed block
+constexpr int VG = 4;              // bins per R25 value group (exact int64 group values)
+constexpr int NBIN = 512 / TC;     // bins per MMA group (tensor memory: 512 / TC accumulators)
+constexpr int GPM = NBIN / VG;     // R25 value groups per MMA group
 #ifndef CASC_I8_NSA
 #define CASC_I8_NSA 9
 #endif
 #ifndef CASC_I8_NSB
-#define CASC_I8_NSB 10
+#define CASC_I8_NSB (CASC_I8_TC == 64 ? 18 : 10)
 #endif
-constexpr int NSA = CASC_I8_NSA, NSB = CASC_I8_NSB;  // smem ring slots (A: 16 KB, B: 8 KB halves)
-constexpr int NBIN = 4;            // bins per group (TMEM: 4 x 128 columns)
-constexpr int NGMAX = (YMAX + NBIN - 1) / NBIN;  // groups per panel, at most
-constexpr int64_t WS_PER_CTA = (2 + NGMAX) * 128 * 128;  // doubles / int64 per CTA
+constexpr int NSA = CASC_I8_NSA, NSB = CASC_I8_NSB;  // smem ring slots (A: 16 KB; B: TC/2 rows)
+constexpr int NGMAX = (YMAX + VG - 1) / VG;  // R25 value groups per panel, at most
+constexpr int64_t WS_PER_CTA = (int64_t)(2 + NGMAX) * TR * TC;  // doubles / int64 per CTA
 // (320 threads: up to 204 registers each, room for the epilogue's 64 exact
 // group values)
 constexpr int THREADS = 320;
@@ -108,7 +122,7 @@ constexpr int EPI_SUB = CASC_I8_EPI_SUB;  // elements per phase-2 step of the ep
 #define CASC_I8_GROUP_M 6
 #endif
 constexpr int GROUP_M = CASC_I8_GROUP_M;  // tile raster: GROUP_M row-pair blocks sweep the columns
-constexpr size_t SMEM = (size_t)NSA * CHUNK + (size_t)NSB * (CHUNK / 2) + 1024 + 1024;
+constexpr size_t SMEM = (size_t)NSA * CHUNK + (size_t)NSB * (TC / 2) * KB + 1024 + 1024;
 
 struct Pack {
   int64_t R;    // 128-row blocks (even: the GEMM's CTA pairs take them two at a time)
@@ -564,10 +578,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 256 (CTA pair), N = 128
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 256 (CTA pair), N = TC
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC >> 3) << 17) |
                            ((uint32_t)(256 >> 4) << 24);
-constexpr int BHALF = CHUNK / 2;   // each CTA of the pair holds 64 of the 128 B rows
+constexpr int BHALF = (TC / 2) * KB;  // each CTA of the pair holds TC/2 of a B chunk's rows
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -773,42 +787,46 @@ __device__ __forceinline__ void mma_chain(bool first_kb, uint32_t& aseq, uint32_
     }
     if (CASC_I8_WAITS_ON) I8_PROF_WAIT(32 + S, mbar_wait_uniform(&fullA[as], (aq / NSA) & 1));
     tc_fence_after();
-    constexpr int JHI_ = TOP;  // (per i below)
-    (void)JHI_;
     const int jhi = TOP - i, jlo = (S - i > 0 ? S - i : 0);
-    constexpr int PMAX = 4;
-    uint32_t d[PMAX];
-    uint64_t bd[PMAX];
-#pragma unroll
-    for (int u = 0; u < PMAX; ++u) {
-      const int j = jhi - u;
-      if (j >= jlo) {
-        const uint32_t bq = j >= S ? bbase + (TOP - j) : bbase + NB + (S - 1 - j);
-        bd[u] = sdesc(b0 + (bq % NSB) * BHALF);
-        d[u] = tmem + (i + j - S) * 128;
-      } else {
-        bd[u] = 0;
-        d[u] = 0;
-      }
-    }
     const uint64_t ad = sdesc(a0 + as * CHUNK);
+    // partners of A_i in batches of up to four, each batch through the A
+    // collector (A read from shared memory once per batch and 32-byte k step)
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      // at the panel's first k block every bin is first written at i = 0, kk = 0
-      const uint32_t acc = (first_kb && i == 0 && kk == 0) ? 0u : 1u;
-      const uint64_t bk[4] = {bd[0] + 2 * kk, bd[1] + 2 * kk, bd[2] + 2 * kk, bd[3] + 2 * kk};
-      const int np = jhi - jlo + 1;
+    for (int pb = 0; pb < (NB + 3) / 4; ++pb) {
+      const int jtop = jhi - 4 * pb;  // this batch: j = jtop .. max(jlo, jtop - 3)
+      if (jtop < jlo) break;
+      uint32_t d[4];
+      uint64_t bd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = jtop - u;
+        if (j >= jlo) {
+          const uint32_t bq = j >= S ? bbase + (TOP - j) : bbase + NB + (S - 1 - j);
+          bd[u] = sdesc(b0 + (bq % NSB) * BHALF);
+          d[u] = tmem + (i + j - S) * TC;
+        } else {
+          bd[u] = 0;
+          d[u] = 0;
+        }
+      }
+      const int np = (jtop - jlo + 1) < 4 ? (jtop - jlo + 1) : 4;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        // at the panel's first k block every bin is first written at i = 0, kk = 0
+        const uint32_t acc = (first_kb && i == 0 && kk == 0) ? 0u : 1u;
+        const uint64_t bk[4] = {bd[0] + 2 * kk, bd[1] + 2 * kk, bd[2] + 2 * kk, bd[3] + 2 * kk};
 #ifdef CASC_I8_NOMMA  // timing study only: no tensor-core work at all
-      if (np > 0) continue;
+        if (np > 0) continue;
 #endif
-      if (np == 4)
-        mma_i8_astat<4>(d, ad + 2 * kk, bk, acc);
-      else if (np == 3)
-        mma_i8_astat<3>(d, ad + 2 * kk, bk, acc);
-      else if (np == 2)
-        mma_i8_astat<2>(d, ad + 2 * kk, bk, acc);
-      else
-        mma_i8_astat<1>(d, ad + 2 * kk, bk, acc);
+        if (np == 4)
+          mma_i8_astat<4>(d, ad + 2 * kk, bk, acc);
+        else if (np == 3)
+          mma_i8_astat<3>(d, ad + 2 * kk, bk, acc);
+        else if (np == 2)
+          mma_i8_astat<2>(d, ad + 2 * kk, bk, acc);
+        else
+          mma_i8_astat<1>(d, ad + 2 * kk, bk, acc);
+      }
     }
     // A_i is done; B_(TOP-i) has met its last partner
     const int jr = TOP - i;
@@ -828,11 +846,18 @@ __device__ __forceinline__ void mma_kblock(int s, int nb, bool first_kb, uint32_
     mma_chain<SS, NN>(first_kb, aseq, bseq, tmem, a0, b0, fullA, emptyA, fullB, emptyB); \
     return;                                                                               \
   }
-  // (first bin, bins) of the R25 groups for y = 3 .. 15
+  // (first bin, bins) of the MMA groups for y = 3 .. 15
+#if CASC_I8_TC == 128  // one R25 value group each
   CASC_I8_CHAIN(0, 1) CASC_I8_CHAIN(0, 2) CASC_I8_CHAIN(0, 3) CASC_I8_CHAIN(0, 4)
   CASC_I8_CHAIN(1, 4) CASC_I8_CHAIN(2, 4) CASC_I8_CHAIN(3, 4) CASC_I8_CHAIN(4, 4)
   CASC_I8_CHAIN(5, 4) CASC_I8_CHAIN(6, 4) CASC_I8_CHAIN(7, 4) CASC_I8_CHAIN(8, 4)
   CASC_I8_CHAIN(9, 4) CASC_I8_CHAIN(10, 4) CASC_I8_CHAIN(11, 4)
+#else  // two R25 value groups each: (0, r0 [+ 4]), then (r0 + 4, 4 | 8)
+  CASC_I8_CHAIN(0, 3) CASC_I8_CHAIN(0, 4) CASC_I8_CHAIN(0, 5) CASC_I8_CHAIN(0, 6)
+  CASC_I8_CHAIN(0, 7) CASC_I8_CHAIN(0, 8) CASC_I8_CHAIN(5, 4) CASC_I8_CHAIN(6, 4)
+  CASC_I8_CHAIN(7, 4) CASC_I8_CHAIN(8, 4) CASC_I8_CHAIN(5, 8) CASC_I8_CHAIN(6, 8)
+  CASC_I8_CHAIN(7, 8)
+#endif
 #undef CASC_I8_CHAIN
 }
 
@@ -880,10 +905,11 @@ __device__ __forceinline__ int64_t tile_index(int64_t rp, int64_t cb, int64_t RP
   return grp * GROUP_M * RB + cb * gs + (rp - first);
 }
 
-// SYRK work list: the pair tiles (256 rows x 128 columns) that hold elements of
-// the triangle, row pair by row pair: lower cb <= 2 rp + 1, upper cb >= 2 rp
+// SYRK work list: the pair tiles (256 rows x TC columns) that hold elements of
+// the triangle, row pair by row pair: lower cb < 2 CPB (rp + 1), upper cb >= 2 CPB rp
+// (RB: pair-tile column blocks of TC columns; a row pair covers 256 / TC of them)
 __device__ __forceinline__ int64_t tri_count(int tri, int64_t rp, int64_t RB) {
-  return tri == 1 ? min(2 * rp + 2, RB) : max(RB - 2 * rp, (int64_t)0);
+  return tri == 1 ? min(2 * CPB * (rp + 1), RB) : max(RB - 2 * CPB * rp, (int64_t)0);
 }
 __device__ __forceinline__ void tri_tile_of(int tile, int tri, int64_t RP, int64_t RB,
                                             int64_t& rp, int64_t& cb) {
@@ -893,7 +919,25 @@ __device__ __forceinline__ void tri_tile_of(int tile, int tri, int64_t RP, int64
     if (t < c) break;
     t -= c;
   }
-  cb = tri == 1 ? t : 2 * rp + t;
+  cb = tri == 1 ? t : 2 * CPB * rp + t;
+}
+
+// R25 value group g of a panel: bins s .. s + nb - 1 (bins 0 .. r0-1 first,
+// then fours aligned at the least significant bin)
+__device__ __forceinline__ void vgroup(int g, int r0, int& s, int& nb) {
+  s = g ? r0 + (g - 1) * VG : 0;
+  nb = g ? VG : r0;
+}
+// MMA group G: the value groups [g0, g1) (GPM of them), bins S .. S + NB - 1
+// swept together over k (tensor memory holds them all)
+__device__ __forceinline__ void mgroup(int G, int r0, int ngroups, int& S, int& NB, int& g0,
+                                       int& g1) {
+  g0 = G * GPM;
+  g1 = min(ngroups, g0 + GPM);
+  int s1, n1;
+  vgroup(g1 - 1, r0, s1, n1);
+  vgroup(g0, r0, S, NB);
+  NB = s1 + n1 - S;
 }
 
 // The fused kernel on CTA pairs (cluster of 2, tcgen05 cta_group::2): the pair
@@ -949,9 +993,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   const int y = p.ga.y;
   // R25 groups: bins 0 .. r0-1, then fours (aligned at the least significant bin)
-  const int r0 = (y - 1) % NBIN + 1;
-  const int ngroups = 1 + (y - r0) / NBIN;
-  const int64_t RA = p.ga.R, RB = p.gb.R, KBn = p.ga.KBn;
+  const int r0 = (y - 1) % VG + 1;
+  const int ngroups = 1 + (y - r0) / VG;
+  const int nmg = (ngroups + GPM - 1) / GPM;  // MMA groups (sweeps over k) per panel
+  const int64_t RA = p.ga.R, RB = p.gb.R * CPB, KBn = p.ga.KBn;
   const int64_t RP = RA / 2;
   const int P = (int)p.ga.P;
   int tiles = (int)(RP * RB);
@@ -989,7 +1034,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto loadB = [&](int j, int64_t cb, int64_t kb) {
       const uint32_t s = bseq % NSB;
       mbar_wait_sleep(&emptyB[s], ((bseq / NSB) & 1) ^ 1);
-      const int row = (int)(chunk_off(p.gb, j, cb, kb) / KB + rank * (TR / 2));
+      const int row = (int)(chunk_off(p.gb, j, cb / CPB, kb) / KB + (cb % CPB) * TC +
+                            rank * (TC / 2));
       tma_pair_elect(sB + s * BHALF, &mapB, row, &fullB[s], leader_addr(&fullB[s]),
                      leader ? 2 * BHALF : 0);
       ++bseq;
@@ -1008,9 +1054,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int q = 0; q < P; ++q) {
         int64_t kb0, kb1;
         kb_range(item, q, kb0, kb1);
-        for (int go = 0; go < ngroups; ++go) {
-          const int grp = ngroups - 1 - go;  // the MMA issuer's group order
-          const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0, top = s + nb - 1;
+        for (int go = 0; go < nmg; ++go) {
+          int s, nb, g0_, g1_;
+          mgroup(nmg - 1 - go, r0, ngroups, s, nb, g0_, g1_);  // the MMA issuer's order
+          const int top = s + nb - 1;
           for (int64_t kb = kb0; kb < kb1; ++kb) {
             if (synced && (kb - kb0) % CASC_I8_SYNC_KB == 0) {
               // Soft wave synchronisation: the producers of all CTAs start each
@@ -1064,9 +1111,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // 0 .. r-1 (most significant, fewest products) ends the panel, so the
           // epilogue's once-per-panel phase 2 overlaps the longest group's MMAs
           // instead of delaying the drain of the shortest one
-          for (int go = 0; go < ngroups; ++go, ++gcount) {
-            const int grp = ngroups - 1 - go;
-            const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
+          for (int go = 0; go < nmg; ++go, ++gcount) {
+            int s, nb, g0_, g1_;
+            mgroup(nmg - 1 - go, r0, ngroups, s, nb, g0_, g1_);
 #ifndef CASC_I8_NOWAIT
             I8_PROF_WAIT(s, mbar_wait_cluster(tempty, (gcount & 1) ^ 1));
 #endif
@@ -1097,8 +1144,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // per-CTA workspace: C accumulator (hi, lo) of the tile, then the exact
     // group values V of the panel's groups [NGMAX][128 x 128]
     double* Ch = p.ws + (int64_t)blockIdx.x * WS_PER_CTA;
-    double* Cl = Ch + TR * TR;
-    long long* Vw = reinterpret_cast<long long*>(Cl + TR * TR);
+    double* Cl = Ch + TR * TC;
+    long long* Vw = reinterpret_cast<long long*>(Cl + TR * TC);
+    constexpr int CW = TC / 2;  // columns of the tile per epilogue thread
     uint32_t gcount = 0;
     for (int item = pair; item < items; item += npairs) {
       const int tile = item / ks;
@@ -1108,54 +1156,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       else
         tile_of(tile, RP, RB, rp, cb);
       const int64_t gi = (2 * rp + rank) * TR + lr;
-      uint64_t fl = 0;  // detector bits of this thread's 64 columns
+      uint64_t fl = 0;  // detector bits of this thread's CW columns
       for (int q = 0; q < P; ++q) {
         const int64_t kp = min((int64_t)KC8, p.k - (int64_t)q * KC8);
         const int ei = *reinterpret_cast<const int32_t*>(p.pa + exp_at(p.ga, gi, q));
         // column exponents of this (tile, panel) -> shared memory
         epi_bar_sync();
-        if (ew < 4)
+        if (ew < TC / 32)
           sF[ew * 32 + lane] =
-              *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, cb * TR + ew * 32 + lane, q));
+              *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, cb * TC + ew * 32 + lane, q));
         epi_bar_sync();
-        for (int go = 0; go < ngroups; ++go, ++gcount) {
-          const int grp = ngroups - 1 - go;  // the MMA issuer's group order
-          const int s = grp ? r0 + (grp - 1) * NBIN : 0, nb = grp ? NBIN : r0;
-          const bool lastg = go + 1 == ngroups;
+        for (int go = 0; go < nmg; ++go, ++gcount) {
+          int S_, NB_, g0, g1;
+          mgroup(nmg - 1 - go, r0, ngroups, S_, NB_, g0, g1);  // the MMA issuer's order
+          const bool lastg = go + 1 == nmg;
           mbar_wait_sleep(tfull, gcount & 1);
           tc_fence_after();
           // Phase 1: drain this warp's part of TMEM into the exact group values
-          // V = sum_u bin_(s+u) 2^(8(nb-1-u)) (int64, |V| < 2^56; R25), then
-          // release TMEM so that the MMAs of the next group start at once.
+          // V = sum_u bin_(s+u) 2^(8(nb-1-u)) (int64, |V| < 2^56; R25) of each
+          // value group of this MMA group, then release TMEM so that the MMAs of
+          // the next group start at once.
+          for (int grp = g0; grp < g1; ++grp) {
+            int s, nb;
+            vgroup(grp, r0, s, nb);
+            const uint32_t tb = trow + (uint32_t)((s - S_) * TC);
 #pragma unroll 2
-          for (int cc = 0; cc < 8; ++cc) {
-            const int c0 = half * 64 + cc * 8;
-            uint32_t r0[8], r1[8], r2[8], r3[8];
-            tmem_ld8(trow + 0 * 128 + c0, r0);
-            if (nb > 1) tmem_ld8(trow + 1 * 128 + c0, r1);
-            if (nb > 2) tmem_ld8(trow + 2 * 128 + c0, r2);
-            if (nb > 3) tmem_ld8(trow + 3 * 128 + c0, r3);
-            tmem_wait_ld();
-            if (DBG && q == p.dbg_panel) {
+            for (int cc = 0; cc < CW / 8; ++cc) {
+              const int c0 = half * CW + cc * 8;
+              uint32_t r0[8], r1[8], r2[8], r3[8];
+              tmem_ld8(tb + 0 * TC + c0, r0);
+              if (nb > 1) tmem_ld8(tb + 1 * TC + c0, r1);
+              if (nb > 2) tmem_ld8(tb + 2 * TC + c0, r2);
+              if (nb > 3) tmem_ld8(tb + 3 * TC + c0, r3);
+              tmem_wait_ld();
+              if (DBG && q == p.dbg_panel) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int64_t gj = cb * TR + c0 + i;
-                if (gi < p.m && gj < p.n) {
-                  const int64_t mn = p.m * p.n, o = gi * p.n + gj;
-                  p.dbg[(int64_t)(s + 0) * mn + o] = (int32_t)r0[i];
-                  if (nb > 1) p.dbg[(int64_t)(s + 1) * mn + o] = (int32_t)r1[i];
-                  if (nb > 2) p.dbg[(int64_t)(s + 2) * mn + o] = (int32_t)r2[i];
-                  if (nb > 3) p.dbg[(int64_t)(s + 3) * mn + o] = (int32_t)r3[i];
+                for (int i = 0; i < 8; ++i) {
+                  const int64_t gj = cb * TC + c0 + i;
+                  if (gi < p.m && gj < p.n) {
+                    const int64_t mn = p.m * p.n, o = gi * p.n + gj;
+                    p.dbg[(int64_t)(s + 0) * mn + o] = (int32_t)r0[i];
+                    if (nb > 1) p.dbg[(int64_t)(s + 1) * mn + o] = (int32_t)r1[i];
+                    if (nb > 2) p.dbg[(int64_t)(s + 2) * mn + o] = (int32_t)r2[i];
+                    if (nb > 3) p.dbg[(int64_t)(s + 3) * mn + o] = (int32_t)r3[i];
+                  }
                 }
               }
-            }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              long long v = (int32_t)r0[i];
-              if (nb > 1) v = v * 256 + (int32_t)r1[i];
-              if (nb > 2) v = v * 256 + (int32_t)r2[i];
-              if (nb > 3) v = v * 256 + (int32_t)r3[i];
-              Vw[(int64_t)grp * TR * TR + (c0 + i) * TR + lr] = v;
+              for (int i = 0; i < 8; ++i) {
+                long long v = (int32_t)r0[i];
+                if (nb > 1) v = v * 256 + (int32_t)r1[i];
+                if (nb > 2) v = v * 256 + (int32_t)r2[i];
+                if (nb > 3) v = v * 256 + (int32_t)r3[i];
+                Vw[(int64_t)grp * TR * TC + (c0 + i) * TR + lr] = v;
+              }
             }
           }
           tc_fence_before();
@@ -1173,8 +1227,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // the next panel / tile): the FP64x2 panel sum T over the groups' exact
           // values, most significant first (R25), the detector (R26) and C.
 #pragma unroll 1
-          for (int cc = 0; cc < 64 / EPI_SUB; ++cc) {
-            const int c0 = half * 64 + cc * EPI_SUB;
+          for (int cc = 0; cc < CW / EPI_SUB; ++cc) {
+            const int c0 = half * CW + cc * EPI_SUB;
             double th[EPI_SUB], tl[EPI_SUB], xch[EPI_SUB], xcl[EPI_SUB];
             if (q > 0) {
 #pragma unroll
@@ -1191,7 +1245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (g2 < ngroups) {
 #pragma unroll
                 for (int i = 0; i < EPI_SUB; ++i)
-                  xv[g2][i] = ld_na(&Vw[(int64_t)g2 * TR * TR + (c0 + i) * TR + lr]);
+                  xv[g2][i] = ld_na(&Vw[(int64_t)g2 * TR * TC + (c0 + i) * TR + lr]);
               }
 #ifdef CASC_I8_PROF
             long long tpa = clock64();
@@ -1210,10 +1264,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 if (g2 < ngroups) S = u192_add(S, u192_from_shifted(xv[g2][i], ngroups - 1 - g2));
               if (SPLITK) {  // the exact partial S of this k-block part
                 unsigned long long* sw =
-                    p.split_ws + ((int64_t)(item * 2 + (int)rank) * 3) * TR * TR + (c0 + i) * TR + lr;
+                    p.split_ws + ((int64_t)(item * 2 + (int)rank) * 3) * TR * TC + (c0 + i) * TR + lr;
                 sw[0] = S.l0;
-                sw[TR * TR] = S.l1;
-                sw[2 * TR * TR] = S.l2;
+                sw[TR * TC] = S.l1;
+                sw[2 * TR * TC] = S.l2;
                 continue;
               }
               rn_pair(S, ei + sF[c0 + i] - 12 - 8 * (y - 1), th[i], tl[i]);
@@ -1229,14 +1283,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               const int fj = sF[lc];
               const int widx = lc * TR + lr;
               // R26 detector, then C (+)= T
-              if (fabs(th[i]) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * 64);
+              if (fabs(th[i]) <= mulp2((double)kp, ei + fj - 50)) fl |= 1ull << (lc - half * CW);
               double ch = th[i], cl = tl[i];
               if (q > 0) dd_add(xch[i], xcl[i], th[i], tl[i], ch, cl);
               if (q + 1 < P) {
                 Ch[widx] = ch;
                 Cl[widx] = cl;
               } else {
-                const int64_t gj = cb * TR + lc;
+                const int64_t gj = cb * TC + lc;
                 if (gi < p.m && gj < p.n && (!TRI || (p.tri == 1 ? gi >= gj : gi <= gj))) {
                   double* oh = p.C_hi + gi * p.ldc + gj;
                   double* ol = p.C_lo + gi * p.ldc + gj;
@@ -1246,7 +1300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                      p.ab == 2 ? *ol : 0.0, p.ab == 2);
                   *oh = ch;
                   *ol = cl;
-                  if (p.flags) p.flags[gi * p.ldf + gj] = (uint8_t)((fl >> (lc - half * 64)) & 1);
+                  if (p.flags) p.flags[gi * p.ldf + gj] = (uint8_t)((fl >> (lc - half * CW)) & 1);
                 }
               }
             }
@@ -1306,14 +1360,14 @@ cudaError_t unpack(const void* packed, int64_t rows, int64_t k, int y, int8_t* D
 }
 
 int grid_for(int64_t m, int64_t n, int sms) {  // CTAs: 2 per pair, one pair per 2 SMs
-  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TC - 1) / TC);
   const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
   return (int)(2 * pairs);
 }
 // CTAs the GEMM scratch is sized for: small problems may run in split mode on
 // every CTA pair (split_parts)
 int ws_grid(int64_t m, int64_t n, int sms) {
-  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TC - 1) / TC);
   return tiles < 2 * (int64_t)(sms / 2) ? 2 * (sms / 2) : grid_for(m, n, sms);
 }
 // per-CTA T / C scratch, then the wave-sync counter
@@ -1353,7 +1407,7 @@ cudaError_t slice_map(CUtensorMap* map, const void* packed, const Pack& g, uint3
 // R26 detector, C = T, the R21 update -- the unsplit epilogue's steps on the
 // same exact S, hence bitwise the same C and flags.
 __global__ void __launch_bounds__(256) i8_split_reduce_kernel(const GemmArgs p) {
-  const int64_t RP = p.ga.R / 2, RB = p.gb.R;
+  const int64_t RP = p.ga.R / 2, RB = p.gb.R * CPB;
   const int y = p.ga.y;
   const int64_t mn = p.m * p.n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < mn;
@@ -1362,13 +1416,13 @@ __global__ void __launch_bounds__(256) i8_split_reduce_kernel(const GemmArgs p) 
     // column-major per tile)
     const int64_t j = idx / p.m, i = idx - j * p.m;
     const int64_t rp = i / (2 * TR), rank = (i / TR) & 1, lr = i % TR;
-    const int64_t cb = j / TR, col = j % TR;
+    const int64_t cb = j / TC, col = j % TC;
     const int64_t tile = tile_index(rp, cb, RP, RB);
     U192 S{0ull, 0ull, 0ull};
     for (int part = 0; part < p.ks; ++part) {
       const unsigned long long* sw =
-          p.split_ws + ((tile * p.ks + part) * 2 + rank) * 3 * TR * TR + col * TR + lr;
-      S = u192_add(S, U192{sw[0], sw[TR * TR], sw[2 * TR * TR]});
+          p.split_ws + ((tile * p.ks + part) * 2 + rank) * 3 * TR * TC + col * TR + lr;
+      S = u192_add(S, U192{sw[0], sw[TR * TC], sw[2 * TR * TC]});
     }
     const int ei = *reinterpret_cast<const int32_t*>(p.pa + exp_at(p.ga, i, 0));
     const int fj = *reinterpret_cast<const int32_t*>(p.pb + exp_at(p.gb, j, 0));
@@ -1393,7 +1447,7 @@ int split_parts(int64_t m, int64_t n, int64_t k, int sms) {
   const char* env = getenv("CASC_I8_SPLIT");  // "0": never (tests compare both)
   if (env && env[0] == '0') return 1;
   if (k > KC8) return 1;
-  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+  const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TC - 1) / TC);
   const int64_t np = sms / 2, kbn = (k + KB - 1) / KB;
   if (tiles >= 2 * np) return 1;
   auto eff = [&](int64_t ks) {
@@ -1449,7 +1503,7 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   }
   CUtensorMap mA, mB;
   cudaError_t e = slice_map(&mA, pa, a.ga, TR);
-  if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TR / 2);
+  if (e == cudaSuccess) e = slice_map(&mB, pb, a.gb, TC / 2);
   if (e != cudaSuccess) return e;
   if (dbg) {
     cudaFuncSetAttribute(i8_gemm_kernel<true, false, false>,
@@ -1459,14 +1513,14 @@ cudaError_t gemm(const void* pa, const void* pb, int64_t m, int64_t n, int64_t k
   }
   const int ks = tri ? 1 : split_parts(m, n, k, sms);
   if (ks > 1) {
-    const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TR - 1) / TR);
+    const int64_t tiles = ((m + 2 * TR - 1) / (2 * TR)) * ((n + TC - 1) / TC);
     const int64_t items = tiles * ks;
     const int g = (int)(2 * min(items, (int64_t)(sms / 2)));
     if (g > grid) return cudaErrorInvalidValue;  // ws sized for `grid` CTAs
     a.ks = ks;
     a.sync = nullptr;  // no wave synchronisation for a few waves
     if (cudaMallocAsync(reinterpret_cast<void**>(&a.split_ws),
-                        (size_t)items * 2 * 3 * TR * TR * sizeof(unsigned long long),
+                        (size_t)items * 2 * 3 * TR * TC * sizeof(unsigned long long),
                         st) != cudaSuccess)
       return cudaErrorMemoryAllocation;
     cudaFuncSetAttribute(i8_gemm_kernel<false, true, false>,

@@ -25,6 +25,10 @@ VARIANTS = {
     "skb32": ["CASC_I8_SYNC_KB=32"],
     "skb16": ["CASC_I8_SYNC_KB=16"],
     "skb8": ["CASC_I8_SYNC_KB=8"],
+    "tc64": ["CASC_I8_TC=64"],
+    "tc64a10": ["CASC_I8_TC=64", "CASC_I8_NSA=10", "CASC_I8_NSB=16"],
+    "tc64gm8": ["CASC_I8_TC=64", "CASC_I8_GROUP_M=8"],
+    "oldi8": [],
 }
 if sys.argv[1] == "build":
     import importlib.util
