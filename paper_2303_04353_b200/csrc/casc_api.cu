@@ -400,8 +400,13 @@ int casc_gemm_fp64x2_ws(int64_t m, int64_t n, int64_t k, const double* A_hi, con
   // the fused kernel's scratch head is zeroed first, so that the split launch
   // and the product launch are adjacent (programmatic dependent launch)
   void* scr = ws_counter(workspace, m, n, k);
-  if (cudaMemsetAsync(scr, 0, 2 * sizeof(unsigned int), S(stream)) != cudaSuccess)
-    return CASC_ERR_CUDA;
+  {  // the launch's work items: one per tile, or per (tile, panel) in split mode
+    const int Pz = split_plan(m, n, k, sms);
+    const int64_t items = ((m + casc::TM - 1) / casc::TM) * ((n + casc::TN - 1) / casc::TN) *
+                          (Pz ? Pz : 1);
+    if (cudaMemsetAsync(scr, 0, casc::gemm_scratch_zero_bytes(items), S(stream)) != cudaSuccess)
+      return CASC_ERR_CUDA;
+  }
   // phase 1: both splits in one launch
   cudaError_t e = casc::launch_split_ab(A_hi, A_lo, lda, m, B_hi, B_lo, ldb, n, k, w, pa, pb,
                                         S(stream), false, false);

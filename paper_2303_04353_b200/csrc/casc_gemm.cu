@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
         }
         if (tile >= ntiles) continue;
         int mb, nb, s0, s1, q0;
-        item_coords<TRI, AB && !SPLIT>(p, split_p, WIDE ? (int)(p.wide_list[tile] >> 3) : tile, mb,
+        item_coords<TRI, AB && !SPLIT>(p, split_p, WIDE ? (int)p.wide_list[tile] : tile, mb,
                                        nb, s0, s1,
                          q0);
         const uint8_t* srcA = p.pa + mb * p.a_blk + (int64_t)s0 * A_STAGE * 8;
@@ -264,14 +264,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
   uint32_t it = 0, pc = 0;  // stage counter (smem ring), panel counter (exponent ring)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int mb, nb, s0, s1, q0;
-    const unsigned int entry = WIDE ? p.wide_list[tile] : 0u;
-    const int item = WIDE ? (int)(entry >> 3) : tile;
+    const int item = WIDE ? (int)p.wide_list[tile] : tile;
+    // WIDE: the warps of this item that met a wide scale in the first launch
+    const unsigned int wmask = WIDE ? p.wide_mask[item] : 0u;
     item_coords<TRI, AB && !SPLIT>(p, split_p, item, mb, nb, s0, s1, q0);
     // Scales 2^(e_i + f_j) outside the normal powers of two (reading R16) are
     // rare; the combine of this kernel assumes one exact power of two per
     // element, and a warp that meets another scale in any panel of the item
-    // stores no C (so C and beta C stay intact) and lists (item, warp) for the
-    // WIDE re-run, whose combine scales ldexp-exactly.  Keeping that scaling out
+    // stores no C (so C and beta C stay intact), sets its bit in the item's warp
+    // mask and the item is listed once for the WIDE re-run, whose combine scales
+    // ldexp-exactly and which stores the masked warps' elements.  Keeping that scaling out
     // of this kernel keeps its registers spill-free (measured: a warp-uniform
     // branch between the two scalings made ptxas spill in the k loop, -3%).
     bool wide_seen = false;
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
           }
         wide_seen |= !__all_sync(0xffffffffu, emin + fmin >= -1022 && emax + fmax <= 1023);
       }
-      const bool store_c = WIDE ? (cw == (int)(entry & 7u)) : !wide_seen;
+      const bool store_c = WIDE ? ((wmask >> cw) & 1u) != 0 : !wide_seen;
       // two halves (m-subtiles 0-1, 2-3): 8 elements = 32 TMEM columns each
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -443,8 +445,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) casc_gemm_kernel(const GemmAr
       }
       if (!last) tmem_wait_st();
     }
-    if (!WIDE && wide_seen && lane == 0)  // C of this warp's elements: the WIDE re-run
-      p.wide_list[atomicAdd(p.wide_count, 1u)] = ((unsigned int)item << 3) | (unsigned int)cw;
+    if (!WIDE && wide_seen && lane == 0) {  // C of this warp's elements: the WIDE re-run
+      // one list entry per item (the first of its warps to get here), a mask of
+      // its warps: the re-run computes the item once and stores those warps
+      if (atomicOr(&p.wide_mask[item], 1u << cw) == 0u)
+        p.wide_list[atomicAdd(p.wide_count, 1u)] = (unsigned int)item;
+    }
     // ------------------------------ cancellation flags of this tile
     // (independent of the scales: the first launch stores them for every warp)
     if (!DBG && !WIDE && dst_fl) {
@@ -503,8 +509,12 @@ static bool wave_sync_on() {
   return !(s && s[0] == '0');
 }
 
+static size_t mask_bytes(int64_t items) {
+  return ((size_t)items * sizeof(unsigned int) + 255) / 256 * 256;
+}
+size_t gemm_scratch_zero_bytes(int64_t items) { return GEMM_SCRATCH_HEAD + mask_bytes(items); }
 size_t gemm_scratch_bytes(int64_t items) {
-  return ((size_t)GEMM_SCRATCH_HEAD + (size_t)items * NCW * sizeof(unsigned int) + 255) / 256 * 256;
+  return gemm_scratch_zero_bytes(items) + mask_bytes(items);
 }
 
 // a.scratch: gemm_scratch_bytes(work items) bytes of the caller's device memory,
@@ -522,9 +532,11 @@ cudaError_t launch_gemm(const GemmArgs& a_in, int num_sms, cudaStream_t st) {
   if (!a.scratch) return cudaErrorInvalidValue;
   a.wave_counter = reinterpret_cast<unsigned int*>(a.scratch);
   a.wide_count = a.wave_counter + 1;
-  a.wide_list = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(a.scratch) + GEMM_SCRATCH_HEAD);
+  a.wide_mask = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(a.scratch) + GEMM_SCRATCH_HEAD);
+  a.wide_list = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(a.scratch) +
+                                                gemm_scratch_zero_bytes(ntiles));
   if (!a.pdl) {  // else zeroed by the caller before the split launch (PDL edge kept)
-    cudaError_t e = cudaMemsetAsync(a.scratch, 0, 2 * sizeof(unsigned int), st);
+    cudaError_t e = cudaMemsetAsync(a.scratch, 0, gemm_scratch_zero_bytes(ntiles), st);
     if (e != cudaSuccess) return e;
   }
   // no wave barrier for few waves, split mode, or banded tiles of unequal length

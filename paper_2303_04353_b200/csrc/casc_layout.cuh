@@ -139,7 +139,8 @@ struct GemmArgs {
   void* scratch;               // per launch (caller memory, gemm_scratch_bytes): the
                                // three below, set and zeroed by launch_gemm
   unsigned int* wave_counter;  // producers meet here at each tile wave (or null)
-  unsigned int* wide_count;    // work items * 8 + warp listed for the WIDE re-run
+  unsigned int* wide_count;    // work items listed for the WIDE re-run
+  unsigned int* wide_mask;     // per work item: the warps that met a wide scale
   unsigned int* wide_list;
   // NEXT-4 BLAS update at the tile's last panel: C := alpha (x) AB (+) beta (x) C
   int ab;        // 0: plain C := AB; 1: apply alpha; 2: apply alpha and beta (reads C)
@@ -164,9 +165,13 @@ struct GemmArgs {
   int band;
 };
 
-constexpr int GEMM_SCRATCH_HEAD = 256;  // wave counter, WIDE count; then the WIDE list
+// scratch: [256-byte head: wave counter, WIDE count][WIDE warp masks, one u32
+// per item][WIDE list, one u32 per item]; the head and the masks are zeroed
+// per launch (gemm_scratch_zero_bytes)
+constexpr int GEMM_SCRATCH_HEAD = 256;
 cudaError_t launch_gemm(const GemmArgs& a, int num_sms, cudaStream_t st);
 size_t gemm_scratch_bytes(int64_t work_items);
+size_t gemm_scratch_zero_bytes(int64_t work_items);
 
 // Arguments of the single slice-GEMM kernel of the simple path (casc_simple.cu).
 struct SliceArgs {
