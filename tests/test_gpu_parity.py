@@ -748,20 +748,22 @@ def test_cfg1_all_entries_exact(casc, orc):
     assert np.array_equal(flags, o_fl) and flags.sum() == 0
 
 
-def test_cfg3b_full_size(casc, orc):
-    """cfg3 variant b (in-panel pairing, reading R13) at FULL size 4096 x 4096 x
-    32768 on the FP64 path: every entry flagged (bin 0 cancels in every panel),
-    flags equal the oracle's on sampled rows, and sampled entries stay within
-    eq:cascerr of the exact product (the north-star bound is not the bound for
-    adversarial cancellation, reading R14; the flag is)."""
+@pytest.mark.parametrize("variant", ["b", "c"])
+def test_cfg3bc_full_size(casc, orc, variant):
+    """cfg3 variants b (in-panel pairing) and c (cross-panel pairing), reading
+    R13, at FULL size 4096 x 4096 x 32768 on the FP64 path: b flags every entry
+    (bin 0 cancels in every panel), c none (the detector is blind across
+    panels); flags equal the oracle's on sampled rows, and sampled
+    entries stay within eq:cascerr of the exact product (the north-star bound is
+    not the bound for adversarial cancellation, reading R14; the flag is)."""
     import torch
-    d = I.make_config(3, variant="b")
+    d = I.make_config(3, variant=variant)
     m, n, k = d["m"], d["n"], d["k"]
     C_hi, C_lo, flags = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
                                               T(d["B_lo"]))
     torch.cuda.synchronize()
     C_hi, C_lo, flags = N(C_hi), N(C_lo), N(flags)
-    assert flags.all()
+    assert flags.all() if variant == "b" else not flags.any()
     rows = [0, 2049]
     o_hi, o_lo, o_fl = _sub_oracle(orc, d, rows, n - 64, n)
     assert np.array_equal(flags[rows, n - 64:], o_fl)
