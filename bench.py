@@ -167,7 +167,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
                      "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
                      "frac_vs_measured_peaks_bf16x2": achieved / _bf16x2_peak(),
                      "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
-                     if (mloc, n, k) == (16384, 16384, 16384) else None,
+                     if (mloc, n, k) == (16384, 16384, 16384) and y == 14 else None,
                      "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
                                "combine)",
                      "peak_source": f"{src}, sustained (burst {peak_burst:.0f}); "
@@ -662,6 +662,22 @@ def main():
                                     if world == 1 and not args.no_e2e else None)
             except Exception as ex:  # reported, never silently replaced
                 int8 = {"error": repr(ex)}
+            # the paper's "FP64 in terms of INT8" (§6: seven int8
+            # splits hold an FP64 mantissa): the same cascade with y = 7, 28
+            # products per panel -- FP64-class accuracy, context line
+            if isinstance(int8, dict) and "value" in int8:
+                try:
+                    f64 = measure_int8(casc, A_hi, A_lo, Bi_hi, Bi_lo, m, n, k, args.steps,
+                                       args.warmup, world=world, barrier=barrier,
+                                       max_over_ranks=mx, y=7)
+                    int8["fp64_class_y7"] = {
+                        "value": f64["value"], "unit": UNIT, "ms_per_step": f64["ms_per_step"],
+                        "roofline": f64["roofline"], "clocks": f64["clocks"],
+                        "note": "casc_i8 cascade with y = 7 slices (28 int8 products per "
+                                "panel): the paper's FP64-in-terms-of-INT8 (P:L3749-3751); "
+                                "FP64-class, not FP64x2-class, accuracy"}
+                except Exception as ex:
+                    int8["fp64_class_y7"] = {"error": repr(ex)}
             del Bi_hi, Bi_lo
 
     if rank != 0:
