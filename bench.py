@@ -333,11 +333,12 @@ def _num(s):
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=512, nthreads=0):
-    """ORACLE-CASCADE (as it stands; ORACLE-I8CASCADE with int8=True) on a
-    bounded sample of the workload: the first R rows x first C columns of C
-    with the full k.  R is calibrated so the run takes ~target_s seconds on
-    this host's cores."""
+def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=512, nthreads=0,
+                      dd=False):
+    """ORACLE-CASCADE (as it stands; ORACLE-I8CASCADE with int8=True, ORACLE-DD,
+    the triple-loop FP64x2 GEMM, with dd=True) on a bounded sample of the
+    workload: the first R rows x first C columns of C with the full k.  R is
+    calibrated so the run takes ~target_s seconds on this host's cores."""
     import oracle
     oracle.build()
     m, k = A_hi.shape
@@ -345,11 +346,11 @@ def cpu_oracle_sample(A_hi, A_lo, B_hi, B_lo, target_s=12.0, int8=False, cols=51
     C = min(n, cols)
     Bh, Bl = B_hi[:, :C].copy(), B_lo[:, :C].copy()
     R = min(m, 8)
-    fn = oracle.i8_casc_gemm if int8 else oracle.casc_gemm
+    fn = oracle.dd_gemm if dd else (oracle.i8_casc_gemm if int8 else oracle.casc_gemm)
     if nthreads <= 0:  # all host cores (explicit: the oracle's OpenMP setting is global)
         nthreads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else \
             (os.cpu_count() or 1)
-    name = "ORACLE-I8CASCADE" if int8 else "ORACLE-CASCADE"
+    name = "ORACLE-DD" if dd else ("ORACLE-I8CASCADE" if int8 else "ORACLE-CASCADE")
     while True:
         t0 = time.perf_counter()
         fn(A_hi[:R], A_lo[:R], Bh, Bl, nthreads=nthreads)
@@ -414,7 +415,7 @@ def _config(args, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cascade", choices=["cascade", "reference"])
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
@@ -797,6 +798,11 @@ def main():
         c1 = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=3.0, cols=64,
                                nthreads=1)
         cpu["one_core"] = {"value": c1["value"], "unit": UNIT, "sample": c1["sample"]}
+        # the paper's other CPU program (both baselines timed)
+        cdd = cpu_oracle_sample(A_hi_h, A_lo_h, B_full_hi, B_full_lo, target_s=4.0, cols=64,
+                                dd=True)
+        cpu["oracle_dd"] = {"value": cdd["value"], "unit": UNIT, "cores": cdd["cores"],
+                            "sample": cdd["sample"]}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
