@@ -366,3 +366,54 @@ def test_all_wide_costs_one_rerun(casc):
         return e0.elapsed_time(e1) / 3
     t_norm, t_wide = t(norm), t(wide)
     assert t_wide < 2.5 * t_norm, (t_norm, t_wide)
+
+
+def test_split_mode_mixed_wide_panels_bitwise(casc, orc):
+    """Split mode with the fold inside the product launch: a (tile, warp) whose
+    scales leave the normal powers of two in ONE panel only (rows of A and
+    rows of B in panel 1 scaled by 2^-600 / 2^-500: e + f < -1022 there) is
+    folded by the WIDE re-run, the others by the product launch.  C and the
+    flags are bitwise the per-tile mode's and the oracle's combine of the
+    GPU's own bins; an alpha / beta update likewise."""
+    import torch
+    m, n, k = 128, 192, 768
+    d = I.make_config(1, m=m, n=n, k=k, seed=71)
+    rows = np.arange(m) % 3 == 0
+    for x in ("A_hi", "A_lo"):
+        d[x][rows, 256:512] = np.ldexp(d[x][rows, 256:512], -600)
+    for x in ("B_hi", "B_lo"):
+        d[x][256:512, :] = np.ldexp(d[x][256:512, :], -500)
+    d["m"], d["n"], d["k"] = m, n, k
+    c = orc.select_widths(k)
+    _, e1 = orc.split_a_panel(d["A_hi"][:, 256:512], d["A_lo"][:, 256:512], c)
+    _, f1 = orc.split_b_panel(d["B_hi"][256:512], d["B_lo"][256:512], c)
+    es1 = e1[:, None].astype(int) + f1[None, :].astype(int)
+    assert (es1 < -1022).any() and (es1 >= -1022).any() and (_escales(orc, d) >= -1022).all()
+    args = [T(d[x]) for x in ("A_hi", "A_lo", "B_hi", "B_lo")]
+    split = [N(x) for x in casc.casc_gemm_fp64x2(*args)]
+    os.environ["CASC_SPLIT_MODE"] = "0"
+    try:
+        whole = [N(x) for x in casc.casc_gemm_fp64x2(*args)]
+    finally:
+        del os.environ["CASC_SPLIT_MODE"]
+    for a, b in zip(split, whole):
+        assert np.array_equal(bits(a) if a.dtype == np.float64 else a,
+                              bits(b) if b.dtype == np.float64 else b)
+    ref_hi, ref_lo, ref_fl = _oracle_combined(orc, d, lambda q: N(casc.casc_debug_bins(*args, q)))
+    assert np.array_equal(bits(split[0]), bits(ref_hi)) and np.array_equal(bits(split[1]),
+                                                                            bits(ref_lo))
+    assert np.array_equal(split[2], ref_fl)
+    al, be = (0.75, 2.0**-60), (1.5, 0.0)
+    C0 = np.random.default_rng(5).uniform(-1, 1, (m, n))
+    outs = []
+    for mode in ("1", "0"):
+        os.environ["CASC_SPLIT_MODE"] = mode
+        try:
+            C_hi, C_lo = T(C0), T(np.zeros((m, n)))
+            fl = torch.full((m, n), 7, dtype=torch.uint8, device="cuda")
+            casc.casc_gemm_fp64x2_ex("N", "N", al, *args, be, C_hi, C_lo, flags=fl)
+            outs.append((bits(N(C_hi)), bits(N(C_lo)), N(fl)))
+        finally:
+            del os.environ["CASC_SPLIT_MODE"]
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
