@@ -464,8 +464,22 @@ int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi, c
     const int64_t l = (lim + blk - 1) / blk * blk;
     return v < l ? v : l;
   };
-  const int64_t sr = fit(slab_rows ? slab_rows : casc::hostpipe::default_slab(m), casc::TM, m);
-  const int64_t sc = fit(slab_cols ? slab_cols : casc::hostpipe::default_slab(n), casc::TN, n);
+  int64_t dr = casc::hostpipe::default_slab(m), dc = casc::hostpipe::default_slab(n);
+  if (m >= 8192 && n >= 8192) {
+    // large operands: wave-aligned blocks, so that no block GEMM ends on a
+    // partly filled wave of 64 x 64 tiles (16384^3 on 148 SMs: 4096 x 2368 =
+    // 2368 tiles = 16 full waves; 4096 x 4096 would be 27.7 waves; measured
+    // e2e 2532 -> 2499 ms, scripts/e2e_slabs.py)
+    dr = 4096;
+    const int64_t rb = dr / casc::TM;
+    for (int64_t nb = 32; nb <= 96; ++nb)
+      if ((rb * nb) % sms == 0) {
+        dc = nb * casc::TN;
+        break;
+      }
+  }
+  const int64_t sr = fit(slab_rows ? slab_rows : dr, casc::TM, m);
+  const int64_t sc = fit(slab_cols ? slab_cols : dc, casc::TN, n);
   const casc::Widths w = widths_for(k);
   const int nst = (int)(casc::kpad_of(k) / casc::BK);
   int launches = 0;
