@@ -36,7 +36,9 @@ def bitwise(x, y):
 @pytest.mark.parametrize("m,n,k,slab,scol,pinned", [
     (300, 257, 700, 64, 64, True), (130, 200, 513, 64, 128, False), (1000, 300, 1100, 0, 0, True),
     (2048, 1024, 1024, 512, 256, True), (65, 64, 9000, 128, 0, True), (1, 1, 1, 0, 0, False),
-    (200, 1000, 300, 0, 192, True)])
+    (200, 1000, 300, 0, 192, True),
+    # m, n >= 8192: the default wave-aligned blocks (4096 x 2368 on 148 SMs), ragged both ways
+    (8200, 9000, 300, 0, 0, True)])
 def test_host_bitwise_device(casc, m, n, k, slab, scol, pinned):
     import torch
     d = I.make_config(2, m=m, n=n, k=k, seed=51)
