@@ -97,7 +97,8 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
     import torch
     from paper_2303_04353_b200.multigpu import I8_BLOCK, ShardedCascGemm, i8_cuda_ops
     dev = A_hi.device
-    op = ShardedCascGemm(m, n, k, ops=i8_cuda_ops(y), device=dev, block=I8_BLOCK)
+    op = ShardedCascGemm(m, n, k, ops=i8_cuda_ops(y), device=dev, block=I8_BLOCK,
+                         gather=choose_gather(world, dev, "packed"))
     mloc = op.r1 - op.r0
     C_hi = torch.empty((mloc, n), dtype=torch.float64, device=dev)
     C_lo = torch.empty_like(C_hi)
@@ -155,6 +156,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
     ops = 2.0 * prods * mloc * n * k
     peak_sus, peak_burst, src = load_int8_peak()
     achieved = ops / (gemm_ms * 1e-3) / 1e12
+    op.close()  # p2p: peer mappings and the exported buffer (collective)
     del op, C_hi, C_lo, fl
     return {
         "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3754), y=%d slices, "
@@ -248,7 +250,30 @@ def _gemm_ms(ph):
     (that interval also holds any exchange time the first did not hide)."""
     if "gemm" in ph:
         return ph["gemm"]
-    return ph.get("gemm_own_cols", 0.0) + ph.get("gemm_other_cols", 0.0)
+    return (ph.get("gemm_own_cols", 0.0) + ph.get("gemm_other_cols", 0.0) +
+            ph.get("gemm_other_cols_p2p", 0.0))
+
+
+def choose_gather(world, dev, fallback):
+    """N > 1: "p2p" (the packed slabs pulled from the other ranks' exported
+    buffers by the copy engines, no collective and no SM for the exchange) when
+    every pair of this node's GPUs has peer access -- decided collectively so
+    all ranks agree; else `fallback` (an NCCL all-gather).  CASC_BENCH_GATHER
+    overrides."""
+    import torch
+    import torch.distributed as dist
+    forced = os.environ.get("CASC_BENCH_GATHER")
+    if forced:
+        return forced
+    if world == 1:
+        return fallback
+    me = dev.index
+    ok = all(torch.cuda.can_device_access_peer(me, o) for o in range(torch.cuda.device_count())
+             if o != me)
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                     device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return "p2p" if t.item() == 1 else fallback
 
 
 def _bf16x2_peak():
@@ -401,12 +426,17 @@ def _cfg4_block(I, rows):
     return I.make_config(4, rows=slice(0, rows))
 
 
-def _config(args, world):
+def _config(args, world, gather=None):
     m, n, k = CONFIGS[args.config]
+    par = "single B200"
+    if world > 1:
+        par = (f"C row-sharded x{world}, packed B slabs pulled from the other ranks' exported "
+               "buffers by the copy engines (CUDA IPC over NVLink), each slab's GEMM as it lands"
+               if gather == "p2p" else
+               f"C row-sharded x{world}, FP64x2 B slabs all-gathered (NCCL) and split on every "
+               "rank; INT8 path: packed slabs all-gathered")
     return {"workload": CONFIG_TEXT[args.config], "m": m, "n": n, "k": k,
-            "parallelism": f"C row-sharded x{world}, FP64x2 B slabs all-gathered (NCCL) and "
-                           "split on every rank; INT8 path: packed slabs all-gathered"
-            if world > 1 else "single B200",
+            "parallelism": par,
             "l2": "inputs (16 B/elt x (mk+kn)) larger than the 126 MB L2; no flush",
             "k_panel": 256, "widths": [22, 21, 21] if k >= 256 else None}
 
@@ -496,7 +526,8 @@ def main():
     # N > 1: the FP64x2 slabs of B are all-gathered (16 B / element) and every
     # rank splits all of B locally: fewer NVLink bytes than gathering the
     # 56 B / element packed slices
-    op = ShardedCascGemm(m, n, k, device=dev, gather="raw")
+    gather = choose_gather(world, dev, "raw")
+    op = ShardedCascGemm(m, n, k, device=dev, gather=gather)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -684,6 +715,7 @@ def main():
     if rank != 0:
         if world > 1:
             dist.barrier()
+            op.close()
             dist.destroy_process_group()
         return
 
@@ -809,7 +841,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "step_stats": step_stats,
         "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config(args, world),
+        "config": _config(args, world, gather),
         "frac_of_fp64tc_roofline": value / 1e3 / (world * peak_sus / 10.0),
         "paper_convention_gflops": 10.0 * value,
         "t_over_cublas_dgemm": dgemm_ratio,
@@ -831,6 +863,7 @@ def main():
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
+        op.close()
         dist.destroy_process_group()
 
 

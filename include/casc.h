@@ -568,6 +568,38 @@ int casc_i8_debug_bins(int64_t m, int64_t n, int64_t k,
                        const double* B_hi, const double* B_lo, int64_t ldb,
                        int y, int64_t panel, int32_t* bins, casc_stream_t stream);
 
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU exchange over peer memory (north star: "B      */
+/* slices broadcast over NVLink"; paper_2303_04353_b200/multigpu.py,        */
+/* gather = "p2p").  Each rank exports the device buffer holding its packed  */
+/* column slab of B; the other ranks map it and pull the slab with the copy  */
+/* engines (no SM is used by the exchange; a slab's GEMM starts when that    */
+/* slab has landed).  Host code; ordering between ranks is the caller's       */
+/* (host-side barriers), no kernel waits on another rank.                     */
+#define CASC_IPC_HANDLE_BYTES 64
+
+/* cudaMalloc `bytes` (> 0) on the current device and export it:
+ *   *ptr    the device pointer (owned by the caller; release with casc_ipc_free);
+ *   handle  CASC_IPC_HANDLE_BYTES bytes of host memory receiving the
+ *           cudaIpcMemHandle_t to send to the other ranks.
+ * CASC_ERR_INVALID for NULL arguments or bytes == 0, CASC_ERR_CUDA if the
+ * allocation or the export fails (*ptr = NULL then). */
+int casc_ipc_alloc(size_t bytes, void** ptr, void* handle);
+/* cudaFree of a casc_ipc_alloc buffer (NULL: no-op).  Host-synchronising as cudaFree. */
+int casc_ipc_free(void* ptr);
+/* Map another process's exported buffer into this process (current device,
+ * peer access enabled lazily): *ptr = its base address here.  CASC_ERR_CUDA
+ * if the handle cannot be opened (e.g. no peer access between the devices,
+ * or a handle of this same process). */
+int casc_ipc_open(const void* handle, void** ptr);
+/* Unmap a casc_ipc_open pointer (NULL: no-op). */
+int casc_ipc_close(void* ptr);
+/* Enqueue a copy of `bytes` bytes from src to dst on `stream` (device, peer
+ * or host pointers: cudaMemcpyDefault; a peer-mapped src is read over NVLink
+ * by the copy engine).  bytes == 0 is a no-op; NULL with bytes > 0 is
+ * CASC_ERR_INVALID. */
+int casc_copy_async(void* dst, const void* src, size_t bytes, casc_stream_t stream);
+
 /* Number of kernel launches the last successful call of the given entry point
  * family enqueued on this host thread (for launch accounting in bench.py). */
 int casc_last_launch_count(void);

@@ -813,3 +813,55 @@ def casc_i8_gemm_packed(m, n, k, packed_a, packed_b, y: int = I8_DEFAULT_SLICES,
                                        _ptr(ws), ws.numel(), _stream(stream)),
            "casc_i8_gemm_packed_ld")
     return C_hi, C_lo, flags
+
+
+# ------------------------------------------------------------ peer-memory exchange
+# (include/casc.h: casc_ipc_alloc / _free / _open / _close, casc_copy_async)
+_sig("casc_ipc_alloc", [_sz, ctypes.POINTER(_vp), _vp])
+_sig("casc_ipc_free", [_vp])
+_sig("casc_ipc_open", [_vp, ctypes.POINTER(_vp)])
+_sig("casc_ipc_close", [_vp])
+_sig("casc_copy_async", [_vp, _vp, _sz, _vp])
+CASC_IPC_HANDLE_BYTES = 64
+EXPORTED += ["casc_ipc_alloc", "casc_ipc_free", "casc_ipc_open", "casc_ipc_close",
+             "casc_copy_async"]
+
+
+class _DevBuf:
+    """__cuda_array_interface__ of a raw device byte range (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def casc_ipc_alloc(nbytes: int):
+    """Exported device buffer: (ptr, handle bytes, uint8 tensor view of it)."""
+    ptr = _vp()
+    handle = ctypes.create_string_buffer(CASC_IPC_HANDLE_BYTES)
+    _check(_lib.casc_ipc_alloc(int(nbytes), ctypes.byref(ptr), handle), "casc_ipc_alloc")
+    view = torch.as_tensor(_DevBuf(ptr.value, int(nbytes)), device="cuda")
+    return ptr.value, handle.raw, view
+
+
+def casc_ipc_free(ptr: int):
+    _check(_lib.casc_ipc_free(ptr), "casc_ipc_free")
+
+
+def casc_ipc_open(handle: bytes) -> int:
+    """Map another process's exported buffer; returns its base address here."""
+    if len(handle) != CASC_IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be 64 bytes")
+    ptr = _vp()
+    buf = ctypes.create_string_buffer(handle, CASC_IPC_HANDLE_BYTES)
+    _check(_lib.casc_ipc_open(buf, ctypes.byref(ptr)), "casc_ipc_open")
+    return ptr.value
+
+
+def casc_ipc_close(ptr: int):
+    _check(_lib.casc_ipc_close(ptr), "casc_ipc_close")
+
+
+def casc_copy_async(dst: int, src: int, nbytes: int, stream=None):
+    """Enqueue a copy-engine copy (cudaMemcpyDefault) of nbytes on `stream`."""
+    _check(_lib.casc_copy_async(dst, src, int(nbytes), _stream(stream)), "casc_copy_async")

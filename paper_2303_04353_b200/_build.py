@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcasc.so")
 SOURCES = ["casc_split.cu", "casc_gemm.cu", "casc_simple.cu", "casc_blas.cu", "casc_api.cu",
-           "casc_i8.cu", "casc_level3.cu"]
+           "casc_i8.cu", "casc_level3.cu", "casc_exchange.cu"]
 HEADERS = ["casc_layout.cuh", "casc_ptx.cuh", "casc_dd.cuh", "casc_host.cuh", os.path.join("..", "..", "include", "casc.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -103,13 +103,19 @@ class ShardedCascGemm:
         themselves are all-gathered (16 B per element) and every rank splits all
         of B locally, slab by slab into the packed layout (the byte-cheaper
         choice for the FP64 cascade).  Bitwise the same result.
+        "p2p": no collective; every rank exports the device buffer holding its
+        packed slab (CUDA IPC), maps the others' and PULLS their slabs with the
+        copy engines (casc_copy_async on two copy streams), so the exchange takes
+        no SM from the GEMM and each slab's GEMM starts as soon as that slab has
+        landed (own slab first, then r+1, r+2, ...); ordering between ranks is
+        two CPU barriers per call (gloo group), no kernel waits on another rank.
         overlap (N > 1): the exchange runs while the GEMM multiplies the rank's
         own column slab (casc_gemm_packed_ld on a column block of C), then the
         other columns are multiplied once it has landed -- two stream-ordered
         launches, no kernel waits on another (B200_PROFILING.md); bitwise the
         same C, since every element depends only on its row and column."""
-        if gather not in ("packed", "raw"):
-            raise ValueError("gather must be 'packed' or 'raw'")
+        if gather not in ("packed", "raw", "p2p"):
+            raise ValueError("gather must be 'packed', 'raw' or 'p2p'")
         self.m, self.n, self.k = m, n, k
         self.block = block
         self.gather = gather
@@ -127,8 +133,29 @@ class ShardedCascGemm:
         # packed B of all ranks: chunk r = rank r's column slab (column-block major,
         # so the gathered buffer IS the packed B of the whole matrix); with one
         # rank it is just the local pack
-        self.packed_b_full = torch.zeros(self.chunk * self.world, dtype=torch.uint8,
-                                         device=self.device)
+        self.p2p = gather == "p2p" and self.world > 1
+        self._ipc_ptr = None
+        if self.p2p:
+            import paper_2303_04353_b200 as casc
+            self._casc = casc
+            self.cpu_group = dist.new_group(backend="gloo")
+            with torch.cuda.device(self.device):
+                self._ipc_ptr, handle, self.packed_b_full = casc.casc_ipc_alloc(
+                    self.chunk * self.world)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, handle, group=self.cpu_group)
+            self.peer_ptrs = {}
+            with torch.cuda.device(self.device):
+                for q in range(self.world):
+                    if q != self.rank:
+                        self.peer_ptrs[q] = casc.casc_ipc_open(handles[q])
+                self.copy_streams = [torch.cuda.Stream(self.device) for _ in range(2)]
+                self.slab_events = [torch.cuda.Event() for _ in range(self.world)]
+                self.copy_done = [torch.cuda.Event() for _ in self.copy_streams]
+            self.copies_pending = False
+        else:
+            self.packed_b_full = torch.zeros(self.chunk * self.world, dtype=torch.uint8,
+                                             device=self.device)
         self.own = self.packed_b_full[self.rank * self.chunk:(self.rank + 1) * self.chunk]
         self.packed_a = None
         self.raw = self.gather == "raw" and self.world > 1
@@ -138,7 +165,10 @@ class ShardedCascGemm:
                                         device=self.device)
         self.slabs = [col_slab(n, self.world, r, block)[:2] for r in range(self.world)]
         # names of the intervals between the 5 events of __call__ (bench phases)
-        if self.overlap:
+        if self.p2p:
+            self.phase_names = ["split_a", "split_b_own", "gemm_own_cols",
+                                "gemm_other_cols_p2p"]
+        elif self.overlap:
             self.phase_names = ["split_a", "split_b_own", "gemm_own_cols", "gemm_other_cols"]
         elif self.raw:
             self.phase_names = ["split_a", "allgather_raw", "split_b", "gemm"]
@@ -200,6 +230,9 @@ class ShardedCascGemm:
             self._gemm_cols(self.packed_a, 0, self.n, C_hi, C_lo, flags, count)
             rec(3)
             return C_hi, C_lo, flags
+        if self.p2p:
+            return self._call_p2p(A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi, C_lo, flags,
+                                  rec, count)
         if self.raw:
             mine = self.raw_full[self.rank]
             if w > 0:
@@ -245,3 +278,60 @@ class ShardedCascGemm:
         self._gemm_cols(self.packed_a, 0, self.n, C_hi, C_lo, flags, count)
         rec(3)
         return C_hi, C_lo, flags
+
+    def _call_p2p(self, A_hi_rows, A_lo_rows, B_hi_slab, B_lo_slab, C_hi, C_lo, flags, rec,
+                  count):
+        """gather = "p2p" (see __init__).  A's pack is already enqueued."""
+        cur = torch.cuda.current_stream(self.device)
+        # every rank has finished pulling the slabs of the previous call before
+        # any rank overwrites its own slab (host waits for its own copy streams)
+        if self.copies_pending:
+            for ev in self.copy_done:
+                ev.synchronize()
+        dist.barrier(group=self.cpu_group)
+        self._pack_slab(self.rank, B_hi_slab, B_lo_slab, count)
+        rec(1)
+        packed = torch.cuda.Event()
+        packed.record(cur)
+        packed.synchronize()  # own slab packed (also: the previous call's GEMMs are done)
+        dist.barrier(group=self.cpu_group)  # every rank's own slab is packed
+        self._gemm_cols(self.packed_a, self.c0, self.c1, C_hi, C_lo, flags, count)
+        rec(2)
+        order = [(self.rank + i) % self.world for i in range(1, self.world)]
+        for i, q in enumerate(order):  # copy-engine pulls, two streams, neighbours first
+            a0, a1 = self.slabs[q]
+            if a1 <= a0:
+                continue
+            cs = self.copy_streams[i % len(self.copy_streams)]
+            off = q * self.chunk
+            self._casc.casc_copy_async(self._ipc_ptr + off, self.peer_ptrs[q] + off,
+                                       self._used(a0, a1), stream=cs)
+            self.slab_events[q].record(cs)
+        for ev, cs in zip(self.copy_done, self.copy_streams):
+            ev.record(cs)
+        self.copies_pending = True
+        for q in order:  # each slab's columns as soon as that slab has landed
+            a0, a1 = self.slabs[q]
+            if a1 <= a0:
+                continue
+            cur.wait_event(self.slab_events[q])
+            self._gemm_cols(self.packed_a, a0, a1, C_hi, C_lo, flags, count)
+        rec(3)
+        return C_hi, C_lo, flags
+
+    def close(self):
+        """Release the peer mappings and the exported buffer (p2p; collective)."""
+        if not self.p2p or self._ipc_ptr is None:
+            return
+        torch.cuda.synchronize(self.device)
+        if self.copies_pending:
+            for ev in self.copy_done:
+                ev.synchronize()
+        dist.barrier(group=self.cpu_group)  # no rank still copies from a peer
+        for ptr in self.peer_ptrs.values():
+            self._casc.casc_ipc_close(ptr)
+        dist.barrier(group=self.cpu_group)  # every mapping closed before the frees
+        self.packed_b_full = None
+        self.own = None
+        self._casc.casc_ipc_free(self._ipc_ptr)
+        self._ipc_ptr = None

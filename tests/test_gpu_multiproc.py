@@ -3,8 +3,10 @@ this build has (gloo backend for the exchange; the ranks' kernels never wait
 on each other, so sharing a device is safe): every rank runs the production
 pack / all-gather / packed-GEMM sequence of ShardedCascGemm on its rows, and
 the gathered C is bitwise the single-process result (P-invariance: k is never
-split), for the FP64 cascade ('raw' and 'packed' exchanges) and the INT8
-cascade."""
+split), for the FP64 cascade ('raw' and 'packed' exchanges, and 'p2p': the
+slabs pulled from the other process's exported buffer by the copy engine, CUDA
+IPC within the one device, called twice to exercise the reuse ordering) and
+the INT8 cascade ('packed', 'p2p')."""
 
 import os
 import socket
@@ -37,26 +39,32 @@ def _rank(rank, world, port, m, n, k, kind, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        i8 = kind == "i8"
+        i8 = kind in ("i8", "i8p2p")
         block = I8_BLOCK if i8 else BLOCK
         r0, r1 = row_shard(m, world, rank)
         c0, c1, _ = col_slab(n, world, rank, block)
         d = I.make_config(1, m=m, n=n, k=k, seed=77)
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        gather = {"i8": "packed", "packed": "packed", "raw": "raw", "p2p": "p2p",
+                  "i8p2p": "p2p"}[kind]
         op = ShardedCascGemm(m, n, k, ops=i8_cuda_ops() if i8 else None,
-                             device=torch.device("cuda", 0), block=block,
-                             gather="packed" if kind in ("i8", "packed") else "raw")
-        C_hi, C_lo, fl = op(T(d["A_hi"][r0:r1]), T(d["A_lo"][r0:r1]), T(d["B_hi"][:, c0:c1]),
-                            T(d["B_lo"][:, c0:c1]))
+                             device=torch.device("cuda", 0), block=block, gather=gather)
+        args = (T(d["A_hi"][r0:r1]), T(d["A_lo"][r0:r1]), T(d["B_hi"][:, c0:c1]),
+                T(d["B_lo"][:, c0:c1]))
+        C_hi, C_lo, fl = op(*args)
+        if gather == "p2p":  # a second call reuses the exported buffers (ordering barriers)
+            C_hi, C_lo, fl = op(*args)
         torch.cuda.synchronize()
         q.put((rank, C_hi.cpu().numpy(), C_lo.cpu().numpy(), fl.cpu().numpy()))
+        op.close()
         dist.barrier()
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("kind,m,n,k", [("raw", 300, 520, 700), ("packed", 257, 200, 300),
-                                        ("i8", 600, 700, 900)])
+                                        ("i8", 600, 700, 900), ("p2p", 300, 520, 700),
+                                        ("i8p2p", 600, 700, 900)])
 def test_two_processes_one_gpu_bitwise(kind, m, n, k):
     import torch
 
@@ -74,7 +82,7 @@ def test_two_processes_one_gpu_bitwise(kind, m, n, k):
     C = [np.concatenate([got[0][i], got[1][i]]) for i in range(3)]
     d = I.make_config(1, m=m, n=n, k=k, seed=77)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    fn = casc.casc_i8_gemm_fp64x2 if kind == "i8" else casc.casc_gemm_fp64x2
+    fn = casc.casc_i8_gemm_fp64x2 if kind in ("i8", "i8p2p") else casc.casc_gemm_fp64x2
     ref = [x.cpu().numpy() for x in fn(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]), T(d["B_lo"]))]
     for a, b in zip(C, ref):
         assert np.array_equal(np.ascontiguousarray(a).view(np.uint8),
