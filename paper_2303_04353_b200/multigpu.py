@@ -135,25 +135,12 @@ class ShardedCascGemm:
         # rank it is just the local pack
         self.p2p = gather == "p2p" and self.world > 1
         self._ipc_ptr = None
-        if self.p2p:
-            import paper_2303_04353_b200 as casc
-            self._casc = casc
-            self.cpu_group = dist.new_group(backend="gloo")
-            with torch.cuda.device(self.device):
-                self._ipc_ptr, handle, self.packed_b_full = casc.casc_ipc_alloc(
-                    self.chunk * self.world)
-            handles = [None] * self.world
-            dist.all_gather_object(handles, handle, group=self.cpu_group)
-            self.peer_ptrs = {}
-            with torch.cuda.device(self.device):
-                for q in range(self.world):
-                    if q != self.rank:
-                        self.peer_ptrs[q] = casc.casc_ipc_open(handles[q])
-                self.copy_streams = [torch.cuda.Stream(self.device) for _ in range(2)]
-                self.slab_events = [torch.cuda.Event() for _ in range(self.world)]
-                self.copy_done = [torch.cuda.Event() for _ in self.copy_streams]
-            self.copies_pending = False
-        else:
+        if self.p2p and not self._setup_p2p():
+            # some rank could not export or map a buffer: every rank falls back
+            # (decided collectively) to the NCCL all-gather of raw slabs
+            self.p2p = False
+            self.gather = gather = "raw"
+        if not self.p2p:
             self.packed_b_full = torch.zeros(self.chunk * self.world, dtype=torch.uint8,
                                              device=self.device)
         self.own = self.packed_b_full[self.rank * self.chunk:(self.rank + 1) * self.chunk]
@@ -175,6 +162,51 @@ class ShardedCascGemm:
         else:
             self.phase_names = ["split_a", "split_b", "allgather", "gemm"]
         self.launches = 0
+
+    def _setup_p2p(self) -> bool:
+        """Export this rank's packed-B buffer, map every other rank's (CUDA IPC).
+        Collective over a gloo group; returns False on every rank (after undoing
+        what was set up) if any rank failed."""
+        import paper_2303_04353_b200 as casc
+        self._casc = casc
+        self.cpu_group = dist.new_group(backend="gloo")
+        self.peer_ptrs = {}
+        handle, ok = None, True
+        try:
+            with torch.cuda.device(self.device):
+                self._ipc_ptr, handle, self.packed_b_full = casc.casc_ipc_alloc(
+                    self.chunk * self.world)
+        except Exception:
+            ok = False
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle if ok else None, group=self.cpu_group)
+        ok = ok and all(h is not None for h in handles)
+        if ok:
+            try:
+                with torch.cuda.device(self.device):
+                    for q in range(self.world):
+                        if q != self.rank:
+                            self.peer_ptrs[q] = casc.casc_ipc_open(handles[q])
+            except Exception:
+                ok = False
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=self.cpu_group)
+        if all(oks):
+            with torch.cuda.device(self.device):
+                self.copy_streams = [torch.cuda.Stream(self.device) for _ in range(2)]
+                self.slab_events = [torch.cuda.Event() for _ in range(self.world)]
+                self.copy_done = [torch.cuda.Event() for _ in self.copy_streams]
+            self.copies_pending = False
+            return True
+        for ptr in self.peer_ptrs.values():
+            casc.casc_ipc_close(ptr)
+        dist.barrier(group=self.cpu_group)  # every mapping closed before the frees
+        self.peer_ptrs = {}
+        self.packed_b_full = None
+        if self._ipc_ptr is not None:
+            casc.casc_ipc_free(self._ipc_ptr)
+            self._ipc_ptr = None
+        return False
 
     def _all_gather(self, full, mine, async_op=False):
         """In-place all-gather of equal chunks (rank r's chunk at offset r): one

@@ -102,7 +102,7 @@ def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed", overlap=
     B_lo = torch.from_numpy(d["B_lo"][:, op.c0:op.c1].copy())
     C_hi, C_lo, fl = op(A_hi, A_lo, B_hi, B_lo)
     np.savez(os.path.join(out, f"r{rank}.npz"), C_hi=C_hi.numpy(), C_lo=C_lo.numpy(),
-             fl=fl.numpy(), r0=op.r0, r1=op.r1)
+             fl=fl.numpy(), r0=op.r0, r1=op.r1, gather=op.gather)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -111,14 +111,17 @@ def _worker(rank, world, port, m, n, k, out, i8=False, gather="packed", overlap=
     (2, 10, 150, 300, "packed", True), (2, 7, 64, 40, "packed", True),
     (2, 10, 150, 300, "raw", True), (2, 5, 200, 70, "raw", True),
     (2, 10, 150, 300, "packed", False), (2, 5, 200, 70, "raw", False),
-    (4, 9, 300, 80, "packed", True), (4, 6, 200, 70, "raw", True), (4, 9, 130, 40, "packed", False)])
+    (4, 9, 300, 80, "packed", True), (4, 6, 200, 70, "raw", True), (4, 9, 130, 40, "packed", False),
+    (2, 10, 150, 300, "p2p", True), (4, 6, 200, 70, "p2p", True)])
 def test_gloo_world_p_invariance(tmp_path, orc, world, m, n, k, gather, overlap):
     """The production exchange (in-place all_gather_into_tensor, the call NCCL
     runs on the GPUs) on gloo: world 2 and 4, packed and raw exchanges, with
     the overlapped schedule (own column slab multiplied while the exchange
     runs, then the other columns) and the serial one: the same bits as one
     process.  gather="raw" exchanges the FP64x2 slabs and packs all of B on
-    every rank (SURVEY §8(e) byte-cheaper alternative)."""
+    every rank (SURVEY §8(e) byte-cheaper alternative).  gather="p2p" needs
+    CUDA IPC: here no rank can export a device buffer, so every rank falls back
+    together (collective decision) to the raw all-gather: the same bits."""
     mp.spawn(_worker, args=(world, _free_port(), m, n, k, str(tmp_path), False, gather, overlap),
              nprocs=world, join=True)
     d = I.make_config(1, m=m, n=n, k=k, seed=21)
@@ -130,6 +133,7 @@ def test_gloo_world_p_invariance(tmp_path, orc, world, m, n, k, gather, overlap)
         assert np.array_equal(z["C_hi"], ref_hi[r0:r1])
         assert np.array_equal(z["C_lo"], ref_lo[r0:r1])
         assert np.array_equal(z["fl"], ref_fl[r0:r1])
+        assert str(z["gather"]) == ("raw" if gather == "p2p" else gather)
         rows += r1 - r0
     assert rows == m
 
