@@ -22,8 +22,12 @@ values from exact integer arithmetic instead:
    exact value of every entry is assembled as a Python integer in units of
    2^-1100 (every binary64 number is an integer multiple of 2^-1074), with
    the row / column scales applied as shifts.
+5. k > 1024: C* = sum over k-chunks of 1024 of the chunks' exact products,
+   each assembled as above (its own row / column scales) in the same integer
+   units, added as Python integers -- exact, so the chunking is invisible.
 Pinned against the superaccumulator (tests/test_oracle_bounds.py): equal
-RN(C*) (hi, lo) bit for bit on sampled entries of cfg1 / cfg2-style data.
+RN(C*) (hi, lo) bit for bit on sampled entries of cfg1 / cfg2-style data,
+also with k > 1024.
 """
 
 from __future__ import annotations
@@ -71,7 +75,18 @@ def _needed_digits(*limbs):
 
 def exact_product(A_hi, A_lo, B_hi, B_lo):
     """Exact C* = (A_hi + A_lo)(B_hi + B_lo) for every entry, as an object array
-    of Python ints in units of 2^UNIT_EXP (m x n)."""
+    of Python ints in units of 2^UNIT_EXP (m x n); k > 1024 in exact chunks."""
+    k = A_hi.shape[1]
+    X = None
+    for p0 in range(0, max(k, 1), MAX_K):
+        p1 = min(k, p0 + MAX_K)
+        part = _exact_chunk(A_hi[:, p0:p1], A_lo[:, p0:p1], B_hi[p0:p1], B_lo[p0:p1])
+        X = part if X is None else X + part  # Python integers: exact
+    return X
+
+
+def _exact_chunk(A_hi, A_lo, B_hi, B_lo):
+    """exact_product for k <= MAX_K"""
     m, k = A_hi.shape
     n = B_hi.shape[1]
     if k > MAX_K:

@@ -305,9 +305,27 @@ def test_exact_fixed_equals_superaccumulator(orc, cfg, m, n, k):
                               C_hi, Cl)
         assert np.array_equal(err.ravel(), r["err"])
         assert np.array_equal(absx.ravel(), np.abs(r["ex_hi"]))  # |RN(C*)|
-    with pytest.raises(ValueError):
-        EF.exact_product(np.ones((2, 1025)), np.zeros((2, 1025)), np.ones((1025, 2)),
-                         np.zeros((1025, 2)))
+    with pytest.raises(ValueError):  # one digit GEMM must stay exact
+        EF._exact_chunk(np.ones((2, 1025)), np.zeros((2, 1025)), np.ones((1025, 2)),
+                        np.zeros((1025, 2)))
+
+
+@pytest.mark.parametrize("cfg,m,n,k", [(1, 12, 9, 2500), (2, 10, 7, 3000)])
+def test_exact_fixed_chunked_k_equals_superaccumulator(orc, cfg, m, n, k):
+    """k > 1024: the exact sum of the exact k-chunk products (used for the
+    full-size cfg2-4 line checks) equals the superaccumulator's exact error on
+    every entry, and all-ones rows give the integer k exactly."""
+    from oracle import exact_fixed as EF
+    d = I.make_config(cfg, m=m, n=n, k=k)
+    C_hi, C_lo, _ = orc.casc_gemm(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"])
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    err, _ = EF.errors(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], C_hi, C_lo)
+    r = orc.exact_entries(d["A_hi"], d["A_lo"], d["B_hi"], d["B_lo"], ii.ravel(), jj.ravel(),
+                          C_hi, C_lo)
+    assert np.array_equal(err.ravel(), r["err"])
+    one = np.ones((1, k))
+    X = EF.exact_product(one, 0 * one, one.T.copy(), 0 * one.T)
+    assert X[0, 0] == k << -EF.UNIT_EXP
 
 
 # ----------------------------------------------------------------- SYMM / TRMM / right TRSM (R28, R29)
