@@ -320,6 +320,43 @@ def test_full_size_configs_sampled(casc, orc, cfg, variant):
     assert flags.sum() == 0
 
 
+@pytest.mark.parametrize("cfg,variant", [(2, "a"), (3, "a"), (4, "a")])
+def test_full_size_exact_lines(casc, orc, cfg, variant):
+    """BASELINE configs 2, 3 and 4 at FULL size, as bench.py launches them:
+    EVERY entry of one full row, one full column (cfg2, cfg3: the column needs
+    all of A's digits, minutes at cfg4) and a 64 x 128 block of C against the
+    exact product (oracle/exact_fixed.py, k in exact chunks) within the
+    north-star bound, and the full row against ORACLE-CASCADE (flags identical,
+    C within twice the bound)."""
+    import torch
+    from oracle import exact_fixed as EF
+    d = I.make_config(cfg, variant=variant)
+    m, n, k = d["m"], d["n"], d["k"]
+    C_hi, C_lo, flags = casc.casc_gemm_fp64x2(T(d["A_hi"]), T(d["A_lo"]), T(d["B_hi"]),
+                                              T(d["B_lo"]))
+    torch.cuda.synchronize()
+    C_hi, C_lo, flags = N(C_hi), N(C_lo), N(flags)
+    rng = np.random.default_rng(100 + cfg)
+    i, j = int(rng.integers(0, m)), int(rng.integers(0, n))
+    b0, b1 = int(rng.integers(0, m - 64)), int(rng.integers(0, n - 128))
+    absA = np.abs(d["A_hi"]) + np.abs(d["A_lo"])
+    absB = np.abs(d["B_hi"]) + np.abs(d["B_lo"])
+    lines = [(slice(i, i + 1), slice(0, n)), (slice(b0, b0 + 64), slice(b1, b1 + 128))]
+    if cfg != 4:
+        lines.append((slice(0, m), slice(j, j + 1)))
+    for rows, cols in lines:
+        Bh = np.ascontiguousarray(d["B_hi"][:, cols])
+        Bl = np.ascontiguousarray(d["B_lo"][:, cols])
+        err, _ = EF.errors(d["A_hi"][rows], d["A_lo"][rows], Bh, Bl, C_hi[rows, cols],
+                           C_lo[rows, cols])
+        bound = orc.north_star_bound(k, (absA[rows] @ absB[:, cols]) * (1 - 2.0 ** -40))
+        assert np.all(np.abs(err) <= bound), (rows, cols)
+    o_hi, o_lo, o_fl = _sub_oracle(orc, d, [i], 0, n)
+    assert np.array_equal(flags[[i]], o_fl)
+    diff = np.abs((C_hi[[i]] - o_hi) + (C_lo[[i]] - o_lo))
+    assert np.all(diff <= 2 * orc.north_star_bound(k, absA[[i]] @ absB))
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_p_invariance_emulated_ranks(casc, world):
     """The multi-GPU data path run rank by rank on one GPU (no collective is
