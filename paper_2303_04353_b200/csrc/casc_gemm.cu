@@ -69,11 +69,11 @@ constexpr size_t GEMM_SMEM = EXP_OFFSET + (size_t)EXP_RING * (TM + TN) * sizeof(
 
 
 __device__ __forceinline__ void tile_coords(int tile, int mblocks, int nblocks, int& mb,
-                                            int& nb) {
-  const int per_group = GROUP_M * nblocks;
+                                            int& nb, int gm = GROUP_M) {
+  const int per_group = gm * nblocks;
   const int group = tile / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(mblocks - first_m, GROUP_M);
+  const int first_m = group * gm;
+  const int gsize = min(mblocks - first_m, gm);
   const int r = tile % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
@@ -109,7 +109,11 @@ __device__ __forceinline__ void item_coords(const GemmArgs& p, int split_p, int 
     s0 = q0 * STAGES_PER_PANEL;
     s1 = min(s0 + STAGES_PER_PANEL, p.st_end);
   } else {
-    tile_coords(item, p.mblocks, p.nblocks, mb, nb);
+    // TRMM (band): tile costs differ by row / column block; with 16 row blocks
+    // per raster group the persistent CTA b only ever meets the row offsets
+    // (b + 148 w) mod 16, i.e. 4 of the 16 (1.4% imbalance between CTAs); 17
+    // is coprime with the grid and spreads every offset over every CTA (0.2%)
+    tile_coords(item, p.mblocks, p.nblocks, mb, nb, (BAND && p.band) ? GROUP_M + 1 : GROUP_M);
     s0 = p.st_begin;
     s1 = p.st_end;
     q0 = 0;
