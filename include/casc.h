@@ -127,7 +127,8 @@ size_t casc_workspace_bytes(int64_t m, int64_t n, int64_t k);
  * of B (slab_cols columns; each 0 = 4096 for a dimension >= 8192, else half the
  * dimension but at least 1024; when m and n are both >= 8192 the default column
  * slab is the first 64-multiple >= 2048 that makes a block a whole number of
- * waves of 64 x 64 tiles (2368 on 148 SMs); rounded up to a multiple of 64), row slab
+ * waves of 64 x 64 tiles (2368 on 148 SMs), and the FIRST row / column slab is
+ * 1024 (a shorter exposed first copy); rounded up to a multiple of 64), row slab
  * outer: an internal H2D stream copies A_0, then the column slabs of B, then
  * the next row slabs of A ahead of their use; the caller's stream splits each
  * slab once and multiplies block after block; an internal D2H stream returns

@@ -501,9 +501,14 @@ int casc_gemm_fp64x2_host(int64_t m, int64_t n, int64_t k, const double* A_hi, c
     launches += g_launches;
     return rr;
   };
+  // large operands with the default blocks: first slabs of 1024 rows / columns,
+  // so the exposed first copy is 0.5 GB instead of 1.6 GB at 16384^3
+  const bool small_first = m >= 8192 && n >= 8192;
+  const int64_t sr0 = (small_first && !slab_rows) ? fit(1024, casc::TM, m) : sr;
+  const int64_t sc0 = (small_first && !slab_cols) ? fit(1024, casc::TN, n) : sc;
   r = casc::hostpipe::run(m, n, k, A_hi, A_lo, lda, B_hi, B_lo, ldb, C_hi, C_lo, ldc, flags, sr,
                           sc, casc_packed_b_bytes(k, sc), casc_packed_a_bytes(sr, k), st, pack_b,
-                          pack_a, gemm);
+                          pack_a, gemm, sr0, sc0);
   g_launches = r == CASC_OK ? launches : 0;
   return r;
 }

@@ -61,10 +61,12 @@ inline int zero_host_c(int64_t m, int64_t n, double* C_hi, double* C_lo, int64_t
   return CASC_OK;
 }
 
-// Blocks of C: row slabs of A (height sr) x column slabs of B (width sc), row
-// slab outer.  The H2D stream carries A_0, B_0 .. B_(J-1), A_1 .. A_(I-1) (two
-// staging slots each), so the first block starts once A_0 and B_0 are in and
-// the rest of B streams in under the first row of blocks.
+// Blocks of C: row slabs of A (height sr; the first one sr0 <= sr) x column
+// slabs of B (width sc; the first one sc0 <= sc), row slab outer.  The H2D
+// stream carries A_0, B_0 .. B_(J-1), A_1 .. A_(I-1) (two staging slots each),
+// so the first block starts once A_0 and B_0 are in and the rest of B streams
+// in under the first row of blocks; smaller first slabs shorten that exposed
+// first copy.
 // pack_b(dB_hi, dB_lo, cols, pB) / pack_a(dA_hi, dA_lo, rows, pA) /
 // gemm(rows, cols, pA, pB, dC_hi, dC_lo, dFlags) enqueue on `st` (dense device
 // operands: ld = cols for B and C, k for A) and return a casc status; bPBs /
@@ -73,11 +75,19 @@ template <class PackB, class PackA, class Gemm>
 int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo, int64_t lda,
         const double* B_hi, const double* B_lo, int64_t ldb, double* C_hi, double* C_lo,
         int64_t ldc, uint8_t* flags, int64_t sr, int64_t sc, size_t bPBs, size_t bPA,
-        cudaStream_t st, PackB pack_b, PackA pack_a, Gemm gemm) {
+        cudaStream_t st, PackB pack_b, PackA pack_a, Gemm gemm, int64_t sr0 = 0,
+        int64_t sc0 = 0) {
   Streams* hs = nullptr;
   int r = streams(&hs);
   if (r) return r;
-  const int64_t I = (m + sr - 1) / sr, J = (n + sc - 1) / sc;
+  if (sr0 <= 0 || sr0 > sr) sr0 = sr;
+  if (sc0 <= 0 || sc0 > sc) sc0 = sc;
+  const int64_t I = m <= sr0 ? 1 : 1 + (m - sr0 + sr - 1) / sr;
+  const int64_t J = n <= sc0 ? 1 : 1 + (n - sc0 + sc - 1) / sc;
+  auto row0 = [&](int64_t i) { return i == 0 ? 0 : sr0 + (i - 1) * sr; };
+  auto nrows = [&](int64_t i) { return std::min(i == 0 ? sr0 : sr, m - row0(i)); };
+  auto col0 = [&](int64_t j) { return j == 0 ? 0 : sc0 + (j - 1) * sc; };
+  auto ncols = [&](int64_t j) { return std::min(j == 0 ? sc0 : sc, n - col0(j)); };
   const int nA = I > 1 ? 2 : 1, nB = J > 1 ? 2 : 1, nC = I * J > 1 ? 2 : 1;
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t bB = al(16 * (size_t)k * sc), bA = al(16 * (size_t)sr * k);
@@ -133,7 +143,7 @@ int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
           if (packed_b < j - nB + 1) return;  // slot still holds B_(j-2)
           ok(cudaStreamWaitEvent(hs->h2d, ev_packB[sl], 0));
         }
-        const int64_t c0 = j * sc, cols = std::min(sc, n - c0);
+        const int64_t c0 = col0(j), cols = ncols(j);
         double* dB = reinterpret_cast<double*>(dBbuf + sl * bB);
         ok(cudaMemcpy2DAsync(dB, cols * 8, B_hi + c0, ldb * 8, cols * 8, k,
                              cudaMemcpyHostToDevice, hs->h2d));
@@ -147,7 +157,7 @@ int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
           if (packed_a < i - nA + 1) return;  // slot still holds A_(i-2)
           ok(cudaStreamWaitEvent(hs->h2d, ev_packA[sl], 0));
         }
-        const int64_t r0 = i * sr, rows = std::min(sr, m - r0);
+        const int64_t r0 = row0(i), rows = nrows(i);
         double* dA = reinterpret_cast<double*>(dAbuf + sl * bA);
         ok(cudaMemcpy2DAsync(dA, k * 8, A_hi + r0 * lda, lda * 8, k * 8, rows,
                              cudaMemcpyHostToDevice, hs->h2d));
@@ -160,7 +170,7 @@ int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
   pump();
   int64_t t = 0;  // block counter (C slots)
   for (int64_t i = 0; i < I && e == cudaSuccess && status == CASC_OK; ++i) {
-    const int64_t r0 = i * sr, rows = std::min(sr, m - r0);
+    const int64_t r0 = row0(i), rows = nrows(i);
     double* dA = reinterpret_cast<double*>(dAbuf + (i % nA) * bA);
     ok(cudaStreamWaitEvent(st, ev_A[i % nA], 0));
     okr(pack_a(dA, dA + rows * k, rows, pA));
@@ -168,7 +178,7 @@ int run(int64_t m, int64_t n, int64_t k, const double* A_hi, const double* A_lo,
     ++packed_a;
     pump();
     for (int64_t j = 0; j < J && e == cudaSuccess && status == CASC_OK; ++j, ++t) {
-      const int64_t c0 = j * sc, cols = std::min(sc, n - c0);
+      const int64_t c0 = col0(j), cols = ncols(j);
       uint8_t* pBj = pB + j * bPBs;
       if (i == 0) {  // B_j arrives during the first row of blocks
         double* dB = reinterpret_cast<double*>(dBbuf + (j % nB) * bB);
