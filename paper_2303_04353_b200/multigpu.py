@@ -109,6 +109,9 @@ class ShardedCascGemm:
         no SM from the GEMM and each slab's GEMM starts as soon as that slab has
         landed (own slab first, then r+1, r+2, ...); ordering between ranks is
         two CPU barriers per call (gloo group), no kernel waits on another rank.
+        Call close() on every rank when done (it unmaps the peers' buffers and
+        frees the exported one; collective).  If any rank cannot export or map
+        a buffer, every rank falls back to "raw" (collective decision).
         overlap (N > 1): the exchange runs while the GEMM multiplies the rank's
         own column slab (casc_gemm_packed_ld on a column block of C), then the
         other columns are multiplied once it has landed -- two stream-ordered
