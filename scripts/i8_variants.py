@@ -29,6 +29,7 @@ VARIANTS = {
     "tc64a10": ["CASC_I8_TC=64", "CASC_I8_NSA=10", "CASC_I8_NSB=16"],
     "tc64gm8": ["CASC_I8_TC=64", "CASC_I8_GROUP_M=8"],
     "oldi8": [],
+    "nowait_noepi": ["CASC_I8_NOWAIT", "CASC_I8_NO_EPI"],
 }
 if sys.argv[1] == "build":
     import importlib.util
