@@ -64,6 +64,15 @@ def load_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _int8_probe_mhz():
+    """median SM clock of the sustained INT8 probe run (power-capped)"""
+    try:
+        with open(os.path.join(ROOT, "peaks", "MEASURED_INT8_r01.json")) as f:
+            return float(json.load(f)["probe_sm_mhz_sustained"])
+    except Exception:
+        return None
+
+
 def load_int8_peak():
     """INT8 dense tensor peak for the NEXT-3 kernel: our own INT8 measurement
     (peaks/MEASURED_INT8_r01.json: tcgen05 kind::i8 CTA-pair probe, random
@@ -158,6 +167,8 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
     achieved = ops / (gemm_ms * 1e-3) / 1e12
     op.close()  # p2p: peer mappings and the exported buffer (collective)
     del op, C_hi, C_lo, fl
+    clk = cs.summary()
+    probe_mhz = _int8_probe_mhz()
     return {
         "method": "NEXT-3: FP64x2 via INT8 tensor cores (paper P:L3753-3754), y=%d slices, "
                   "%d int8 products per k panel of 8192; readings R22-R26" % (y, prods),
@@ -168,6 +179,11 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_sus,
                      "unit": "TOP/s (int8)", "frac": achieved / peak_sus,
                      "frac_vs_measured_peaks_bf16x2": achieved / _bf16x2_peak(),
+                     # both runs are power-capped: the peak scaled to the SM clock this
+                     # kernel ran at (its own data movement sets it), i.e. how busy the
+                     # tensor pipe is at that clock -- an explanation, not the headline
+                     "frac_at_kernel_clock": (achieved / (peak_sus * clk["sm_mhz"] / probe_mhz)
+                                              if clk.get("sm_mhz") and probe_mhz else None),
                      "traffic": (load_ncu_traffic() or {}).get("i8_gemm_dram_bytes_per_launch")
                      if (mloc, n, k) == (16384, 16384, 16384) and y == 14 else None,
                      "kernel": "i8_gemm_kernel (tcgen05.mma cta_group::2 kind::i8, fused "
@@ -180,7 +196,7 @@ def measure_int8(casc, A_hi, A_lo, B_hi, B_lo, m, n, k, steps, warmup, world=1, 
                                      "slices (tensor memory holds 4 bins); tile waves sweep in "
                                      "lockstep (soft wave sync) so each is read ~once per wave, "
                                      "plus the epilogue's group-value workspace"},
-        "clocks": cs.summary(),
+        "clocks": clk,
     }
 
 
