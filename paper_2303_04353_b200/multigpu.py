@@ -186,6 +186,10 @@ class ShardedCascGemm:
         ok = ok and all(h is not None for h in handles)
         if ok:
             try:
+                import os
+                # test hook: this rank fails to map its peers' buffers
+                if os.environ.get("CASC_P2P_FAIL_RANK") == str(self.rank):
+                    raise RuntimeError("CASC_P2P_FAIL_RANK")
                 with torch.cuda.device(self.device):
                     for q in range(self.world):
                         if q != self.rank:

@@ -6,7 +6,8 @@ the gathered C is bitwise the single-process result (P-invariance: k is never
 split), for the FP64 cascade ('raw' and 'packed' exchanges, and 'p2p': the
 slabs pulled from the other process's exported buffer by the copy engine, CUDA
 IPC within the one device, called twice to exercise the reuse ordering) and
-the INT8 cascade ('packed', 'p2p')."""
+the INT8 cascade ('packed', 'p2p'); 'p2pfail': one rank cannot map the
+other's buffer, so both fall back to the raw all-gather together."""
 
 import os
 import socket
@@ -46,11 +47,15 @@ def _rank(rank, world, port, m, n, k, kind, q):
         d = I.make_config(1, m=m, n=n, k=k, seed=77)
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
         gather = {"i8": "packed", "packed": "packed", "raw": "raw", "p2p": "p2p",
-                  "i8p2p": "p2p"}[kind]
+                  "i8p2p": "p2p", "p2pfail": "p2p"}[kind]
+        if kind == "p2pfail":  # rank 1 cannot map rank 0's buffer: both fall back
+            os.environ["CASC_P2P_FAIL_RANK"] = "1"
         op = ShardedCascGemm(m, n, k, ops=i8_cuda_ops() if i8 else None,
                              device=torch.device("cuda", 0), block=block, gather=gather)
         args = (T(d["A_hi"][r0:r1]), T(d["A_lo"][r0:r1]), T(d["B_hi"][:, c0:c1]),
                 T(d["B_lo"][:, c0:c1]))
+        if kind == "p2pfail":
+            assert op.gather == "raw" and not op.p2p
         C_hi, C_lo, fl = op(*args)
         if gather == "p2p":  # a second call reuses the exported buffers (ordering barriers)
             C_hi, C_lo, fl = op(*args)
@@ -64,7 +69,7 @@ def _rank(rank, world, port, m, n, k, kind, q):
 
 @pytest.mark.parametrize("kind,m,n,k", [("raw", 300, 520, 700), ("packed", 257, 200, 300),
                                         ("i8", 600, 700, 900), ("p2p", 300, 520, 700),
-                                        ("i8p2p", 600, 700, 900)])
+                                        ("i8p2p", 600, 700, 900), ("p2pfail", 300, 520, 700)])
 def test_two_processes_one_gpu_bitwise(kind, m, n, k):
     import torch
 
