@@ -463,7 +463,10 @@ def _config(args, world, gather=None):
                "rank; INT8 path: packed slabs all-gathered")
     return {"workload": CONFIG_TEXT[args.config], "m": m, "n": n, "k": k,
             "parallelism": par,
-            "l2": "inputs (16 B/elt x (mk+kn)) larger than the 126 MB L2; no flush",
+            "l2": ("inputs (16 B/elt x (mk+kn)) larger than the 126 MB L2; no flush"
+                   if 16 * (m * k + k * n) > (126 << 20) else
+                   "inputs smaller than the 126 MB L2 and NOT flushed between steps: a context "
+                   "figure (the small_problems line times such sizes with a flush per call)"),
             "k_panel": 256, "widths": [22, 21, 21] if k >= 256 else None}
 
 
